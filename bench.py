@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- AIREBO NVE throughput (atom-steps/s) of the B200 engine on BASELINE.json's config.
+
+Contract (driver): python bench.py --gpus N --steps K --warmup W [--impl reference]
+  * one JSON line on rank 0; value = whole-job atom-steps/s (all ranks), device-timed with CUDA
+    events on the engine's stream, max over ranks; inputs resident in HBM before the timed region.
+  * workload (N=1): BASELINE configs[1] = polyethylene 12x16x14 cells (32,256 atoms), +-0.02 A
+    jitter, 300 K, dt = 0.5 fs, NVE (velocity Verlet, skin 1 A, lists rebuilt on demand).
+    Each "step" = one full MD step (integrate, rebuild check, short list, REBO + bond order +
+    torsion, C_ij + LJ, b* batch, integrate).  L2 is flushed (256 MiB write) between timed steps.
+  * e2e: the same metric through the C-ABI with HOST buffers: per step ab_set_velocities (H2D
+    from pinned memory) + ab_run_nve(1 step, thermo row D2H) + ab_get_positions (D2H).
+  * --impl reference: the fp64 CPU oracle (oracle/) on the host cores, same workload.
+Multi-GPU (N > 1): the slab decomposition is not implemented yet; every rank runs an independent
+replica of the workload (scaling "weak", parallelism "replicas") and value sums the replicas.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AIREBO atom-steps/s (fp64 and mixed) at 1/2/4/8 B200; % of FP64/FP32 peak"
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_flops(stats):
+    """Per-phase algorithmic flop counts per launch (SURVEY §8(d) op weights)."""
+    lj = 31 * stats["n_lj"] + 9 * max(0, stats["n_lj_entries"] // 2 - stats["n_lj"])
+    rebo = 700 * stats["n_bonds"] + 65 * stats["n_angles"] + 260 * stats["n_quads"]
+    return {"short": 15 * stats["n_short"], "rebo": rebo, "lj": lj, "bstar": 1500 * stats["n_bstar"]}
+
+
+PHASES = ["short", "rebo", "lj", "bstar", "integrate", "rebuild"]
+KERNEL_OF = {"short": "k_short", "rebo": "k_rebo", "lj": "k_lj", "bstar": "k_bstar"}
+
+
+def fp64_peak_tflops(sm_mhz, nsm=148):
+    """148 SMs x 64 FP64 FMA/clk x 2 flop x f_SM (B200_PROFILING / SURVEY §8(d) unit counts)."""
+    return nsm * 64 * 2 * sm_mhz * 1e6 / 1e12
+
+
+def fp32_peak_tflops(sm_mhz, nsm=148):
+    return nsm * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_1810_07026_b200 import build as B
+    from paper_1810_07026_b200 import engine as E
+    from paper_1810_07026_b200 import inputs as I
+
+    if rank == 0:
+        B.build()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    s = I.config(args.config)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def leg(precision):
+        eng = E.make(s, precision, device=local)
+        eng.set_stream(stream.cuda_stream)
+        eng.run_nve(args.warmup, s.dt)  # warm-up (untimed): builds lists, JIT-free
+        torch.cuda.synchronize()
+        eng.L.ab_set_profiling(eng.h, 1)
+        l0 = eng.device_info()["kernel_launches"]
+        times = []
+        barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                flush.zero_()  # L2 flush between timed steps (untimed)
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                eng.run_nve(1, s.dt)
+                b.record(stream)
+                b.synchronize()
+                times.append(a.elapsed_time(b))
+        torch.cuda.synchronize()
+        barrier()
+        launches = eng.device_info()["kernel_launches"] - l0
+        import ctypes as C
+        ms = (C.c_double * 6)()
+        n = (C.c_int64 * 6)()
+        eng.L.ab_get_phase_ms(eng.h, ms, n)
+        eng.L.ab_set_profiling(eng.h, 0)
+        st = eng.stats()
+        total_ms = max_over_ranks(sum(times))
+        out = dict(eng=eng, times=times, total_ms=total_ms, clocks=clk.summary(), launches=launches,
+                   phase={p: (ms[q], int(n[q])) for q, p in enumerate(PHASES)}, stats=st)
+        return out
+
+    res = {}
+    for prec in ([args.precision] + (["mixed"] if args.precision == "fp64" and not args.no_mixed else [])):
+        res[prec] = leg(prec)
+
+    main = res[args.precision]
+    eng = main["eng"]
+    st = main["stats"]
+    n_atoms = s.n
+    K = args.steps
+    value = ws * n_atoms * K / (main["total_ms"] * 1e-3)
+    ms_per_step = main["total_ms"] / K
+
+    def roofline(r, precision):
+        flops = algorithmic_flops(r["stats"])
+        dom = max(("short", "rebo", "lj", "bstar"), key=lambda p: r["phase"][p][0])
+        tot_ms, cnt = r["phase"][dom]
+        avg_s = tot_ms / max(cnt, 1) * 1e-3
+        achieved = flops[dom] / avg_s / 1e12 if avg_s > 0 else 0.0
+        clk = r["clocks"]["sm_mhz"] or 1965.0
+        peak = fp64_peak_tflops(clk) if precision == "fp64" else fp32_peak_tflops(clk)
+        traffic = None
+        if os.path.exists(PROFILE_SUMMARY):
+            try:
+                summ = json.load(open(PROFILE_SUMMARY))
+                traffic = summ.get(precision, {}).get(KERNEL_OF[dom], {}).get("dram_bytes_per_launch")
+            except (ValueError, OSError):
+                traffic = None
+        step_flops = sum(flops.values())
+        step_s = r["total_ms"] / K * 1e-3
+        return {"bound": "alu", "kernel": KERNEL_OF[dom], "achieved": round(achieved, 4), "peak": round(peak, 3),
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 5), "traffic": traffic,
+                "peak_basis": f"{'FP64' if precision == 'fp64' else 'FP32'} FMA units x 2 x median SM clock "
+                              f"{clk:.0f} MHz under load (no FP64 entry in MEASURED_PEAKS.json)",
+                "algorithmic_flops_per_launch": flops[dom], "avg_launch_ms": round(avg_s * 1e3, 5),
+                "kernel_share_of_step": round(tot_ms / max(sum(v[0] for v in r["phase"].values()), 1e-9), 4),
+                "whole_step_tflops": round(step_flops / step_s / 1e12, 4),
+                "whole_step_frac": round(step_flops / step_s / 1e12 / peak, 5),
+                "phase_ms_per_step": {p: round(v[0] / K, 5) for p, v in r["phase"].items()}}
+
+    peak_meas = {}
+    for p, code in (("fp64", E.AB_FP64), ("fp32", E.AB_MIXED)):
+        import ctypes as C
+        tf = C.c_double()
+        if eng.L.ab_peak_flops(eng.h, code, C.byref(tf)) == 0:
+            peak_meas[p] = round(tf.value, 2)
+
+    # ---- e2e through the C-ABI with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        import torch
+        eng2 = E.make(s, args.precision, device=local)
+        eng2.set_stream(stream.cuda_stream)
+        eng2.run_nve(args.warmup, s.dt)
+        vh = torch.from_numpy(eng2.get_velocities()).pin_memory()
+        xh = torch.empty((n_atoms, 3), dtype=torch.float64).pin_memory()
+        th = np.zeros((2, 4))
+        import ctypes as C
+        dp = C.POINTER(C.c_double)
+        vptr = C.cast(vh.data_ptr(), dp)
+        xptr = C.cast(xh.data_ptr(), dp)
+        thp = th.ctypes.data_as(dp)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            eng2._ck(eng2.L.ab_set_velocities(eng2.h, vptr))
+            eng2._ck(eng2.L.ab_run_nve(eng2.h, 1, s.dt, 1, thp))
+            eng2._ck(eng2.L.ab_get_positions(eng2.h, xptr))
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": ws * n_atoms * K / t_e2e, "unit": "atom-steps/s", "h2d_bytes_per_step": 24 * n_atoms,
+               "d2h_bytes_per_step": 24 * n_atoms + 64}
+        eng2.close()
+
+    # ---- CPU baseline: the oracle as it stands, on this host's cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_baseline(s, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "atom-steps/s", "n_gpus": ws, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32+f64acc",
+            "data": "synthetic (seeded generator, paper_1810_07026_b200/inputs.py)",
+            "config": {"workload": s.name + " (BASELINE configs[1]: PE 12x16x14 cells, 32,256 atoms, 300 K, "
+                                            "dt 0.5 fs, NVE, LJ cutoff 3 sigma, torsion on)",
+                       "atoms": n_atoms, "dt_fs": s.dt, "precision": args.precision,
+                       "parallelism": "single GPU" if ws == 1 else "replicas (slab decomposition pending)",
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "timed_step": "ab_run_nve(1): integrate, rebuild check, forces, integrate"},
+            "roofline": roofline(main, args.precision),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": main["clocks"],
+            "gpu_launches": main["launches"],
+            "peak_measured_fma_tflops": peak_meas,
+            "counters": {k: st[k] for k in ("n_lj", "n_C0", "n_bstar", "n_sb_trans", "n_bonds", "n_quads",
+                                            "n_rebuilds", "n_ghosts")},
+            "step_ms_all": [round(t, 4) for t in main["times"]],
+        }
+        if "mixed" in res and args.precision == "fp64":
+            r = res["mixed"]
+            line["mixed"] = {"value": ws * n_atoms * K / (r["total_ms"] * 1e-3), "ms_per_step": r["total_ms"] / K,
+                             "roofline": roofline(r, "mixed"), "clocks": r["clocks"]}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_oracle_baseline(s, budget_s=15.0, max_steps=20):
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    x, v = s.x.copy(), s.v.copy()
+    steps = 0
+    t0 = time.perf_counter()
+    while steps < max_steps and time.perf_counter() - t0 < budget_s:
+        x, v, _ = O.nve(s.types, x, v, s.box, 1, s.dt, every=0, threads=cores)
+        steps += 1
+    t = time.perf_counter() - t0
+    return {"value": s.n * steps / t, "unit": "atom-steps/s", "cores": cores, "kind": "oracle",
+            "sample": f"{steps} velocity-Verlet steps of the full {s.n}-atom {s.name} (oracle recomputes lists and "
+                      f"AD forces from scratch every step), {t:.1f} s wall"}
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args, ws, rank, local):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_1810_07026_b200 import inputs as I
+    s = I.config(args.config)
+    cores = os.cpu_count() or 1
+    x, v = s.x.copy(), s.v.copy()
+    x, v, _ = O.nve(s.types, x, v, s.box, args.warmup, s.dt, every=0, threads=cores)
+    t0 = time.perf_counter()
+    x, v, _ = O.nve(s.types, x, v, s.box, args.steps, s.dt, every=0, threads=cores)
+    t = time.perf_counter() - t0
+    val = s.n * args.steps / t
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "atom-steps/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": s.name + " (BASELINE configs[1])", "atoms": s.n, "dt_fs": s.dt},
+            "cpu_baseline": {"value": val, "unit": "atom-steps/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} NVE steps of the full {s.n}-atom workload"},
+            "e2e": {"value": val, "unit": "atom-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
+    ap.add_argument("--config", default=2, type=lambda v: int(v) if v.isdigit() else v)
+    ap.add_argument("--no-mixed", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank, local)
+    else:
+        run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,34 @@
+"""Builds libairebo_b200.so in-tree with nvcc for sm_100a (no JIT cache, no CPU fallback)."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libairebo_b200.so")
+SOURCES = ["engine.cu", "params.cpp"]
+HEADERS = ["dev_common.cuh", "k_lists.cuh", "k_bond.cuh", "k_lj.cuh", "k_misc.cuh", "params.h"]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared"]
+
+
+def _inputs():
+    root = os.path.dirname(HERE)
+    return [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(root, "include", "airebo_b200.h")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    newest = max(os.path.getmtime(p) for p in _inputs())
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+        return LIB
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
+        [os.path.join(CSRC, s) for s in SOURCES] + ["-o", LIB + ".tmp"]
+    subprocess.run(cmd, check=True, cwd=CSRC)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True))

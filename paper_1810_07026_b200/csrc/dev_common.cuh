@@ -1,0 +1,324 @@
+// dev_common.cuh -- device-side constants, scalar building blocks and reduction helpers.
+//
+// Scalar forms:
+//   switch S(x; lo, hi): t = (x-lo)/(hi-lo); 1 (t<=0), 0 (t>=1), (1+cos(pi t))/2 inside
+//   g_i(cos): cubic Hermite on non-uniform knots, central-difference knot slopes, zero end slopes
+//   P / pi^rc / T: tensor products of the same Hermite scheme on integer knot grids
+// Precision: R = double (AB_FP64) or float (AB_MIXED); positions, displacements, r^2 list
+// decisions and all accumulators are always double.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace ab {
+
+constexpr int NBMAX = 16;         // short-list entries per atom the bond-order kernels accept
+constexpr int REACH_SLOTS = 256;  // per-warp open-addressing table of the C_ij reach set
+constexpr int REACH_EMPTY = -1;
+
+template <typename R>
+struct Tab {
+  R rmin[3], rmax[3], Q[3], alpha[3], A[3], B[3][3], beta[3][3];
+  R eps[3], sigma[3], sigma2[3], rc[3], rlo[3], bmin[3], bmax[3], rho[3], srhi[3];
+  R explam[2][2][2];  // e^{lambda_{jik}} [t_j][t_i][t_k]
+  int gn[2];
+  R gx[2][16], gy[2][16], gm[2][16];
+  R P[2][25], Rt[3][225], Tt[3][225];
+  R conj_lo, conj_hi, s2lo, s2hi;
+  R tors[2][2][2][2];
+};
+
+struct Geo {  // double-only quantities: exact list / gate decisions, box, integrator
+  double rmax2[3], rc2[3], rmax_s2[3], rc_s2[3], reach2;
+  double L[3];
+  double mass[2], ftm2v, mvv2e;
+};
+
+__constant__ Tab<double> c_tabd;
+__constant__ Tab<float> c_tabf;
+__constant__ Geo c_geo;
+
+template <typename R>
+__device__ __forceinline__ const Tab<R>& tab();
+template <>
+__device__ __forceinline__ const Tab<double>& tab<double>() {
+  return c_tabd;
+}
+template <>
+__device__ __forceinline__ const Tab<float>& tab<float>() {
+  return c_tabf;
+}
+
+// ------------------------------------------------------------------ vectors
+template <typename R>
+struct V3 {
+  R x, y, z;
+};
+template <typename R>
+__device__ __forceinline__ V3<R> mk3(R a, R b, R c) {
+  V3<R> v;
+  v.x = a, v.y = b, v.z = c;
+  return v;
+}
+template <typename R>
+__device__ __forceinline__ V3<R> operator+(V3<R> a, V3<R> b) {
+  return mk3(a.x + b.x, a.y + b.y, a.z + b.z);
+}
+template <typename R>
+__device__ __forceinline__ V3<R> operator-(V3<R> a, V3<R> b) {
+  return mk3(a.x - b.x, a.y - b.y, a.z - b.z);
+}
+template <typename R>
+__device__ __forceinline__ V3<R> operator*(R s, V3<R> a) {
+  return mk3(s * a.x, s * a.y, s * a.z);
+}
+template <typename R>
+__device__ __forceinline__ R dot3(V3<R> a, V3<R> b) {
+  return a.x * b.x + a.y * b.y + a.z * b.z;
+}
+template <typename R>
+__device__ __forceinline__ V3<R> cross3(V3<R> a, V3<R> b) {
+  return mk3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+template <typename R>
+__device__ __forceinline__ void addto(V3<R>& a, V3<R> b) {
+  a.x += b.x, a.y += b.y, a.z += b.z;
+}
+
+__device__ __forceinline__ double rsq(double x) { return rsqrt(x); }
+__device__ __forceinline__ float rsq(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double sqr_t(double x) { return sqrt(x); }
+__device__ __forceinline__ float sqr_t(float x) { return sqrtf(x); }
+__device__ __forceinline__ double ex(double x) { return exp(x); }
+__device__ __forceinline__ float ex(float x) { return expf(x); }
+__device__ __forceinline__ void scpi(double t, double* s, double* c) { sincospi(t, s, c); }
+__device__ __forceinline__ void scpi(float t, float* s, float* c) { sincospif(t, s, c); }
+
+// exact (no-FMA) displacement and squared length: the list / gate decisions must reproduce the
+// oracle's IEEE operations bit for bit
+__device__ __forceinline__ double r2_exact(double dx, double dy, double dz) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+// ------------------------------------------------------------------ switch
+template <typename R>
+__device__ __forceinline__ R sw(R x, R lo, R hi, R& dv) {
+  R t = (x - lo) / (hi - lo);
+  if (t <= R(0)) {
+    dv = R(0);
+    return R(1);
+  }
+  if (t >= R(1)) {
+    dv = R(0);
+    return R(0);
+  }
+  R s, c;
+  scpi(t, &s, &c);
+  dv = R(-0.5) * R(CUDART_PI) * s / (hi - lo);
+  return R(0.5) * (R(1) + c);
+}
+
+// ------------------------------------------------------------------ splines
+// g_i(c): cubic Hermite on the species' non-uniform knots; clamped (zero slope) outside
+template <typename R>
+__device__ __forceinline__ R gspline(int sp, R c, R& dg) {
+  const Tab<R>& T = tab<R>();
+  int n = T.gn[sp];
+  if (c <= T.gx[sp][0]) {
+    dg = R(0);
+    return T.gy[sp][0];
+  }
+  if (c >= T.gx[sp][n - 1]) {
+    dg = R(0);
+    return T.gy[sp][n - 1];
+  }
+  int i = 0;
+#pragma unroll 1
+  while (i < n - 2 && T.gx[sp][i + 1] <= c) ++i;
+  R h = T.gx[sp][i + 1] - T.gx[sp][i];
+  R t = (c - T.gx[sp][i]) / h;
+  R t2 = t * t, t3 = t2 * t;
+  R y0 = T.gy[sp][i], y1 = T.gy[sp][i + 1], m0 = h * T.gm[sp][i], m1 = h * T.gm[sp][i + 1];
+  R v = (R(2) * t3 - R(3) * t2 + R(1)) * y0 + (t3 - R(2) * t2 + t) * m0 + (R(-2) * t3 + R(3) * t2) * y1 +
+        (t3 - t2) * m1;
+  R dvt = (R(6) * t2 - R(6) * t) * y0 + (R(3) * t2 - R(4) * t + R(1)) * m0 + (R(-6) * t2 + R(6) * t) * y1 +
+          (R(3) * t2 - R(2) * t) * m1;
+  dg = dvt / h;
+  return v;
+}
+
+// 4 knot weights (knots i-1 .. i+2) of the integer-grid Hermite scheme and their x-derivatives.
+// grid: knots lo, lo+1, ..., lo+n-1; slopes (y_{i+1}-y_{i-1})/2 inside and 0 at the two ends.
+template <typename R>
+__device__ __forceinline__ int gridw(R x, R lo, int n, R w[4], R dw[4]) {
+  R hi = lo + R(n - 1);
+  bool clamped = false;
+  if (x <= lo) x = lo, clamped = true;
+  else if (x >= hi) x = hi, clamped = true;
+  int i = (int)floor(x - lo);
+  if (i > n - 2) i = n - 2;
+  if (i < 0) i = 0;
+  R t = x - (lo + R(i));
+  R t2 = t * t, t3 = t2 * t;
+  R h00 = R(2) * t3 - R(3) * t2 + R(1), h10 = t3 - R(2) * t2 + t, h01 = R(-2) * t3 + R(3) * t2, h11 = t3 - t2;
+  R d00 = R(6) * t2 - R(6) * t, d10 = R(3) * t2 - R(4) * t + R(1), d01 = R(-6) * t2 + R(6) * t,
+    d11 = R(3) * t2 - R(2) * t;
+  bool mi = (i > 0 && i < n - 1), mi1 = (i + 1 < n - 1);
+  // knot i-1 (q=0), i (1), i+1 (2), i+2 (3)
+  w[0] = mi ? R(-0.5) * h10 : R(0);
+  w[1] = h00 - (mi1 ? R(0.5) * h11 : R(0));
+  w[2] = h01 + (mi ? R(0.5) * h10 : R(0));
+  w[3] = mi1 ? R(0.5) * h11 : R(0);
+  dw[0] = mi ? R(-0.5) * d10 : R(0);
+  dw[1] = d00 - (mi1 ? R(0.5) * d11 : R(0));
+  dw[2] = d01 + (mi ? R(0.5) * d10 : R(0));
+  dw[3] = mi1 ? R(0.5) * d11 : R(0);
+  if (clamped)
+    for (int q = 0; q < 4; ++q) dw[q] = R(0);
+  return i - 1;  // knot index of weight 0
+}
+
+// P_ij(N^C, N^H) for a C centre (table index = partner species); value and gradient
+template <typename R>
+__device__ __forceinline__ R pspline(int tj, R x, R y, R& dx, R& dy) {
+  const Tab<R>& T = tab<R>();
+  R wx[4], dwx[4], wy[4], dwy[4];
+  int ax = gridw(x, R(0), 5, wx, dwx);
+  int ay = gridw(y, R(0), 5, wy, dwy);
+  R f = 0, fx = 0, fy = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    int ka = ax + a;
+    if (ka < 0 || ka > 4) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      int kb = ay + b;
+      if (kb < 0 || kb > 4) continue;
+      R v = T.P[tj][ka * 5 + kb];
+      f += wx[a] * wy[b] * v;
+      fx += dwx[a] * wy[b] * v;
+      fy += wx[a] * dwy[b] * v;
+    }
+  }
+  dx = fx, dy = fy;
+  return f;
+}
+
+// tricubic pi^rc / T table (which 0 = R, 1 = T) of pair p at (x, y, z) on 5 x 5 x 9 knots from (0,0,1)
+template <typename R>
+__device__ __forceinline__ R rtspline(int which, int p, R x, R y, R z, R& gx, R& gy, R& gz) {
+  const Tab<R>& T = tab<R>();
+  const R* tb = which == 0 ? T.Rt[p] : T.Tt[p];
+  R wx[4], dwx[4], wy[4], dwy[4], wz[4], dwz[4];
+  int ax = gridw(x, R(0), 5, wx, dwx);
+  int ay = gridw(y, R(0), 5, wy, dwy);
+  int az = gridw(z, R(1), 9, wz, dwz);
+  R f = 0, fx = 0, fy = 0, fz = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    int ka = ax + a;
+    if (ka < 0 || ka > 4) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      int kb = ay + b;
+      if (kb < 0 || kb > 4) continue;
+      R wab = wx[a] * wy[b], dxab = dwx[a] * wy[b], dyab = wx[a] * dwy[b];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        int kc = az + c;
+        if (kc < 0 || kc > 8) continue;
+        R v = tb[(ka * 5 + kb) * 9 + kc];
+        f += wab * wz[c] * v;
+        fx += dxab * wz[c] * v;
+        fy += dyab * wz[c] * v;
+        fz += wab * dwz[c] * v;
+      }
+    }
+  }
+  gx = fx, gy = fy, gz = fz;
+  return f;
+}
+
+// ------------------------------------------------------------------ atomics and reductions
+__device__ __forceinline__ void atomic_add3(double* F, int a, double x, double y, double z) {
+  atomicAdd(F + 3 * a + 0, x);
+  atomicAdd(F + 3 * a + 1, y);
+  atomicAdd(F + 3 * a + 2, z);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_sum_u(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ long long warp_max_i(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, (long long)__shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Accumulators of one force evaluation (device memory, zeroed per evaluation)
+enum {
+  ACC_EREBO = 0,
+  ACC_ETORS,
+  ACC_ELJ,
+  ACC_W,  // 6 virial components follow: xx yy zz xy xz yz
+  ACC_KE = ACC_W + 6,
+  ACC_N
+};
+enum {
+  CT_SHORT = 0,
+  CT_BONDS,
+  CT_QUADS,
+  CT_LJ,
+  CT_C0,
+  CT_BSTAR,
+  CT_SBTRANS,
+  CT_MAXSHORT,
+  CT_MAXREACH,
+  CT_BADARG,
+  CT_OVF_REACH,   // reach table overflows (fallback path search used)
+  CT_OVF_QUEUE,   // b* queue overflow (evaluation must be redone)
+  CT_OVF_SHORT,   // more than NBMAX short neighbours (hard error)
+  CT_OVF_STAGE,
+  CT_LJENT,       // skinned LJ list entries streamed
+  CT_ANGLES,      // bond-order angle terms
+  CT_N
+};
+
+// warp-reduce an array of doubles and add lane 0's totals into global accumulators.
+// Must be called by all 32 lanes of a warp.
+template <int K>
+__device__ __forceinline__ void warp_acc(double (&v)[K], double* acc) {
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    double s = warp_sum(v[q]);
+    if ((threadIdx.x & 31) == 0 && s != 0.0) atomicAdd(acc + q, s);
+  }
+}
+
+// virial of a vector v = x_b - x_a with energy gradient g = dE/dv:  W -= v (x) g
+template <typename R>
+__device__ __forceinline__ void vir_add(double W[6], V3<R> v, V3<R> g) {
+  W[0] -= (double)v.x * (double)g.x;
+  W[1] -= (double)v.y * (double)g.y;
+  W[2] -= (double)v.z * (double)g.z;
+  W[3] -= (double)v.x * (double)g.y;
+  W[4] -= (double)v.x * (double)g.z;
+  W[5] -= (double)v.y * (double)g.z;
+}
+
+// Half convention: the pair (i, J) belongs to i iff gid_i < gid_J, or the same atom
+// with image s_J >_lex 0.  shift is packed as char4.
+__device__ __forceinline__ bool canonical_pair(int gi, int gj, char4 sj) {
+  if (gi != gj) return gi < gj;
+  return sj.x > 0 || (sj.x == 0 && (sj.y > 0 || (sj.y == 0 && sj.z > 0)));
+}
+
+}  // namespace ab

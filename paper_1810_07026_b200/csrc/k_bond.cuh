@@ -1,0 +1,651 @@
+// k_bond.cuh -- bond order b_ij (forward + hand-derived reverse pass), REBO + torsion per bond,
+// and the deferred b* batch of the LJ term.
+//
+// Paper: E^REBO_ij = f_R(r) + b_ij f_A(r) (Alg. 1); b_ij = 1/2(p_ij + p_ji)
+// + pi^rc + pi^dh (reading A1: sum); p_ij = [1 + sum_k w_ik g_i(cos th_jik) e^{lam}
+// + P_ij]^{-1/2}; pi^rc spline in N_ij, N_ji, N^conj; pi^dh =
+// T_ij sum_k sum_l (1 - cos^2 w) w_ik w_jl G G; torsion (Alg. 2)
+// merged with REBO as in P:789; b* at the fictitious distance (reading A8) in batches
+// "calculated in the same manner as short-ranged forces".
+// Forward/reverse two-pass chain rule of P:242-253: the forward pass forms the sums, the reverse
+// pass turns dE/db into gradients on every relative vector (d_ij, d_ik, d_jl, d_km, d_ln) which
+// are scattered as forces with fp64 atomics (force on b -= g, on a += g for v = x_b - x_a) and
+// folded into the virial W -= v (x) g.
+// GPU mapping: one thread per REBO half bond / per queued b* pair (interaction-wise).
+#pragma once
+#include "dev_common.cuh"
+#include "k_lists.cuh"
+
+namespace ab {
+
+template <typename R>
+struct BoState {
+  int i, J, ti, tj;
+  V3<R> d, u;  // the bond vector used for angles (d_ij or rho d_hat) and its unit vector
+  R r;
+  int nI, nJ;
+  unsigned char sk[NBMAX], sl[NBMAX];  // slots in S of i's / J's neighbours (partner excluded)
+  R cl[NBMAX], Gl[NBMAX], dGl[NBMAX];
+  R Si, Sj, PxI, PyI, PxJ, PyJ;
+  R pij, pji, Nij, Nji, Nconj;
+  R Rv, Rx, Ry, Rz, Tv, Tx, Ty, Tz;  // derivatives w.r.t. (N_ij, N_ji, N^conj)
+  R D, Tsum;
+  int nquads;
+  bool bad;
+};
+
+template <typename R>
+__device__ __forceinline__ R clamp_cos(R c) {
+  return c > R(1) ? R(1) : (c < R(-1) ? R(-1) : c);
+}
+
+// collinearity guard G(c) = 1 - S(1 - c^2; s2lo, s2hi) (reading A9) and dG/dc
+template <typename R>
+__device__ __forceinline__ R guardG(R c, R& dG) {
+  const Tab<R>& T = tab<R>();
+  R ds;
+  R s = sw<R>(R(1) - c * c, T.s2lo, T.s2hi, ds);
+  dG = R(2) * c * ds;
+  return R(1) - s;
+}
+
+// V_tors(c) = (256/405) ((1+c)/2)^5 - 1/10 and its derivative
+template <typename R>
+__device__ __forceinline__ R vtors(R c, R& dv) {
+  R h = R(0.5) * (R(1) + c);
+  R h2 = h * h, h4 = h2 * h2;
+  dv = R(128.0 / 81.0) * h4;
+  return R(256.0 / 405.0) * h4 * h - R(0.1);
+}
+
+template <typename R>
+__device__ __forceinline__ R F_conj(R x, R& dF) {
+  const Tab<R>& T = tab<R>();
+  return sw<R>(x, T.conj_lo, T.conj_hi, dF);
+}
+
+// ---------------------------------------------------------------- forward pass
+template <typename R, bool TORS>
+__device__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i, int J, V3<R> d, R r,
+                           BoState<R>& st) {
+  const Tab<R>& T = tab<R>();
+  st.i = i, st.J = J, st.ti = typ[i], st.tj = typ[J], st.d = d, st.r = r;
+  const int ti = st.ti, tj = st.tj;
+  R ir = R(1) / r;
+  st.u = ir * d;
+  st.bad = false;
+  // ---- i side: k in N(i) \ {J}
+  R sumI = 0, NCi = 0, NHi = 0, Si = 0;
+  int nI = 0;
+  size_t bi = (size_t)i * S.capS;
+  int ni = S.cnt[i];
+  for (int q = 0; q < ni; ++q) {
+    int k = S.nbr[bi + q];
+    if (k == J) continue;
+    st.sk[nI++] = (unsigned char)q;
+    R rk;
+    V3<R> dk = sl_d(S, i, q, rk);
+    R wk = S.w[bi + q].x;
+    int tk = typ[k];
+    R c = clamp_cos(dot3(d, dk) * ir / rk);
+    R dg;
+    R g = gspline<R>(ti, c, dg);
+    sumI += wk * g * T.explam[tj][ti][tk];
+    if (tk == 0) {
+      NCi += wk;
+      R dF;
+      Si += wk * F_conj<R>(S.Ntot[k] - wk, dF);
+    } else {
+      NHi += wk;
+    }
+  }
+  st.nI = nI;
+  // ---- J side: l in N(J) \ {i}
+  R sumJ = 0, NCj = 0, NHj = 0, Sj = 0;
+  int nJ = 0;
+  size_t bj = (size_t)J * S.capS;
+  int nj = S.cnt[J];
+  V3<R> md = mk3(-d.x, -d.y, -d.z);
+  for (int q = 0; q < nj; ++q) {
+    int l = S.nbr[bj + q];
+    if (l == i) continue;
+    R rl;
+    V3<R> dl = sl_d(S, J, q, rl);
+    R wl = S.w[bj + q].x;
+    int tl = typ[l];
+    R c = clamp_cos(dot3(md, dl) * ir / rl);
+    R dg;
+    R g = gspline<R>(tj, c, dg);
+    sumJ += wl * g * T.explam[ti][tj][tl];
+    if (tl == 0) {
+      NCj += wl;
+      R dF;
+      Sj += wl * F_conj<R>(S.Ntot[l] - wl, dF);
+    } else {
+      NHj += wl;
+    }
+    st.sl[nJ] = (unsigned char)q;
+    st.cl[nJ] = c;
+    R dG;
+    st.Gl[nJ] = guardG<R>(c, dG);
+    st.dGl[nJ] = dG;
+    ++nJ;
+  }
+  st.nJ = nJ;
+  R PI = 0, PJ = 0;
+  st.PxI = st.PyI = st.PxJ = st.PyJ = 0;
+  if (ti == 0) PI = pspline<R>(tj, NCi, NHi, st.PxI, st.PyI);
+  if (tj == 0) PJ = pspline<R>(ti, NCj, NHj, st.PxJ, st.PyJ);
+  R argI = R(1) + sumI + PI, argJ = R(1) + sumJ + PJ;
+  st.bad = !(argI > R(0)) || !(argJ > R(0));
+  st.pij = rsq(argI);
+  st.pji = rsq(argJ);
+  st.Si = Si, st.Sj = Sj;
+  st.Nij = NCi + NHi;
+  st.Nji = NCj + NHj;
+  st.Nconj = R(1) + Si * Si + Sj * Sj;
+  int p = ti + tj;
+  if (ti == 1 && tj == 0) {  // CH tables take the carbon-side N first
+    st.Rv = rtspline<R>(0, p, st.Nji, st.Nij, st.Nconj, st.Ry, st.Rx, st.Rz);
+    st.Tv = rtspline<R>(1, p, st.Nji, st.Nij, st.Nconj, st.Ty, st.Tx, st.Tz);
+  } else {
+    st.Rv = rtspline<R>(0, p, st.Nij, st.Nji, st.Nconj, st.Rx, st.Ry, st.Rz);
+    st.Tv = rtspline<R>(1, p, st.Nij, st.Nji, st.Nconj, st.Tx, st.Ty, st.Tz);
+  }
+  // ---- dihedral sum (and torsion sum): k in N(i)\J, l in N(J)\{i, k}
+  R D = 0, Ts = 0;
+  int nq = 0;
+  for (int a = 0; a < nI; ++a) {
+    int q = st.sk[a];
+    int k = S.nbr[bi + q];
+    R rk;
+    V3<R> dk = sl_d(S, i, q, rk);
+    R wk = S.w[bi + q].x;
+    R ck = clamp_cos(dot3(d, dk) * ir / rk);
+    R dGk;
+    R Gk = guardG<R>(ck, dGk);
+    V3<R> n1 = cross3(dk, d);
+    R n1s = dot3(n1, n1);
+    for (int c = 0; c < nJ; ++c) {
+      int ql = st.sl[c];
+      int l = S.nbr[bj + ql];
+      if (l == k) continue;
+      ++nq;
+      if (Gk == R(0) || st.Gl[c] == R(0)) continue;
+      R rl;
+      V3<R> dl = sl_d(S, J, ql, rl);
+      R wl = S.w[bj + ql].x;
+      V3<R> n2 = cross3(md, dl);
+      R cw = dot3(n1, n2) * rsq(n1s * dot3(n2, n2));
+      R base = wk * wl * Gk * st.Gl[c];
+      D += (R(1) - cw * cw) * base;
+      if (TORS) {
+        R dv;
+        Ts += T.tors[typ[k]][ti][tj][typ[l]] * base * vtors<R>(cw, dv);
+      }
+    }
+  }
+  st.D = D;
+  st.Tsum = Ts;
+  st.nquads = nq;
+}
+
+template <typename R>
+__device__ __forceinline__ R bo_value(const BoState<R>& st) {
+  return R(0.5) * (st.pij + st.pji) + st.Rv + st.Tv * st.D;
+}
+
+template <typename R>
+__device__ __forceinline__ void scatter_vec(double* F, const int* owner, int a_to, int a_from, V3<R> g) {
+  // vector v = x_to - x_from with gradient g: F_to -= g, F_from += g
+  atomic_add3(F, owner[a_to], -(double)g.x, -(double)g.y, -(double)g.z);
+  atomic_add3(F, owner[a_from], (double)g.x, (double)g.y, (double)g.z);
+}
+
+// ---------------------------------------------------------------- reverse pass
+// cb = dE/db.  wij: weight of the bond for the merged torsion term (TORS only).
+// Output gd = dE/d(d) through the bond-order (and torsion) terms; fi / fj = force contributions
+// on i / J from the k and l vectors (already scattered onto k, l, m, n).
+template <typename R, bool TORS>
+__device__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const int* owner, const BoState<R>& st,
+                           R cb, R wij, double* F, double W[6], V3<R>& gd, V3<R>& fi, V3<R>& fj) {
+  const Tab<R>& T = tab<R>();
+  const int i = st.i, J = st.J, ti = st.ti, tj = st.tj;
+  const V3<R> d = st.d, u = st.u;
+  const V3<R> md = mk3(-d.x, -d.y, -d.z);
+  const R r = st.r, ir = R(1) / r;
+  const R cI = R(-0.25) * cb * st.pij * st.pij * st.pij;
+  const R cJ = R(-0.25) * cb * st.pji * st.pji * st.pji;
+  const R dNij = cb * (st.Rx + st.Tx * st.D);
+  const R dNji = cb * (st.Ry + st.Ty * st.D);
+  const R dNc = cb * (st.Rz + st.Tz * st.D);
+  const R cD = cb * st.Tv;
+  size_t bi = (size_t)i * S.capS, bj = (size_t)J * S.capS;
+  gd = mk3<R>(0, 0, 0);
+  fi = mk3<R>(0, 0, 0);
+  fj = mk3<R>(0, 0, 0);
+  R Wl[NBMAX], Cl[NBMAX];
+  V3<R> gl[NBMAX];
+  for (int c = 0; c < st.nJ; ++c) {
+    int q = st.sl[c];
+    int l = S.nbr[bj + q];
+    int tl = typ[l];
+    R wl = S.w[bj + q].x;
+    R dg;
+    R g = gspline<R>(tj, st.cl[c], dg);
+    R el = T.explam[ti][tj][tl];
+    R Pd = tl == 0 ? st.PxJ : st.PyJ;
+    Wl[c] = cJ * (g * el + Pd) + dNji;
+    if (tl == 0) {
+      R dF;
+      R Fl = F_conj<R>(S.Ntot[l] - wl, dF);
+      Wl[c] += dNc * R(2) * st.Sj * Fl;
+    }
+    Cl[c] = cJ * wl * dg * el;
+    gl[c] = mk3<R>(0, 0, 0);
+  }
+  for (int a = 0; a < st.nI; ++a) {
+    int q = st.sk[a];
+    int k = S.nbr[bi + q];
+    int tk = typ[k];
+    R rk;
+    V3<R> dk = sl_d(S, i, q, rk);
+    R wk = S.w[bi + q].x, dwk = S.w[bi + q].y;
+    R irk = R(1) / rk;
+    V3<R> uk = irk * dk;
+    R ck = clamp_cos(dot3(u, uk));
+    R dg;
+    R g = gspline<R>(ti, ck, dg);
+    R ek = T.explam[tj][ti][tk];
+    R Wk = cI * (g * ek + (tk == 0 ? st.PxI : st.PyI)) + dNij;
+    R Ck = cI * wk * dg * ek;
+    R chain = 0;
+    if (tk == 0) {
+      R dF;
+      R Fk = F_conj<R>(S.Ntot[k] - wk, dF);
+      Wk += dNc * R(2) * st.Si * Fk;
+      chain = dNc * R(2) * st.Si * wk * dF;
+    }
+    V3<R> gk = mk3<R>(0, 0, 0);
+    R dGk;
+    R Gk = guardG<R>(ck, dGk);
+    if (Gk != R(0)) {
+      V3<R> n1 = cross3(dk, d);
+      R inv1 = rsq(dot3(n1, n1));
+      for (int c = 0; c < st.nJ; ++c) {
+        int ql = st.sl[c];
+        int l = S.nbr[bj + ql];
+        if (l == k || st.Gl[c] == R(0)) continue;
+        R rl;
+        V3<R> dl = sl_d(S, J, ql, rl);
+        R wl = S.w[bj + ql].x;
+        V3<R> n2 = cross3(md, dl);
+        R inv2 = rsq(dot3(n2, n2));
+        R cw = dot3(n1, n2) * inv1 * inv2;
+        R Gl = st.Gl[c];
+        R coef = cD * (R(1) - cw * cw);
+        R dcoef = cD * (R(-2) * cw);
+        if (TORS) {
+          R eps = T.tors[tk][ti][tj][typ[l]] * wij;
+          R dv;
+          R v = vtors<R>(cw, dv);
+          coef += eps * v;
+          dcoef += eps * dv;
+        }
+        R wG = wk * wl;
+        R GG = Gk * Gl;
+        R dEdcw = dcoef * wG * GG;
+        Wk += coef * wl * GG;
+        Wl[c] += coef * wk * GG;
+        Ck += coef * wG * Gl * dGk;
+        Cl[c] += coef * wG * Gk * st.dGl[c];
+        // d cos w / d a = b x g1, / d e = b x g2, / d b = g1 x a + g2 x e  (a = d_ik, b = d, e = d_jl)
+        V3<R> g1 = inv1 * (inv2 * n2 - (cw * inv1) * n1);
+        V3<R> g2 = inv2 * (inv1 * n1 - (cw * inv2) * n2);
+        addto(gk, dEdcw * cross3(d, g1));
+        addto(gl[c], dEdcw * cross3(d, g2));
+        addto(gd, dEdcw * (cross3(g1, dk) + cross3(g2, dl)));
+      }
+    }
+    // w_ik(r_ik) and cos(theta_jik) derivatives
+    addto(gk, (Wk * dwk) * uk);
+    addto(gk, (Ck * irk) * (u - ck * uk));
+    addto(gd, (Ck * ir) * (uk - ck * u));
+    // force on k now; the +gk on i is accumulated in fi (one atomic per bond for i)
+    atomic_add3(F, owner[k], -(double)gk.x, -(double)gk.y, -(double)gk.z);
+    addto(fi, gk);
+    vir_add(W, dk, gk);
+    // N^conj chain through N_k = sum_m w_km (m != i)
+    if (chain != R(0)) {
+      size_t bk = (size_t)k * S.capS;
+      int nk = S.cnt[k];
+      for (int q2 = 0; q2 < nk; ++q2) {
+        int m = S.nbr[bk + q2];
+        if (m == i) continue;
+        R dw = S.w[bk + q2].y;
+        if (dw == R(0)) continue;
+        R rkm;
+        V3<R> dkm = sl_d(S, k, q2, rkm);
+        V3<R> g = (chain * dw / rkm) * dkm;
+        scatter_vec(F, owner, m, k, g);
+        vir_add(W, dkm, g);
+      }
+    }
+  }
+  for (int c = 0; c < st.nJ; ++c) {
+    int q = st.sl[c];
+    int l = S.nbr[bj + q];
+    int tl = typ[l];
+    R rl;
+    V3<R> dl = sl_d(S, J, q, rl);
+    R wl = S.w[bj + q].x, dwl = S.w[bj + q].y;
+    R irl = R(1) / rl;
+    V3<R> ul = irl * dl;
+    R cl = st.cl[c];
+    V3<R> g = gl[c];
+    addto(g, (Wl[c] * dwl) * ul);
+    addto(g, (Cl[c] * irl) * (mk3(-u.x, -u.y, -u.z) - cl * ul));
+    addto(gd, (-Cl[c] * ir) * (ul + cl * u));
+    atomic_add3(F, owner[l], -(double)g.x, -(double)g.y, -(double)g.z);
+    addto(fj, g);
+    vir_add(W, dl, g);
+    if (tl == 0) {
+      R dF;
+      F_conj<R>(S.Ntot[l] - wl, dF);
+      R chain = dNc * R(2) * st.Sj * wl * dF;
+      if (chain != R(0)) {
+        size_t bl = (size_t)l * S.capS;
+        int nl = S.cnt[l];
+        for (int q2 = 0; q2 < nl; ++q2) {
+          int n = S.nbr[bl + q2];
+          if (n == J) continue;
+          R dw = S.w[bl + q2].y;
+          if (dw == R(0)) continue;
+          R rln;
+          V3<R> dln = sl_d(S, l, q2, rln);
+          V3<R> gg = (chain * dw / rln) * dln;
+          scatter_vec(F, owner, n, l, gg);
+          vir_add(W, dln, gg);
+        }
+      }
+    }
+  }
+}
+
+struct StageBuf {
+  double* rows;
+  int* count;
+  int cap;
+};
+
+__device__ __forceinline__ double* stage_row(StageBuf sb, int width) {
+  int k = atomicAdd(sb.count, 1);
+  if (k >= sb.cap) return nullptr;
+  return sb.rows + (size_t)k * width;
+}
+
+// ---------------------------------------------------------------- REBO + torsion, one thread per bond
+template <typename R>
+__global__ void __launch_bounds__(128) k_rebo(const int2* bonds, const int* nbonds, ShortList<R> S,
+                                              const signed char* typ, const int* owner, const int* gid,
+                                              const char4* shift, double* F, double* acc, unsigned long long* ct,
+                                              StageBuf stage) {
+  const Tab<R>& T = tab<R>();
+  int nb = *nbonds;
+  double e[3 + 6] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long nq = 0, nbad = 0, ncount = 0, nang = 0;
+  int stride = gridDim.x * blockDim.x;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t - (int)threadIdx.x < nb; t += stride) {
+    if (t < nb) {
+      int2 bd = bonds[t];
+      int i = bd.x, q = bd.y;
+      size_t e0 = (size_t)i * S.capS + q;
+      int J = S.nbr[e0];
+      R r;
+      V3<R> d = sl_d(S, i, q, r);
+      R w = S.w[e0].x, dw = S.w[e0].y;
+      int ti = typ[i], tj = typ[J], p = ti + tj;
+      // pair terms f_R = w (1 + Q/r) A e^{-alpha r},  f_A = -w sum_n B_n e^{-beta_n r}
+      R ir = R(1) / r;
+      R ea = ex(-T.alpha[p] * r);
+      R qr = R(1) + T.Q[p] * ir;
+      R VR = w * qr * T.A[p] * ea;
+      R dVR = dw * qr * T.A[p] * ea + w * T.A[p] * ea * (-T.Q[p] * ir * ir - T.alpha[p] * qr);
+      R sb = 0, sbb = 0;
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        R eb = T.B[p][n] * ex(-T.beta[p][n] * r);
+        sb += eb;
+        sbb += T.beta[p][n] * eb;
+      }
+      R VA = -w * sb;
+      R dVA = -dw * sb + w * sbb;
+      BoState<R> st;
+      bo_forward<R, true>(S, typ, i, J, d, r, st);
+      R b = bo_value(st);
+      V3<R> gd, fi, fj;
+      bo_reverse<R, true>(S, typ, owner, st, VA, w, F, e + 3, gd, fi, fj);
+      R dEdr = dVR + b * dVA + dw * st.Tsum;
+      addto(gd, (dEdr * ir) * d);
+      atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
+      atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
+      vir_add(e + 3, d, gd);
+      e[0] += (double)(VR + b * VA);
+      e[1] += (double)(w * st.Tsum);
+      nq += st.nquads;
+      nbad += st.bad;
+      ncount += 1;
+      nang += st.nI + st.nJ;
+      if (stage.rows) {
+        double* row = stage_row(stage, 13);
+        if (row) {
+          char4 s = shift[J];
+          row[0] = gid[i], row[1] = gid[J], row[2] = s.x, row[3] = s.y, row[4] = s.z;
+          row[5] = b, row[6] = st.pij, row[7] = st.pji, row[8] = st.Rv, row[9] = st.Tv * st.D;
+          row[10] = st.Nij, row[11] = st.Nji, row[12] = st.Nconj;
+        }
+      }
+    }
+    // keep the warp converged for the reductions below
+  }
+  warp_acc(e, acc + ACC_EREBO);
+  unsigned long long s1 = warp_sum_u(nq), s2 = warp_sum_u(nbad), s3 = warp_sum_u(ncount), s4 = warp_sum_u(nang);
+  if ((threadIdx.x & 31) == 0) {
+    if (s4) atomicAdd(ct + CT_ANGLES, s4);
+    if (s1) atomicAdd(ct + CT_QUADS, s1);
+    if (s2) atomicAdd(ct + CT_BADARG, s2);
+    if (s3) atomicAdd(ct + CT_BONDS, s3);
+  }
+}
+
+// ---------------------------------------------------------------- C_ij path search
+// Direct nested search for M = max{w_ij, w_ik w_kj, w_ik w_kl w_lj} and its maximising path,
+// used when 0 < C_ij < 1 (forces along the path) or when the per-atom reach table overflowed.
+template <typename R>
+struct PathRes {
+  R M;
+  int hops;
+  int a0, q0, a1, q1, a2, q2;  // (atom, slot) of each path edge in the short list
+};
+
+template <typename R>
+__device__ PathRes<R> path_search(const ShortList<R>& S, int i, int J) {
+  PathRes<R> pr;
+  pr.M = 0;
+  pr.hops = 0;
+  size_t bi = (size_t)i * S.capS;
+  int ni = S.cnt[i];
+  for (int a = 0; a < ni; ++a)
+    if (S.nbr[bi + a] == J) {
+      R c = S.w[bi + a].x;
+      if (c > pr.M) pr.M = c, pr.hops = 1, pr.a0 = i, pr.q0 = a;
+    }
+  for (int a = 0; a < ni; ++a) {
+    int k = S.nbr[bi + a];
+    if (k == J) continue;
+    R w1 = S.w[bi + a].x;
+    size_t bk = (size_t)k * S.capS;
+    int nk = S.cnt[k];
+    for (int b = 0; b < nk; ++b) {
+      int l = S.nbr[bk + b];
+      if (l != J) continue;
+      R c = w1 * S.w[bk + b].x;
+      if (c > pr.M) pr.M = c, pr.hops = 2, pr.a0 = i, pr.q0 = a, pr.a1 = k, pr.q1 = b;
+    }
+  }
+  for (int a = 0; a < ni; ++a) {
+    int k = S.nbr[bi + a];
+    if (k == J) continue;
+    R w1 = S.w[bi + a].x;
+    size_t bk = (size_t)k * S.capS;
+    int nk = S.cnt[k];
+    for (int b = 0; b < nk; ++b) {
+      int l = S.nbr[bk + b];
+      if (l == i || l == J) continue;
+      R w2 = S.w[bk + b].x;
+      size_t bl = (size_t)l * S.capS;
+      int nl = S.cnt[l];
+      for (int c2 = 0; c2 < nl; ++c2) {
+        if (S.nbr[bl + c2] != J) continue;
+        R c = (w1 * w2) * S.w[bl + c2].x;
+        if (c > pr.M) pr.M = c, pr.hops = 3, pr.a0 = i, pr.q0 = a, pr.a1 = k, pr.q1 = b, pr.a2 = l, pr.q2 = c2;
+      }
+    }
+  }
+  return pr;
+}
+
+// forces of E = f(M) along the maximising path: dE/dM = cM
+template <typename R>
+__device__ void path_forces(const ShortList<R>& S, const int* owner, const PathRes<R>& pr, R cM, double* F,
+                            double W[6]) {
+  int at[3] = {pr.a0, pr.a1, pr.a2}, sl[3] = {pr.q0, pr.q1, pr.q2};
+  R w[3], dw[3];
+  for (int h = 0; h < pr.hops; ++h) {
+    auto wv = S.w[(size_t)at[h] * S.capS + sl[h]];
+    w[h] = wv.x;
+    dw[h] = wv.y;
+  }
+  for (int h = 0; h < pr.hops; ++h) {
+    if (dw[h] == R(0)) continue;
+    R others = 1;
+    for (int o = 0; o < pr.hops; ++o)
+      if (o != h) others *= w[o];
+    R rr;
+    V3<R> v = sl_d(S, at[h], sl[h], rr);
+    int to = S.nbr[(size_t)at[h] * S.capS + sl[h]];
+    V3<R> g = (cM * others * dw[h] / rr) * v;
+    scatter_vec(F, owner, to, at[h], g);
+    vir_add(W, v, g);
+  }
+}
+
+// LJ radial part V(r) = 4 eps [(s/r)^12 - (s/r)^6] S(r; r_lo, r_c) (reading A10) with (dV/dr)/r.
+template <typename R>
+__device__ __forceinline__ R lj_v(int p, R r2, double r2d, R& dVr_over_r) {
+  const Tab<R>& T = tab<R>();
+  R sr2 = T.sigma2[p] / r2;
+  R sr6 = sr2 * sr2 * sr2;
+  R e4 = R(4) * T.eps[p];
+  R V = e4 * (sr6 * sr6 - sr6);
+  R dv = -e4 * (R(12) * sr6 * sr6 - R(6) * sr6) / r2;  // (dV0/dr)/r
+  if (r2d > c_tabd.rlo[p] * c_tabd.rlo[p]) {
+    R r = sqr_t(r2);
+    R ds;
+    R s = sw<R>(r, T.rlo[p], T.rc[p], ds);
+    dv = dv * s + V * ds / r;
+    V = V * s;
+  }
+  dVr_over_r = dv;
+  return V;
+}
+
+struct BstarQueue {
+  int4* item;  // i, J, -, -
+  double* M;
+  int* count;
+  int cap;
+};
+
+// ---------------------------------------------------------------- deferred b* batch
+// E = (S_r S_b(b*) + 1 - S_r) C V for every canonical LJ pair with C != 0 and S_r != 0.
+template <typename R>
+__global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const double4* pos, ShortList<R> S,
+                                               const signed char* typ, const int* owner, const int* gid,
+                                               const char4* shift, double* F, double* acc,
+                                               unsigned long long* ct, StageBuf stage) {
+  const Tab<R>& T = tab<R>();
+  int nq = min(*Qu.count, Qu.cap);
+  double e[1 + 6] = {0, 0, 0, 0, 0, 0, 0};
+  unsigned long long ntr = 0, nb = 0, nbad = 0;
+  int stride = gridDim.x * blockDim.x;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t - (int)threadIdx.x < nq; t += stride) {
+    if (t < nq) {
+      int4 it = Qu.item[t];
+      int i = it.x, J = it.y;
+      double Md = Qu.M[t];
+      double4 pi = pos[i], pj = pos[J];
+      double dxd = pj.x - pi.x, dyd = pj.y - pi.y, dzd = pj.z - pi.z;
+      double r2d = r2_exact(dxd, dyd, dzd);
+      double rd = sqrt(r2d);
+      int ti = typ[i], tj = typ[J], p = ti + tj;
+      V3<R> d = mk3<R>((R)dxd, (R)dyd, (R)dzd);
+      R r = (R)rd, ir = R(1) / r;
+      R dP;
+      R P = sw<R>(r, T.sigma[p], T.srhi[p], dP);
+      R dVr;
+      R V = lj_v<R>(p, (R)r2d, r2d, dVr);
+      R M = (R)Md, C = R(1) - M;
+      R rho = T.rho[p];
+      V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
+      BoState<R> st;
+      bo_forward<R, false>(S, typ, i, J, ds, rho, st);
+      R bs = bo_value(st);
+      R dB;
+      R B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
+      R tb = (bs - T.bmin[p]) / (T.bmax[p] - T.bmin[p]);
+      if (tb > R(0) && tb < R(1)) ++ntr;
+      R Q = P * B + R(1) - P;
+      R E = Q * C * V;
+      V3<R> gd = ((C * (Q * dVr + V * (B - R(1)) * dP * ir))) * d;
+      V3<R> fi = mk3<R>(0, 0, 0), fj = mk3<R>(0, 0, 0);
+      if (dB != R(0)) {
+        V3<R> gs;
+        bo_reverse<R, false>(S, typ, owner, st, C * V * P * dB, R(0), F, e + 1, gs, fi, fj);
+        // chain through d* = rho d / |d|: dE/dd = (rho/r) (I - u u^T) dE/dd*
+        V3<R> u = ir * d;
+        addto(gd, (rho * ir) * (gs - dot3(u, gs) * u));
+      }
+      if (M > R(0)) {
+        PathRes<R> pr = path_search(S, i, J);
+        path_forces(S, owner, pr, -Q * V, F, e + 1);
+      }
+      atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
+      atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
+      vir_add(e + 1, d, gd);
+      e[0] += (double)E;
+      ++nb;
+      nbad += st.bad;
+      if (stage.rows) {
+        double* row = stage_row(stage, 7);
+        if (row) {
+          char4 s = shift[J];
+          row[0] = gid[i], row[1] = gid[J], row[2] = s.x, row[3] = s.y, row[4] = s.z;
+          row[5] = C, row[6] = bs;
+        }
+      }
+    }
+  }
+  double e1[1] = {e[0]};
+  warp_acc(e1, acc + ACC_ELJ);
+  double w6[6] = {e[1], e[2], e[3], e[4], e[5], e[6]};
+  warp_acc(w6, acc + ACC_W);
+  unsigned long long s1 = warp_sum_u(ntr), s2 = warp_sum_u(nb), s3 = warp_sum_u(nbad);
+  if ((threadIdx.x & 31) == 0) {
+    if (s1) atomicAdd(ct + CT_SBTRANS, s1);
+    if (s2) atomicAdd(ct + CT_BSTAR, s2);
+    if (s3) atomicAdd(ct + CT_BADARG, s3);
+  }
+}
+
+}  // namespace ab

@@ -1,0 +1,287 @@
+// k_lists.cuh -- binning, periodic-image ghosts, skinned lists and the per-step exact short list.
+//
+// Paper: neighbour lists by binning, half-list convention, skin with
+// rebuild when an atom moved too far, long list built by binning and short list
+// derived from it, intermediate skinned short list refreshed into the exact short list
+// every step.  B200 layout: positions double4 (x, y, z, type) for local atoms
+// followed by ghost images; lists are per-atom fixed-stride int32 rows (atom a's entries at
+// a*cap .. a*cap+cnt[a]-1), written in (stencil cell, sorted index) order, so every rebuild is
+// deterministic.  All r^2 decisions use un-fused IEEE operations identical to the oracle's.
+#pragma once
+#include "dev_common.cuh"
+#include <type_traits>
+
+namespace ab {
+
+struct Grid {
+  int nc[3];
+  double lo[3];  // lower corner of the padded region (= -halo)
+  double cs[3];  // cell edge
+};
+
+__device__ __forceinline__ int cell_coord(double x, double lo, double cs, int n) {
+  int c = (int)floor((x - lo) / cs);
+  return c < 0 ? 0 : (c >= n ? n - 1 : c);
+}
+__device__ __forceinline__ int cell_of(double4 p, const Grid& g) {
+  int cx = cell_coord(p.x, g.lo[0], g.cs[0], g.nc[0]);
+  int cy = cell_coord(p.y, g.lo[1], g.cs[1], g.nc[1]);
+  int cz = cell_coord(p.z, g.lo[2], g.cs[2], g.nc[2]);
+  return (cx * g.nc[1] + cy) * g.nc[2] + cz;
+}
+
+// wrap x into [0, L): y = x - L floor(x/L); y >= L -> y -= L; y < 0 -> y += L
+__device__ __forceinline__ double wrap1(double x, double L) {
+  double y = __dsub_rn(x, __dmul_rn(L, floor(__ddiv_rn(x, L))));
+  if (y >= L) y = __dsub_rn(y, L);
+  if (y < 0.0) y = __dadd_rn(y, L);
+  return y;
+}
+
+__global__ void k_wrap_and_key(int N, double4* pos, Grid g, int* key, int* val) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double4 p = pos[i];
+  p.x = wrap1(p.x, c_geo.L[0]);
+  p.y = wrap1(p.y, c_geo.L[1]);
+  p.z = wrap1(p.z, c_geo.L[2]);
+  pos[i] = p;
+  key[i] = cell_of(p, g);
+  val[i] = i;
+}
+
+// gather per-atom state into the new (cell-sorted) order
+__global__ void k_permute(int N, const int* perm, const double4* pos_in, double4* pos_out, const double* v_in,
+                          double* v_out, const int* gid_in, int* gid_out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int o = perm[i];
+  pos_out[i] = pos_in[o];
+  v_out[3 * i + 0] = v_in[3 * o + 0];
+  v_out[3 * i + 1] = v_in[3 * o + 1];
+  v_out[3 * i + 2] = v_in[3 * o + 2];
+  gid_out[i] = gid_in[o];
+}
+
+// image position u = x + s L evaluated as t = s*L; u = x + t (bitwise as the oracle)
+__device__ __forceinline__ double img(double x, int s, double L) { return __dadd_rn(x, __dmul_rn((double)s, L)); }
+
+__device__ __forceinline__ bool in_padded(double u, double L, double h) { return u >= -h && u < L + h; }
+
+// ghosts: every image (s != 0) of a local atom inside [-h, L+h)^3 (explicit images)
+__global__ void k_ghost_count(int N, const double4* pos, int3 smax, double h, int* cnt) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double4 p = pos[i];
+  int c = 0;
+  for (int sx = -smax.x; sx <= smax.x; ++sx) {
+    double ux = img(p.x, sx, c_geo.L[0]);
+    if (!in_padded(ux, c_geo.L[0], h)) continue;
+    for (int sy = -smax.y; sy <= smax.y; ++sy) {
+      double uy = img(p.y, sy, c_geo.L[1]);
+      if (!in_padded(uy, c_geo.L[1], h)) continue;
+      for (int sz = -smax.z; sz <= smax.z; ++sz) {
+        if (sx == 0 && sy == 0 && sz == 0) continue;
+        double uz = img(p.z, sz, c_geo.L[2]);
+        if (in_padded(uz, c_geo.L[2], h)) ++c;
+      }
+    }
+  }
+  cnt[i] = c;
+}
+
+__global__ void k_ghost_fill(int N, double4* pos, int3 smax, double h, const int* off, int* owner, int* gid,
+                             char4* shift) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double4 p = pos[i];
+  int w = N + off[i];
+  owner[i] = i;
+  shift[i] = make_char4(0, 0, 0, 0);
+  for (int sx = -smax.x; sx <= smax.x; ++sx) {
+    double ux = img(p.x, sx, c_geo.L[0]);
+    if (!in_padded(ux, c_geo.L[0], h)) continue;
+    for (int sy = -smax.y; sy <= smax.y; ++sy) {
+      double uy = img(p.y, sy, c_geo.L[1]);
+      if (!in_padded(uy, c_geo.L[1], h)) continue;
+      for (int sz = -smax.z; sz <= smax.z; ++sz) {
+        if (sx == 0 && sy == 0 && sz == 0) continue;
+        double uz = img(p.z, sz, c_geo.L[2]);
+        if (!in_padded(uz, c_geo.L[2], h)) continue;
+        pos[w] = make_double4(ux, uy, uz, p.w);
+        owner[w] = i;
+        gid[w] = gid[i];
+        shift[w] = make_char4((signed char)sx, (signed char)sy, (signed char)sz, 0);
+        ++w;
+      }
+    }
+  }
+}
+
+// per step: ghost image positions follow their owners (same IEEE ops as at creation)
+__global__ void k_ghost_update(int N, int NT, double4* pos, const int* owner, const char4* shift) {
+  int g = N + blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= NT) return;
+  double4 p = pos[owner[g]];
+  char4 s = shift[g];
+  pos[g] = make_double4(img(p.x, s.x, c_geo.L[0]), img(p.y, s.y, c_geo.L[1]), img(p.z, s.z, c_geo.L[2]), p.w);
+}
+
+__global__ void k_cell_keys(int NT, const double4* pos, Grid g, int* key, int* val) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= NT) return;
+  key[a] = cell_of(pos[a], g);
+  val[a] = a;
+}
+
+__global__ void k_cell_bounds(int NT, int ncell, const int* sorted_key, int* cell_start) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a > NT) return;
+  if (a == 0) {
+    for (int c = 0; c <= (NT ? sorted_key[0] : ncell - 1); ++c) cell_start[c] = 0;
+  }
+  if (a == NT) {
+    int last = NT ? sorted_key[NT - 1] : -1;
+    for (int c = last + 1; c <= ncell; ++c) cell_start[c] = NT;
+    return;
+  }
+  if (a > 0) {
+    int k0 = sorted_key[a - 1], k1 = sorted_key[a];
+    for (int c = k0 + 1; c <= k1; ++c) cell_start[c] = a;
+  }
+}
+
+// Skinned list of atom a: all b != a with r^2 <= cut2[pair] over the stencil +-nr cells.
+// Used for the LJ list (local atoms, cut = r_c + skin, full / both directions) and the
+// intermediate REBO list (all atoms, cut = r_max + skin) of P:719-723.
+__global__ void k_build_list(int NA, const double4* pos, Grid g, const int* cell_start, const int* cell_atoms,
+                             int nr, int which /*0 = LJ, 1 = intermediate*/, int cap, int* cnt, int* nbr,
+                             int* maxcnt) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= NA) return;
+  double4 p = pos[a];
+  int ta = (int)p.w;
+  int cx = cell_coord(p.x, g.lo[0], g.cs[0], g.nc[0]);
+  int cy = cell_coord(p.y, g.lo[1], g.cs[1], g.nc[1]);
+  int cz = cell_coord(p.z, g.lo[2], g.cs[2], g.nc[2]);
+  int c = 0;
+  int* out = nbr + (size_t)a * cap;
+  for (int ax = max(0, cx - nr); ax <= min(g.nc[0] - 1, cx + nr); ++ax)
+    for (int ay = max(0, cy - nr); ay <= min(g.nc[1] - 1, cy + nr); ++ay)
+      for (int az = max(0, cz - nr); az <= min(g.nc[2] - 1, cz + nr); ++az) {
+        int cell = (ax * g.nc[1] + ay) * g.nc[2] + az;
+        for (int q = cell_start[cell]; q < cell_start[cell + 1]; ++q) {
+          int b = cell_atoms[q];
+          if (b == a) continue;
+          double4 pb = pos[b];
+          double r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
+          int pr = ta + (int)pb.w;
+          double cut2 = which == 0 ? c_geo.rc_s2[pr] : c_geo.rmax_s2[pr];
+          if (r2 <= cut2) {
+            if (c < cap) out[c] = b;
+            ++c;
+          }
+        }
+      }
+  cnt[a] = c;
+  atomicMax(maxcnt, c);
+}
+
+// Short-list storage: per atom up to capS entries: neighbour index, (d, r) and (w, dw/dr).
+template <typename R>
+struct ShortList {
+  int capS;
+  int* cnt;
+  int* nbr;
+  typename std::conditional<sizeof(R) == 8, double4, float4>::type* dr;  // d.x d.y d.z r
+  typename std::conditional<sizeof(R) == 8, double2, float2>::type* w;   // w, dw/dr
+  R* Ntot;  // N_a = N^C_a + N^H_a
+  R* NC;
+  R* NH;
+};
+
+template <typename R>
+__device__ __forceinline__ V3<R> sl_d(const ShortList<R>& S, int a, int n, R& r) {
+  auto v = S.dr[(size_t)a * S.capS + n];
+  r = v.w;
+  return mk3<R>(v.x, v.y, v.z);
+}
+
+// Exact short list every step: filter the intermediate list at r <= r_max
+// (closed boundary), store d, r, w = S(r; r_min, r_max), dw/dr; N^C, N^H per atom.
+// Local atoms also append their canonical entries to the REBO bond list.
+template <typename R>
+__global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, const int* in_nbr, int capI,
+                        ShortList<R> S, const int* gid, const char4* shift, int2* bonds, int* nbonds,
+                        unsigned long long* ct) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  bool live = a < NT;
+  int nloc = 0, nbond = 0;
+  if (live) {
+    const Tab<R>& T = tab<R>();
+    double4 p = pos[a];
+    int ta = (int)p.w;
+    int n = 0;
+    R nc = 0, nh = 0;
+    int ci = in_cnt[a];
+    size_t base = (size_t)a * S.capS;
+    for (int q = 0; q < ci; ++q) {
+      int b = in_nbr[(size_t)a * capI + q];
+      double4 pb = pos[b];
+      double dx = __dsub_rn(pb.x, p.x), dy = __dsub_rn(pb.y, p.y), dz = __dsub_rn(pb.z, p.z);
+      double r2 = r2_exact(dx, dy, dz);
+      int tb = (int)pb.w;
+      int pr = ta + tb;
+      if (r2 <= c_geo.rmax2[pr]) {
+        if (n < S.capS) {
+          double r = sqrt(r2);
+          R dw;
+          R w = sw<R>((R)r, T.rmin[pr], T.rmax[pr], dw);
+          S.nbr[base + n] = b;
+          S.dr[base + n] = {(R)dx, (R)dy, (R)dz, (R)r};
+          S.w[base + n] = {w, dw};
+          if (tb == 0) nc += w;
+          else nh += w;
+          if (a < N && canonical_pair(gid[a], gid[b], shift[b])) ++nbond;
+        }
+        ++n;
+      }
+    }
+    if (n > S.capS) atomicAdd(ct + CT_OVF_SHORT, 1ull);
+    n = min(n, S.capS);
+    S.cnt[a] = n;
+    S.NC[a] = nc;
+    S.NH[a] = nh;
+    S.Ntot[a] = nc + nh;
+    if (a < N) nloc = n;
+  }
+  // bond list compaction (warp-aggregated atomics) -- order is irrelevant to the physics
+  unsigned lane = threadIdx.x & 31;
+  int incl = nbond;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (unsigned)o) incl += v;
+  }
+  int total = __shfl_sync(0xffffffffu, incl, 31);
+  int basew = 0;
+  if (lane == 31 && total) basew = atomicAdd(nbonds, total);
+  basew = __shfl_sync(0xffffffffu, basew, 31);
+  int w = basew + incl - nbond;
+  if (live && a < N && nbond) {
+    size_t base = (size_t)a * S.capS;
+    int n = S.cnt[a];
+    for (int q = 0; q < n; ++q) {
+      int b = S.nbr[base + q];
+      if (canonical_pair(gid[a], gid[b], shift[b])) bonds[w++] = make_int2(a, q);
+    }
+  }
+  unsigned long long s = warp_sum_u((unsigned long long)nloc);
+  long long m = warp_max_i((long long)nloc);
+  if (lane == 0) {
+    if (s) atomicAdd(ct + CT_SHORT, s);
+    atomicMax(ct + CT_MAXSHORT, (unsigned long long)m);
+  }
+}
+
+}  // namespace ab

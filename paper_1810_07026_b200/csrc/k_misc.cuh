@@ -1,0 +1,106 @@
+// k_misc.cuh -- velocity-Verlet NVE, skin-displacement trigger,
+// kinetic energy, and caller-order <-> cell-sorted-order transfers.
+#pragma once
+#include "dev_common.cuh"
+
+namespace ab {
+
+// v += dt/2 F/m ftm2v;  x += dt v;  max |x - x_ref|^2 since the last list build
+__global__ void k_integrate1(int N, double4* pos, double* v, const double* F, double dtf0, double dtf1, double dt,
+                             const double4* xref, unsigned long long* maxd2) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double d2 = 0.0;
+  if (i < N) {
+    double4 p = pos[i];
+    double dtf = ((int)p.w == 0) ? dtf0 : dtf1;
+    double vx = v[3 * i + 0] + dtf * F[3 * i + 0];
+    double vy = v[3 * i + 1] + dtf * F[3 * i + 1];
+    double vz = v[3 * i + 2] + dtf * F[3 * i + 2];
+    v[3 * i + 0] = vx, v[3 * i + 1] = vy, v[3 * i + 2] = vz;
+    p.x += dt * vx, p.y += dt * vy, p.z += dt * vz;
+    pos[i] = p;
+    double4 r = xref[i];
+    double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
+    d2 = dx * dx + dy * dy + dz * dz;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+  if ((threadIdx.x & 31) == 0 && d2 > 0.0) atomicMax(maxd2, (unsigned long long)__double_as_longlong(d2));
+}
+
+__global__ void k_integrate2(int N, const double4* pos, double* v, const double* F, double dtf0, double dtf1) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double dtf = ((int)pos[i].w == 0) ? dtf0 : dtf1;
+  v[3 * i + 0] += dtf * F[3 * i + 0];
+  v[3 * i + 1] += dtf * F[3 * i + 1];
+  v[3 * i + 2] += dtf * F[3 * i + 2];
+}
+
+__global__ void k_maxdisp(int N, const double4* pos, const double4* xref, unsigned long long* maxd2) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double d2 = 0.0;
+  if (i < N) {
+    double4 p = pos[i], r = xref[i];
+    double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
+    d2 = dx * dx + dy * dy + dz * dz;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+  if ((threadIdx.x & 31) == 0 && d2 > 0.0) atomicMax(maxd2, (unsigned long long)__double_as_longlong(d2));
+}
+
+// sum m v^2 / 2 (mvv2e applied on the host)
+__global__ void k_ke(int N, const double4* pos, const double* v, double m0, double m1, double* acc) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double k = 0.0;
+  if (i < N) {
+    double m = ((int)pos[i].w == 0) ? m0 : m1;
+    double a = v[3 * i], b = v[3 * i + 1], c = v[3 * i + 2];
+    k = 0.5 * m * (a * a + b * b + c * c);
+  }
+  k = warp_sum(k);
+  if ((threadIdx.x & 31) == 0 && k != 0.0) atomicAdd(acc + ACC_KE, k);
+}
+
+__global__ void k_copy_xref(int N, const double4* pos, double4* xref) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) xref[i] = pos[i];
+}
+
+__global__ void k_types(int NT, const double4* pos, signed char* typ) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a < NT) typ[a] = (signed char)(int)pos[a].w;
+}
+
+// caller-order array (n*3) -> internal positions / velocities
+__global__ void k_from_caller_pos(int N, const int* gid, const double* in, double4* pos) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int g = gid[i];
+  double4 p = pos[i];
+  p.x = in[3 * g], p.y = in[3 * g + 1], p.z = in[3 * g + 2];
+  pos[i] = p;
+}
+__global__ void k_from_caller_vec(int N, const int* gid, const double* in, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int g = gid[i];
+  out[3 * i] = in[3 * g], out[3 * i + 1] = in[3 * g + 1], out[3 * i + 2] = in[3 * g + 2];
+}
+// internal -> caller order
+__global__ void k_to_caller_vec(int N, const int* gid, const double* in, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int g = gid[i];
+  out[3 * g] = in[3 * i], out[3 * g + 1] = in[3 * i + 1], out[3 * g + 2] = in[3 * i + 2];
+}
+__global__ void k_to_caller_pos(int N, const int* gid, const double4* pos, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int g = gid[i];
+  double4 p = pos[i];
+  out[3 * g] = p.x, out[3 * g + 1] = p.y, out[3 * g + 2] = p.z;
+}
+
+}  // namespace ab

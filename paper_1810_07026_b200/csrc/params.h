@@ -1,0 +1,35 @@
+// params.h -- host-side parameter set of the engine (parsed from params/toy_ch.param text).
+// Independent of oracle/params.hpp (no shared code).  Functional forms: SURVEY A2.
+#pragma once
+#include <string>
+#include <vector>
+
+namespace ab {
+
+enum { kC = 0, kH = 1 };
+inline int pair_index(int ta, int tb) { return ta + tb; }  // CC 0, CH 1, HH 2
+
+struct PairSet {
+  double rmin, rmax, Q, alpha, A, B[3], beta[3];      // REBO f_R / f_A
+  double eps, sigma, rc, rlo, bmin, bmax, rho;        // LJ, S_r, S_b, fictitious distance
+};
+
+struct HostParams {
+  double mass[2] = {0, 0}, kB = 0, mvv2e = 0, ftm2v = 0, skin = 0;
+  PairSet pr[3];
+  std::vector<double> gknot[2], gval[2];  // g_C, g_H knots (cos theta) and values
+  double lam[2][2][2];                    // lambda_{jik} as [t_j][t_i][t_k]
+  double grid_p_lo[2];
+  int grid_p_n[2];
+  double grid_rt_lo[3];
+  int grid_rt_n[3];
+  std::vector<double> Ptab[2];            // P_CC, P_CH
+  std::vector<double> Rtab[3], Ttab[3];   // CC CH HH
+  double conj_lo = 0, conj_hi = 0, sin2_lo = 0, sin2_hi = 0;
+  double tors[2][2][2][2];                // eps_tors[t_k][t_i][t_j][t_l]
+};
+
+// Parses `text` (len bytes).  Returns "" on success or an error that names the line or key.
+std::string parse_host_params(const char* text, size_t len, HostParams& hp);
+
+}  // namespace ab

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 CPU oracle on the same seeded
+inputs.  Tolerances (BASELINE.json north_star, SURVEY reading A25):
+  fp64 : max |F_gpu - F_orc| <= 1e-9 eV/A per component;  |E_gpu - E_orc| <= 1e-11 |E_orc|
+  mixed: ||F_gpu - F_orc||_2 / ||F_orc||_2 <= 1e-4 (RMS over atoms);  |dE| <= 1e-6 |E|
+  lists: bit-exact as sorted (i, j, sx, sy, sz) sets; integer counters equal (fp64).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1810_07026_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+COUNTERS = ["n_short", "n_bonds", "n_quads", "n_lj", "n_C0", "n_bstar", "n_sb_trans", "max_short", "max_reach",
+            "n_badarg"]
+
+
+@pytest.fixture(scope="module")
+def eng_mod():
+    from paper_1810_07026_b200 import build, engine
+    build.build()
+    return engine
+
+
+def run_gpu(engine, s, precision="fp64"):
+    e = engine.make(s, precision)
+    res = e.compute()
+    res["stats"] = e.stats()
+    res["eng"] = e
+    return res
+
+
+def systems_small():
+    out = [I.config(1), I.diamond((2, 2, 2), 0.04, 21, name="diamond-2x2x2"),
+           I.diamond((1, 1, 1), 0.05, 9, name="diamond-1x1x1-multi-image"),
+           I.polyethylene((1, 1, 1), 0.03, 5, None, name="pe-cell-multi-image")]
+    for seed in range(4):
+        out.append(I.random_cluster(30, seed, spread=5.0, dmin=1.0, name=f"cluster{seed}"))
+    out.append(I.random_cluster(60, 11, spread=7.0, dmin=0.95, frac_c=0.4, name="cluster-big"))
+    return out
+
+
+def check_fp64(s, g, o):
+    E_o = o["E"]
+    assert abs(g["E"] - E_o) <= 1e-11 * abs(E_o) + 1e-13, (s.name, g["E"], E_o)
+    for t in range(3):
+        assert abs(g["terms"][t] - o["terms"][t]) <= 1e-11 * max(abs(E_o), 1.0), (s.name, t)
+    dF = np.abs(g["F"] - o["F"]).max()
+    assert dF <= 1e-9, (s.name, dF)
+    dW = np.abs(g["W"] - o["W"]).max()
+    assert dW <= 1e-10 * max(np.abs(o["W"]).max(), 1.0), (s.name, dW)
+
+
+@pytest.mark.parametrize("idx", range(9))
+def test_fp64_parity_small(eng_mod, idx):
+    s = systems_small()[idx]
+    o = O.compute(s.types, s.x, s.box)
+    g = run_gpu(eng_mod, s)
+    check_fp64(s, g, o)
+    for k in COUNTERS:
+        assert g["stats"][k] == o["counters"][k], (s.name, k, g["stats"][k], o["counters"][k])
+
+
+@pytest.mark.parametrize("idx", range(9))
+def test_lists_bit_exact(eng_mod, idx):
+    s = systems_small()[idx]
+    e = eng_mod.make(s)
+    for which in (0, 1, 2):
+        a = e.get_list(which)
+        b = O.get_list(s.types, s.x, s.box, which)
+        assert a.shape == b.shape and np.array_equal(a, b), (s.name, which)
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_fp64_parity_configs(eng_mod, cfg):
+    s = I.config(cfg)
+    o = O.compute(s.types, s.x, s.box)
+    g = run_gpu(eng_mod, s)
+    check_fp64(s, g, o)
+    for k in COUNTERS:
+        assert g["stats"][k] == o["counters"][k], (s.name, k)
+    for which in (0, 1, 2):
+        a = g["eng"].get_list(which)
+        b = O.get_list(s.types, s.x, s.box, which)
+        assert np.array_equal(a, b), (s.name, which)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, "diamond"])
+def test_mixed_parity(eng_mod, cfg):
+    s = I.diamond((4, 4, 4), 0.03, 105) if cfg == "diamond" else I.config(cfg)
+    o = O.compute(s.types, s.x, s.box)
+    g = run_gpu(eng_mod, s, "mixed")
+    rel = np.sqrt(((g["F"] - o["F"]) ** 2).sum()) / np.sqrt((o["F"] ** 2).sum())
+    assert rel <= 1e-4, rel
+    assert abs(g["E"] - o["E"]) <= 1e-6 * abs(o["E"])
+    assert np.array_equal(g["eng"].get_list(2), O.get_list(s.types, s.x, s.box, 2))
+
+
+def test_stage_parity_bond_orders_and_cij(eng_mod):
+    """Stage-wise parity: b_ij and its parts per bond, C_ij and b* per LJ pair."""
+    for s in (I.config(1), I.random_cluster(40, 3, spread=6.0, dmin=1.0)):
+        e = eng_mod.make(s)
+        e.record_stages(True)
+        e.compute()
+        B_o, L_o = O.stages(s.types, s.x, s.box)
+        rb = O.get_list(s.types, s.x, s.box, 1)
+        rl = O.get_list(s.types, s.x, s.box, 2)
+        st0 = e.get_stage(0)
+        st1 = e.get_stage(1)
+        key0 = {tuple(int(v) for v in r[:5]): r[5:] for r in st0}
+        assert len(key0) == len(rb)
+        for row, ref in zip(rb, B_o):
+            got = key0[tuple(int(v) for v in row)]
+            assert np.allclose(got, ref, rtol=1e-12, atol=1e-13), (row, got, ref)
+        key1 = {tuple(int(v) for v in r[:5]): r[5:] for r in st1}
+        assert len(key1) == len(rl)
+        for row, ref in zip(rl, L_o):
+            got = key1[tuple(int(v) for v in row)]
+            assert abs(got[0] - ref[0]) <= 1e-13
+            assert abs(got[1] - ref[1]) <= 1e-12
+
+
+def test_edge_cases(eng_mod):
+    box = np.array([30.0, 30.0, 30.0])
+    # single atom: no terms
+    e = eng_mod.Engine("fp64")
+    e.set_box(box)
+    e.set_atoms([0], [[1.0, 2.0, 3.0]])
+    r = e.compute()
+    assert r["E"] == 0.0 and np.all(r["F"] == 0.0)
+    # pair exactly at r_max (closed boundary, w = 0) and exactly at r_c
+    for x in ([[10.0, 10, 10], [12.0, 10, 10]], [[5.0, 5, 5], [15.2, 5, 5]]):
+        x = np.array(x)
+        o = O.compute([0, 0], x, box)
+        e.set_atoms([0, 0], x)
+        g = e.compute()
+        assert abs(g["E"] - o["E"]) <= 1e-15 and np.abs(g["F"] - o["F"]).max() <= 1e-12
+        assert np.array_equal(e.get_list(0), O.get_list([0, 0], x, box, 0))
+        assert np.array_equal(e.get_list(2), O.get_list([0, 0], x, box, 2))
+    # tiny box: an atom interacting with its own images (box < r_c)
+    s = I.diamond((1, 1, 1), 0.0)
+    o = O.compute(s.types, s.x, s.box)
+    g = run_gpu(eng_mod, s)
+    check_fp64(s, g, o)
+    # bad arguments fail loudly
+    with pytest.raises(eng_mod.ABError):
+        e.set_box([0.0, 1.0, 1.0])
+    with pytest.raises(eng_mod.ABError):
+        e.set_atoms([2], [[0.0, 0, 0]])
+
+
+def test_caller_order_and_permutation(eng_mod):
+    s = I.config(1)
+    rng = np.random.default_rng(4)
+    p = rng.permutation(s.n)
+    g1 = run_gpu(eng_mod, s)
+    s2 = I.System("perm", s.types[p], s.x[p], s.box)
+    g2 = run_gpu(eng_mod, s2)
+    assert np.abs(g2["F"] - g1["F"][p]).max() <= 1e-12
+    assert abs(g2["E"] - g1["E"]) <= 1e-12 * abs(g1["E"])
+
+
+def test_nve_replay_parity_and_conservation(eng_mod):
+    """NVE on the GPU; the oracle re-evaluates forces at the GPU's own frames (dump/rerun)."""
+    s = I.config(1)
+    e = eng_mod.make(s)
+    frames = []
+    th_all = []
+    for k in range(10):
+        th = e.run_nve(10, 0.5, every=10)
+        th_all.append(th)
+        x = e.get_positions()
+        F = e.compute()["F"]
+        frames.append((x, F))
+    for x, F in frames[::3]:
+        o = O.compute(s.types, x, s.box)
+        assert np.abs(F - o["F"]).max() <= 1e-9
+    # compare the free-running oracle trajectory (report-only quantity: must stay tiny for 100 steps)
+    xo, vo, tho = O.nve(s.types, s.x, s.v, s.box, 100, 0.5, every=10)
+    dx = frames[-1][0] - xo
+    dx -= s.box * np.round(dx / s.box)
+    assert np.abs(dx).max() < 1e-6
+    # energy conservation: dt^2 scaling of the max drift
+    d = []
+    for dt, n in ((0.5, 100), (0.25, 200)):
+        e2 = eng_mod.make(s)
+        th = e2.run_nve(n, dt, every=1)
+        d.append(np.abs(th[:, 3] - th[0, 3]).max())
+    assert 3.0 <= d[0] / d[1] <= 5.0, d
+
+
+def test_nve_rebuild_path_matches_fresh_lists(eng_mod):
+    """After many steps with skin-triggered rebuilds, the lists equal a from-scratch build."""
+    s = I.config(3)
+    e = eng_mod.make(s)
+    e.run_nve(30, 0.25)
+    x = e.get_positions()
+    F = e.compute()["F"]
+    smp = np.arange(0, s.n, 997)
+    Fs = O.forces_sampled(s.types, x, s.box, smp)
+    assert np.abs(F[smp] - Fs).max() <= 1e-9
+
+
+@pytest.mark.parametrize("cfg", [4, "5a", "5b"])
+def test_full_size_sampled_forces(eng_mod, cfg):
+    """BASELINE full sizes (1M PE, 2M diamond, 2M PE): forces of sampled atoms vs the oracle, and
+    properties that hold at any size (net force ~ 0, finite energy)."""
+    s = I.config(cfg)
+    g = run_gpu(eng_mod, s)
+    rng = np.random.default_rng(7)
+    smp = np.sort(rng.choice(s.n, 24, replace=False))
+    Fs = O.forces_sampled(s.types, s.x, s.box, smp)
+    assert np.abs(g["F"][smp] - Fs).max() <= 1e-9
+    assert np.abs(g["F"].sum(0)).max() <= 1e-7
+    assert g["stats"]["n_badarg"] == 0
+    gm = run_gpu(eng_mod, s, "mixed")
+    rel = np.sqrt(((gm["F"][smp] - Fs) ** 2).sum()) / np.sqrt((Fs ** 2).sum())
+    assert rel <= 1e-4
