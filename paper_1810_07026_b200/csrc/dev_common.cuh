@@ -30,7 +30,7 @@ struct Tab {
 };
 
 struct Geo {  // double-only quantities: exact list / gate decisions, box, integrator
-  double rmax2[3], rc2[3], rmax_s2[3], rc_s2[3], reach2;
+  double rmax2[3], rc2[3], rmax_s2[3], rc_s2[3], rlo2[3], reach2;
   double L[3];
   double mass[2], ftm2v, mvv2e;
 };
@@ -320,5 +320,16 @@ __device__ __forceinline__ bool canonical_pair(int gi, int gj, char4 sj) {
   if (gi != gj) return gi < gj;
   return sj.x > 0 || (sj.x == 0 && (sj.y > 0 || (sj.y == 0 && sj.z > 0)));
 }
+
+// Instance key stored in the w slot of every position (bit pattern of an int64, never used in
+// FP arithmetic): gid << 26 | (sx+128) << 18 | (sy+128) << 10 | (sz+128) << 2 | type.
+// Lexicographic (gid, image) order == integer order, so the half convention is key_i < key_J
+// and the species comes with the same 32-byte position load.
+__host__ __device__ __forceinline__ long long make_key(int gid, int sx, int sy, int sz, int type) {
+  return ((long long)gid << 26) | ((long long)(sx + 128) << 18) | ((long long)(sy + 128) << 10) |
+         ((long long)(sz + 128) << 2) | (long long)type;
+}
+__device__ __forceinline__ long long key_of(const double4& p) { return __double_as_longlong(p.w); }
+__device__ __forceinline__ int type_of(const double4& p) { return (int)(__double_as_longlong(p.w) & 3); }
 
 }  // namespace ab

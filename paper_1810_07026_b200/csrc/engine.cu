@@ -69,7 +69,7 @@ struct ab_engine {
   double halo = 0, rcmax = 0, rmaxmax = 0;
   Grid grid{};
   int ncell = 0, nrLJ = 1, nrI = 1;
-  int capLJ = 0, capI = 0, capS = 0, capQ = 0;
+  int capI = 0, capS = 0, capQ = 0;
   long long launches = 0, rebuilds = 0, steps = 0, retries = 0;
   // device state
   DBuf<double4> pos, pos_tmp, xref;
@@ -77,7 +77,9 @@ struct ab_engine {
   DBuf<int> gid, gid_tmp, owner, key, key2, val, val2, cell_start, gcnt, goff;
   DBuf<char4> shift;
   DBuf<signed char> typ;
-  DBuf<int> lj_cnt, lj_nbr, in_cnt, in_nbr;
+  DBuf<int> ljc[3], ljn[3], in_cnt, in_nbr;  // LJ near / pure / band lists, intermediate list
+  int capL[3] = {0, 0, 0};
+  bool want_virial = true;
   DBuf<int> s_cnt, s_nbr;
   DBuf<unsigned char> s_dr, s_w, s_N;  // typed by precision at use
   DBuf<int2> bonds;
@@ -235,6 +237,7 @@ ab_status upload_geo(ab_engine* e) {
     g.rc2[p] = s.rc * s.rc;
     g.rmax_s2[p] = (s.rmax + hp.skin) * (s.rmax + hp.skin);
     g.rc_s2[p] = (s.rc + hp.skin) * (s.rc + hp.skin);
+    g.rlo2[p] = s.rlo * s.rlo;
     rmm = std::max(rmm, s.rmax);
     rcm = std::max(rcm, s.rc);
   }
@@ -377,26 +380,49 @@ ab_status rebuild_impl(ab_engine* e) {
   CKL();
   // 4. skinned lists: LJ (local atoms, full) and intermediate REBO (all atoms)
   CK(e->small_i.ensure(8));
-  CK(e->lj_cnt.ensure(N));
+  for (int c = 0; c < 3; ++c) CK(e->ljc[c].ensure(N));
   CK(e->in_cnt.ensure(NT));
-  if (e->capLJ == 0) e->capLJ = 64;
+  const double skin = e->hp.skin;
+  const double rnear = 3 * e->rmaxmax + skin;
+  if (e->capL[0] == 0) {  // first build: capacities from the mean density (grown on overflow)
+    double rho = N / (e->L[0] * e->L[1] * e->L[2]), fpi = 4.18879020478639;
+    double rlo_max = 0;
+    for (int p = 0; p < 3; ++p) rlo_max = std::max(rlo_max, e->hp.pr[p].rlo);
+    double r1 = std::max(rnear, rlo_max - skin), r2 = e->rcmax + skin;
+    e->capL[0] = 32 + (int)(1.3 * rho * fpi * rnear * rnear * rnear);
+    e->capL[1] = 32 + (int)(1.3 * rho * fpi * (r1 * r1 * r1 - rnear * rnear * rnear));
+    e->capL[2] = 32 + (int)(1.3 * rho * fpi * (r2 * r2 * r2 - std::min(r1, rnear) * std::min(r1, rnear) * std::min(r1, rnear)));
+  }
   if (e->capI == 0) e->capI = 16;
+  LJLists Lg;
+  Lg.near2 = rnear * rnear;
+  for (int p = 0; p < 3; ++p) {
+    double b = e->hp.pr[p].rlo - skin;
+    Lg.pure2[p] = b > rnear ? b * b : -1.0;
+  }
   for (int attempt = 0; attempt < 4; ++attempt) {
-    CK(e->lj_nbr.ensure((size_t)N * e->capLJ));
+    for (int c = 0; c < 3; ++c) {
+      CK(e->ljn[c].ensure((size_t)N * e->capL[c]));
+      Lg.cap[c] = e->capL[c];
+      Lg.cnt[c] = e->ljc[c].p;
+      Lg.nbr[c] = e->ljn[c].p;
+    }
     CK(e->in_nbr.ensure((size_t)NT * e->capI));
-    CK(cudaMemsetAsync(e->small_i.p + 2, 0, 2 * sizeof(int), st));
-    k_build_list<<<nblk(N, 128), 128, 0, st>>>(N, e->pos.p, e->grid, e->cell_start.p, e->val2.p, e->nrLJ, 0,
-                                               e->capLJ, e->lj_cnt.p, e->lj_nbr.p, e->small_i.p + 2);
+    CK(cudaMemsetAsync(e->small_i.p + 2, 0, 4 * sizeof(int), st));
+    k_build_lj<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
+                                                              e->nrLJ, Lg, e->small_i.p + 2);
     CKL();
-    k_build_list<<<nblk(NT, 128), 128, 0, st>>>(NT, e->pos.p, e->grid, e->cell_start.p, e->val2.p, e->nrI, 1,
-                                                e->capI, e->in_cnt.p, e->in_nbr.p, e->small_i.p + 3);
+    k_build_inter<<<nblk((long long)NT * 32, 128), 128, 0, st>>>(NT, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
+                                                                  e->nrI, e->capI, e->in_cnt.p, e->in_nbr.p,
+                                                                  e->small_i.p + 5);
     CKL();
-    int mx[2];
-    CK(cudaMemcpyAsync(mx, e->small_i.p + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    int mx[4];
+    CK(cudaMemcpyAsync(mx, e->small_i.p + 2, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    bool ok = mx[0] <= e->capLJ && mx[1] <= e->capI;
-    if (mx[0] > e->capLJ) e->capLJ = mx[0] + mx[0] / 8 + 8;
-    if (mx[1] > e->capI) e->capI = mx[1] + 4;
+    bool ok = true;
+    for (int c = 0; c < 3; ++c)
+      if (mx[c] > e->capL[c]) e->capL[c] = mx[c] + mx[c] / 8 + 32, ok = false;
+    if (mx[3] > e->capI) e->capI = mx[3] + 4, ok = false;
     if (ok) break;
     ++e->retries;
   }
@@ -428,18 +454,18 @@ ab_status forces_impl(ab_engine* e) {
   }
   StageBuf sb0{nullptr, nullptr, 0}, sb1{nullptr, nullptr, 0};
   if (e->record) {
-    size_t n0 = (size_t)N * e->capS + 16, n1 = (size_t)N * e->capLJ + 16;
+    size_t n0 = (size_t)N * e->capS + 16, n1 = (size_t)N * (e->capL[0] + e->capL[1] + e->capL[2]) + 16;
     CK(e->stage0.ensure(n0 * 13));
     CK(e->stage1.ensure(n1 * 7));
-    sb0 = StageBuf{e->stage0.p, e->small_i.p + 4, (int)n0};
-    sb1 = StageBuf{e->stage1.p, e->small_i.p + 5, (int)n1};
+    sb0 = StageBuf{e->stage0.p, e->small_i.p + 6, (int)n0};
+    sb1 = StageBuf{e->stage1.p, e->small_i.p + 7, (int)n1};
   }
   for (int attempt = 0; attempt < 3; ++attempt) {
     CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * N, st));
     CK(cudaMemsetAsync(e->acc.p, 0, sizeof(double) * ACC_N, st));
     CK(cudaMemsetAsync(e->ct.p, 0, sizeof(unsigned long long) * CT_N, st));
     CK(cudaMemsetAsync(e->small_i.p, 0, 2 * sizeof(int), st));
-    CK(cudaMemsetAsync(e->small_i.p + 4, 0, 2 * sizeof(int), st));
+    CK(cudaMemsetAsync(e->small_i.p + 6, 0, 2 * sizeof(int), st));
     ShortList<R> S = short_view<R>(e);
     prof_begin(e, 0);
     k_short<R><<<nblk(NT, 128), 128, 0, st>>>(N, NT, e->pos.p, e->in_cnt.p, e->in_nbr.p, e->capI, S, e->gid.p,
@@ -454,9 +480,16 @@ ab_status forces_impl(ab_engine* e) {
     prof_end(e);
     BstarQueue Qu{e->q_item.p, e->q_M.p, e->small_i.p + 1, e->capQ};
     prof_begin(e, 2);
-    k_lj<R><<<nblk(N, LJ_WARPS), 32 * LJ_WARPS, 0, st>>>(N, e->pos.p, e->lj_cnt.p, e->lj_nbr.p, e->capLJ, S,
-                                                         e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                                         e->acc.p, e->ct.p, Qu, sb1);
+    LJArgs A;
+    A.N = N;
+    A.pos = e->pos.p;
+    for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
+    if (e->want_virial)
+      k_lj<R, true><<<nblk(N, LJ_WARPS), 32 * LJ_WARPS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p,
+                                                                 e->acc.p, e->ct.p, Qu, sb1);
+    else
+      k_lj<R, false><<<nblk(N, LJ_WARPS), 32 * LJ_WARPS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p,
+                                                                  e->acc.p, e->ct.p, Qu, sb1);
     CKL();
     prof_end(e);
     prof_begin(e, 3);
@@ -591,7 +624,8 @@ void ab_destroy(ab_engine* e) {
   DBuf<double>* bd[] = {&e->vel, &e->vel_tmp, &e->F, &e->io, &e->q_M, &e->acc, &e->stage0, &e->stage1};
   for (auto* b : bd) b->release();
   DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->key2, &e->val, &e->val2, &e->cell_start,
-                     &e->gcnt, &e->goff, &e->lj_cnt, &e->lj_nbr, &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr,
+                     &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
+                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr,
                      &e->small_i};
   for (auto* b : bi) b->release();
   e->shift.release();
@@ -660,7 +694,10 @@ ab_status ab_set_atoms(ab_engine* e, int64_t n, const int32_t* type, const doubl
         e->err = "non-finite coordinate of atom " + std::to_string(i);
         return AB_E_NONFINITE;
       }
-    p[i] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], (double)type[i]);
+    long long key = make_key((int)i, 0, 0, 0, type[i]);
+    double kd;
+    std::memcpy(&kd, &key, sizeof(kd));
+    p[i] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], kd);
     g[i] = (int)i;
   }
   e->N = (int)n;
@@ -677,7 +714,7 @@ ab_status ab_set_atoms(ab_engine* e, int64_t n, const int32_t* type, const doubl
   e->have_atoms = true;
   e->lists_valid = false;
   e->forces_valid = false;
-  e->capLJ = e->capI = 0;
+  e->capL[0] = e->capL[1] = e->capL[2] = e->capI = 0;
   return AB_OK;
 }
 
@@ -723,8 +760,19 @@ ab_status ab_compute(ab_engine* e, double* f, double* energy, double virial[6], 
   return AB_OK;
 }
 
+static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t every, double* thermo);
+
+// The NVE loop needs forces and energies but no virial: the per-pair virial accumulation is
+// compiled out of the LJ kernel for these steps (ab_compute always evaluates it).
 ab_status ab_run_nve(ab_engine* e, int64_t nsteps, double dt, int64_t every, double* thermo) {
   TRY(need_atoms(e));
+  e->want_virial = false;
+  ab_status s = run_nve_impl(e, nsteps, dt, every, thermo);
+  e->want_virial = true;
+  return s;
+}
+
+static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t every, double* thermo) {
   if (nsteps < 0 || !(dt > 0)) {
     e->err = "nsteps must be >= 0 and dt > 0";
     return AB_E_ARG;
@@ -831,41 +879,44 @@ ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows
   CK(cudaMemcpyAsync(gid.data(), e->gid.p, sizeof(int) * NT, cudaMemcpyDeviceToHost, e->st));
   CK(cudaMemcpyAsync(sh.data(), e->shift.p, sizeof(char4) * NT, cudaMemcpyDeviceToHost, e->st));
   CK(cudaMemcpyAsync(pos.data(), e->pos.p, sizeof(double4) * NT, cudaMemcpyDeviceToHost, e->st));
-  std::vector<int> cnt, nbr;
-  int cap;
-  if (which == AB_LIST_LJ) {
-    cap = e->capLJ;
-    cnt.resize(N);
-    nbr.resize((size_t)N * cap);
-    CK(cudaMemcpyAsync(cnt.data(), e->lj_cnt.p, sizeof(int) * N, cudaMemcpyDeviceToHost, e->st));
-    CK(cudaMemcpyAsync(nbr.data(), e->lj_nbr.p, sizeof(int) * N * cap, cudaMemcpyDeviceToHost, e->st));
-  } else {
-    cap = e->capS;
-    cnt.resize(N);
-    nbr.resize((size_t)N * cap);
-    CK(cudaMemcpyAsync(cnt.data(), e->s_cnt.p, sizeof(int) * N, cudaMemcpyDeviceToHost, e->st));
-    CK(cudaMemcpyAsync(nbr.data(), e->s_nbr.p, sizeof(int) * N * cap, cudaMemcpyDeviceToHost, e->st));
+  // (count, neighbour) tables of the requested list(s)
+  int nl = which == AB_LIST_LJ ? 3 : 1;
+  std::vector<int> cnt[3], nbr[3];
+  int cap[3];
+  for (int c = 0; c < nl; ++c) {
+    cap[c] = which == AB_LIST_LJ ? e->capL[c] : e->capS;
+    const int* dc = which == AB_LIST_LJ ? e->ljc[c].p : e->s_cnt.p;
+    const int* dn = which == AB_LIST_LJ ? e->ljn[c].p : e->s_nbr.p;
+    cnt[c].resize(N);
+    nbr[c].resize((size_t)N * cap[c]);
+    CK(cudaMemcpyAsync(cnt[c].data(), dc, sizeof(int) * N, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(nbr[c].data(), dn, sizeof(int) * N * (size_t)cap[c], cudaMemcpyDeviceToHost, e->st));
   }
   CK(cudaStreamSynchronize(e->st));
+  auto type_h = [&](int a) {
+    long long k;
+    std::memcpy(&k, &pos[a].w, sizeof(k));
+    return (int)(k & 3);
+  };
   std::vector<std::array<int64_t, 5>> out;
-  for (int i = 0; i < N; ++i)
-    for (int q = 0; q < cnt[i]; ++q) {
-      int J = nbr[(size_t)i * cap + q];
-      char4 s = sh[J];
-      bool canon = gid[i] != gid[J] ? gid[i] < gid[J]
-                                    : (s.x > 0 || (s.x == 0 && (s.y > 0 || (s.y == 0 && s.z > 0))));
-      if (which != AB_LIST_SHORT && !canon) continue;
-      if (which == AB_LIST_LJ) {
-        volatile double dx = pos[J].x - pos[i].x, dy = pos[J].y - pos[i].y, dz = pos[J].z - pos[i].z;
-        volatile double a = dx * dx, b = dy * dy, c = dz * dz;
-        volatile double ab = a + b;
-        double r2 = ab + c;
-        int p = (int)pos[i].w + (int)pos[J].w;
-        double rc = e->hp.pr[p].rc;
-        if (!(r2 <= rc * rc)) continue;
+  for (int c = 0; c < nl; ++c)
+    for (int i = 0; i < N; ++i)
+      for (int q = 0; q < cnt[c][i]; ++q) {
+        int J = nbr[c][(size_t)i * cap[c] + q];
+        char4 s = sh[J];
+        bool canon = gid[i] != gid[J] ? gid[i] < gid[J]
+                                      : (s.x > 0 || (s.x == 0 && (s.y > 0 || (s.y == 0 && s.z > 0))));
+        if (which != AB_LIST_SHORT && !canon) continue;
+        if (which == AB_LIST_LJ) {  // exact (un-fused) r^2 <= r_c^2 as on the device
+          volatile double dx = pos[J].x - pos[i].x, dy = pos[J].y - pos[i].y, dz = pos[J].z - pos[i].z;
+          volatile double a = dx * dx, b = dy * dy, cc = dz * dz;
+          volatile double ab = a + b;
+          double r2 = ab + cc;
+          double rc = e->hp.pr[type_h(i) + type_h(J)].rc;
+          if (!(r2 <= rc * rc)) continue;
+        }
+        out.push_back({gid[i], gid[J], s.x, s.y, s.z});
       }
-      out.push_back({gid[i], gid[J], s.x, s.y, s.z});
-    }
   std::sort(out.begin(), out.end());
   *count = (int64_t)out.size();
   if (rows)
@@ -882,7 +933,7 @@ ab_status ab_get_stats(ab_engine* e, ab_stats* s) {
   s->max_reach = c[CT_MAXREACH], s->n_badarg = c[CT_BADARG];
   s->n_atoms = e->N, s->n_ghosts = e->G, s->n_rebuilds = e->rebuilds, s->n_steps = e->steps;
   s->n_overflow_retries = e->retries + c[CT_OVF_REACH];
-  s->lj_capacity = e->capLJ, s->inter_capacity = e->capI;
+  s->lj_capacity = e->capL[0] + e->capL[1] + e->capL[2], s->inter_capacity = e->capI;
   s->n_lj_entries = c[CT_LJENT], s->n_angles = c[CT_ANGLES];
   return AB_OK;
 }
@@ -902,7 +953,7 @@ ab_status ab_get_stage(ab_engine* e, int stage, int64_t* count, double* out) {
     return AB_E_STATE;
   }
   int n[2];
-  CK(cudaMemcpyAsync(n, e->small_i.p + 4, 2 * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+  CK(cudaMemcpyAsync(n, e->small_i.p + 6, 2 * sizeof(int), cudaMemcpyDeviceToHost, e->st));
   CK(cudaStreamSynchronize(e->st));
   int width = stage == 0 ? 13 : 7;
   int rows = n[stage];

@@ -108,7 +108,8 @@ __global__ void k_ghost_fill(int N, double4* pos, int3 smax, double h, const int
         if (sx == 0 && sy == 0 && sz == 0) continue;
         double uz = img(p.z, sz, c_geo.L[2]);
         if (!in_padded(uz, c_geo.L[2], h)) continue;
-        pos[w] = make_double4(ux, uy, uz, p.w);
+        long long key = key_of(p) + ((long long)sx << 18) + ((long long)sy << 10) + ((long long)sz << 2);
+        pos[w] = make_double4(ux, uy, uz, __longlong_as_double(key));
         owner[w] = i;
         gid[w] = gid[i];
         shift[w] = make_char4((signed char)sx, (signed char)sy, (signed char)sz, 0);
@@ -124,7 +125,9 @@ __global__ void k_ghost_update(int N, int NT, double4* pos, const int* owner, co
   if (g >= NT) return;
   double4 p = pos[owner[g]];
   char4 s = shift[g];
-  pos[g] = make_double4(img(p.x, s.x, c_geo.L[0]), img(p.y, s.y, c_geo.L[1]), img(p.z, s.z, c_geo.L[2]), p.w);
+  long long key = key_of(p) + ((long long)s.x << 18) + ((long long)s.y << 10) + ((long long)s.z << 2);
+  pos[g] = make_double4(img(p.x, s.x, c_geo.L[0]), img(p.y, s.y, c_geo.L[1]), img(p.z, s.z, c_geo.L[2]),
+                        __longlong_as_double(key));
 }
 
 __global__ void k_cell_keys(int NT, const double4* pos, Grid g, int* key, int* val) {
@@ -151,40 +154,114 @@ __global__ void k_cell_bounds(int NT, int ncell, const int* sorted_key, int* cel
   }
 }
 
-// Skinned list of atom a: all b != a with r^2 <= cut2[pair] over the stencil +-nr cells.
-// Used for the LJ list (local atoms, cut = r_c + skin, full / both directions) and the
-// intermediate REBO list (all atoms, cut = r_max + skin) of P:719-723.
-__global__ void k_build_list(int NA, const double4* pos, Grid g, const int* cell_start, const int* cell_atoms,
-                             int nr, int which /*0 = LJ, 1 = intermediate*/, int cap, int* cnt, int* nbr,
-                             int* maxcnt) {
-  int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= NA) return;
+// Skinned LJ lists of a local atom (full, both directions), split at build time by what the
+// pair can need at evaluation time (atoms move < skin/2 between builds):
+//   near : r_b <= 3 r_max,max + skin     -> may need C_ij (r <= 3 r_max) or b* (r < 2^(1/6) sigma)
+//   pure : near < r_b <= r_lo(p) - skin  -> C = 1, Q = 1, S_taper = 1 guaranteed: plain 12-6 LJ
+//   band : the rest, r_b <= r_c + skin   -> C = 1, Q = 1, taper and cutoff tested per pair
+// One warp per atom; candidates stream over contiguous z-runs of the cell stencil and are
+// appended with warp-ballot compaction in candidate order (the paper's "inserting at once
+// multiple elements into a single neighbor list"), so lists are deterministic.
+struct LJLists {
+  int cap[3];
+  int* cnt[3];
+  int* nbr[3];
+  double near2;    // (3 r_max,max + skin)^2
+  double pure2[3]; // (r_lo(p) - skin)^2, or -1 if that band is empty
+};
+
+__device__ __forceinline__ void warp_append(bool take, int* row, int cap, int& n, int b) {
+  unsigned m = __ballot_sync(0xffffffffu, take);
+  if (take) {
+    int slot = n + __popc(m & ((1u << (threadIdx.x & 31)) - 1u));
+    if (slot < cap) row[slot] = b;
+  }
+  n += __popc(m);
+}
+
+__global__ void k_build_lj(int N, const double4* pos, Grid g, const int* cell_start, const int* cell_atoms, int nr,
+                           LJLists Lg, int* maxcnt) {
+  int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (a >= N) return;
+  int lane = threadIdx.x & 31;
   double4 p = pos[a];
-  int ta = (int)p.w;
+  int ta = type_of(p);
   int cx = cell_coord(p.x, g.lo[0], g.cs[0], g.nc[0]);
   int cy = cell_coord(p.y, g.lo[1], g.cs[1], g.nc[1]);
   int cz = cell_coord(p.z, g.lo[2], g.cs[2], g.nc[2]);
-  int c = 0;
-  int* out = nbr + (size_t)a * cap;
+  int z0 = max(0, cz - nr), z1 = min(g.nc[2] - 1, cz + nr);
+  int n[3] = {0, 0, 0};
+  int* row[3];
+  for (int c = 0; c < 3; ++c) row[c] = Lg.nbr[c] + (size_t)a * Lg.cap[c];
   for (int ax = max(0, cx - nr); ax <= min(g.nc[0] - 1, cx + nr); ++ax)
-    for (int ay = max(0, cy - nr); ay <= min(g.nc[1] - 1, cy + nr); ++ay)
-      for (int az = max(0, cz - nr); az <= min(g.nc[2] - 1, cz + nr); ++az) {
-        int cell = (ax * g.nc[1] + ay) * g.nc[2] + az;
-        for (int q = cell_start[cell]; q < cell_start[cell + 1]; ++q) {
-          int b = cell_atoms[q];
-          if (b == a) continue;
+    for (int ay = max(0, cy - nr); ay <= min(g.nc[1] - 1, cy + nr); ++ay) {
+      int c0 = (ax * g.nc[1] + ay) * g.nc[2];
+      int beg = cell_start[c0 + z0], end = cell_start[c0 + z1 + 1];
+      for (int base = beg; base < end; base += 32) {
+        int q = base + lane;
+        bool ok = q < end;
+        int b = ok ? cell_atoms[q] : -1;
+        ok = ok && b != a;
+        double r2 = 1e300;
+        int pr = 0;
+        if (ok) {
+          double4 pb = pos[b];
+          r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
+          pr = ta + type_of(pb);
+        }
+        bool in = ok && r2 <= c_geo.rc_s2[pr];
+        bool nearp = in && r2 <= Lg.near2;
+        bool purep = in && !nearp && r2 <= Lg.pure2[pr];
+        bool bandp = in && !nearp && !purep;
+        warp_append(nearp, row[0], Lg.cap[0], n[0], b);
+        warp_append(purep, row[1], Lg.cap[1], n[1], b);
+        warp_append(bandp, row[2], Lg.cap[2], n[2], b);
+      }
+    }
+  if (lane == 0) {
+    for (int c = 0; c < 3; ++c) {
+      Lg.cnt[c][a] = n[c];
+      atomicMax(maxcnt + c, n[c]);
+    }
+  }
+}
+
+// intermediate REBO list: all atoms (locals + ghosts), r_b <= r_max(p) + skin
+__global__ void k_build_inter(int NT, const double4* pos, Grid g, const int* cell_start, const int* cell_atoms,
+                              int nr, int cap, int* cnt, int* nbr, int* maxcnt) {
+  int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (a >= NT) return;
+  int lane = threadIdx.x & 31;
+  double4 p = pos[a];
+  int ta = type_of(p);
+  int cx = cell_coord(p.x, g.lo[0], g.cs[0], g.nc[0]);
+  int cy = cell_coord(p.y, g.lo[1], g.cs[1], g.nc[1]);
+  int cz = cell_coord(p.z, g.lo[2], g.cs[2], g.nc[2]);
+  int z0 = max(0, cz - nr), z1 = min(g.nc[2] - 1, cz + nr);
+  int n = 0;
+  int* row = nbr + (size_t)a * cap;
+  for (int ax = max(0, cx - nr); ax <= min(g.nc[0] - 1, cx + nr); ++ax)
+    for (int ay = max(0, cy - nr); ay <= min(g.nc[1] - 1, cy + nr); ++ay) {
+      int c0 = (ax * g.nc[1] + ay) * g.nc[2];
+      int beg = cell_start[c0 + z0], end = cell_start[c0 + z1 + 1];
+      for (int base = beg; base < end; base += 32) {
+        int q = base + lane;
+        bool ok = q < end;
+        int b = ok ? cell_atoms[q] : -1;
+        ok = ok && b != a;
+        bool in = false;
+        if (ok) {
           double4 pb = pos[b];
           double r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
-          int pr = ta + (int)pb.w;
-          double cut2 = which == 0 ? c_geo.rc_s2[pr] : c_geo.rmax_s2[pr];
-          if (r2 <= cut2) {
-            if (c < cap) out[c] = b;
-            ++c;
-          }
+          in = r2 <= c_geo.rmax_s2[ta + type_of(pb)];
         }
+        warp_append(in, row, cap, n, b);
       }
-  cnt[a] = c;
-  atomicMax(maxcnt, c);
+    }
+  if (lane == 0) {
+    cnt[a] = n;
+    atomicMax(maxcnt, n);
+  }
 }
 
 // Short-list storage: per atom up to capS entries: neighbour index, (d, r) and (w, dw/dr).
@@ -220,7 +297,8 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
   if (live) {
     const Tab<R>& T = tab<R>();
     double4 p = pos[a];
-    int ta = (int)p.w;
+    int ta = type_of(p);
+    long long ka = key_of(p);
     int n = 0;
     R nc = 0, nh = 0;
     int ci = in_cnt[a];
@@ -230,7 +308,7 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
       double4 pb = pos[b];
       double dx = __dsub_rn(pb.x, p.x), dy = __dsub_rn(pb.y, p.y), dz = __dsub_rn(pb.z, p.z);
       double r2 = r2_exact(dx, dy, dz);
-      int tb = (int)pb.w;
+      int tb = type_of(pb);
       int pr = ta + tb;
       if (r2 <= c_geo.rmax2[pr]) {
         if (n < S.capS) {
@@ -242,7 +320,7 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
           S.w[base + n] = {w, dw};
           if (tb == 0) nc += w;
           else nh += w;
-          if (a < N && canonical_pair(gid[a], gid[b], shift[b])) ++nbond;
+          if (a < N && ka < key_of(pb)) ++nbond;
         }
         ++n;
       }
@@ -273,7 +351,7 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
     int n = S.cnt[a];
     for (int q = 0; q < n; ++q) {
       int b = S.nbr[base + q];
-      if (canonical_pair(gid[a], gid[b], shift[b])) bonds[w++] = make_int2(a, q);
+      if (key_of(pos[a]) < key_of(pos[b])) bonds[w++] = make_int2(a, q);
     }
   }
   unsigned long long s = warp_sum_u((unsigned long long)nloc);

@@ -12,7 +12,7 @@ __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, do
   double d2 = 0.0;
   if (i < N) {
     double4 p = pos[i];
-    double dtf = ((int)p.w == 0) ? dtf0 : dtf1;
+    double dtf = (type_of(p) == 0) ? dtf0 : dtf1;
     double vx = v[3 * i + 0] + dtf * F[3 * i + 0];
     double vy = v[3 * i + 1] + dtf * F[3 * i + 1];
     double vz = v[3 * i + 2] + dtf * F[3 * i + 2];
@@ -31,7 +31,7 @@ __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, do
 __global__ void k_integrate2(int N, const double4* pos, double* v, const double* F, double dtf0, double dtf1) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
-  double dtf = ((int)pos[i].w == 0) ? dtf0 : dtf1;
+  double dtf = (type_of(pos[i]) == 0) ? dtf0 : dtf1;
   v[3 * i + 0] += dtf * F[3 * i + 0];
   v[3 * i + 1] += dtf * F[3 * i + 1];
   v[3 * i + 2] += dtf * F[3 * i + 2];
@@ -55,7 +55,7 @@ __global__ void k_ke(int N, const double4* pos, const double* v, double m0, doub
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double k = 0.0;
   if (i < N) {
-    double m = ((int)pos[i].w == 0) ? m0 : m1;
+    double m = (type_of(pos[i]) == 0) ? m0 : m1;
     double a = v[3 * i], b = v[3 * i + 1], c = v[3 * i + 2];
     k = 0.5 * m * (a * a + b * b + c * c);
   }
@@ -70,7 +70,7 @@ __global__ void k_copy_xref(int N, const double4* pos, double4* xref) {
 
 __global__ void k_types(int NT, const double4* pos, signed char* typ) {
   int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a < NT) typ[a] = (signed char)(int)pos[a].w;
+  if (a < NT) typ[a] = (signed char)type_of(pos[a]);
 }
 
 // caller-order array (n*3) -> internal positions / velocities
