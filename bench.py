@@ -96,14 +96,19 @@ class ClockSampler:
 
 
 def algorithmic_flops(stats):
-    """Per-phase algorithmic flop counts per launch (SURVEY §8(d) op weights)."""
-    lj = 31 * stats["n_lj"] + 9 * max(0, stats["n_lj_entries"] // 2 - stats["n_lj"])
+    """Per-phase algorithmic flop counts per launch (SURVEY §8(d) op weights).
+    LJ: 31 flops per half pair inside r_c, 9 per half list entry outside (skin); REBO: 700 per
+    bond (pair terms, P, pi^rc, T) + 65 per angle term + 260 per dihedral quad (pi^dh + torsion,
+    forward and reverse); b*: 1500 per evaluated pair; short list: 15 per entry."""
+    far_in, far_ent = stats["n_lj_far"], stats["n_lj_entries_far"] // 2
+    near_in, near_ent = stats["n_lj"] - far_in, (stats["n_lj_entries"] - stats["n_lj_entries_far"]) // 2
     rebo = 700 * stats["n_bonds"] + 65 * stats["n_angles"] + 260 * stats["n_quads"]
-    return {"short": 15 * stats["n_short"], "rebo": rebo, "lj": lj, "bstar": 1500 * stats["n_bstar"]}
+    return {"short": 15 * stats["n_short"], "rebo": rebo, "lj_near": 31 * near_in + 9 * max(0, near_ent - near_in),
+            "bstar": 1500 * stats["n_bstar"], "lj_far": 31 * far_in + 9 * max(0, far_ent - far_in)}
 
 
-PHASES = ["short", "rebo", "lj", "bstar", "integrate", "rebuild"]
-KERNEL_OF = {"short": "k_short", "rebo": "k_rebo", "lj": "k_lj", "bstar": "k_bstar"}
+PHASES = ["short", "rebo", "lj_near", "bstar", "integrate", "rebuild", "lj_far", "spare"]
+KERNEL_OF = {"short": "k_short", "rebo": "k_rebo", "lj_near": "k_lj_near", "bstar": "k_bstar", "lj_far": "k_lj_far"}
 
 
 def fp64_peak_tflops(sm_mhz, nsm=148):
@@ -171,8 +176,8 @@ def run_ours(args, ws, rank, local):
         barrier()
         launches = eng.device_info()["kernel_launches"] - l0
         import ctypes as C
-        ms = (C.c_double * 6)()
-        n = (C.c_int64 * 6)()
+        ms = (C.c_double * 8)()
+        n = (C.c_int64 * 8)()
         eng.L.ab_get_phase_ms(eng.h, ms, n)
         eng.L.ab_set_profiling(eng.h, 0)
         st = eng.stats()
@@ -195,7 +200,7 @@ def run_ours(args, ws, rank, local):
 
     def roofline(r, precision):
         flops = algorithmic_flops(r["stats"])
-        dom = max(("short", "rebo", "lj", "bstar"), key=lambda p: r["phase"][p][0])
+        dom = max(("short", "rebo", "lj_near", "bstar", "lj_far"), key=lambda p: r["phase"][p][0])
         tot_ms, cnt = r["phase"][dom]
         avg_s = tot_ms / max(cnt, 1) * 1e-3
         achieved = flops[dom] / avg_s / 1e12 if avg_s > 0 else 0.0

@@ -70,6 +70,8 @@ typedef struct ab_stats {
   int64_t lj_capacity, inter_capacity;
   int64_t n_lj_entries; /* skinned full LJ-list entries streamed (both directions) */
   int64_t n_angles;     /* bond-order angle terms (k in N(i)\j plus l in N(j)\i, per half bond) */
+  int64_t n_lj_far;     /* ... of n_lj, pairs evaluated by the far-pair kernel (C = Q = 1 by construction) */
+  int64_t n_lj_entries_far;
 } ab_stats;
 
 /* Create an engine on CUDA device `cuda_device` from parameter-file text (params/toy_ch.param
@@ -130,11 +132,13 @@ ab_status ab_record_stages(ab_engine* e, int on);
 ab_status ab_get_stage(ab_engine* e, int stage, int64_t* count, double* out);
 
 /* Per-phase device timing with CUDA events on the engine's stream (the paper's profile labels,
- * P:359-360): phase 0 short list + N_i, 1 REBO + bond order + torsion, 2 LJ + C_ij,
- * 3 b* batch, 4 integrator, 5 list rebuild.  ab_get_phase_ms returns accumulated milliseconds
- * ms[6] and launch counts n[6] since profiling was switched on (on != 0 resets them). */
+ * P:359-360): phase 0 short list + N_i, 1 REBO + bond order + torsion, 2 LJ near
+ * pairs + C_ij reach sets, 3 b* batch, 4 integrator, 5 list rebuild, 6 LJ far pairs, 7 spare.
+ * ab_get_phase_ms returns accumulated milliseconds ms[AB_NPHASE] and launch counts n[AB_NPHASE]
+ * since profiling was switched on (on != 0 resets them). */
+#define AB_NPHASE 8
 ab_status ab_set_profiling(ab_engine* e, int on);
-ab_status ab_get_phase_ms(ab_engine* e, double ms[6], int64_t n[6]);
+ab_status ab_get_phase_ms(ab_engine* e, double ms[AB_NPHASE], int64_t n[AB_NPHASE]);
 
 /* FP64 (prec = AB_FP64) or FP32 (AB_MIXED) FMA-throughput microbenchmark on the engine's GPU:
  * all SMs, 8 independent FMA chains per thread; returns the achieved TFLOP/s (2 flops per FMA).

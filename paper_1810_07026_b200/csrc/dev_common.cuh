@@ -21,6 +21,7 @@ template <typename R>
 struct Tab {
   R rmin[3], rmax[3], Q[3], alpha[3], A[3], B[3][3], beta[3][3];
   R eps[3], sigma[3], sigma2[3], rc[3], rlo[3], bmin[3], bmax[3], rho[3], srhi[3];
+  R inv_taper[3];  // 1 / (r_c - r_lo)
   R explam[2][2][2];  // e^{lambda_{jik}} [t_j][t_i][t_k]
   int gn[2];
   R gx[2][16], gy[2][16], gm[2][16];
@@ -31,6 +32,7 @@ struct Tab {
 
 struct Geo {  // double-only quantities: exact list / gate decisions, box, integrator
   double rmax2[3], rc2[3], rmax_s2[3], rc_s2[3], rlo2[3], reach2;
+  double srhi2_hi[3];  // (2^(1/6) sigma)^2 (1 + 1e-9): pre-filter of the exact S_r window test
   double L[3];
   double mass[2], ftm2v, mvv2e;
 };
@@ -117,6 +119,70 @@ __device__ __forceinline__ R sw(R x, R lo, R hi, R& dv) {
   scpi(t, &s, &c);
   dv = R(-0.5) * R(CUDART_PI) * s / (hi - lo);
   return R(0.5) * (R(1) + c);
+}
+
+// 1/sqrt(a) without the slow-path call of the IEEE routines: hardware approximation + two
+// Newton steps (fp64: ~1 ulp; fp32: MUFU rsqrt).  a > 0 and finite.
+__device__ __forceinline__ double rsqrt_fast(double a) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double ha = 0.5 * a;
+  y = y * fma(-ha * y, y, 1.5);
+  y = y * fma(-ha * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ float rsqrt_fast(float a) { return rsqrtf(a); }
+
+// Branch-free half-cosine on t in [0, 1] (caller clamps): S = (1 + cos(pi t))/2 and dS/dt, from
+// x = pi (t - 1/2) in [-pi/2, pi/2]: cos(pi t) = -sin x, sin(pi t) = cos x, Taylor polynomials
+// truncated below the working precision (fp64: x^21 / x^20 terms, error < 3e-17; fp32: x^13 / x^12).
+__device__ __forceinline__ void halfcos_poly(double t, double& S, double& dSdt) {
+  double x = (t - 0.5) * CUDART_PI;
+  double x2 = x * x;
+  double s = -1.9572941063391263e-20;  // -1/21!
+  s = fma(s, x2, 8.2206352466243295e-18);   // 1/19!
+  s = fma(s, x2, -2.8114572543455206e-15);  // -1/17!
+  s = fma(s, x2, 7.6471637318198164e-13);   // 1/15!
+  s = fma(s, x2, -1.6059043836821613e-10);  // -1/13!
+  s = fma(s, x2, 2.5052108385441720e-08);   // 1/11!
+  s = fma(s, x2, -2.7557319223985893e-06);  // -1/9!
+  s = fma(s, x2, 1.9841269841269841e-04);   // 1/7!
+  s = fma(s, x2, -8.3333333333333333e-03);  // -1/5!
+  s = fma(s, x2, 1.6666666666666667e-01);   // -(-1/3!)
+  s = x - x * x2 * s;                       // sin x
+  double c = 4.1103176233121648e-19;        // 1/20!
+  c = fma(c, x2, -1.5619206968586225e-16);  // -1/18!
+  c = fma(c, x2, 4.7794773323873853e-14);   // 1/16!
+  c = fma(c, x2, -1.1470745597729725e-11);  // -1/14!
+  c = fma(c, x2, 2.0876756987868099e-09);   // 1/12!
+  c = fma(c, x2, -2.7557319223985891e-07);  // -1/10!
+  c = fma(c, x2, 2.4801587301587302e-05);   // 1/8!
+  c = fma(c, x2, -1.3888888888888889e-03);  // -1/6!
+  c = fma(c, x2, 4.1666666666666667e-02);   // 1/4!
+  c = fma(c, x2, -0.5);                     // -1/2!
+  c = fma(c, x2, 1.0);                      // cos x
+  S = 0.5 - 0.5 * s;
+  dSdt = -0.5 * CUDART_PI * c;
+}
+__device__ __forceinline__ void halfcos_poly(float t, float& S, float& dSdt) {
+  float x = (t - 0.5f) * 3.14159265358979f;
+  float x2 = x * x;
+  float s = 1.6059043836821613e-10f;
+  s = fmaf(s, x2, -2.5052108385441720e-08f);
+  s = fmaf(s, x2, 2.7557319223985893e-06f);
+  s = fmaf(s, x2, -1.9841269841269841e-04f);
+  s = fmaf(s, x2, 8.3333333333333333e-03f);
+  s = fmaf(s, x2, -1.6666666666666667e-01f);
+  s = fmaf(s * x2, x, x);
+  float c = 2.0876756987868099e-09f;
+  c = fmaf(c, x2, -2.7557319223985891e-07f);
+  c = fmaf(c, x2, 2.4801587301587302e-05f);
+  c = fmaf(c, x2, -1.3888888888888889e-03f);
+  c = fmaf(c, x2, 4.1666666666666667e-02f);
+  c = fmaf(c, x2, -0.5f);
+  c = fmaf(c, x2, 1.0f);
+  S = 0.5f - 0.5f * s;
+  dSdt = -0.5f * 3.14159265358979f * c;
 }
 
 // ------------------------------------------------------------------ splines
@@ -289,8 +355,87 @@ enum {
   CT_OVF_STAGE,
   CT_LJENT,       // skinned LJ list entries streamed
   CT_ANGLES,      // bond-order angle terms
+  CT_LJFAR,       // canonical LJ pairs within r_c handled by the far kernel
+  CT_LJENTFAR,    // far-list entries streamed
   CT_N
 };
+
+// ---- block-partial reductions of energies / virial / counters -----------------------------
+// Thousands of same-address global atomics per launch serialise in L2; instead every block
+// reduces into shared memory and stores one partial row (column-major), and k_reduce sums the
+// rows in a fixed order (deterministic totals).
+struct RedRows {
+  double* d;              // [ACC_N][stride]
+  unsigned long long* u;  // [CT_N][stride]
+  int stride, row0;
+};
+struct RedSmem {
+  double d[ACC_N];
+  unsigned long long u[CT_N];
+};
+__device__ __forceinline__ bool ct_is_max(int c) { return c == CT_MAXSHORT || c == CT_MAXREACH; }
+__device__ __forceinline__ void red_init(RedSmem& s) {
+  for (int c = threadIdx.x; c < ACC_N; c += blockDim.x) s.d[c] = 0.0;
+  for (int c = threadIdx.x; c < CT_N; c += blockDim.x) s.u[c] = 0ull;
+  __syncthreads();
+}
+// warp-reduce v and add it into the block's shared row (all 32 lanes of the warp must call)
+__device__ __forceinline__ void red_add_d(RedSmem& s, int col, double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v != 0.0) atomicAdd(&s.d[col], v);
+}
+__device__ __forceinline__ void red_add_u(RedSmem& s, int col, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s.u[col], v);
+}
+__device__ __forceinline__ void red_max_u(RedSmem& s, int col, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, (unsigned long long)__shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v) atomicMax(&s.u[col], v);
+}
+__device__ __forceinline__ void red_flush(const RedSmem& s, RedRows R) {
+  __syncthreads();
+  int row = R.row0 + blockIdx.x;
+  for (int c = threadIdx.x; c < ACC_N; c += blockDim.x) R.d[(size_t)c * R.stride + row] = s.d[c];
+  for (int c = threadIdx.x; c < CT_N; c += blockDim.x) R.u[(size_t)c * R.stride + row] = s.u[c];
+}
+// one block per column: fixed-order sum (max for the max counters) over nrows partial rows
+__global__ void k_reduce(RedRows R, int nrows, double* acc, unsigned long long* ct) {
+  __shared__ double sd[32];
+  __shared__ unsigned long long su[32];
+  int c = blockIdx.x;
+  bool isd = c < ACC_N;
+  int cc = isd ? c : c - ACC_N;
+  bool mx = !isd && ct_is_max(cc);
+  double vd = 0.0;
+  unsigned long long vu = 0ull;
+  for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+    if (isd) vd += R.d[(size_t)cc * R.stride + r];
+    else {
+      unsigned long long x = R.u[(size_t)cc * R.stride + r];
+      vu = mx ? max(vu, x) : vu + x;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    vd += __shfl_xor_sync(0xffffffffu, vd, o);
+    unsigned long long y = __shfl_xor_sync(0xffffffffu, vu, o);
+    vu = mx ? max(vu, y) : vu + y;
+  }
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sd[w] = vd, su[w] = vu;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) {
+      vd += sd[q];
+      vu = mx ? max(vu, su[q]) : vu + su[q];
+    }
+    if (isd) acc[cc] += vd;  // acc may already hold direct contributions (KE)
+    else ct[cc] = mx ? max(ct[cc], vu) : ct[cc] + vu;
+  }
+}
 
 // warp-reduce an array of doubles and add lane 0's totals into global accumulators.
 // Must be called by all 32 lanes of a warp.

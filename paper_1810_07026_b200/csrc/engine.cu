@@ -88,7 +88,8 @@ struct ab_engine {
   DBuf<int> small_i;                 // [0] nbonds [1] qcount [2] maxLJ [3] maxI [4..5] stage counts
   DBuf<double> acc;                  // ACC_N
   DBuf<unsigned long long> ct;       // CT_N (+1: maxdisp2)
-  DBuf<double> stage0, stage1;
+  DBuf<double> stage0, stage1, red_d;
+  DBuf<unsigned long long> red_u;
   DBuf<unsigned char> cub_tmp;
   // pinned host mirror for small readbacks
   unsigned long long* h_ct = nullptr;
@@ -99,8 +100,8 @@ struct ab_engine {
   unsigned long long last_ct[CT_N] = {0};
   // per-phase CUDA-event profiling (ab_set_profiling)
   bool prof = false;
-  double phase_ms[6] = {0, 0, 0, 0, 0, 0};
-  long long phase_n[6] = {0, 0, 0, 0, 0, 0};
+  double phase_ms[AB_NPHASE] = {0};
+  long long phase_n[AB_NPHASE] = {0};
   struct Pend {
     int phase;
     cudaEvent_t a, b;
@@ -199,6 +200,7 @@ void fill_tab(const HostParams& hp, Tab<R>& t) {
     t.eps[p] = (R)s.eps, t.sigma[p] = (R)s.sigma, t.sigma2[p] = (R)(s.sigma * s.sigma), t.rc[p] = (R)s.rc;
     t.rlo[p] = (R)s.rlo, t.bmin[p] = (R)s.bmin, t.bmax[p] = (R)s.bmax, t.rho[p] = (R)s.rho;
     t.srhi[p] = (R)(s.sigma * 1.122462048309373);  // 2^(1/6) sigma (reading A11)
+    t.inv_taper[p] = (R)(1.0 / (s.rc - s.rlo));
   }
   for (int j = 0; j < 2; ++j)
     for (int i = 0; i < 2; ++i)
@@ -238,6 +240,8 @@ ab_status upload_geo(ab_engine* e) {
     g.rmax_s2[p] = (s.rmax + hp.skin) * (s.rmax + hp.skin);
     g.rc_s2[p] = (s.rc + hp.skin) * (s.rc + hp.skin);
     g.rlo2[p] = s.rlo * s.rlo;
+    double srhi = s.sigma * 1.122462048309373;
+    g.srhi2_hi[p] = srhi * srhi * (1.0 + 1e-9);
     rmm = std::max(rmm, s.rmax);
     rcm = std::max(rcm, s.rc);
   }
@@ -467,36 +471,56 @@ ab_status forces_impl(ab_engine* e) {
     CK(cudaMemsetAsync(e->small_i.p, 0, 2 * sizeof(int), st));
     CK(cudaMemsetAsync(e->small_i.p + 6, 0, 2 * sizeof(int), st));
     ShortList<R> S = short_view<R>(e);
+    // grids and the per-block partial rows of the energy / virial / counter reduction
+    const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
+    const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4;
+    const int nrows = g_short + g_rebo + g_near + g_far + g_bstar;
+    CK(e->red_d.ensure((size_t)ACC_N * nrows));
+    CK(e->red_u.ensure((size_t)CT_N * nrows));
+    RedRows RR{e->red_d.p, e->red_u.p, nrows, 0};
     prof_begin(e, 0);
-    k_short<R><<<nblk(NT, 128), 128, 0, st>>>(N, NT, e->pos.p, e->in_cnt.p, e->in_nbr.p, e->capI, S, e->gid.p,
-                                              e->shift.p, e->bonds.p, e->small_i.p, e->ct.p);
+    k_short<R><<<g_short, 128, 0, st>>>(N, NT, e->pos.p, e->in_cnt.p, e->in_nbr.p, e->capI, S, e->gid.p,
+                                        e->shift.p, e->bonds.p, e->small_i.p, e->ct.p, RR);
     CKL();
     prof_end(e);
-    int gb = e->nsm * 4;
+    RR.row0 += g_short;
     prof_begin(e, 1);
-    k_rebo<R><<<gb, 128, 0, st>>>(e->bonds.p, e->small_i.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                  e->acc.p, e->ct.p, sb0);
+    k_rebo<R><<<g_rebo, 128, 0, st>>>(e->bonds.p, e->small_i.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p,
+                                      e->F.p, e->acc.p, e->ct.p, sb0, RR);
     CKL();
     prof_end(e);
+    RR.row0 += g_rebo;
     BstarQueue Qu{e->q_item.p, e->q_M.p, e->small_i.p + 1, e->capQ};
-    prof_begin(e, 2);
     LJArgs A;
     A.N = N;
     A.pos = e->pos.p;
     for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
+    prof_begin(e, 2);
     if (e->want_virial)
-      k_lj<R, true><<<nblk(N, LJ_WARPS), 32 * LJ_WARPS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                                                 e->acc.p, e->ct.p, Qu, sb1);
+      k_lj_near<R, true><<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p,
+                                                                     e->acc.p, e->ct.p, Qu, sb1, RR);
     else
-      k_lj<R, false><<<nblk(N, LJ_WARPS), 32 * LJ_WARPS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                                                  e->acc.p, e->ct.p, Qu, sb1);
+      k_lj_near<R, false><<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p,
+                                                                      e->acc.p, e->ct.p, Qu, sb1, RR);
     CKL();
     prof_end(e);
+    RR.row0 += g_near;
+    prof_begin(e, 6);
+    if (e->want_virial)
+      k_lj_far<R, true><<<g_far, 128, 0, st>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, RR);
+    else
+      k_lj_far<R, false><<<g_far, 128, 0, st>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, RR);
+    CKL();
+    prof_end(e);
+    RR.row0 += g_far;
     prof_begin(e, 3);
-    k_bstar<R><<<gb, 128, 0, st>>>(Qu, e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, e->acc.p,
-                                   e->ct.p, sb1);
+    k_bstar<R><<<g_bstar, 128, 0, st>>>(Qu, e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p,
+                                        e->acc.p, e->ct.p, sb1, RR);
     CKL();
     prof_end(e);
+    RR.row0 = 0;
+    k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows, e->acc.p, e->ct.p);
+    CKL();
     CK(cudaMemcpyAsync(e->h_ct, e->ct.p, sizeof(unsigned long long) * CT_N, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(e->h_acc, e->acc.p, sizeof(double) * ACC_N, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -636,6 +660,8 @@ void ab_destroy(ab_engine* e) {
   e->bonds.release();
   e->q_item.release();
   e->ct.release();
+  e->red_d.release();
+  e->red_u.release();
   e->cub_tmp.release();
   if (e->h_ct) cudaFreeHost(e->h_ct);
   if (e->h_acc) cudaFreeHost(e->h_acc);
@@ -935,6 +961,7 @@ ab_status ab_get_stats(ab_engine* e, ab_stats* s) {
   s->n_overflow_retries = e->retries + c[CT_OVF_REACH];
   s->lj_capacity = e->capL[0] + e->capL[1] + e->capL[2], s->inter_capacity = e->capI;
   s->n_lj_entries = c[CT_LJENT], s->n_angles = c[CT_ANGLES];
+  s->n_lj_far = c[CT_LJFAR], s->n_lj_entries_far = c[CT_LJENTFAR];
   return AB_OK;
 }
 
@@ -970,16 +997,16 @@ ab_status ab_set_profiling(ab_engine* e, int on) {
   CK(cudaStreamSynchronize(e->st));
   prof_collect(e);
   e->prof = on != 0;
-  for (int q = 0; q < 6; ++q) e->phase_ms[q] = 0, e->phase_n[q] = 0;
+  for (int q = 0; q < AB_NPHASE; ++q) e->phase_ms[q] = 0, e->phase_n[q] = 0;
   return AB_OK;
 }
 
-ab_status ab_get_phase_ms(ab_engine* e, double ms[6], int64_t n[6]) {
+ab_status ab_get_phase_ms(ab_engine* e, double ms[AB_NPHASE], int64_t n[AB_NPHASE]) {
   if (!e || !ms || !n) return AB_E_ARG;
   cudaSetDevice(e->dev);
   CK(cudaStreamSynchronize(e->st));
   prof_collect(e);
-  for (int q = 0; q < 6; ++q) ms[q] = e->phase_ms[q], n[q] = e->phase_n[q];
+  for (int q = 0; q < AB_NPHASE; ++q) ms[q] = e->phase_ms[q], n[q] = e->phase_n[q];
   return AB_OK;
 }
 

@@ -389,7 +389,9 @@ template <typename R>
 __global__ void __launch_bounds__(128) k_rebo(const int2* bonds, const int* nbonds, ShortList<R> S,
                                               const signed char* typ, const int* owner, const int* gid,
                                               const char4* shift, double* F, double* acc, unsigned long long* ct,
-                                              StageBuf stage) {
+                                              StageBuf stage, RedRows RR) {
+  __shared__ RedSmem rs;
+  red_init(rs);
   const Tab<R>& T = tab<R>();
   int nb = *nbonds;
   double e[3 + 6] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -448,14 +450,14 @@ __global__ void __launch_bounds__(128) k_rebo(const int2* bonds, const int* nbon
     }
     // keep the warp converged for the reductions below
   }
-  warp_acc(e, acc + ACC_EREBO);
-  unsigned long long s1 = warp_sum_u(nq), s2 = warp_sum_u(nbad), s3 = warp_sum_u(ncount), s4 = warp_sum_u(nang);
-  if ((threadIdx.x & 31) == 0) {
-    if (s4) atomicAdd(ct + CT_ANGLES, s4);
-    if (s1) atomicAdd(ct + CT_QUADS, s1);
-    if (s2) atomicAdd(ct + CT_BADARG, s2);
-    if (s3) atomicAdd(ct + CT_BONDS, s3);
-  }
+  red_add_d(rs, ACC_EREBO, e[0]);
+  red_add_d(rs, ACC_ETORS, e[1]);
+  for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, e[3 + c]);
+  red_add_u(rs, CT_ANGLES, nang);
+  red_add_u(rs, CT_QUADS, nq);
+  red_add_u(rs, CT_BADARG, nbad);
+  red_add_u(rs, CT_BONDS, ncount);
+  red_flush(rs, RR);
 }
 
 // ---------------------------------------------------------------- C_ij path search
@@ -573,7 +575,9 @@ template <typename R>
 __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const double4* pos, ShortList<R> S,
                                                const signed char* typ, const int* owner, const int* gid,
                                                const char4* shift, double* F, double* acc,
-                                               unsigned long long* ct, StageBuf stage) {
+                                               unsigned long long* ct, StageBuf stage, RedRows RR) {
+  __shared__ RedSmem rs;
+  red_init(rs);
   const Tab<R>& T = tab<R>();
   int nq = min(*Qu.count, Qu.cap);
   double e[1 + 6] = {0, 0, 0, 0, 0, 0, 0};
@@ -636,16 +640,12 @@ __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const double4* pos
       }
     }
   }
-  double e1[1] = {e[0]};
-  warp_acc(e1, acc + ACC_ELJ);
-  double w6[6] = {e[1], e[2], e[3], e[4], e[5], e[6]};
-  warp_acc(w6, acc + ACC_W);
-  unsigned long long s1 = warp_sum_u(ntr), s2 = warp_sum_u(nb), s3 = warp_sum_u(nbad);
-  if ((threadIdx.x & 31) == 0) {
-    if (s1) atomicAdd(ct + CT_SBTRANS, s1);
-    if (s2) atomicAdd(ct + CT_BSTAR, s2);
-    if (s3) atomicAdd(ct + CT_BADARG, s3);
-  }
+  red_add_d(rs, ACC_ELJ, e[0]);
+  for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, e[1 + c]);
+  red_add_u(rs, CT_SBTRANS, ntr);
+  red_add_u(rs, CT_BSTAR, nb);
+  red_add_u(rs, CT_BADARG, nbad);
+  red_flush(rs, RR);
 }
 
 }  // namespace ab

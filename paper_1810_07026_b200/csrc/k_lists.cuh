@@ -290,7 +290,9 @@ __device__ __forceinline__ V3<R> sl_d(const ShortList<R>& S, int a, int n, R& r)
 template <typename R>
 __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, const int* in_nbr, int capI,
                         ShortList<R> S, const int* gid, const char4* shift, int2* bonds, int* nbonds,
-                        unsigned long long* ct) {
+                        unsigned long long* ct, RedRows RR) {
+  __shared__ RedSmem rs;
+  red_init(rs);
   int a = blockIdx.x * blockDim.x + threadIdx.x;
   bool live = a < NT;
   int nloc = 0, nbond = 0;
@@ -354,12 +356,9 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
       if (key_of(pos[a]) < key_of(pos[b])) bonds[w++] = make_int2(a, q);
     }
   }
-  unsigned long long s = warp_sum_u((unsigned long long)nloc);
-  long long m = warp_max_i((long long)nloc);
-  if (lane == 0) {
-    if (s) atomicAdd(ct + CT_SHORT, s);
-    atomicMax(ct + CT_MAXSHORT, (unsigned long long)m);
-  }
+  red_add_u(rs, CT_SHORT, (unsigned long long)nloc);
+  red_max_u(rs, CT_MAXSHORT, (unsigned long long)nloc);
+  red_flush(rs, RR);
 }
 
 }  // namespace ab

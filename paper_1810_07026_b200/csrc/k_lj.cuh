@@ -1,19 +1,23 @@
 // k_lj.cuh -- the LJ term gated by C_ij (Alg. 3; E = Q C V) with the
 // per-atom reach set of the C_ij connectivity switch.
 //
-// GPU mapping: one warp per local atom i, streaming i's FULL skinned LJ lists (both directions,
-// so no force scatter onto j: every pair is evaluated from both ends and F_i is a gather).
-//   near list (r_b <= 3 r_max + skin): the warp first maps out every atom image reachable from i
-//     in 1, 2 or 3 bonds with the maximum path-weight product M (the paper's "map out all the
-//     atoms j connected to atom i once") into an open-addressing table in shared memory
-//     (keys = image index, value = M via atomicMax on its bit pattern, M >= 0).  Overflow
-//     -> the direct nested search of P:844-853 for that atom ("sequential fallback").
-//     Per pair: cutoff, C = 1 - M (lookup within 3 r_max), skip if C == 0 (gate order of
-//     P:824-830), pairs inside the S_r window are deferred to the b* batch (canonical direction
-//     only), others give E/2 = C V/2 and the pair force on i.
-//   pure list: C = Q = S_taper = 1 guaranteed by the build: branch-free 12-6 LJ.
-//   band list: C = Q = 1; cutoff and taper per pair.
-// Forces from dC (0 < C < 1, reactive systems only) are applied once, by the canonical direction.
+// Both kernels stream FULL skinned lists (both directions): every pair is evaluated from both
+// ends, so F_i is a register gather with one atomic per atom and nothing is scattered onto j.
+// The lists are split at build time (k_build_lj) by what a pair can need at evaluation time:
+//
+// k_lj_near -- 8 lanes per local atom i (4 atoms per warp), near list (r_b <= 3 r_max + skin).
+//   The lane group first maps out every atom image reachable from i in 1, 2 or 3 bonds with the
+//   maximum path-weight product M (the paper's "map out all the atoms j connected to atom i
+//   once") into a 64-slot open-addressing table in shared memory (keys = image
+//   index, value = M via atomicMax on its bit pattern, M >= 0).  Overflow (table or 2-hop list)
+//   -> the direct nested search of P:844-853 for that atom (the paper's "sequential fallback",
+//   P:866).  Per pair: cutoff, C = 1 - M (lookup within 3 r_max), skip if C == 0 (gate order of
+//   P:824-830), pairs inside the S_r window are deferred to the b* batch (canonical direction
+//   only), others give E/2 = C V/2 and the pair force on i.  Forces from dC
+//   (0 < C < 1, reactive systems only) are applied once, by the canonical direction.
+// k_lj_far -- one warp per local atom i, pure + band lists: C = Q = 1 guaranteed by the build.
+//   No shared memory, branch-free bodies (taper evaluated for every band lane and selected),
+//   4 independent gathers in flight per lane.
 // Counters count canonical directions only (key_i < key_J), so they equal the oracle's half sums.
 #pragma once
 #include "dev_common.cuh"
@@ -21,40 +25,42 @@
 
 namespace ab {
 
-constexpr int LJ_WARPS = 4;
-constexpr int TWOHOP_CAP = NBMAX * NBMAX;
+constexpr int NEAR_GROUP = 8;                    // lanes per atom
+constexpr int NEAR_ATOMS = 16;                   // atoms per 128-thread block
+constexpr int NEAR_SLOTS = 64;                   // reach table slots per atom
+constexpr int NEAR_TWO = 64;                     // 2-hop frontier capacity per atom
 
 struct ReachSmem {
-  int keys[REACH_SLOTS];
-  unsigned long long mbits[REACH_SLOTS];
-  int two_l[TWOHOP_CAP];
-  double two_w[TWOHOP_CAP];
+  int keys[NEAR_SLOTS];
+  unsigned long long mbits[NEAR_SLOTS];
+  int two_l[NEAR_TWO];
+  double two_w[NEAR_TWO];
   int ntwo, nins, ovf;
 };
 
-__device__ __forceinline__ unsigned reach_hash(int key) { return ((unsigned)key * 2654435761u) >> 24; }
+__device__ __forceinline__ unsigned reach_hash(int key) { return ((unsigned)key * 2654435761u) >> 26; }
 
 __device__ __forceinline__ void reach_insert(ReachSmem& s, int key, double M) {
-  unsigned h = reach_hash(key) & (REACH_SLOTS - 1);
-  for (int probe = 0; probe < REACH_SLOTS; ++probe) {
+  unsigned h = reach_hash(key);
+  for (int probe = 0; probe < NEAR_SLOTS; ++probe) {
     int old = atomicCAS(&s.keys[h], REACH_EMPTY, key);
     if (old == REACH_EMPTY || old == key) {
       if (old == REACH_EMPTY) atomicAdd(&s.nins, 1);
       atomicMax(&s.mbits[h], (unsigned long long)__double_as_longlong(M));
       return;
     }
-    h = (h + 1) & (REACH_SLOTS - 1);
+    h = (h + 1) & (NEAR_SLOTS - 1);
   }
   s.ovf = 1;
 }
 
 __device__ __forceinline__ double reach_lookup(const ReachSmem& s, int key) {
-  unsigned h = reach_hash(key) & (REACH_SLOTS - 1);
-  for (int probe = 0; probe < REACH_SLOTS; ++probe) {
+  unsigned h = reach_hash(key);
+  for (int probe = 0; probe < NEAR_SLOTS; ++probe) {
     int k = s.keys[h];
     if (k == key) return __longlong_as_double((long long)s.mbits[h]);
     if (k == REACH_EMPTY) return 0.0;
-    h = (h + 1) & (REACH_SLOTS - 1);
+    h = (h + 1) & (NEAR_SLOTS - 1);
   }
   return 0.0;
 }
@@ -76,75 +82,89 @@ struct LJArgs {
   const int* nbr[3];
 };
 
-template <typename R>
-__device__ __forceinline__ R to_r(double x) {
-  return (R)x;
+__device__ __forceinline__ void stage_lj_row(StageBuf stage, int gi, int gj, char4 sh, double C, double bs) {
+  double* rw = stage_row(stage, 7);
+  if (rw) rw[0] = gi, rw[1] = gj, rw[2] = sh.x, rw[3] = sh.y, rw[4] = sh.z, rw[5] = C, rw[6] = bs;
 }
 
-template <typename R, bool VIRIAL>
-__global__ void __launch_bounds__(32 * LJ_WARPS) k_lj(LJArgs A, ShortList<R> S, const int* owner, const int* gid,
-                                                     const char4* shift, double* F, double* acc,
-                                                     unsigned long long* ct, BstarQueue Qu, StageBuf stage) {
-  __shared__ ReachSmem sm_all[LJ_WARPS];
-  const Tab<R>& T = tab<R>();
-  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  ReachSmem& s = sm_all[warp];
-  int i = blockIdx.x * LJ_WARPS + warp;
-  if (i >= A.N) return;  // whole warp exits together
+template <int W>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
-  const double4 pi = A.pos[i];
-  const int ti = type_of(pi);
-  const long long ki = key_of(pi);
+// ---------------------------------------------------------------------------------- near pairs
+template <typename R, bool VIRIAL>
+__global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, ShortList<R> S, const int* owner,
+                                                                    const int* gid, const char4* shift, double* F,
+                                                                    double* acc, unsigned long long* ct,
+                                                                    BstarQueue Qu, StageBuf stage, RedRows RR) {
+  __shared__ ReachSmem sm_all[NEAR_ATOMS];
+  __shared__ RedSmem rs;
+  red_init(rs);
+  const Tab<R>& T = tab<R>();
+  const int grp = threadIdx.x / NEAR_GROUP, gl = threadIdx.x % NEAR_GROUP;
+  ReachSmem& s = sm_all[grp];
+  const int i = blockIdx.x * NEAR_ATOMS + grp;
+  const bool active = i < A.N;
+  const int cntN = active ? A.cnt[0][i] : 0;
+
+  // 1. reach set of i (1-, 2-, 3-bond paths)
+  for (int q = gl; q < NEAR_SLOTS; q += NEAR_GROUP) {
+    s.keys[q] = REACH_EMPTY;
+    s.mbits[q] = 0ull;
+  }
+  if (gl == 0) s.ntwo = 0, s.nins = 0, s.ovf = 0;
+  __syncwarp();
+  const size_t bi = (size_t)(active ? i : 0) * S.capS;
+  const int ni = cntN > 0 ? S.cnt[i] : 0;
+  for (int t = gl; t < ni; t += NEAR_GROUP) {
+    int k = S.nbr[bi + t];
+    R w1 = S.w[bi + t].x;
+    reach_insert(s, k, (double)w1);
+    size_t bk = (size_t)k * S.capS;
+    int nk = S.cnt[k];
+    for (int b = 0; b < nk; ++b) {
+      int l = S.nbr[bk + b];
+      if (l == i) continue;
+      R w12 = w1 * S.w[bk + b].x;
+      reach_insert(s, l, (double)w12);
+      int slot = atomicAdd(&s.ntwo, 1);
+      if (slot < NEAR_TWO) {
+        s.two_l[slot] = l;
+        s.two_w[slot] = (double)w12;
+      } else {
+        s.ovf = 1;
+      }
+    }
+  }
+  __syncwarp();
+  const int ntwo = min(s.ntwo, NEAR_TWO);
+  for (int t = gl; t < ntwo; t += NEAR_GROUP) {
+    int l = s.two_l[t];
+    R w12 = (R)s.two_w[t];
+    size_t bl = (size_t)l * S.capS;
+    int nl = S.cnt[l];
+    for (int c = 0; c < nl; ++c) {
+      int m = S.nbr[bl + c];
+      if (m == i) continue;
+      reach_insert(s, m, (double)(w12 * S.w[bl + c].x));
+    }
+  }
+  __syncwarp();
+  const bool ovf = s.ovf != 0;
+
+  // 2. pairs
   double fx = 0, fy = 0, fz = 0, en = 0;
   double W[6] = {0, 0, 0, 0, 0, 0};
   unsigned long long nlj = 0, nc0 = 0;
-
-  // ------------------------------------------------------------ near list
-  const int cntN = A.cnt[0][i];
   if (cntN > 0) {
-    // 1. reach set of i (1-, 2-, 3-bond paths)
-    for (int q = lane; q < REACH_SLOTS; q += 32) {
-      s.keys[q] = REACH_EMPTY;
-      s.mbits[q] = 0ull;
-    }
-    if (lane == 0) s.ntwo = 0, s.nins = 0, s.ovf = 0;
-    __syncwarp();
-    size_t bi = (size_t)i * S.capS;
-    int ni = S.cnt[i];
-    if (lane < ni) {
-      int k = S.nbr[bi + lane];
-      R w1 = S.w[bi + lane].x;
-      reach_insert(s, k, (double)w1);
-      size_t bk = (size_t)k * S.capS;
-      int nk = S.cnt[k];
-      for (int b = 0; b < nk; ++b) {
-        int l = S.nbr[bk + b];
-        if (l == i) continue;
-        R w12 = w1 * S.w[bk + b].x;
-        reach_insert(s, l, (double)w12);
-        int slot = atomicAdd(&s.ntwo, 1);
-        s.two_l[slot] = l;
-        s.two_w[slot] = (double)w12;
-      }
-    }
-    __syncwarp();
-    int ntwo = s.ntwo;
-    for (int t = lane; t < ntwo; t += 32) {
-      int l = s.two_l[t];
-      R w12 = (R)s.two_w[t];
-      size_t bl = (size_t)l * S.capS;
-      int nl = S.cnt[l];
-      for (int c = 0; c < nl; ++c) {
-        int m = S.nbr[bl + c];
-        if (m == i) continue;
-        reach_insert(s, m, (double)(w12 * S.w[bl + c].x));
-      }
-    }
-    __syncwarp();
-    const bool ovf = s.ovf != 0;
-    // 2. pairs
+    const double4 pi = A.pos[i];
+    const int ti = type_of(pi);
+    const long long ki = key_of(pi);
     const int* row = A.nbr[0] + (size_t)i * A.cap[0];
-    for (int q = lane; q < cntN; q += 32) {
+    for (int q = gl; q < cntN; q += NEAR_GROUP) {
       int J = row[q];
       double4 pj = A.pos[J];
       double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
@@ -157,36 +177,39 @@ __global__ void __launch_bounds__(32 * LJ_WARPS) k_lj(LJArgs A, ShortList<R> S, 
       if (r2 <= c_geo.reach2) Md = ovf ? (double)path_search(S, i, J).M : reach_lookup(s, J);
       if (Md == 1.0) {  // C_ij == 0 (Alg. 3 "continue")
         nc0 += canon;
-        if (canon && stage.rows) {
-          double* rw = stage_row(stage, 7);
-          if (rw) {
-            char4 sh = shift[J];
-            rw[0] = gid[i], rw[1] = gid[J], rw[2] = sh.x, rw[3] = sh.y, rw[4] = sh.z, rw[5] = 0.0, rw[6] = 0.0;
-          }
-        }
+        if (canon && stage.rows) stage_lj_row(stage, gid[i], gid[J], shift[J], 0.0, 0.0);
         continue;
       }
-      double rd = sqrt(r2);
-      // S_r(r) != 0 decided in fp64 in both precision modes (gates on r are fp64, reading A14)
-      double tP = (rd - c_tabd.sigma[p]) / (c_tabd.srhi[p] - c_tabd.sigma[p]);
-      if (tP < 1.0) {  // deferred b* batch, whole pair evaluated once by the canonical direction
-        if (canon) {
-          int k = atomicAdd(Qu.count, 1);
-          if (k < Qu.cap) {
-            Qu.item[k] = make_int4(i, J, 0, 0);
-            Qu.M[k] = Md;
-          } else {
-            atomicAdd(ct + CT_OVF_QUEUE, 1ull);
+      // S_r(r) != 0 decided exactly in fp64 in both precision modes (reading A14); r^2 pre-filter
+      if (r2 < c_geo.srhi2_hi[p]) {
+        double rd = sqrt(r2);
+        double tP = (rd - c_tabd.sigma[p]) / (c_tabd.srhi[p] - c_tabd.sigma[p]);
+        if (tP < 1.0) {  // deferred b* batch: the whole pair is evaluated once by the canonical side
+          if (canon) {  // warp-aggregated append (one global atomic per converged lane set)
+            unsigned am = __activemask();
+            int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(Qu.count, __popc(am));
+            base = __shfl_sync(am, base, leader);
+            int k = base + __popc(am & ((1u << lane) - 1u));
+            if (k < Qu.cap) {
+              Qu.item[k] = make_int4(i, J, 0, 0);
+              Qu.M[k] = Md;
+            } else {
+              atomicAdd(ct + CT_OVF_QUEUE, 1ull);
+            }
           }
+          continue;
         }
-        continue;
       }
+      R rr2 = (R)r2;
+      R y = rsqrt_fast(rr2);
       R dVr;
-      R V = lj_plain<R>(R(4) * T.eps[p], T.sigma2[p], R(1) / (R)r2, dVr);
+      R V = lj_plain<R>(R(4) * T.eps[p], T.sigma2[p], y * y, dVr);
       if (r2 > c_geo.rlo2[p]) {  // taper S(r; r_lo, r_c) (reading A10)
-        R r = (R)rd, dsw;
+        R r = rr2 * y, dsw;
         R sv = sw<R>(r, T.rlo[p], T.rc[p], dsw);
-        dVr = dVr * sv + V * dsw / r;
+        dVr = dVr * sv + V * dsw * y;
         V = V * sv;
       }
       R C = R(1) - (R)Md;
@@ -206,33 +229,83 @@ __global__ void __launch_bounds__(32 * LJ_WARPS) k_lj(LJArgs A, ShortList<R> S, 
         if (VIRIAL)
           for (int c = 0; c < 6; ++c) W[c] += Wp[c];
       }
-      if (canon && stage.rows) {
-        double* rw = stage_row(stage, 7);
-        if (rw) {
-          char4 sh = shift[J];
-          rw[0] = gid[i], rw[1] = gid[J], rw[2] = sh.x, rw[3] = sh.y, rw[4] = sh.z, rw[5] = (double)C, rw[6] = 0.0;
-        }
-      }
-    }
-    if (lane == 0) {
-      atomicMax(ct + CT_MAXREACH, (unsigned long long)s.nins);
-      if (ovf) atomicAdd(ct + CT_OVF_REACH, 1ull);
+      if (canon && stage.rows) stage_lj_row(stage, gid[i], gid[J], shift[J], (double)C, 0.0);
     }
   }
 
-  // ------------------------------------------------------------ pure list: plain 12-6 LJ
-  {
-    const int cnt = A.cnt[1][i];
-    const int* row = A.nbr[1] + (size_t)i * A.cap[1];
-    for (int q = lane; q < cnt; q += 32) {
-      int J = row[q];
-      double4 pj = A.pos[J];
-      double dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
-      int p = ti + type_of(pj);
-      nlj += ki < key_of(pj);
-      R rx = (R)dx, ry = (R)dy, rz = (R)dz;
+  // 3. reductions (8-lane groups, then one atomic per atom / per warp)
+  fx = group_sum<NEAR_GROUP>(fx);
+  fy = group_sum<NEAR_GROUP>(fy);
+  fz = group_sum<NEAR_GROUP>(fz);
+  if (gl == 0 && cntN > 0) atomic_add3(F, i, fx, fy, fz);
+  red_add_d(rs, ACC_ELJ, 0.5 * en);
+  if (VIRIAL)
+    for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, W[c]);
+  red_add_u(rs, CT_LJ, nlj);
+  red_add_u(rs, CT_C0, nc0);
+  red_max_u(rs, CT_MAXREACH, gl == 0 ? (unsigned long long)s.nins : 0ull);
+  red_add_u(rs, CT_OVF_REACH, gl == 0 && ovf ? 1ull : 0ull);
+  red_add_u(rs, CT_LJENT, gl == 0 ? (unsigned long long)cntN : 0ull);
+  red_flush(rs, RR);
+}
+
+// ---------------------------------------------------------------------------------- far pairs
+constexpr int FAR_UNROLL = 4;
+
+template <typename R, bool VIRIAL, bool BAND>
+__device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, double4 pi, int ti, long long ki,
+                                         const int* gid, const char4* shift, StageBuf stage, double& fx, double& fy,
+                                         double& fz, double& en, double (&W)[6], unsigned long long& nlj) {
+  const Tab<R>& T = tab<R>();
+  const int lane = threadIdx.x & 31;
+  const int cnt = A.cnt[list][i];
+  const int* row = A.nbr[list] + (size_t)i * A.cap[list];
+  // t_i is warp-uniform, so a pair is one of two species pairs: hold both parameter sets in
+  // registers and select (no divergent constant-cache loads in the loop)
+  const R e4a = R(4) * T.eps[ti], e4b = R(4) * T.eps[ti + 1];
+  const R s2a = T.sigma2[ti], s2b = T.sigma2[ti + 1];
+  const R rloa = T.rlo[ti], rlob = T.rlo[ti + 1];
+  const R iva = T.inv_taper[ti], ivb = T.inv_taper[ti + 1];
+  const double rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
+  for (int base = 0; base < cnt; base += 32 * FAR_UNROLL) {
+    int J[FAR_UNROLL];
+    double4 pj[FAR_UNROLL];
+#pragma unroll
+    for (int u = 0; u < FAR_UNROLL; ++u) {
+      int q = base + u * 32 + lane;
+      J[u] = q < cnt ? row[q] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < FAR_UNROLL; ++u) pj[u] = A.pos[J[u] >= 0 ? J[u] : i];
+    // branch-free bodies: every lane evaluates, invalid / out-of-cutoff lanes are weighted by 0
+#pragma unroll
+    for (int u = 0; u < FAR_UNROLL; ++u) {
+      const bool valid = J[u] >= 0;
+      const bool hj = type_of(pj[u]) != 0;
+      double dx = __dsub_rn(pj[u].x, pi.x), dy = __dsub_rn(pj[u].y, pi.y), dz = __dsub_rn(pj[u].z, pi.z);
+      double r2 = r2_exact(dx, dy, dz);
+      // pure entries are inside r_lo <= r_c by construction; band entries: exact cutoff decision
+      bool in = valid && (!BAND || r2 <= (hj ? rcb : rca));
+      nlj += (in && ki < key_of(pj[u]));
+      R rr2 = in ? (R)r2 : R(1);
+      R y = rsqrt_fast(rr2);  // 1/r
       R dVr;
-      R V = lj_plain<R>(R(4) * T.eps[p], T.sigma2[p], R(1) / (rx * rx + ry * ry + rz * rz), dVr);
+      R V = lj_plain<R>(hj ? e4b : e4a, hj ? s2b : s2a, y * y, dVr);
+      if (BAND) {  // taper S(r; r_lo, r_c) (reading A10), branch-free
+        R r = rr2 * y;
+        R iv = hj ? ivb : iva;
+        R tt = (r - (hj ? rlob : rloa)) * iv;
+        R sv, ds;
+        halfcos_poly(tt < R(0) ? R(0) : tt, sv, ds);
+        sv = tt <= R(0) ? R(1) : sv;
+        ds = tt <= R(0) ? R(0) : ds * iv;
+        dVr = dVr * sv + V * ds * y;
+        V = V * sv;
+      }
+      R wgt = in ? R(1) : R(0);
+      dVr *= wgt;
+      V *= wgt;
+      R rx = (R)dx, ry = (R)dy, rz = (R)dz;
       fx += (double)(dVr * rx);
       fy += (double)(dVr * ry);
       fz += (double)(dVr * rz);
@@ -241,69 +314,43 @@ __global__ void __launch_bounds__(32 * LJ_WARPS) k_lj(LJArgs A, ShortList<R> S, 
         V3<R> dd = mk3<R>(rx, ry, rz);
         vir_add(W, dd, (R(0.5) * dVr) * dd);
       }
-      if (stage.rows && ki < key_of(pj)) {
-        double* rw = stage_row(stage, 7);
-        if (rw) {
-          char4 sh = shift[J];
-          rw[0] = gid[i], rw[1] = gid[J], rw[2] = sh.x, rw[3] = sh.y, rw[4] = sh.z, rw[5] = 1.0, rw[6] = 0.0;
-        }
-      }
+      if (stage.rows && in && ki < key_of(pj[u])) stage_lj_row(stage, gid[i], gid[J[u]], shift[J[u]], 1.0, 0.0);
     }
   }
+}
 
-  // ------------------------------------------------------------ band list: cutoff + taper
-  {
-    const int cnt = A.cnt[2][i];
-    const int* row = A.nbr[2] + (size_t)i * A.cap[2];
-    for (int q = lane; q < cnt; q += 32) {
-      int J = row[q];
-      double4 pj = A.pos[J];
-      double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
-      double r2 = r2_exact(dx, dy, dz);
-      int p = ti + type_of(pj);
-      if (r2 > c_geo.rc2[p]) continue;
-      bool canon = ki < key_of(pj);
-      nlj += canon;
-      R dVr;
-      R V = lj_plain<R>(R(4) * T.eps[p], T.sigma2[p], R(1) / (R)r2, dVr);
-      if (r2 > c_geo.rlo2[p]) {
-        R r = (R)sqrt(r2), dsw;
-        R sv = sw<R>(r, T.rlo[p], T.rc[p], dsw);
-        dVr = dVr * sv + V * dsw / r;
-        V = V * sv;
-      }
-      fx += (double)(dVr * (R)dx);
-      fy += (double)(dVr * (R)dy);
-      fz += (double)(dVr * (R)dz);
-      en += (double)V;
-      if (VIRIAL) {
-        V3<R> dd = mk3<R>((R)dx, (R)dy, (R)dz);
-        vir_add(W, dd, (R(0.5) * dVr) * dd);
-      }
-      if (canon && stage.rows) {
-        double* rw = stage_row(stage, 7);
-        if (rw) {
-          char4 sh = shift[J];
-          rw[0] = gid[i], rw[1] = gid[J], rw[2] = sh.x, rw[3] = sh.y, rw[4] = sh.z, rw[5] = 1.0, rw[6] = 0.0;
-        }
-      }
-    }
+template <typename R, bool VIRIAL>
+__global__ void __launch_bounds__(128) k_lj_far(LJArgs A, const int* gid, const char4* shift, double* F, double* acc,
+                                               unsigned long long* ct, StageBuf stage, RedRows RR) {
+  __shared__ RedSmem rs;
+  red_init(rs);
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  double en = 0;
+  double W[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long nlj = 0, ne = 0;
+  // grid-stride over atoms: a resident grid, one warp per atom at a time
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < A.N; i += nwarps) {
+    const double4 pi = A.pos[i];
+    const int ti = type_of(pi);
+    const long long ki = key_of(pi);
+    double fx = 0, fy = 0, fz = 0;
+    far_list<R, VIRIAL, false>(A, 1, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
+    far_list<R, VIRIAL, true>(A, 2, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
+    fx = warp_sum(fx);
+    fy = warp_sum(fy);
+    fz = warp_sum(fz);
+    if (lane == 0) atomic_add3(F, i, fx, fy, fz);
+    if (lane == 0) ne += (unsigned long long)(A.cnt[1][i] + A.cnt[2][i]);
   }
-
-  // ------------------------------------------------------------ reductions
-  fx = warp_sum(fx);
-  fy = warp_sum(fy);
-  fz = warp_sum(fz);
-  if (lane == 0) atomic_add3(F, i, fx, fy, fz);
-  double e1[1] = {0.5 * en};
-  warp_acc(e1, acc + ACC_ELJ);
-  if (VIRIAL) warp_acc(W, acc + ACC_W);
-  unsigned long long s1 = warp_sum_u(nlj), s2 = warp_sum_u(nc0);
-  if (lane == 0) {
-    if (s1) atomicAdd(ct + CT_LJ, s1);
-    if (s2) atomicAdd(ct + CT_C0, s2);
-    atomicAdd(ct + CT_LJENT, (unsigned long long)(A.cnt[0][i] + A.cnt[1][i] + A.cnt[2][i]));
-  }
+  red_add_d(rs, ACC_ELJ, 0.5 * en);
+  if (VIRIAL)
+    for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, W[c]);
+  red_add_u(rs, CT_LJ, nlj);
+  red_add_u(rs, CT_LJFAR, nlj);
+  red_add_u(rs, CT_LJENT, ne);
+  red_add_u(rs, CT_LJENTFAR, ne);
+  red_flush(rs, RR);
 }
 
 }  // namespace ab

@@ -5,6 +5,22 @@
 
 namespace ab {
 
+// block-wide max of non-negative doubles, one atomic per block (bit-pattern order == value order)
+__device__ __forceinline__ void block_max_atomic(double v, unsigned long long* out) {
+  __shared__ double sm[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? sm[l] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (l == 0 && v > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(v));
+  }
+}
+
 // v += dt/2 F/m ftm2v;  x += dt v;  max |x - x_ref|^2 since the last list build
 __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, double dtf0, double dtf1, double dt,
                              const double4* xref, unsigned long long* maxd2) {
@@ -23,9 +39,7 @@ __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, do
     double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
     d2 = dx * dx + dy * dy + dz * dz;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
-  if ((threadIdx.x & 31) == 0 && d2 > 0.0) atomicMax(maxd2, (unsigned long long)__double_as_longlong(d2));
+  block_max_atomic(d2, maxd2);
 }
 
 __global__ void k_integrate2(int N, const double4* pos, double* v, const double* F, double dtf0, double dtf1) {
@@ -45,9 +59,7 @@ __global__ void k_maxdisp(int N, const double4* pos, const double4* xref, unsign
     double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
     d2 = dx * dx + dy * dy + dz * dz;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) d2 = fmax(d2, __shfl_xor_sync(0xffffffffu, d2, o));
-  if ((threadIdx.x & 31) == 0 && d2 > 0.0) atomicMax(maxd2, (unsigned long long)__double_as_longlong(d2));
+  block_max_atomic(d2, maxd2);
 }
 
 // sum m v^2 / 2 (mvv2e applied on the host)
