@@ -84,6 +84,7 @@ struct ab_engine {
   DBuf<unsigned char> s_dr, s_w, s_N;  // typed by precision at use
   DBuf<int2> bonds;
   DBuf<int4> q_item;
+  DBuf<int> ovf_bond, ovf_q;  // overflow (large side / full b*) index lists
   DBuf<double> q_M;
   DBuf<int> small_i;                 // [0] nbonds [1] qcount [2] maxLJ [3] maxI [4..5] stage counts
   DBuf<double> acc;                  // ACC_N
@@ -473,8 +474,11 @@ ab_status forces_impl(ab_engine* e) {
     ShortList<R> S = short_view<R>(e);
     // grids and the per-block partial rows of the energy / virial / counter reduction
     const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
-    const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4;
-    const int nrows = g_short + g_rebo + g_near + g_far + g_bstar;
+    const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4, g_slow = e->nsm;
+    const int nrows = g_short + g_rebo + g_near + g_far + g_bstar + 2 * g_slow;
+    CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
+    CK(e->ovf_q.ensure(e->capQ));
+    CK(cudaMemsetAsync(e->small_i.p + 8, 0, 2 * sizeof(int), st));
     CK(e->red_d.ensure((size_t)ACC_N * nrows));
     CK(e->red_u.ensure((size_t)CT_N * nrows));
     RedRows RR{e->red_d.p, e->red_u.p, nrows, 0};
@@ -485,11 +489,15 @@ ab_status forces_impl(ab_engine* e) {
     prof_end(e);
     RR.row0 += g_short;
     prof_begin(e, 1);
-    k_rebo<R><<<g_rebo, 128, 0, st>>>(e->bonds.p, e->small_i.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p,
-                                      e->F.p, e->acc.p, e->ct.p, sb0, RR);
+    k_rebo<R, NB_FAST><<<g_rebo, 128, 0, st>>>(e->bonds.p, e->small_i.p, nullptr, e->ovf_bond.p, e->small_i.p + 8,
+                                               S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb0, RR);
     CKL();
-    prof_end(e);
     RR.row0 += g_rebo;
+    k_rebo<R, NBMAX><<<g_slow, 128, 0, st>>>(e->bonds.p, e->small_i.p, e->ovf_bond.p, nullptr, e->small_i.p + 8, S,
+                                             e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb0, RR);
+    CKL();
+    RR.row0 += g_slow;
+    prof_end(e);
     BstarQueue Qu{e->q_item.p, e->q_M.p, e->small_i.p + 1, e->capQ};
     LJArgs A;
     A.N = N;
@@ -514,8 +522,12 @@ ab_status forces_impl(ab_engine* e) {
     prof_end(e);
     RR.row0 += g_far;
     prof_begin(e, 3);
-    k_bstar<R><<<g_bstar, 128, 0, st>>>(Qu, e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                        e->acc.p, e->ct.p, sb1, RR);
+    k_bstar<R, NB_FAST, false><<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->pos.p, S,
+                                                        e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+    CKL();
+    RR.row0 += g_bstar;
+    k_bstar<R, NBMAX, true><<<g_slow, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, e->pos.p, S, e->typ.p,
+                                                    e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
     CKL();
     prof_end(e);
     RR.row0 = 0;
@@ -626,7 +638,7 @@ ab_status ab_create(const char* text, size_t len, ab_precision prec, int device,
   fill_tab(e->hp, tf);
   bool ok = cudaMemcpyToSymbol(c_tabd, &td, sizeof(td)) == cudaSuccess &&
             cudaMemcpyToSymbol(c_tabf, &tf, sizeof(tf)) == cudaSuccess && e->acc.ensure(ACC_N) == cudaSuccess &&
-            e->ct.ensure(CT_N + 1) == cudaSuccess && e->small_i.ensure(8) == cudaSuccess &&
+            e->ct.ensure(CT_N + 1) == cudaSuccess && e->small_i.ensure(16) == cudaSuccess &&
             cudaMallocHost(&e->h_ct, sizeof(unsigned long long) * (CT_N + 1)) == cudaSuccess &&
             cudaMallocHost(&e->h_acc, sizeof(double) * ACC_N) == cudaSuccess &&
             cudaMallocHost(&e->h_small, sizeof(int) * 8) == cudaSuccess;
@@ -650,7 +662,7 @@ void ab_destroy(ab_engine* e) {
   DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->key2, &e->val, &e->val2, &e->cell_start,
                      &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
                      &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr,
-                     &e->small_i};
+                     &e->small_i, &e->ovf_bond, &e->ovf_q};
   for (auto* b : bi) b->release();
   e->shift.release();
   e->typ.release();

@@ -12,20 +12,33 @@
 // are scattered as forces with fp64 atomics (force on b -= g, on a += g for v = x_b - x_a) and
 // folded into the virial W -= v (x) g.
 // GPU mapping: one thread per REBO half bond / per queued b* pair (interaction-wise).
+// Register residency: a side (neighbours of i or of j, partner excluded) is held in fully
+// unrolled fixed-size arrays of NB = NB_FAST = 4 entries; bonds with a larger side are appended
+// to an overflow list processed by an NB = NBMAX instantiation (rolled loops).  The b* batch is
+// split the same way: the fast kernel does the forward pass only (S_b on a plateau, C = 0 or 1)
+// and defers transition / fractional-C / large-side pairs to the full kernel.
 #pragma once
 #include "dev_common.cuh"
 #include "k_lists.cuh"
 
 namespace ab {
 
-template <typename R>
+constexpr int NB_FAST = 4;
+
+template <int NB>
+struct Unr {
+  static constexpr int v = NB <= NB_FAST ? NB : 1;
+};
+
+template <typename R, int NB>
 struct BoState {
   int i, J, ti, tj;
   V3<R> d, u;  // the bond vector used for angles (d_ij or rho d_hat) and its unit vector
   R r;
   int nI, nJ;
-  unsigned char sk[NBMAX], sl[NBMAX];  // slots in S of i's / J's neighbours (partner excluded)
-  R cl[NBMAX], Gl[NBMAX], dGl[NBMAX];
+  int pq, pl;     // slot of the partner in N(i) / of i in N(J), -1 if absent
+  bool overflow;  // a side has more than NB neighbours: use the NB = NBMAX instantiation
+  R cl[NB], Gl[NB], dGl[NB];
   R Si, Sj, PxI, PyI, PxJ, PyJ;
   R pij, pji, Nij, Nji, Nconj;
   R Rv, Rx, Ry, Rz, Tv, Tx, Ty, Tz;  // derivatives w.r.t. (N_ij, N_ji, N^conj)
@@ -33,6 +46,11 @@ struct BoState {
   int nquads;
   bool bad;
 };
+
+// slot in the short list of the a-th side neighbour (the partner's slot is skipped)
+__device__ __forceinline__ int side_slot(int a, int partner_slot) {
+  return (partner_slot >= 0 && a >= partner_slot) ? a + 1 : a;
+}
 
 template <typename R>
 __device__ __forceinline__ R clamp_cos(R c) {
@@ -65,24 +83,33 @@ __device__ __forceinline__ R F_conj(R x, R& dF) {
 }
 
 // ---------------------------------------------------------------- forward pass
-template <typename R, bool TORS>
-__device__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i, int J, V3<R> d, R r,
-                           BoState<R>& st) {
+template <typename R, bool TORS, int NB>
+__device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i, int J, V3<R> d, R r,
+                           BoState<R, NB>& st) {
   const Tab<R>& T = tab<R>();
   st.i = i, st.J = J, st.ti = typ[i], st.tj = typ[J], st.d = d, st.r = r;
   const int ti = st.ti, tj = st.tj;
+  const size_t bi = (size_t)i * S.capS, bj = (size_t)J * S.capS;
+  const int ni = S.cnt[i], nj = S.cnt[J];
+  int pq = -1, pl = -1;
+  for (int q = 0; q < ni; ++q)
+    if (S.nbr[bi + q] == J) pq = q;
+  for (int q = 0; q < nj; ++q)
+    if (S.nbr[bj + q] == i) pl = q;
+  const int nI = ni - (pq >= 0), nJ = nj - (pl >= 0);
+  st.pq = pq, st.pl = pl, st.nI = nI, st.nJ = nJ;
+  st.overflow = nI > NB || nJ > NB;
+  st.bad = false;
+  if (st.overflow) return;
   R ir = R(1) / r;
   st.u = ir * d;
-  st.bad = false;
   // ---- i side: k in N(i) \ {J}
   R sumI = 0, NCi = 0, NHi = 0, Si = 0;
-  int nI = 0;
-  size_t bi = (size_t)i * S.capS;
-  int ni = S.cnt[i];
-  for (int q = 0; q < ni; ++q) {
+#pragma unroll(Unr<NB>::v)
+  for (int a = 0; a < NB; ++a) {
+    if (a >= nI) continue;
+    int q = side_slot(a, pq);
     int k = S.nbr[bi + q];
-    if (k == J) continue;
-    st.sk[nI++] = (unsigned char)q;
     R rk;
     V3<R> dk = sl_d(S, i, q, rk);
     R wk = S.w[bi + q].x;
@@ -99,23 +126,21 @@ __device__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i,
       NHi += wk;
     }
   }
-  st.nI = nI;
   // ---- J side: l in N(J) \ {i}
   R sumJ = 0, NCj = 0, NHj = 0, Sj = 0;
-  int nJ = 0;
-  size_t bj = (size_t)J * S.capS;
-  int nj = S.cnt[J];
-  V3<R> md = mk3(-d.x, -d.y, -d.z);
-  for (int q = 0; q < nj; ++q) {
+  const V3<R> md = mk3(-d.x, -d.y, -d.z);
+#pragma unroll(Unr<NB>::v)
+  for (int c = 0; c < NB; ++c) {
+    if (c >= nJ) continue;
+    int q = side_slot(c, pl);
     int l = S.nbr[bj + q];
-    if (l == i) continue;
     R rl;
     V3<R> dl = sl_d(S, J, q, rl);
     R wl = S.w[bj + q].x;
     int tl = typ[l];
-    R c = clamp_cos(dot3(md, dl) * ir / rl);
+    R cc = clamp_cos(dot3(md, dl) * ir / rl);
     R dg;
-    R g = gspline<R>(tj, c, dg);
+    R g = gspline<R>(tj, cc, dg);
     sumJ += wl * g * T.explam[ti][tj][tl];
     if (tl == 0) {
       NCj += wl;
@@ -124,14 +149,11 @@ __device__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i,
     } else {
       NHj += wl;
     }
-    st.sl[nJ] = (unsigned char)q;
-    st.cl[nJ] = c;
+    st.cl[c] = cc;
     R dG;
-    st.Gl[nJ] = guardG<R>(c, dG);
-    st.dGl[nJ] = dG;
-    ++nJ;
+    st.Gl[c] = guardG<R>(cc, dG);
+    st.dGl[c] = dG;
   }
-  st.nJ = nJ;
   R PI = 0, PJ = 0;
   st.PxI = st.PyI = st.PxJ = st.PyJ = 0;
   if (ti == 0) PI = pspline<R>(tj, NCi, NHi, st.PxI, st.PyI);
@@ -155,8 +177,10 @@ __device__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i,
   // ---- dihedral sum (and torsion sum): k in N(i)\J, l in N(J)\{i, k}
   R D = 0, Ts = 0;
   int nq = 0;
-  for (int a = 0; a < nI; ++a) {
-    int q = st.sk[a];
+#pragma unroll(Unr<NB>::v)
+  for (int a = 0; a < NB; ++a) {
+    if (a >= nI) continue;
+    int q = side_slot(a, pq);
     int k = S.nbr[bi + q];
     R rk;
     V3<R> dk = sl_d(S, i, q, rk);
@@ -166,8 +190,10 @@ __device__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i,
     R Gk = guardG<R>(ck, dGk);
     V3<R> n1 = cross3(dk, d);
     R n1s = dot3(n1, n1);
-    for (int c = 0; c < nJ; ++c) {
-      int ql = st.sl[c];
+#pragma unroll(Unr<NB>::v)
+    for (int c = 0; c < NB; ++c) {
+      if (c >= nJ) continue;
+      int ql = side_slot(c, pl);
       int l = S.nbr[bj + ql];
       if (l == k) continue;
       ++nq;
@@ -190,8 +216,8 @@ __device__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i,
   st.nquads = nq;
 }
 
-template <typename R>
-__device__ __forceinline__ R bo_value(const BoState<R>& st) {
+template <typename R, int NB>
+__device__ __forceinline__ R bo_value(const BoState<R, NB>& st) {
   return R(0.5) * (st.pij + st.pji) + st.Rv + st.Tv * st.D;
 }
 
@@ -202,15 +228,34 @@ __device__ __forceinline__ void scatter_vec(double* F, const int* owner, int a_t
   atomic_add3(F, owner[a_from], (double)g.x, (double)g.y, (double)g.z);
 }
 
+// N^conj chain: N_c = sum_m w_cm (m != excluded) -> forces on every m with dw != 0
+template <typename R>
+__device__ __forceinline__ void conj_chain(const ShortList<R>& S, const int* owner, int c, int excl, R chain,
+                                           double* F, double W[6]) {
+  size_t bc = (size_t)c * S.capS;
+  int nc = S.cnt[c];
+  for (int q2 = 0; q2 < nc; ++q2) {
+    int m = S.nbr[bc + q2];
+    if (m == excl) continue;
+    R dw = S.w[bc + q2].y;
+    if (dw == R(0)) continue;
+    R rcm;
+    V3<R> dcm = sl_d(S, c, q2, rcm);
+    V3<R> g = (chain * dw / rcm) * dcm;
+    scatter_vec(F, owner, m, c, g);
+    vir_add(W, dcm, g);
+  }
+}
+
 // ---------------------------------------------------------------- reverse pass
 // cb = dE/db.  wij: weight of the bond for the merged torsion term (TORS only).
 // Output gd = dE/d(d) through the bond-order (and torsion) terms; fi / fj = force contributions
-// on i / J from the k and l vectors (already scattered onto k, l, m, n).
-template <typename R, bool TORS>
-__device__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const int* owner, const BoState<R>& st,
+// on i / J from the k and l vectors (the forces on k, l, m, n are scattered here).
+template <typename R, bool TORS, int NB>
+__device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const int* owner, const BoState<R, NB>& st,
                            R cb, R wij, double* F, double W[6], V3<R>& gd, V3<R>& fi, V3<R>& fj) {
   const Tab<R>& T = tab<R>();
-  const int i = st.i, J = st.J, ti = st.ti, tj = st.tj;
+  const int i = st.i, J = st.J, ti = st.ti, tj = st.tj, nI = st.nI, nJ = st.nJ;
   const V3<R> d = st.d, u = st.u;
   const V3<R> md = mk3(-d.x, -d.y, -d.z);
   const R r = st.r, ir = R(1) / r;
@@ -220,14 +265,16 @@ __device__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const 
   const R dNji = cb * (st.Ry + st.Ty * st.D);
   const R dNc = cb * (st.Rz + st.Tz * st.D);
   const R cD = cb * st.Tv;
-  size_t bi = (size_t)i * S.capS, bj = (size_t)J * S.capS;
+  const size_t bi = (size_t)i * S.capS, bj = (size_t)J * S.capS;
   gd = mk3<R>(0, 0, 0);
   fi = mk3<R>(0, 0, 0);
   fj = mk3<R>(0, 0, 0);
-  R Wl[NBMAX], Cl[NBMAX];
-  V3<R> gl[NBMAX];
-  for (int c = 0; c < st.nJ; ++c) {
-    int q = st.sl[c];
+  R Wl[NB], Cl[NB];
+  V3<R> gl[NB];
+#pragma unroll(Unr<NB>::v)
+  for (int c = 0; c < NB; ++c) {
+    if (c >= nJ) continue;
+    int q = side_slot(c, st.pl);
     int l = S.nbr[bj + q];
     int tl = typ[l];
     R wl = S.w[bj + q].x;
@@ -244,8 +291,10 @@ __device__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const 
     Cl[c] = cJ * wl * dg * el;
     gl[c] = mk3<R>(0, 0, 0);
   }
-  for (int a = 0; a < st.nI; ++a) {
-    int q = st.sk[a];
+#pragma unroll(Unr<NB>::v)
+  for (int a = 0; a < NB; ++a) {
+    if (a >= nI) continue;
+    int q = side_slot(a, st.pq);
     int k = S.nbr[bi + q];
     int tk = typ[k];
     R rk;
@@ -272,8 +321,10 @@ __device__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const 
     if (Gk != R(0)) {
       V3<R> n1 = cross3(dk, d);
       R inv1 = rsq(dot3(n1, n1));
-      for (int c = 0; c < st.nJ; ++c) {
-        int ql = st.sl[c];
+#pragma unroll(Unr<NB>::v)
+      for (int c = 0; c < NB; ++c) {
+        if (c >= nJ) continue;
+        int ql = side_slot(c, st.pl);
         int l = S.nbr[bj + ql];
         if (l == k || st.Gl[c] == R(0)) continue;
         R rl;
@@ -315,25 +366,12 @@ __device__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const 
     atomic_add3(F, owner[k], -(double)gk.x, -(double)gk.y, -(double)gk.z);
     addto(fi, gk);
     vir_add(W, dk, gk);
-    // N^conj chain through N_k = sum_m w_km (m != i)
-    if (chain != R(0)) {
-      size_t bk = (size_t)k * S.capS;
-      int nk = S.cnt[k];
-      for (int q2 = 0; q2 < nk; ++q2) {
-        int m = S.nbr[bk + q2];
-        if (m == i) continue;
-        R dw = S.w[bk + q2].y;
-        if (dw == R(0)) continue;
-        R rkm;
-        V3<R> dkm = sl_d(S, k, q2, rkm);
-        V3<R> g = (chain * dw / rkm) * dkm;
-        scatter_vec(F, owner, m, k, g);
-        vir_add(W, dkm, g);
-      }
-    }
+    if (chain != R(0)) conj_chain(S, owner, k, i, chain, F, W);
   }
-  for (int c = 0; c < st.nJ; ++c) {
-    int q = st.sl[c];
+#pragma unroll(Unr<NB>::v)
+  for (int c = 0; c < NB; ++c) {
+    if (c >= nJ) continue;
+    int q = side_slot(c, st.pl);
     int l = S.nbr[bj + q];
     int tl = typ[l];
     R rl;
@@ -353,21 +391,7 @@ __device__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const 
       R dF;
       F_conj<R>(S.Ntot[l] - wl, dF);
       R chain = dNc * R(2) * st.Sj * wl * dF;
-      if (chain != R(0)) {
-        size_t bl = (size_t)l * S.capS;
-        int nl = S.cnt[l];
-        for (int q2 = 0; q2 < nl; ++q2) {
-          int n = S.nbr[bl + q2];
-          if (n == J) continue;
-          R dw = S.w[bl + q2].y;
-          if (dw == R(0)) continue;
-          R rln;
-          V3<R> dln = sl_d(S, l, q2, rln);
-          V3<R> gg = (chain * dw / rln) * dln;
-          scatter_vec(F, owner, n, l, gg);
-          vir_add(W, dln, gg);
-        }
-      }
+      if (chain != R(0)) conj_chain(S, owner, l, J, chain, F, W);
     }
   }
 }
@@ -384,71 +408,86 @@ __device__ __forceinline__ double* stage_row(StageBuf sb, int width) {
   return sb.rows + (size_t)k * width;
 }
 
+// warp-aggregated append of v to list (count at *cnt); lanes outside `take` do nothing
+__device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v) {
+  unsigned am = __activemask();
+  int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(cnt, __popc(am));
+  base = __shfl_sync(am, base, leader);
+  int k = base + __popc(am & ((1u << lane) - 1u));
+  if (k < cap) list[k] = v;
+}
+
 // ---------------------------------------------------------------- REBO + torsion, one thread per bond
-template <typename R>
-__global__ void __launch_bounds__(128) k_rebo(const int2* bonds, const int* nbonds, ShortList<R> S,
-                                              const signed char* typ, const int* owner, const int* gid,
-                                              const char4* shift, double* F, double* acc, unsigned long long* ct,
+// list = (i, slot) pairs; NB = NB_FAST: bonds with a larger side are appended to ovf (indices into
+// list) for the NB = NBMAX instantiation, which runs over ovf (list_idx != nullptr).
+template <typename R, int NB>
+__global__ void __launch_bounds__(128) k_rebo(const int2* bonds, const int* nbonds, const int* list_idx,
+                                              int* ovf, int* novf, ShortList<R> S, const signed char* typ,
+                                              const int* owner, const int* gid, const char4* shift, double* F,
                                               StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
   red_init(rs);
   const Tab<R>& T = tab<R>();
-  int nb = *nbonds;
+  const int nb = list_idx ? *novf : *nbonds;
   double e[3 + 6] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long nq = 0, nbad = 0, ncount = 0, nang = 0;
   int stride = gridDim.x * blockDim.x;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t - (int)threadIdx.x < nb; t += stride) {
-    if (t < nb) {
-      int2 bd = bonds[t];
-      int i = bd.x, q = bd.y;
-      size_t e0 = (size_t)i * S.capS + q;
-      int J = S.nbr[e0];
-      R r;
-      V3<R> d = sl_d(S, i, q, r);
-      R w = S.w[e0].x, dw = S.w[e0].y;
-      int ti = typ[i], tj = typ[J], p = ti + tj;
-      // pair terms f_R = w (1 + Q/r) A e^{-alpha r},  f_A = -w sum_n B_n e^{-beta_n r}
-      R ir = R(1) / r;
-      R ea = ex(-T.alpha[p] * r);
-      R qr = R(1) + T.Q[p] * ir;
-      R VR = w * qr * T.A[p] * ea;
-      R dVR = dw * qr * T.A[p] * ea + w * T.A[p] * ea * (-T.Q[p] * ir * ir - T.alpha[p] * qr);
-      R sb = 0, sbb = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += stride) {
+    int bidx = list_idx ? list_idx[t] : t;
+    int2 bd = bonds[bidx];
+    int i = bd.x, q = bd.y;
+    size_t e0 = (size_t)i * S.capS + q;
+    int J = S.nbr[e0];
+    R r;
+    V3<R> d = sl_d(S, i, q, r);
+    BoState<R, NB> st;
+    bo_forward<R, true, NB>(S, typ, i, J, d, r, st);
+    if (st.overflow) {  // only possible for NB = NB_FAST
+      list_append(ovf, novf, 1 << 30, bidx);
+      continue;
+    }
+    R w = S.w[e0].x, dw = S.w[e0].y;
+    int ti = typ[i], tj = typ[J], p = ti + tj;
+    // pair terms f_R = w (1 + Q/r) A e^{-alpha r},  f_A = -w sum_n B_n e^{-beta_n r}
+    R ir = R(1) / r;
+    R ea = ex(-T.alpha[p] * r);
+    R qr = R(1) + T.Q[p] * ir;
+    R VR = w * qr * T.A[p] * ea;
+    R dVR = dw * qr * T.A[p] * ea + w * T.A[p] * ea * (-T.Q[p] * ir * ir - T.alpha[p] * qr);
+    R sb = 0, sbb = 0;
 #pragma unroll
-      for (int n = 0; n < 3; ++n) {
-        R eb = T.B[p][n] * ex(-T.beta[p][n] * r);
-        sb += eb;
-        sbb += T.beta[p][n] * eb;
-      }
-      R VA = -w * sb;
-      R dVA = -dw * sb + w * sbb;
-      BoState<R> st;
-      bo_forward<R, true>(S, typ, i, J, d, r, st);
-      R b = bo_value(st);
-      V3<R> gd, fi, fj;
-      bo_reverse<R, true>(S, typ, owner, st, VA, w, F, e + 3, gd, fi, fj);
-      R dEdr = dVR + b * dVA + dw * st.Tsum;
-      addto(gd, (dEdr * ir) * d);
-      atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
-      atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
-      vir_add(e + 3, d, gd);
-      e[0] += (double)(VR + b * VA);
-      e[1] += (double)(w * st.Tsum);
-      nq += st.nquads;
-      nbad += st.bad;
-      ncount += 1;
-      nang += st.nI + st.nJ;
-      if (stage.rows) {
-        double* row = stage_row(stage, 13);
-        if (row) {
-          char4 s = shift[J];
-          row[0] = gid[i], row[1] = gid[J], row[2] = s.x, row[3] = s.y, row[4] = s.z;
-          row[5] = b, row[6] = st.pij, row[7] = st.pji, row[8] = st.Rv, row[9] = st.Tv * st.D;
-          row[10] = st.Nij, row[11] = st.Nji, row[12] = st.Nconj;
-        }
+    for (int n = 0; n < 3; ++n) {
+      R eb = T.B[p][n] * ex(-T.beta[p][n] * r);
+      sb += eb;
+      sbb += T.beta[p][n] * eb;
+    }
+    R VA = -w * sb;
+    R dVA = -dw * sb + w * sbb;
+    R b = bo_value(st);
+    V3<R> gd, fi, fj;
+    bo_reverse<R, true, NB>(S, typ, owner, st, VA, w, F, e + 3, gd, fi, fj);
+    R dEdr = dVR + b * dVA + dw * st.Tsum;
+    addto(gd, (dEdr * ir) * d);
+    atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
+    atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
+    vir_add(e + 3, d, gd);
+    e[0] += (double)(VR + b * VA);
+    e[1] += (double)(w * st.Tsum);
+    nq += st.nquads;
+    nbad += st.bad;
+    ncount += 1;
+    nang += st.nI + st.nJ;
+    if (stage.rows) {
+      double* row = stage_row(stage, 13);
+      if (row) {
+        char4 s = shift[J];
+        row[0] = gid[i], row[1] = gid[J], row[2] = s.x, row[3] = s.y, row[4] = s.z;
+        row[5] = b, row[6] = st.pij, row[7] = st.pji, row[8] = st.Rv, row[9] = st.Tv * st.D;
+        row[10] = st.Nij, row[11] = st.Nji, row[12] = st.Nconj;
       }
     }
-    // keep the warp converged for the reductions below
   }
   red_add_d(rs, ACC_EREBO, e[0]);
   red_add_d(rs, ACC_ETORS, e[1]);
@@ -571,51 +610,66 @@ struct BstarQueue {
 
 // ---------------------------------------------------------------- deferred b* batch
 // E = (S_r S_b(b*) + 1 - S_r) C V for every canonical LJ pair with C != 0 and S_r != 0.
-template <typename R>
-__global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const double4* pos, ShortList<R> S,
-                                               const signed char* typ, const int* owner, const int* gid,
-                                               const char4* shift, double* F, double* acc,
-                                               unsigned long long* ct, StageBuf stage, RedRows RR) {
+// FULL = false: NB_FAST, forward pass only; a pair whose S_b is in its transition (dS_b != 0),
+// whose C is fractional (0 < M) or whose side is too large is deferred to ovf for FULL = true.
+template <typename R, int NB, bool FULL>
+__global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf,
+                                               const double4* pos, ShortList<R> S, const signed char* typ,
+                                               const int* owner, const int* gid, const char4* shift, double* F,
+                                               StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
   red_init(rs);
   const Tab<R>& T = tab<R>();
-  int nq = min(*Qu.count, Qu.cap);
+  const int nq = FULL ? *novf : min(*Qu.count, Qu.cap);
   double e[1 + 6] = {0, 0, 0, 0, 0, 0, 0};
   unsigned long long ntr = 0, nb = 0, nbad = 0;
   int stride = gridDim.x * blockDim.x;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t - (int)threadIdx.x < nq; t += stride) {
-    if (t < nq) {
-      int4 it = Qu.item[t];
-      int i = it.x, J = it.y;
-      double Md = Qu.M[t];
-      double4 pi = pos[i], pj = pos[J];
-      double dxd = pj.x - pi.x, dyd = pj.y - pi.y, dzd = pj.z - pi.z;
-      double r2d = r2_exact(dxd, dyd, dzd);
-      double rd = sqrt(r2d);
-      int ti = typ[i], tj = typ[J], p = ti + tj;
-      V3<R> d = mk3<R>((R)dxd, (R)dyd, (R)dzd);
-      R r = (R)rd, ir = R(1) / r;
-      R dP;
-      R P = sw<R>(r, T.sigma[p], T.srhi[p], dP);
-      R dVr;
-      R V = lj_v<R>(p, (R)r2d, r2d, dVr);
-      R M = (R)Md, C = R(1) - M;
-      R rho = T.rho[p];
-      V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
-      BoState<R> st;
-      bo_forward<R, false>(S, typ, i, J, ds, rho, st);
-      R bs = bo_value(st);
-      R dB;
-      R B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
-      R tb = (bs - T.bmin[p]) / (T.bmax[p] - T.bmin[p]);
-      if (tb > R(0) && tb < R(1)) ++ntr;
-      R Q = P * B + R(1) - P;
-      R E = Q * C * V;
-      V3<R> gd = ((C * (Q * dVr + V * (B - R(1)) * dP * ir))) * d;
-      V3<R> fi = mk3<R>(0, 0, 0), fj = mk3<R>(0, 0, 0);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += stride) {
+    int qi = FULL ? list_idx[t] : t;
+    int4 it = Qu.item[qi];
+    int i = it.x, J = it.y;
+    double Md = Qu.M[qi];
+    if (!FULL && Md > 0.0) {  // fractional C_ij: forces along the path -> full kernel
+      list_append(ovf, novf, 1 << 30, qi);
+      continue;
+    }
+    double4 pi = pos[i], pj = pos[J];
+    double dxd = pj.x - pi.x, dyd = pj.y - pi.y, dzd = pj.z - pi.z;
+    double r2d = r2_exact(dxd, dyd, dzd);
+    double rd = sqrt(r2d);
+    int ti = typ[i], tj = typ[J], p = ti + tj;
+    V3<R> d = mk3<R>((R)dxd, (R)dyd, (R)dzd);
+    R r = (R)rd, ir = R(1) / r;
+    R rho = T.rho[p];
+    V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
+    BoState<R, NB> st;
+    bo_forward<R, false, NB>(S, typ, i, J, ds, rho, st);
+    if (!FULL && st.overflow) {
+      list_append(ovf, novf, 1 << 30, qi);
+      continue;
+    }
+    R bs = bo_value(st);
+    R dB;
+    R B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
+    if (!FULL && dB != R(0)) {  // S_b transition: the reverse pass of b* is needed
+      list_append(ovf, novf, 1 << 30, qi);
+      continue;
+    }
+    R dP;
+    R P = sw<R>(r, T.sigma[p], T.srhi[p], dP);
+    R dVr;
+    R V = lj_v<R>(p, (R)r2d, r2d, dVr);
+    R M = (R)Md, C = R(1) - M;
+    R tb = (bs - T.bmin[p]) / (T.bmax[p] - T.bmin[p]);
+    if (tb > R(0) && tb < R(1)) ++ntr;
+    R Q = P * B + R(1) - P;
+    R E = Q * C * V;
+    V3<R> gd = ((C * (Q * dVr + V * (B - R(1)) * dP * ir))) * d;
+    V3<R> fi = mk3<R>(0, 0, 0), fj = mk3<R>(0, 0, 0);
+    if (FULL) {
       if (dB != R(0)) {
         V3<R> gs;
-        bo_reverse<R, false>(S, typ, owner, st, C * V * P * dB, R(0), F, e + 1, gs, fi, fj);
+        bo_reverse<R, false, NB>(S, typ, owner, st, C * V * P * dB, R(0), F, e + 1, gs, fi, fj);
         // chain through d* = rho d / |d|: dE/dd = (rho/r) (I - u u^T) dE/dd*
         V3<R> u = ir * d;
         addto(gd, (rho * ir) * (gs - dot3(u, gs) * u));
@@ -624,19 +678,19 @@ __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const double4* pos
         PathRes<R> pr = path_search(S, i, J);
         path_forces(S, owner, pr, -Q * V, F, e + 1);
       }
-      atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
-      atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
-      vir_add(e + 1, d, gd);
-      e[0] += (double)E;
-      ++nb;
-      nbad += st.bad;
-      if (stage.rows) {
-        double* row = stage_row(stage, 7);
-        if (row) {
-          char4 s = shift[J];
-          row[0] = gid[i], row[1] = gid[J], row[2] = s.x, row[3] = s.y, row[4] = s.z;
-          row[5] = C, row[6] = bs;
-        }
+    }
+    atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
+    atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
+    vir_add(e + 1, d, gd);
+    e[0] += (double)E;
+    ++nb;
+    nbad += st.bad;
+    if (stage.rows) {
+      double* row = stage_row(stage, 7);
+      if (row) {
+        char4 s = shift[J];
+        row[0] = gid[i], row[1] = gid[J], row[2] = s.x, row[3] = s.y, row[4] = s.z;
+        row[5] = C, row[6] = bs;
       }
     }
   }

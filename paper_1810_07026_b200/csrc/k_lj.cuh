@@ -33,9 +33,7 @@ constexpr int NEAR_TWO = 64;                     // 2-hop frontier capacity per 
 struct ReachSmem {
   int keys[NEAR_SLOTS];
   unsigned long long mbits[NEAR_SLOTS];
-  int two_l[NEAR_TWO];
-  double two_w[NEAR_TWO];
-  int ntwo, nins, ovf;
+  int nins, ovf;
 };
 
 __device__ __forceinline__ unsigned reach_hash(int key) { return ((unsigned)key * 2654435761u) >> 26; }
@@ -95,6 +93,21 @@ __device__ __forceinline__ double group_sum(double v) {
 }
 
 // ---------------------------------------------------------------------------------- near pairs
+// 8 lanes per atom.  The reach table holds the maximal path product per reachable image; the
+// pair loop is branch-light (the rare b* / fractional-C / stage work sits at the end of the
+// body) so the group stays converged through the LJ arithmetic.
+__device__ __forceinline__ double reach_lookup_fast(const ReachSmem& s, int key) {
+  unsigned h = reach_hash(key);
+#pragma unroll
+  for (int probe = 0; probe < 4; ++probe) {
+    int k = s.keys[h];
+    if (k == key) return __longlong_as_double((long long)s.mbits[h]);
+    if (k == REACH_EMPTY) return 0.0;
+    h = (h + 1) & (NEAR_SLOTS - 1);
+  }
+  return reach_lookup(s, key);  // long probe chain: rare
+}
+
 template <typename R, bool VIRIAL>
 __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, ShortList<R> S, const int* owner,
                                                                     const int* gid, const char4* shift, double* F,
@@ -110,12 +123,12 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
   const bool active = i < A.N;
   const int cntN = active ? A.cnt[0][i] : 0;
 
-  // 1. reach set of i (1-, 2-, 3-bond paths)
+  // 1. reach set of i: lane per neighbour k of i enumerates k, l in N(k), m in N(l)
   for (int q = gl; q < NEAR_SLOTS; q += NEAR_GROUP) {
     s.keys[q] = REACH_EMPTY;
     s.mbits[q] = 0ull;
   }
-  if (gl == 0) s.ntwo = 0, s.nins = 0, s.ovf = 0;
+  if (gl == 0) s.nins = 0, s.ovf = 0;
   __syncwarp();
   const size_t bi = (size_t)(active ? i : 0) * S.capS;
   const int ni = cntN > 0 ? S.cnt[i] : 0;
@@ -130,26 +143,13 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
       if (l == i) continue;
       R w12 = w1 * S.w[bk + b].x;
       reach_insert(s, l, (double)w12);
-      int slot = atomicAdd(&s.ntwo, 1);
-      if (slot < NEAR_TWO) {
-        s.two_l[slot] = l;
-        s.two_w[slot] = (double)w12;
-      } else {
-        s.ovf = 1;
+      size_t bl = (size_t)l * S.capS;
+      int nl = S.cnt[l];
+      for (int c = 0; c < nl; ++c) {
+        int m = S.nbr[bl + c];
+        if (m == i) continue;
+        reach_insert(s, m, (double)(w12 * S.w[bl + c].x));
       }
-    }
-  }
-  __syncwarp();
-  const int ntwo = min(s.ntwo, NEAR_TWO);
-  for (int t = gl; t < ntwo; t += NEAR_GROUP) {
-    int l = s.two_l[t];
-    R w12 = (R)s.two_w[t];
-    size_t bl = (size_t)l * S.capS;
-    int nl = S.cnt[l];
-    for (int c = 0; c < nl; ++c) {
-      int m = S.nbr[bl + c];
-      if (m == i) continue;
-      reach_insert(s, m, (double)(w12 * S.w[bl + c].x));
     }
   }
   __syncwarp();
@@ -165,54 +165,37 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
     const long long ki = key_of(pi);
     const int* row = A.nbr[0] + (size_t)i * A.cap[0];
     for (int q = gl; q < cntN; q += NEAR_GROUP) {
-      int J = row[q];
-      double4 pj = A.pos[J];
-      double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
-      double r2 = r2_exact(dx, dy, dz);
-      int p = ti + type_of(pj);
-      if (r2 > c_geo.rc2[p]) continue;
-      bool canon = ki < key_of(pj);
-      nlj += canon;
+      const int J = row[q];
+      const double4 pj = A.pos[J];
+      const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
+      const double r2 = r2_exact(dx, dy, dz);
+      const int p = ti + type_of(pj);
+      const bool inr = r2 <= c_geo.rc2[p];
+      const bool canon = ki < key_of(pj);
       double Md = 0.0;
-      if (r2 <= c_geo.reach2) Md = ovf ? (double)path_search(S, i, J).M : reach_lookup(s, J);
-      if (Md == 1.0) {  // C_ij == 0 (Alg. 3 "continue")
-        nc0 += canon;
-        if (canon && stage.rows) stage_lj_row(stage, gid[i], gid[J], shift[J], 0.0, 0.0);
-        continue;
-      }
+      if (inr && r2 <= c_geo.reach2) Md = ovf ? (double)path_search(S, i, J).M : reach_lookup_fast(s, J);
+      const bool c0 = Md == 1.0;  // C_ij == 0 (Alg. 3 "continue")
       // S_r(r) != 0 decided exactly in fp64 in both precision modes (reading A14); r^2 pre-filter
-      if (r2 < c_geo.srhi2_hi[p]) {
+      bool bst = false;
+      if (inr && !c0 && r2 < c_geo.srhi2_hi[p]) {
         double rd = sqrt(r2);
-        double tP = (rd - c_tabd.sigma[p]) / (c_tabd.srhi[p] - c_tabd.sigma[p]);
-        if (tP < 1.0) {  // deferred b* batch: the whole pair is evaluated once by the canonical side
-          if (canon) {  // warp-aggregated append (one global atomic per converged lane set)
-            unsigned am = __activemask();
-            int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
-            int base = 0;
-            if (lane == leader) base = atomicAdd(Qu.count, __popc(am));
-            base = __shfl_sync(am, base, leader);
-            int k = base + __popc(am & ((1u << lane) - 1u));
-            if (k < Qu.cap) {
-              Qu.item[k] = make_int4(i, J, 0, 0);
-              Qu.M[k] = Md;
-            } else {
-              atomicAdd(ct + CT_OVF_QUEUE, 1ull);
-            }
-          }
-          continue;
-        }
+        bst = (rd - c_tabd.sigma[p]) / (c_tabd.srhi[p] - c_tabd.sigma[p]) < 1.0;
       }
-      R rr2 = (R)r2;
+      const bool norm = inr && !c0 && !bst;
+      nlj += inr && canon;
+      nc0 += c0 && canon;
+      // LJ for every lane (weight 0 unless norm)
+      R rr2 = norm ? (R)r2 : R(1);
       R y = rsqrt_fast(rr2);
       R dVr;
       R V = lj_plain<R>(R(4) * T.eps[p], T.sigma2[p], y * y, dVr);
-      if (r2 > c_geo.rlo2[p]) {  // taper S(r; r_lo, r_c) (reading A10)
+      if (norm && r2 > c_geo.rlo2[p]) {  // taper S(r; r_lo, r_c) (reading A10): rare in the near list
         R r = rr2 * y, dsw;
         R sv = sw<R>(r, T.rlo[p], T.rc[p], dsw);
         dVr = dVr * sv + V * dsw * y;
         V = V * sv;
       }
-      R C = R(1) - (R)Md;
+      R C = norm ? R(1) - (R)Md : R(0);
       R fr = C * dVr;  // F_i += fr d  (E(d), d = x_j - x_i)
       fx += (double)(fr * (R)dx);
       fy += (double)(fr * (R)dy);
@@ -222,18 +205,33 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
         V3<R> dd = mk3<R>((R)dx, (R)dy, (R)dz);
         vir_add(W, dd, (R(0.5) * fr) * dd);
       }
-      if (canon && Md > 0.0) {  // 0 < C < 1: dC/dx along the maximising path, once per pair
+      // rare work last
+      if (bst && canon) {  // deferred b* batch: the whole pair is evaluated once by the canonical side
+        unsigned am = __activemask();
+        int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(Qu.count, __popc(am));
+        base = __shfl_sync(am, base, leader);
+        int k = base + __popc(am & ((1u << lane) - 1u));
+        if (k < Qu.cap) {
+          Qu.item[k] = make_int4(i, J, 0, 0);
+          Qu.M[k] = Md;
+        } else {
+          atomicAdd(ct + CT_OVF_QUEUE, 1ull);
+        }
+      }
+      if (norm && canon && Md > 0.0) {  // 0 < C < 1: dC/dx along the maximising path, once per pair
         PathRes<R> pr = path_search(S, i, J);
         double Wp[6] = {0, 0, 0, 0, 0, 0};
         path_forces(S, owner, pr, -V, F, Wp);
         if (VIRIAL)
           for (int c = 0; c < 6; ++c) W[c] += Wp[c];
       }
-      if (canon && stage.rows) stage_lj_row(stage, gid[i], gid[J], shift[J], (double)C, 0.0);
+      if (stage.rows && canon && inr && !bst) stage_lj_row(stage, gid[i], gid[J], shift[J], c0 ? 0.0 : (double)C, 0.0);
     }
   }
 
-  // 3. reductions (8-lane groups, then one atomic per atom / per warp)
+  // 3. reductions (8-lane groups, then one partial row per block)
   fx = group_sum<NEAR_GROUP>(fx);
   fy = group_sum<NEAR_GROUP>(fy);
   fz = group_sum<NEAR_GROUP>(fz);
