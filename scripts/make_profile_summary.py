@@ -1,0 +1,76 @@
+"""Turn ncu outputs from gpurun_out/ into the committed summaries under profiles/.
+
+usage: python scripts/make_profile_summary.py <launch_list.csv> <full.ncu-rep> <round tag>
+Writes profiles/launches_<tag>.csv (copy), profiles/launch_shares_<tag>.txt,
+profiles/ncu_full_<tag>.txt and profiles/ncu_summary_<tag>.json (per-kernel DRAM bytes per
+launch, read by bench.py as roofline.traffic).
+"""
+import csv
+import json
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+launch_csv, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+prof = os.path.join(ROOT, "profiles")
+os.makedirs(prof, exist_ok=True)
+shutil.copy(launch_csv, os.path.join(prof, f"launches_{tag}.csv"))
+
+rows = list(csv.reader(open(launch_csv)))
+h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+idx = {n: i for i, n in enumerate(rows[h])}
+tot = {}
+for r in rows[h + 1:]:
+    if len(r) < len(rows[h]):
+        continue
+    name = re.sub(r"\(.*", "", r[idx["Kernel Name"]]).replace("void ", "").strip()
+    v = float(r[idx["Metric Value"]].replace(",", ""))
+    unit = r[idx["Metric Unit"]]
+    v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
+    if "k_fma_peak" in name:  # the FMA-peak microbenchmark bench.py runs once, not part of a step
+        continue
+    t = tot.setdefault(name, [0.0, 0])
+    t[0] += v
+    t[1] += 1
+all_us = sum(v[0] for v in tot.values())
+with open(os.path.join(prof, f"launch_shares_{tag}.txt"), "w") as f:
+    f.write(f"# ncu launch list ({os.path.basename(launch_csv)}): gpu__time_duration.sum per kernel, "
+            f"--clock-control none, cold-cache serialised launches; compare SHARES, not absolutes\n")
+    f.write(f"{'kernel':60s} {'total_us':>12s} {'launches':>9s} {'avg_us':>9s} {'share':>7s}\n")
+    for k, (us, n) in sorted(tot.items(), key=lambda x: -x[1][0]):
+        f.write(f"{k[:60]:60s} {us:12.1f} {n:9d} {us / n:9.2f} {100 * us / all_us:6.2f}%\n")
+
+out = subprocess.run(["python", os.path.join(ROOT, "scripts", "ncu_summary.py"), rep], capture_output=True,
+                     text=True).stdout
+open(os.path.join(prof, f"ncu_full_{tag}.txt"), "w").write(
+    f"# ncu --set full --clock-control none --import-source on (scripts/prof_step.py, cfg2, fp64)\n" + out)
+
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rr = list(csv.reader(raw.splitlines()))
+hdr = rr[0]
+col = {n: i for i, n in enumerate(hdr)}
+summ = {"fp64": {}}
+for r in rr[2:]:
+    kname = re.sub(r"<.*|\(.*", "", r[col["Kernel Name"]]).replace("void ", "").replace("ab::", "").strip()
+    d = {}
+    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
+        if key in col:
+            unit = rr[1][col[key]]
+            v = float(r[col[key]].replace(",", ""))
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3,
+                     "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
+            d[key] = v * scale
+    e = summ["fp64"].setdefault(kname, {"launches": 0, "dram_bytes": 0.0, "duration_us": 0.0})
+    e["launches"] += 1
+    e["dram_bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+    e["duration_us"] += d.get("gpu__time_duration.sum", 0)
+for e in summ["fp64"].values():
+    e["dram_bytes_per_launch"] = e["dram_bytes"] / max(e["launches"], 1)
+summ["_note"] = ("ncu --set full capture (cache flushed between replays, i.e. cold-cache DRAM traffic per "
+                 "launch) of scripts/prof_step.py on cfg2, fp64")
+json.dump(summ, open(os.path.join(prof, f"ncu_summary_{tag}.json"), "w"), indent=1)
+print(open(os.path.join(prof, f"launch_shares_{tag}.txt")).read())
+print(json.dumps(summ, indent=1))
