@@ -109,7 +109,9 @@ ab_status ab_compute(ab_engine* e, double* f, double* energy, double virial[6], 
 /* Advance nsteps velocity-Verlet NVE steps of dt_fs: v += dt/2 F/m; x += dt v;
  * (rebuild lists if any atom moved > skin/2); F = F(x); v += dt/2 F/m.  If thermo != NULL and
  * thermo_every > 0 it receives rows (step, PE, KE, Etot) for steps 0, every, 2 every, ... <= nsteps
- * (nsteps/thermo_every + 1 rows, 4 doubles each). */
+ * (nsteps/thermo_every + 1 rows, 4 doubles each).  The call returns once the last step is
+ * enqueued on the engine's stream (it synchronises once per step on the rebuild decision only);
+ * every call that returns data orders after it. */
 ab_status ab_run_nve(ab_engine* e, int64_t nsteps, double dt_fs, int64_t thermo_every, double* thermo);
 
 ab_status ab_get_positions(ab_engine* e, double* xyz);  /* caller order; not re-wrapped between rebuilds */

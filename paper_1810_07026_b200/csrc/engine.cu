@@ -52,6 +52,8 @@ struct DBuf {
 
 inline int nblk(long long n, int t) { return (int)((n + t - 1) / t); }
 
+constexpr size_t SCRATCH_BYTES = 1024, SCRATCH_CT = 128, SCRATCH_SMALL = 512, SCRATCH_ZERO_BYTES = 512 + 64;
+
 }  // namespace
 
 struct ab_engine {
@@ -86,9 +88,15 @@ struct ab_engine {
   DBuf<int4> q_item;
   DBuf<int> ovf_bond, ovf_q;  // overflow (large side / full b*) index lists
   DBuf<double> q_M;
-  DBuf<int> small_i;                 // [0] nbonds [1] qcount [2] maxLJ [3] maxI [4..5] stage counts
-  DBuf<double> acc;                  // ACC_N
-  DBuf<unsigned long long> ct;       // CT_N (+1: maxdisp2)
+  // one small device scratch block, zeroed with a single memset per evaluation:
+  //   acc (ACC_N doubles) at 0, ct (CT_N + 1 u64; [CT_N] = max displacement^2) at 128,
+  //   small_i (16 ints: nbonds, qcount, list maxima x4, stage counts x2, overflow counts x2) at 512
+  DBuf<unsigned char> scratch;
+  DBuf<int> small_i;
+  DBuf<double> acc;
+  DBuf<unsigned long long> ct;
+  bool host_stale = false;  // acc / ct of the last evaluation not yet copied to the host
+  cudaEvent_t ev_disp = nullptr;
   DBuf<double> stage0, stage1, red_d;
   DBuf<unsigned long long> red_u;
   DBuf<unsigned char> cub_tmp;
@@ -449,14 +457,9 @@ ab_status rebuild(ab_engine* e) {
 }
 
 template <typename R>
-ab_status forces_impl(ab_engine* e) {
+ab_status forces_impl(ab_engine* e, bool sync_host) {
   const int N = e->N, NT = e->NT;
   cudaStream_t st = e->st;
-  if (e->capQ == 0) {
-    e->capQ = std::max(4096, 4 * N);
-    CK(e->q_item.ensure(e->capQ));
-    CK(e->q_M.ensure(e->capQ));
-  }
   StageBuf sb0{nullptr, nullptr, 0}, sb1{nullptr, nullptr, 0};
   if (e->record) {
     size_t n0 = (size_t)N * e->capS + 16, n1 = (size_t)N * (e->capL[0] + e->capL[1] + e->capL[2]) + 16;
@@ -465,12 +468,18 @@ ab_status forces_impl(ab_engine* e) {
     sb0 = StageBuf{e->stage0.p, e->small_i.p + 6, (int)n0};
     sb1 = StageBuf{e->stage1.p, e->small_i.p + 7, (int)n1};
   }
+  // b* queue: the canonical near-list pairs bound the queue, so it cannot overflow
+  {
+    long long qb = (long long)N * e->capL[0] / 2 + 1024;
+    if (e->capQ < qb) {
+      e->capQ = (int)std::min<long long>(qb, 1ll << 30);
+      CK(e->q_item.ensure(e->capQ));
+      CK(e->q_M.ensure(e->capQ));
+    }
+  }
   for (int attempt = 0; attempt < 3; ++attempt) {
     CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * N, st));
-    CK(cudaMemsetAsync(e->acc.p, 0, sizeof(double) * ACC_N, st));
-    CK(cudaMemsetAsync(e->ct.p, 0, sizeof(unsigned long long) * CT_N, st));
-    CK(cudaMemsetAsync(e->small_i.p, 0, 2 * sizeof(int), st));
-    CK(cudaMemsetAsync(e->small_i.p + 6, 0, 2 * sizeof(int), st));
+    CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
     ShortList<R> S = short_view<R>(e);
     // grids and the per-block partial rows of the energy / virial / counter reduction
     const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
@@ -478,7 +487,6 @@ ab_status forces_impl(ab_engine* e) {
     const int nrows = g_short + g_rebo + g_near + g_far + g_bstar + 2 * g_slow;
     CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
     CK(e->ovf_q.ensure(e->capQ));
-    CK(cudaMemsetAsync(e->small_i.p + 8, 0, 2 * sizeof(int), st));
     CK(e->red_d.ensure((size_t)ACC_N * nrows));
     CK(e->red_u.ensure((size_t)CT_N * nrows));
     RedRows RR{e->red_d.p, e->red_u.p, nrows, 0};
@@ -533,6 +541,11 @@ ab_status forces_impl(ab_engine* e) {
     RR.row0 = 0;
     k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows, e->acc.p, e->ct.p);
     CKL();
+    if (!sync_host) {  // NVE steps: results stay on the device until somebody needs them
+      e->host_stale = true;
+      e->forces_valid = true;
+      return AB_OK;
+    }
     CK(cudaMemcpyAsync(e->h_ct, e->ct.p, sizeof(unsigned long long) * CT_N, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(e->h_acc, e->acc.p, sizeof(double) * ACC_N, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -559,10 +572,35 @@ ab_status forces_impl(ab_engine* e) {
     return AB_E_NONFINITE;
   }
   e->forces_valid = true;
+  e->host_stale = false;
   return AB_OK;
 }
 
-ab_status forces(ab_engine* e) { return e->prec == AB_FP64 ? forces_impl<double>(e) : forces_impl<float>(e); }
+ab_status forces(ab_engine* e, bool sync_host = true) {
+  return e->prec == AB_FP64 ? forces_impl<double>(e, sync_host) : forces_impl<float>(e, sync_host);
+}
+
+// bring energies / virial / counters of the last (asynchronous) evaluation to the host
+ab_status pull_results(ab_engine* e) {
+  if (!e->host_stale) return AB_OK;
+  CK(cudaMemcpyAsync(e->h_ct, e->ct.p, sizeof(unsigned long long) * CT_N, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaMemcpyAsync(e->h_acc, e->acc.p, sizeof(double) * ACC_N, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  prof_collect(e);
+  e->host_stale = false;
+  if (e->h_ct[CT_OVF_SHORT]) {
+    e->err = "an atom has more than 16 REBO short-list neighbours (NBMAX); unsupported geometry";
+    return AB_E_STATE;
+  }
+  std::memcpy(e->last_ct, e->h_ct, sizeof(e->last_ct));
+  for (int c = 0; c < 3; ++c) e->E3[c] = e->h_acc[ACC_EREBO + c];
+  for (int c = 0; c < 6; ++c) e->W6[c] = e->h_acc[ACC_W + c];
+  if (!std::isfinite(e->E3[0] + e->E3[1] + e->E3[2])) {
+    e->err = "non-finite energy";
+    return AB_E_NONFINITE;
+  }
+  return AB_OK;
+}
 
 // make lists valid for the current positions (rebuild if needed, else move the ghosts)
 ab_status prepare(ab_engine* e, bool check_disp) {
@@ -637,11 +675,19 @@ ab_status ab_create(const char* text, size_t len, ab_precision prec, int device,
   fill_tab(e->hp, td);
   fill_tab(e->hp, tf);
   bool ok = cudaMemcpyToSymbol(c_tabd, &td, sizeof(td)) == cudaSuccess &&
-            cudaMemcpyToSymbol(c_tabf, &tf, sizeof(tf)) == cudaSuccess && e->acc.ensure(ACC_N) == cudaSuccess &&
-            e->ct.ensure(CT_N + 1) == cudaSuccess && e->small_i.ensure(16) == cudaSuccess &&
+            cudaMemcpyToSymbol(c_tabf, &tf, sizeof(tf)) == cudaSuccess &&
+            e->scratch.ensure(SCRATCH_BYTES) == cudaSuccess &&
+            cudaMemset(e->scratch.p, 0, SCRATCH_BYTES) == cudaSuccess &&
             cudaMallocHost(&e->h_ct, sizeof(unsigned long long) * (CT_N + 1)) == cudaSuccess &&
             cudaMallocHost(&e->h_acc, sizeof(double) * ACC_N) == cudaSuccess &&
             cudaMallocHost(&e->h_small, sizeof(int) * 8) == cudaSuccess;
+  static_assert(sizeof(double) * ACC_N <= SCRATCH_CT, "scratch layout");
+  static_assert(SCRATCH_CT + sizeof(unsigned long long) * (CT_N + 1) <= SCRATCH_SMALL, "scratch layout");
+  if (ok) {  // views into the scratch block (not separately allocated)
+    e->acc.p = reinterpret_cast<double*>(e->scratch.p), e->acc.n = ACC_N;
+    e->ct.p = reinterpret_cast<unsigned long long*>(e->scratch.p + SCRATCH_CT), e->ct.n = CT_N + 1;
+    e->small_i.p = reinterpret_cast<int*>(e->scratch.p + SCRATCH_SMALL), e->small_i.n = 16;
+  }
   if (!ok) {
     g_create_error = std::string("CUDA init failed: ") + cudaGetErrorString(cudaGetLastError());
     ab_destroy(e);
@@ -657,7 +703,9 @@ void ab_destroy(ab_engine* e) {
   if (e->st) cudaStreamSynchronize(e->st);
   DBuf<double4>* b4[] = {&e->pos, &e->pos_tmp, &e->xref};
   for (auto* b : b4) b->release();
-  DBuf<double>* bd[] = {&e->vel, &e->vel_tmp, &e->F, &e->io, &e->q_M, &e->acc, &e->stage0, &e->stage1};
+  e->acc.p = nullptr, e->ct.p = nullptr, e->small_i.p = nullptr;  // views into scratch
+  e->scratch.release();
+  DBuf<double>* bd[] = {&e->vel, &e->vel_tmp, &e->F, &e->io, &e->q_M, &e->stage0, &e->stage1};
   for (auto* b : bd) b->release();
   DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->key2, &e->val, &e->val2, &e->cell_start,
                      &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
@@ -678,6 +726,9 @@ void ab_destroy(ab_engine* e) {
   if (e->h_ct) cudaFreeHost(e->h_ct);
   if (e->h_acc) cudaFreeHost(e->h_acc);
   if (e->h_small) cudaFreeHost(e->h_small);
+  if (e->ev_disp) cudaEventDestroy(e->ev_disp);
+  for (auto& p : e->pending) cudaEventDestroy(p.a), cudaEventDestroy(p.b);
+  for (auto& x : e->pool) cudaEventDestroy(x);
   if (e->own) cudaStreamDestroy(e->own);
   delete e;
 }
@@ -838,30 +889,53 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     return AB_OK;
   };
   if (thermo && every > 0) TRY(record(0));
+  // The rebuild decision (max displacement) is the only per-step host round trip and
+  // it is hidden: after the drift the force kernels are enqueued speculatively on the current
+  // lists (they only write F, the scratch block and the b* queue), the host then waits for the
+  // displacement read-back alone and, if a rebuild is needed (rare), rebuilds and re-enqueues
+  // the forces before the second half-kick.  Energies and counters stay on the device except on
+  // thermo steps; the b* queue is sized so it cannot overflow, and the short-list overflow flag
+  // of step s is read at step s+1.
+  if (!e->ev_disp) CK(cudaEventCreateWithFlags(&e->ev_disp, cudaEventDisableTiming));
   for (int64_t s = 1; s <= nsteps; ++s) {
+    const bool th = thermo && every > 0 && s % every == 0;
     CK(cudaMemsetAsync(e->ct.p + CT_N, 0, sizeof(unsigned long long), st));
     prof_begin(e, 4);
     k_integrate1<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->vel.p, e->F.p, dtf0, dtf1, dt, e->xref.p,
                                                 e->ct.p + CT_N);
     CKL();
     prof_end(e);
-    unsigned long long bits;
-    CK(cudaMemcpyAsync(&bits, e->ct.p + CT_N, sizeof(bits), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpyAsync(e->h_ct, e->ct.p, sizeof(unsigned long long) * (CT_N + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(e->ev_disp, st));
+    bool speculated = false;
+    if (e->lists_valid && !th) {
+      TRY(prepare(e, false));
+      TRY(forces(e, false));
+      speculated = true;
+    }
+    CK(cudaEventSynchronize(e->ev_disp));
+    if (e->h_ct[CT_OVF_SHORT]) {
+      e->err = "an atom has more than 16 REBO short-list neighbours (NBMAX); unsupported geometry";
+      return AB_E_STATE;
+    }
     double d2;
-    std::memcpy(&d2, &bits, sizeof(d2));
+    std::memcpy(&d2, &e->h_ct[CT_N], sizeof(d2));
     double half = 0.5 * hp.skin;
-    if (d2 > half * half) e->lists_valid = false;
-    TRY(prepare(e, false));
-    TRY(forces(e));
+    if (d2 > half * half) e->lists_valid = false, speculated = false;
+    if (!speculated) {
+      TRY(prepare(e, false));
+      TRY(forces(e, th));
+    }
     prof_begin(e, 4);
     k_integrate2<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->vel.p, e->F.p, dtf0, dtf1);
     CKL();
     prof_end(e);
     ++e->steps;
-    if (thermo && every > 0 && s % every == 0) TRY(record(s));
+    if (th) TRY(record(s));
   }
-  CK(cudaStreamSynchronize(st));
+  // no final synchronisation: the last step's kernels may still run; every call that returns
+  // data (or the stream itself) orders after them
+  CK(cudaGetLastError());
   return AB_OK;
 }
 
@@ -965,6 +1039,8 @@ ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows
 
 ab_status ab_get_stats(ab_engine* e, ab_stats* s) {
   if (!e || !s) return AB_E_ARG;
+  cudaSetDevice(e->dev);
+  TRY(pull_results(e));
   const unsigned long long* c = e->last_ct;
   s->n_short = c[CT_SHORT], s->n_bonds = c[CT_BONDS], s->n_quads = c[CT_QUADS], s->n_lj = c[CT_LJ];
   s->n_C0 = c[CT_C0], s->n_bstar = c[CT_BSTAR], s->n_sb_trans = c[CT_SBTRANS], s->max_short = c[CT_MAXSHORT];

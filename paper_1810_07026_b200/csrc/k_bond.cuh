@@ -25,9 +25,12 @@ namespace ab {
 
 constexpr int NB_FAST = 4;
 
-template <int NB>
+// Unrolling the side loops keeps the side arrays in registers but multiplies the code size:
+// measured (bench, cfg2): it wins for the forward-only b* kernel and loses for the REBO kernel
+// (instruction-cache stalls), so each caller chooses.
+template <int NB, bool U>
 struct Unr {
-  static constexpr int v = NB <= NB_FAST ? NB : 1;
+  static constexpr int v = (U && NB <= NB_FAST) ? NB : 1;
 };
 
 template <typename R, int NB>
@@ -83,7 +86,7 @@ __device__ __forceinline__ R F_conj(R x, R& dF) {
 }
 
 // ---------------------------------------------------------------- forward pass
-template <typename R, bool TORS, int NB>
+template <typename R, bool TORS, int NB, bool UNROLL = false>
 __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i, int J, V3<R> d, R r,
                            BoState<R, NB>& st) {
   const Tab<R>& T = tab<R>();
@@ -105,7 +108,7 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
   st.u = ir * d;
   // ---- i side: k in N(i) \ {J}
   R sumI = 0, NCi = 0, NHi = 0, Si = 0;
-#pragma unroll(Unr<NB>::v)
+#pragma unroll(Unr<NB, UNROLL>::v)
   for (int a = 0; a < NB; ++a) {
     if (a >= nI) continue;
     int q = side_slot(a, pq);
@@ -129,7 +132,7 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
   // ---- J side: l in N(J) \ {i}
   R sumJ = 0, NCj = 0, NHj = 0, Sj = 0;
   const V3<R> md = mk3(-d.x, -d.y, -d.z);
-#pragma unroll(Unr<NB>::v)
+#pragma unroll(Unr<NB, UNROLL>::v)
   for (int c = 0; c < NB; ++c) {
     if (c >= nJ) continue;
     int q = side_slot(c, pl);
@@ -177,7 +180,7 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
   // ---- dihedral sum (and torsion sum): k in N(i)\J, l in N(J)\{i, k}
   R D = 0, Ts = 0;
   int nq = 0;
-#pragma unroll(Unr<NB>::v)
+#pragma unroll(Unr<NB, UNROLL>::v)
   for (int a = 0; a < NB; ++a) {
     if (a >= nI) continue;
     int q = side_slot(a, pq);
@@ -190,7 +193,7 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
     R Gk = guardG<R>(ck, dGk);
     V3<R> n1 = cross3(dk, d);
     R n1s = dot3(n1, n1);
-#pragma unroll(Unr<NB>::v)
+#pragma unroll(Unr<NB, UNROLL>::v)
     for (int c = 0; c < NB; ++c) {
       if (c >= nJ) continue;
       int ql = side_slot(c, pl);
@@ -251,7 +254,7 @@ __device__ __forceinline__ void conj_chain(const ShortList<R>& S, const int* own
 // cb = dE/db.  wij: weight of the bond for the merged torsion term (TORS only).
 // Output gd = dE/d(d) through the bond-order (and torsion) terms; fi / fj = force contributions
 // on i / J from the k and l vectors (the forces on k, l, m, n are scattered here).
-template <typename R, bool TORS, int NB>
+template <typename R, bool TORS, int NB, bool UNROLL = false>
 __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const int* owner, const BoState<R, NB>& st,
                            R cb, R wij, double* F, double W[6], V3<R>& gd, V3<R>& fi, V3<R>& fj) {
   const Tab<R>& T = tab<R>();
@@ -271,7 +274,7 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
   fj = mk3<R>(0, 0, 0);
   R Wl[NB], Cl[NB];
   V3<R> gl[NB];
-#pragma unroll(Unr<NB>::v)
+#pragma unroll(Unr<NB, UNROLL>::v)
   for (int c = 0; c < NB; ++c) {
     if (c >= nJ) continue;
     int q = side_slot(c, st.pl);
@@ -291,7 +294,7 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     Cl[c] = cJ * wl * dg * el;
     gl[c] = mk3<R>(0, 0, 0);
   }
-#pragma unroll(Unr<NB>::v)
+#pragma unroll(Unr<NB, UNROLL>::v)
   for (int a = 0; a < NB; ++a) {
     if (a >= nI) continue;
     int q = side_slot(a, st.pq);
@@ -321,7 +324,7 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     if (Gk != R(0)) {
       V3<R> n1 = cross3(dk, d);
       R inv1 = rsq(dot3(n1, n1));
-#pragma unroll(Unr<NB>::v)
+#pragma unroll(Unr<NB, UNROLL>::v)
       for (int c = 0; c < NB; ++c) {
         if (c >= nJ) continue;
         int ql = side_slot(c, st.pl);
@@ -368,7 +371,7 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     vir_add(W, dk, gk);
     if (chain != R(0)) conj_chain(S, owner, k, i, chain, F, W);
   }
-#pragma unroll(Unr<NB>::v)
+#pragma unroll(Unr<NB, UNROLL>::v)
   for (int c = 0; c < NB; ++c) {
     if (c >= nJ) continue;
     int q = side_slot(c, st.pl);
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_id
     R rho = T.rho[p];
     V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
     BoState<R, NB> st;
-    bo_forward<R, false, NB>(S, typ, i, J, ds, rho, st);
+    bo_forward<R, false, NB, !FULL>(S, typ, i, J, ds, rho, st);
     if (!FULL && st.overflow) {
       list_append(ovf, novf, 1 << 30, qi);
       continue;

@@ -318,7 +318,10 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
 }
 
 template <typename R, bool VIRIAL>
-__global__ void __launch_bounds__(128) k_lj_far(LJArgs A, const int* gid, const char4* shift, double* F, double* acc,
+#ifndef AB_FAR_MINBLOCKS
+#define AB_FAR_MINBLOCKS 4
+#endif
+__global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, const int* gid, const char4* shift, double* F, double* acc,
                                                unsigned long long* ct, StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
   red_init(rs);

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libairebo_b200.so")
+LIB_PATH = os.environ.get("AIREBO_B200_LIB", os.path.join(HERE, "libairebo_b200.so"))
 PARAMS = os.path.join(os.path.dirname(HERE), "params", "toy_ch.param")
 
 AB_FP64, AB_MIXED = 0, 1
