@@ -11,8 +11,10 @@ Contract (driver): python bench.py --gpus N --steps K --warmup W [--impl referen
   * e2e: the same metric through the C-ABI with HOST buffers: per step ab_set_velocities (H2D
     from pinned memory) + ab_run_nve(1 step, thermo row D2H) + ab_get_positions (D2H).
   * --impl reference: the fp64 CPU oracle (oracle/) on the host cores, same workload.
-Multi-GPU (N > 1): the slab decomposition is not implemented yet; every rank runs an independent
-replica of the workload (scaling "weak", parallelism "replicas") and value sums the replicas.
+Multi-GPU (N > 1, torchrun, one process per GPU): slab decomposition along x with
+  the engine's own NCCL communicator (ab_create_dist): halo positions and ghost forces travel by
+  ncclSend/ncclRecv between slab neighbours every step.  Default weak scaling: the cfg2 block per
+  GPU (PE (12 N) x 16 x 14 cells, N x 32,256 atoms); --scaling strong keeps cfg --config fixed.
 """
 from __future__ import annotations
 
@@ -35,6 +37,26 @@ PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
 
 
 # ------------------------------------------------------------------ helpers
+def reduce_max(x, ws, device=None):
+    """Max of a host scalar over all ranks (torch.distributed; identity for one rank)."""
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def workload(config, ws, scaling):
+    """The bench system: BASELINE configs[1] (cfg2) at N = 1; weak scaling replicates the cfg2
+    block along x (same seeds), strong scaling keeps the configured system."""
+    from paper_1810_07026_b200 import inputs as I
+    if ws == 1 or scaling == "strong" or config != 2:
+        return I.config(config)
+    return I.polyethylene((12 * ws, 16, 14), 0.02, 102, 202, name=f"cfg2-pe-32k-x{ws}")
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -129,13 +151,17 @@ def run_ours(args, ws, rank, local):
 
     if rank == 0:
         B.build()
+    uid = None
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [E.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
         dist.barrier()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    s = I.config(args.config)
+    s = workload(args.config, ws, args.scaling)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -145,15 +171,14 @@ def run_ours(args, ws, rank, local):
             dist.barrier()
 
     def max_over_ranks(x):
-        if ws == 1:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_max(x, ws, dev)
+
+    def make_engine(precision):
+        ranks = ("nccl", rank, ws, uid) if ws > 1 else None
+        return E.make(s, precision, device=local, ranks=ranks)
 
     def leg(precision):
-        eng = E.make(s, precision, device=local)
+        eng = make_engine(precision)
         eng.set_stream(stream.cuda_stream)
         eng.run_nve(args.warmup, s.dt)  # warm-up (untimed): builds lists, JIT-free
         torch.cuda.synchronize()
@@ -195,7 +220,7 @@ def run_ours(args, ws, rank, local):
     st = main["stats"]
     n_atoms = s.n
     K = args.steps
-    value = ws * n_atoms * K / (main["total_ms"] * 1e-3)
+    value = n_atoms * K / (main["total_ms"] * 1e-3)  # all ranks' atoms / max-over-ranks time
     ms_per_step = main["total_ms"] / K
 
     def roofline(r, precision):
@@ -236,7 +261,7 @@ def run_ours(args, ws, rank, local):
     e2e = None
     if not args.no_e2e:
         import torch
-        eng2 = E.make(s, args.precision, device=local)
+        eng2 = make_engine(args.precision)
         eng2.set_stream(stream.cuda_stream)
         eng2.run_nve(args.warmup, s.dt)
         vh = torch.from_numpy(eng2.get_velocities()).pin_memory()
@@ -256,7 +281,7 @@ def run_ours(args, ws, rank, local):
             eng2._ck(eng2.L.ab_get_positions(eng2.h, xptr))
         torch.cuda.synchronize()
         t_e2e = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": ws * n_atoms * K / t_e2e, "unit": "atom-steps/s", "h2d_bytes_per_step": 24 * n_atoms,
+        e2e = {"value": n_atoms * K / t_e2e, "unit": "atom-steps/s", "h2d_bytes_per_step": 24 * n_atoms,
                "d2h_bytes_per_step": 24 * n_atoms + 64}
         eng2.close()
 
@@ -268,13 +293,15 @@ def run_ours(args, ws, rank, local):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "atom-steps/s", "n_gpus": ws, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if (ws > 1 and args.scaling == "strong") else "weak",
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32+f64acc",
             "data": "synthetic (seeded generator, paper_1810_07026_b200/inputs.py)",
-            "config": {"workload": s.name + " (BASELINE configs[1]: PE 12x16x14 cells, 32,256 atoms, 300 K, "
-                                            "dt 0.5 fs, NVE, LJ cutoff 3 sigma, torsion on)",
+            "config": {"workload": s.name + (" (BASELINE configs[1]: PE 12x16x14 cells, 32,256 atoms, 300 K, "
+                                             "dt 0.5 fs, NVE, LJ cutoff 3 sigma, torsion on)" if ws == 1 else
+                                             f" (cfg2 block per GPU along x, {ws} slabs)"),
                        "atoms": n_atoms, "dt_fs": s.dt, "precision": args.precision,
-                       "parallelism": "single GPU" if ws == 1 else "replicas (slab decomposition pending)",
+                       "parallelism": "single GPU" if ws == 1 else f"slab{ws} (x slabs, NCCL halo send/recv)",
                        "l2": "flushed between timed steps (256 MiB write)",
                        "timed_step": "ab_run_nve(1): integrate, rebuild check, forces, integrate"},
             "roofline": roofline(main, args.precision),
@@ -289,7 +316,7 @@ def run_ours(args, ws, rank, local):
         }
         if "mixed" in res and args.precision == "fp64":
             r = res["mixed"]
-            line["mixed"] = {"value": ws * n_atoms * K / (r["total_ms"] * 1e-3), "ms_per_step": r["total_ms"] / K,
+            line["mixed"] = {"value": n_atoms * K / (r["total_ms"] * 1e-3), "ms_per_step": r["total_ms"] / K,
                              "roofline": roofline(r, "mixed"), "clocks": r["clocks"]}
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -317,8 +344,7 @@ def run_reference(args, ws, rank, local):
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_1810_07026_b200 import inputs as I
-    s = I.config(args.config)
+    s = workload(args.config, ws, args.scaling)
     cores = os.cpu_count() or 1
     x, v = s.x.copy(), s.v.copy()
     x, v, _ = O.nve(s.types, x, v, s.box, args.warmup, s.dt, every=0, threads=cores)
@@ -344,6 +370,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
     ap.add_argument("--config", default=2, type=lambda v: int(v) if v.isdigit() else v)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--no-mixed", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -33,11 +33,11 @@ typedef enum {
   AB_OK = 0,
   AB_E_ARG = -1,       /* bad argument (NULL pointer, n < 0, unknown enum) */
   AB_E_PARAM = -2,     /* parameter text: parse error (names line or key) or invariant violation */
-  AB_E_BOX = -3,       /* box edge <= 0 or not finite */
+  AB_E_BOX = -3,       /* box edge <= 0 or not finite; slab narrower than the halo */
   AB_E_STATE = -4,     /* call order (e.g. compute before set_atoms) or capacity beyond a hard limit */
   AB_E_OOM = -5,       /* device allocation failed */
   AB_E_CUDA = -6,      /* CUDA error or no sm_100 device; engine unusable */
-  AB_E_NCCL = -7,      /* reserved for the multi-GPU path */
+  AB_E_NCCL = -7,      /* NCCL library missing or a collective failed (distributed mode) */
   AB_E_NONFINITE = -8  /* non-finite input coordinate or non-finite energy */
 } ab_status;
 
@@ -78,6 +78,40 @@ typedef struct ab_stats {
  * grammar).  `len` = bytes of param_text (need not be NUL-terminated).  *out receives the handle.
  * Errors: AB_E_ARG, AB_E_PARAM (message names the line or key), AB_E_CUDA (no sm_100 device). */
 ab_status ab_create(const char* param_text, size_t len, ab_precision prec, int cuda_device, ab_engine** out);
+
+/* ---- Spatial slab decomposition (the paper's MPI domains of LAMMPS).
+ * The box is cut into nranks equal slabs along x; slab r owns the atoms whose wrapped x lies in
+ * [r L_x / n, (r+1) L_x / n).  Each slab keeps a halo of ghost atom instances within
+ * h = r_c,max + skin of its faces (LJ partners, C_ij paths, b* neighbourhoods and complete ghost
+ * short lists all lie inside it); halo positions are exchanged every step and the forces the
+ * slab puts on ghosts are returned to their owners and added there.  Each pair / bond /
+ * dihedral term is computed once globally by the owner of its lower (gid, image) instance.
+ * Requirement: slab width L_x / n >= h, else ab_set_box fails with AB_E_BOX.
+ * In both modes every rank passes the same GLOBAL arrays to ab_set_atoms / ab_set_positions /
+ * ab_set_velocities and receives complete global arrays from ab_get_* (gathered over ranks);
+ * energies, virial and counters are sums over all ranks.
+ *
+ * ab_create_dist: one process per GPU.  All ranks call it collectively with the same 128-byte
+ * NCCL unique id (from ab_nccl_unique_id on one rank, broadcast by the caller).  The halo and
+ * force exchanges are ncclSend / ncclRecv between slab neighbours on the engine's stream, the
+ * rebuild decision and results are NCCL all-reduces; libnccl.so.2 is loaded at run time.
+ * Every call on a distributed engine is collective (all ranks, same order).  ab_get_list
+ * returns the rows of this rank's owned atoms only.  Errors: AB_E_NCCL (library or comm).
+ *
+ * ab_create_virtual: nranks slab domains driven by one handle on one GPU, exchanging the halo by
+ * device-to-device copies (the same decomposition code; only the transport differs).  Used to
+ * check the decomposition against the whole-box engine and the oracle on a single GPU. */
+ab_status ab_nccl_unique_id(void* id128 /* out: 128 bytes */);
+ab_status ab_create_dist(const char* param_text, size_t len, ab_precision prec, int cuda_device, int rank,
+                         int nranks, const void* id128, ab_engine** out);
+ab_status ab_create_virtual(const char* param_text, size_t len, ab_precision prec, int cuda_device, int nranks,
+                            ab_engine** out);
+/* Host-only slab geometry (no GPU needed): bounds [xlo, xhi) of slab `rank`, and AB_E_BOX if the
+ * slab width L[0]/nranks is below `halo`; ab_slab_of: owning slab of coordinate x (wrapped into
+ * [0, Lx) first), -1 on bad arguments. */
+ab_status ab_slab_info(const double L[3], double halo, int nranks, int rank, double* xlo, double* xhi);
+int ab_slab_of(double x, double Lx, int nranks);
+
 void ab_destroy(ab_engine* e);
 /* Text of the last error on this engine (or of the last failed ab_create if e == NULL). */
 const char* ab_last_error(const ab_engine* e);

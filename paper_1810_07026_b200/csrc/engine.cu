@@ -5,10 +5,23 @@
 // order + torsion per bond (k_rebo) -> C_ij reach set + LJ per atom (k_lj) -> deferred b* batch
 // (k_bstar).  List rebuilds (binning, ghosts, skinned lists) happen when an atom moved more than
 // skin/2.  No CPU fallback: every step of the path is a kernel below.
+//
+// Domains.  An engine handle drives one or more spatial domains:
+//   * single GPU, whole box (nranks == 1): the handle is the domain; ghosts are periodic images;
+//   * NCCL rank r of n (ab_create_dist): the handle is slab r; the halo travels with ncclSend /
+//     ncclRecv on the engine stream, ghost forces come back the same way;
+//   * n virtual slabs on one GPU (ab_create_virtual): the handle owns n domain engines (subs) and
+//     the halo travels by device-to-device copies on the shared stream.  Every phase is enqueued
+//     for all domains by the host in order, so no kernel ever waits on another domain's kernel.
+// Only the transfer (xfer) differs between the last two; the slab logic is the same code.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is dlopen'ed by the distributed mode
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +31,7 @@
 #include "../../include/airebo_b200.h"
 #include "dev_common.cuh"
 #include "k_bond.cuh"
+#include "k_dist.cuh"
 #include "k_lists.cuh"
 #include "k_lj.cuh"
 #include "k_misc.cuh"
@@ -33,12 +47,14 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  // grows with 25 % slack: atom / ghost counts drift between list rebuilds, and a reallocation
+  // (cudaFree synchronises the device) in every rebuild would cost milliseconds
   cudaError_t ensure(size_t cnt) {
     if (cnt <= n && p) return cudaSuccess;
+    size_t c = std::max<size_t>(p ? cnt + cnt / 4 : cnt, 1);
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
-    size_t c = std::max<size_t>(cnt, 1);
     cudaError_t e = cudaMalloc(&p, c * sizeof(T));
     if (e == cudaSuccess) n = c;
     return e;
@@ -50,24 +66,81 @@ struct DBuf {
   }
 };
 
-inline int nblk(long long n, int t) { return (int)((n + t - 1) / t); }
+// at least one block: every kernel bounds-checks, and an empty domain must still launch cleanly
+inline int nblk(long long n, int t) { return (int)std::max<long long>(1, (n + t - 1) / t); }
 
 constexpr size_t SCRATCH_BYTES = 1024, SCRATCH_CT = 128, SCRATCH_SMALL = 512, SCRATCH_ZERO_BYTES = 512 + 64;
+
+// ---- NCCL, resolved at run time (only the distributed mode needs it)
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl(std::string& err) {
+  static NcclApi api;
+  static bool tried = false;
+  static std::string why;
+  if (!tried) {
+    tried = true;
+    const char* env = std::getenv("AB_NCCL_LIB");
+    void* h = nullptr;
+    if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the copy torch already loaded
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      why = std::string("cannot load libnccl.so.2: ") + dlerror();
+    } else {
+      bool all = true;
+      auto sym = [&](auto& fp, const char* name) {
+        fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+        if (!fp) all = false;
+      };
+      sym(api.getUniqueId, "ncclGetUniqueId");
+      sym(api.commInitRank, "ncclCommInitRank");
+      sym(api.commDestroy, "ncclCommDestroy");
+      sym(api.groupStart, "ncclGroupStart");
+      sym(api.groupEnd, "ncclGroupEnd");
+      sym(api.send, "ncclSend");
+      sym(api.recv, "ncclRecv");
+      sym(api.allReduce, "ncclAllReduce");
+      sym(api.errStr, "ncclGetErrorString");
+      api.ok = all;
+      if (!all) why = "libnccl.so.2 lacks a required symbol";
+    }
+  }
+  if (!api.ok) err = why;
+  return api;
+}
 
 }  // namespace
 
 struct ab_engine {
   std::string err;
   HostParams hp;
+  Tab<double> td;
+  Tab<float> tf;
   ab_precision prec = AB_FP64;
   int dev = 0;
   char devname[256] = {0};
   int nsm = 148;
   cudaStream_t own = nullptr, st = nullptr;
+  cudaStream_t aux[2] = {nullptr, nullptr};     // concurrent force kernels (REBO, LJ far)
+  cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
   bool have_box = false, have_atoms = false, lists_valid = false, forces_valid = false;
   bool record = false;
   double L[3] = {0, 0, 0};
   int N = 0, NT = 0, G = 0;
+  int NX = 0;  // locals + x-ghosts (== N on a whole-box domain); image ghosts follow
   double halo = 0, rcmax = 0, rmaxmax = 0;
   Grid grid{};
   int ncell = 0, nrLJ = 1, nrI = 1;
@@ -77,7 +150,7 @@ struct ab_engine {
   DBuf<double4> pos, pos_tmp, xref;
   DBuf<double> vel, vel_tmp, F, io;
   DBuf<int> gid, gid_tmp, owner, key, key2, val, val2, cell_start, gcnt, goff;
-  DBuf<char4> shift;
+  DBuf<char4> shift, rshift;
   DBuf<signed char> typ;
   DBuf<int> ljc[3], ljn[3], in_cnt, in_nbr;  // LJ near / pure / band lists, intermediate list
   int capL[3] = {0, 0, 0};
@@ -104,7 +177,7 @@ struct ab_engine {
   unsigned long long* h_ct = nullptr;
   double* h_acc = nullptr;
   int* h_small = nullptr;
-  // results of the last evaluation
+  // results of the last evaluation (whole system: summed over domains / ranks)
   double E3[3] = {0, 0, 0}, W6[6] = {0, 0, 0, 0, 0, 0};
   unsigned long long last_ct[CT_N] = {0};
   // per-phase CUDA-event profiling (ab_set_profiling)
@@ -119,9 +192,39 @@ struct ab_engine {
   std::vector<cudaEvent_t> pool;
   int open_phase = -1;
   cudaEvent_t open_ev = nullptr;
+  // ---- slab decomposition; nranks == 1: whole box
+  int rank = 0, nranks = 1;
+  int Nglob = 0;                     // atoms of the whole system (caller arrays)
+  double xlo = 0, xhi = 0;           // owned slab [xlo, xhi) along x
+  std::vector<ab_engine*> subs;      // virtual mode: the domains driven by this handle
+  ab_engine* root = nullptr;         // a sub's handle
+  ncclComm_t comm = nullptr;         // NCCL mode
+  int ns[2] = {0, 0}, nr[2] = {0, 0};  // halo atoms sent to / ghosts received from (left, right)
+  DBuf<int> sendl[2];                // local indices of the halo atoms per channel
+  DBuf<unsigned char> sb[2], rb[2];  // transfer buffers per channel
+  size_t xs[2] = {0, 0}, xr[2] = {0, 0};  // bytes of the next transfer
+  DBuf<int> fl[3], idx[3];           // selection scratch (flags, selected indices)
+  DBuf<int> cnt_d;                   // selection counts (device)
+  DBuf<unsigned char> redx;          // all-reduce staging
+  DBuf<double> gio;                  // caller-order global array (3 Nglob) of a handle
+  unsigned long long h_flag[2] = {0, 0};
+  // host-side time breakdown of the NVE loop (AB_HOST_TIMING=1: printed by ab_destroy)
+  double host_ms[6] = {0, 0, 0, 0, 0, 0};  // integrate1+flags, speculative enqueue, wait, rebuild path, integrate2
+  long long host_steps = 0;
+  double rb_ms[4] = {0, 0, 0, 0};  // rebuild: sort, image count (sync), image fill + binning, lists (sync)
+  long long rb_n = 0;
 };
 
 namespace {
+
+const ab_engine* g_const_owner = nullptr;  // whose box / tables the __constant__ banks hold
+
+std::vector<ab_engine*> doms(ab_engine* e) {
+  if (e->subs.empty()) return {e};
+  return e->subs;
+}
+inline bool slabbed(const ab_engine* e) { return e->nranks > 1; }
+
 cudaEvent_t ev_get(ab_engine* e) {
   if (!e->pool.empty()) {
     cudaEvent_t x = e->pool.back();
@@ -132,18 +235,27 @@ cudaEvent_t ev_get(ab_engine* e) {
   cudaEventCreate(&x);
   return x;
 }
+// phase timing with events on the stream the phase runs on (phases may overlap on different
+// streams); prof_start returns nullptr when profiling is off
+cudaEvent_t prof_start(ab_engine* e, cudaStream_t s) {
+  if (!e->prof) return nullptr;
+  cudaEvent_t a = ev_get(e);
+  cudaEventRecord(a, s);
+  return a;
+}
+void prof_stop(ab_engine* e, int phase, cudaStream_t s, cudaEvent_t a) {
+  if (!a) return;
+  cudaEvent_t b = ev_get(e);
+  cudaEventRecord(b, s);
+  e->pending.push_back({phase, a, b});
+}
 void prof_begin(ab_engine* e, int phase) {
-  if (!e->prof) return;
   e->open_phase = phase;
-  e->open_ev = ev_get(e);
-  cudaEventRecord(e->open_ev, e->st);
+  e->open_ev = prof_start(e, e->st);
 }
 void prof_end(ab_engine* e) {
-  if (!e->prof || e->open_phase < 0) return;
-  cudaEvent_t b = ev_get(e);
-  cudaEventRecord(b, e->st);
-  e->pending.push_back({e->open_phase, e->open_ev, b});
-  e->open_phase = -1;
+  prof_stop(e, e->open_phase, e->st, e->open_ev);
+  e->open_ev = nullptr;
 }
 // call after a stream synchronisation
 void prof_collect(ab_engine* e) {
@@ -197,6 +309,23 @@ __global__ void k_fma_peak(T* out, int iters, T a, T b) {
     ab_status s_ = (x);          \
     if (s_ != AB_OK) return s_;  \
   } while (0)
+// per-domain call from a handle-level function: the domain's error text moves to the handle
+#define TRYD(d, x)                         \
+  do {                                     \
+    ab_status s_ = (x);                    \
+    if (s_ != AB_OK) {                     \
+      if ((d) != e) e->err = (d)->err;     \
+      return s_;                           \
+    }                                      \
+  } while (0)
+#define CKN(call)                                                                         \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess) {                                                              \
+      e->err = std::string("NCCL error: ") + NC.errStr(r_) + " at " #call;                \
+      return AB_E_NCCL;                                                                   \
+    }                                                                                     \
+  } while (0)
 
 namespace {
 
@@ -238,10 +367,23 @@ void fill_tab(const HostParams& hp, Tab<R>& t) {
         for (int l = 0; l < 2; ++l) t.tors[k][i][j][l] = (R)hp.tors[k][i][j][l];
 }
 
-ab_status upload_geo(ab_engine* e) {
+// host-side geometry of the engine (cutoffs, halo); no device work
+void geo_fields(ab_engine* e) {
+  double rmm = 0, rcm = 0;
+  for (int p = 0; p < 3; ++p) rmm = std::max(rmm, e->hp.pr[p].rmax), rcm = std::max(rcm, e->hp.pr[p].rc);
+  e->rmaxmax = rmm;
+  e->rcmax = rcm;
+  e->halo = rcm + e->hp.skin;  // LJ cutoff + skin covers every REBO/torsion/C_ij/b* reach
+}
+
+// The __constant__ banks (box, cutoffs, parameter tables) are per process: (re)load them when a
+// different handle than the last one launches kernels (several engines may live in one process).
+ab_status bind_consts(ab_engine* e) {
+  const ab_engine* owner = e->root ? e->root : e;
+  if (g_const_owner == owner) return AB_OK;
   Geo g;
   const HostParams& hp = e->hp;
-  double rmm = 0, rcm = 0;
+  double rmm = 0;
   for (int p = 0; p < 3; ++p) {
     const PairSet& s = hp.pr[p];
     g.rmax2[p] = s.rmax * s.rmax;
@@ -252,15 +394,14 @@ ab_status upload_geo(ab_engine* e) {
     double srhi = s.sigma * 1.122462048309373;
     g.srhi2_hi[p] = srhi * srhi * (1.0 + 1e-9);
     rmm = std::max(rmm, s.rmax);
-    rcm = std::max(rcm, s.rc);
   }
   g.reach2 = (3 * rmm) * (3 * rmm);
   for (int c = 0; c < 3; ++c) g.L[c] = e->L[c];
   g.mass[0] = hp.mass[0], g.mass[1] = hp.mass[1], g.ftm2v = hp.ftm2v, g.mvv2e = hp.mvv2e;
-  e->rmaxmax = rmm;
-  e->rcmax = rcm;
-  e->halo = rcm + hp.skin;  // LJ cutoff + skin covers every REBO/torsion/C_ij/b* reach
   CK(cudaMemcpyToSymbolAsync(c_geo, &g, sizeof(Geo), 0, cudaMemcpyHostToDevice, e->st));
+  CK(cudaMemcpyToSymbolAsync(c_tabd, &e->td, sizeof(e->td), 0, cudaMemcpyHostToDevice, e->st));
+  CK(cudaMemcpyToSymbolAsync(c_tabf, &e->tf, sizeof(e->tf), 0, cudaMemcpyHostToDevice, e->st));
+  g_const_owner = owner;
   return AB_OK;
 }
 
@@ -293,25 +434,105 @@ ab_status ensure_short(ab_engine* e) {
   return AB_OK;
 }
 
+// grow a position / index array to cap entries keeping the first keep entries
+template <class T>
+ab_status grow_keep(ab_engine* e, DBuf<T>& b, size_t cap, size_t keep) {
+  if (b.n >= cap && b.p) return AB_OK;
+  DBuf<T> nb;
+  CK(nb.ensure(cap + cap / 8));
+  keep = b.p ? std::min(keep, b.n) : 0;
+  if (keep) CK(cudaMemcpyAsync(nb.p, b.p, sizeof(T) * keep, cudaMemcpyDeviceToDevice, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  b.release();
+  b = nb;
+  return AB_OK;
+}
+
+// stable index selection: out = indices q < n with flag[q] != 0 (in order), count at *num
+ab_status select_flagged(ab_engine* e, int n, const int* flags, int* out, int* num) {
+  thrust::counting_iterator<int> it(0);
+  size_t need = 0;
+  cub::DeviceSelect::Flagged(nullptr, need, it, flags, out, num, n, e->st);
+  CK(e->cub_tmp.ensure(need));
+  size_t have = e->cub_tmp.n;
+  CK(cub::DeviceSelect::Flagged(e->cub_tmp.p, have, it, flags, out, num, n, e->st));
+  ++e->launches;
+  return AB_OK;
+}
+
+// ---------------------------------------------------------------- transfer between domains
+// Channel 0 goes to / comes from the left neighbour (rank - 1), channel 1 the right one (rank + 1),
+// periodic.  Each domain sends sb[c] (xs[c] bytes) and receives rb[c] (xr[c] bytes); what the
+// left neighbour sends on its channel 1 arrives in my rb[0] and vice versa.  NCCL order per
+// rank: send(left) recv(right) send(right) recv(left) -- with two ranks (left == right) the pairs
+// match in issue order: my first send lands in the peer's first receive (its rb[1]).
+ab_status xfer(ab_engine* e) {
+  if (!slabbed(e)) return AB_OK;
+  if (!e->subs.empty()) {
+    const int n = (int)e->subs.size();
+    for (int r = 0; r < n; ++r) {
+      ab_engine* d = e->subs[r];
+      ab_engine* left = e->subs[(r + n - 1) % n];
+      ab_engine* right = e->subs[(r + 1) % n];
+      if (d->xr[0] != left->xs[1] || d->xr[1] != right->xs[0]) {
+        e->err = "internal: halo transfer sizes disagree between domains";
+        return AB_E_STATE;
+      }
+      if (d->xr[0]) CK(cudaMemcpyAsync(d->rb[0].p, left->sb[1].p, d->xr[0], cudaMemcpyDeviceToDevice, e->st));
+      if (d->xr[1]) CK(cudaMemcpyAsync(d->rb[1].p, right->sb[0].p, d->xr[1], cudaMemcpyDeviceToDevice, e->st));
+    }
+    return AB_OK;
+  }
+  NcclApi& NC = nccl(e->err);
+  if (!NC.ok || !e->comm) return AB_E_NCCL;
+  const int left = (e->rank + e->nranks - 1) % e->nranks, right = (e->rank + 1) % e->nranks;
+  CKN(NC.groupStart());
+  if (e->xs[0]) CKN(NC.send(e->sb[0].p, e->xs[0], ncclUint8, left, e->comm, e->st));
+  if (e->xr[1]) CKN(NC.recv(e->rb[1].p, e->xr[1], ncclUint8, right, e->comm, e->st));
+  if (e->xs[1]) CKN(NC.send(e->sb[1].p, e->xs[1], ncclUint8, right, e->comm, e->st));
+  if (e->xr[0]) CKN(NC.recv(e->rb[0].p, e->xr[0], ncclUint8, left, e->comm, e->st));
+  CKN(NC.groupEnd());
+  return AB_OK;
+}
+
+ab_status ensure_xbufs(ab_engine* e, size_t s0, size_t s1, size_t r0, size_t r1) {
+  CK(e->sb[0].ensure(s0 + 16));
+  CK(e->sb[1].ensure(s1 + 16));
+  CK(e->rb[0].ensure(r0 + 16));
+  CK(e->rb[1].ensure(r1 + 16));
+  e->xs[0] = s0, e->xs[1] = s1, e->xr[0] = r0, e->xr[1] = r1;
+  return AB_OK;
+}
+
+// image shift of the ghosts received on a channel (periodic wrap across x = 0 / x = L)
+inline int chan_sx(const ab_engine* d, int c) {
+  if (c == 0) return d->rank == 0 ? -1 : 0;
+  return d->rank == d->nranks - 1 ? 1 : 0;
+}
+
 // ---------------------------------------------------------------- list build
-ab_status rebuild_impl(ab_engine* e) {
-  const int N = e->N;
-  cudaStream_t st = e->st;
+void setup_grid(ab_engine* e) {
   const double h = e->halo;
-  // cell grid over the padded region [-h, L+h): edge >= (r_c,max + skin)/3 >= r_max + skin
+  // cell grid over the padded region: edge >= (r_c,max + skin)/3 >= r_max + skin
   double cs_t = std::max((e->rcmax + e->hp.skin) / 3.0, e->rmaxmax + e->hp.skin);
   double csmin = 1e300;
   for (int c = 0; c < 3; ++c) {
-    double span = e->L[c] + 2 * h;
+    double lo = -h, span = e->L[c] + 2 * h;
+    if (c == 0 && slabbed(e)) lo = e->xlo - h, span = (e->xhi - e->xlo) + 2 * h;
     e->grid.nc[c] = std::max(1, (int)std::floor(span / cs_t));
     e->grid.cs[c] = span / e->grid.nc[c];
-    e->grid.lo[c] = -h;
+    e->grid.lo[c] = lo;
     csmin = std::min(csmin, e->grid.cs[c]);
   }
   e->ncell = e->grid.nc[0] * e->grid.nc[1] * e->grid.nc[2];
   e->nrLJ = (int)std::ceil((e->rcmax + e->hp.skin) / csmin);
   e->nrI = (int)std::ceil((e->rmaxmax + e->hp.skin) / csmin);
-  // 1. wrap + spatial sort of the local atoms
+}
+
+// wrap + spatial sort of the local atoms (pos, vel, gid permuted together)
+ab_status sort_locals(ab_engine* e) {
+  const int N = e->N;
+  cudaStream_t st = e->st;
   CK(e->key.ensure(N));
   CK(e->val.ensure(N));
   CK(e->key2.ensure(N));
@@ -330,48 +551,59 @@ ab_status rebuild_impl(ab_engine* e) {
   k_permute<<<nblk(N, 256), 256, 0, st>>>(N, e->val2.p, e->pos.p, e->pos_tmp.p, e->vel.p, e->vel_tmp.p, e->gid.p,
                                           e->gid_tmp.p);
   CKL();
-  CK(cudaMemcpyAsync(e->pos.p, e->pos_tmp.p, sizeof(double4) * N, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(e->vel.p, e->vel_tmp.p, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(e->gid.p, e->gid_tmp.p, sizeof(int) * N, cudaMemcpyDeviceToDevice, st));
-  // 2. periodic images (ghosts) within the halo
+  if (N) {
+    CK(cudaMemcpyAsync(e->pos.p, e->pos_tmp.p, sizeof(double4) * N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(e->vel.p, e->vel_tmp.p, sizeof(double) * 3 * N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(e->gid.p, e->gid_tmp.p, sizeof(int) * N, cudaMemcpyDeviceToDevice, st));
+  }
+  return AB_OK;
+}
+
+// images of the base atoms [0, NX) + binning of all atoms + skinned lists.  On entry: locals
+// sorted at [0, N), x-ghosts (slab domains) at [N, NX) with their bookkeeping set.
+ab_status images_and_lists(ab_engine* e) {
+  const int N = e->N, NB = e->NX;
+  cudaStream_t st = e->st;
+  const double h = e->halo;
+  // 2. periodic images (ghosts) within the halo: all three directions on a whole-box domain, y/z
+  // only on a slab domain (its x halo came from the neighbours)
   int3 smax = make_int3((int)std::ceil(h / e->L[0]), (int)std::ceil(h / e->L[1]), (int)std::ceil(h / e->L[2]));
-  CK(e->gcnt.ensure(N));
-  CK(e->goff.ensure(N));
-  k_ghost_count<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, smax, h, e->gcnt.p);
+  double3 lo = make_double3(-h, -h, -h), hi = make_double3(e->L[0] + h, e->L[1] + h, e->L[2] + h);
+  if (slabbed(e)) smax.x = 0, lo.x = e->xlo - h, hi.x = e->xhi + h;
+  CK(e->gcnt.ensure(NB));
+  CK(e->goff.ensure(NB));
+  k_image_count<<<nblk(NB, 256), 256, 0, st>>>(NB, e->pos.p, smax, lo, hi, e->gcnt.p);
   CKL();
-  need = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, need, e->gcnt.p, e->goff.p, N, st);
+  size_t need = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, need, e->gcnt.p, e->goff.p, NB, st);
   CK(e->cub_tmp.ensure(need));
-  have = e->cub_tmp.n;
-  CK(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, have, e->gcnt.p, e->goff.p, N, st));
+  size_t have = e->cub_tmp.n;
+  CK(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, have, e->gcnt.p, e->goff.p, NB, st));
   ++e->launches;
-  int tail[2];
-  CK(cudaMemcpyAsync(&tail[0], e->goff.p + N - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&tail[1], e->gcnt.p + N - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int tail[2] = {0, 0};
+  if (NB) {
+    CK(cudaMemcpyAsync(&tail[0], e->goff.p + NB - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&tail[1], e->gcnt.p + NB - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+  auto tq = std::chrono::steady_clock::now();
   CK(cudaStreamSynchronize(st));
-  e->G = tail[0] + tail[1];
-  e->NT = N + e->G;
+  auto tms = [](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  };
+  e->rb_ms[1] += tms(tq);
+  tq = std::chrono::steady_clock::now();
+  e->NT = NB + tail[0] + tail[1];
+  e->G = e->NT - N;
   const int NT = e->NT;
-  if (e->pos.n < (size_t)NT) {  // grow, keeping the local part
-    DBuf<double4> np;
-    CK(np.ensure((size_t)NT + NT / 8));
-    CK(cudaMemcpyAsync(np.p, e->pos.p, sizeof(double4) * N, cudaMemcpyDeviceToDevice, st));
-    CK(cudaStreamSynchronize(st));
-    e->pos.release();
-    e->pos = np;
-  }
-  if (e->gid.n < (size_t)NT) {
-    DBuf<int> ng;
-    CK(ng.ensure((size_t)NT + NT / 8));
-    CK(cudaMemcpyAsync(ng.p, e->gid.p, sizeof(int) * N, cudaMemcpyDeviceToDevice, st));
-    CK(cudaStreamSynchronize(st));
-    e->gid.release();
-    e->gid = ng;
-  }
-  CK(e->owner.ensure(NT));
-  CK(e->shift.ensure(NT));
+  TRY(grow_keep(e, e->pos, NT, NB));
+  TRY(grow_keep(e, e->gid, NT, NB));
+  TRY(grow_keep(e, e->owner, NT, NB));
+  TRY(grow_keep(e, e->shift, NT, NB));
+  TRY(grow_keep(e, e->rshift, NT, NB));
   CK(e->typ.ensure(NT));
-  k_ghost_fill<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, smax, h, e->goff.p, e->owner.p, e->gid.p, e->shift.p);
+  CK(e->F.ensure(3 * (size_t)NT));
+  k_image_fill<<<nblk(NB, 256), 256, 0, st>>>(NB, N, NB, e->pos.p, smax, lo, hi, e->goff.p, e->owner.p, e->gid.p,
+                                             e->shift.p, e->rshift.p);
   CKL();
   k_types<<<nblk(NT, 256), 256, 0, st>>>(NT, e->pos.p, e->typ.p);
   CKL();
@@ -391,6 +623,8 @@ ab_status rebuild_impl(ab_engine* e) {
   ++e->launches;
   k_cell_bounds<<<nblk(NT + 1, 256), 256, 0, st>>>(NT, e->ncell, e->key2.p, e->cell_start.p);
   CKL();
+  e->rb_ms[2] += tms(tq);
+  tq = std::chrono::steady_clock::now();
   // 4. skinned lists: LJ (local atoms, full) and intermediate REBO (all atoms)
   CK(e->small_i.ensure(8));
   for (int c = 0; c < 3; ++c) CK(e->ljc[c].ensure(N));
@@ -398,7 +632,9 @@ ab_status rebuild_impl(ab_engine* e) {
   const double skin = e->hp.skin;
   const double rnear = 3 * e->rmaxmax + skin;
   if (e->capL[0] == 0) {  // first build: capacities from the mean density (grown on overflow)
-    double rho = N / (e->L[0] * e->L[1] * e->L[2]), fpi = 4.18879020478639;
+    double vol = e->L[0] * e->L[1] * e->L[2];
+    if (slabbed(e)) vol = (e->xhi - e->xlo) * e->L[1] * e->L[2];
+    double rho = std::max(N, 1) / vol, fpi = 4.18879020478639;
     double rlo_max = 0;
     for (int p = 0; p < 3; ++p) rlo_max = std::max(rlo_max, e->hp.pr[p].rlo);
     double r1 = std::max(rnear, rlo_max - skin), r2 = e->rcmax + skin;
@@ -441,6 +677,7 @@ ab_status rebuild_impl(ab_engine* e) {
   }
   e->capS = std::min(e->capI, 32);
   TRY(ensure_short(e));
+  e->rb_ms[3] += tms(tq);
   CK(e->xref.ensure(N));
   k_copy_xref<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->xref.p);
   CKL();
@@ -449,15 +686,202 @@ ab_status rebuild_impl(ab_engine* e) {
   return AB_OK;
 }
 
-ab_status rebuild(ab_engine* e) {
-  prof_begin(e, 5);
-  ab_status s = rebuild_impl(e);
-  prof_end(e);
-  return s;
+// ---- slab rebuild phases (per domain; the handle transfers between them)
+// M1: wrap, classify, select stayers / leavers; leaver counts into sb[c]
+ab_status mig_select(ab_engine* e) {
+  const int N = e->N;
+  cudaStream_t st = e->st;
+  for (int c = 0; c < 3; ++c) {
+    CK(e->fl[c].ensure(N));
+    CK(e->idx[c].ensure(N));
+  }
+  CK(e->cnt_d.ensure(8));
+  TRY(ensure_xbufs(e, 4, 4, 4, 4));
+  CK(cudaMemsetAsync(e->cnt_d.p, 0, 8 * sizeof(int), st));
+  k_wrap<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p);
+  CKL();
+  k_mig_flags<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->nranks, e->rank, e->fl[0].p, e->fl[1].p, e->fl[2].p,
+                                            reinterpret_cast<unsigned long long*>(e->cnt_d.p + 4));
+  CKL();
+  TRY(select_flagged(e, N, e->fl[0].p, e->idx[0].p, e->cnt_d.p));
+  TRY(select_flagged(e, N, e->fl[1].p, e->idx[1].p, reinterpret_cast<int*>(e->sb[0].p)));
+  TRY(select_flagged(e, N, e->fl[2].p, e->idx[2].p, reinterpret_cast<int*>(e->sb[1].p)));
+  return AB_OK;
 }
 
+// M2 (after the count transfer): pack the migrants' records into sb[c]
+ab_status mig_pack(ab_engine* e) {
+  cudaStream_t st = e->st;
+  int h[8];
+  int rin[2];
+  CK(cudaMemcpyAsync(h, e->cnt_d.p, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  int sent[2];
+  CK(cudaMemcpyAsync(&sent[0], e->sb[0].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&sent[1], e->sb[1].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&rin[0], e->rb[0].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&rin[1], e->rb[1].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  unsigned long long bad;
+  std::memcpy(&bad, &h[4], sizeof(bad));
+  if (bad) {
+    e->err = "an atom crossed more than one slab between two list builds (rank " + std::to_string(e->rank) + ")";
+    return AB_E_STATE;
+  }
+  e->ns[0] = sent[0], e->ns[1] = sent[1];  // reused as migrant counts until the halo selection
+  e->nr[0] = rin[0], e->nr[1] = rin[1];
+  e->NX = h[0];                            // stayers
+  const size_t rec = 8 * sizeof(double);
+  TRY(ensure_xbufs(e, rec * sent[0], rec * sent[1], rec * rin[0], rec * rin[1]));
+  for (int c = 0; c < 2; ++c) {
+    k_mig_pack<<<nblk(sent[c], 128), 128, 0, st>>>(sent[c], e->idx[1 + c].p, e->pos.p, e->vel.p, e->gid.p,
+                                                   reinterpret_cast<double*>(e->sb[c].p));
+    CKL();
+  }
+  return AB_OK;
+}
+
+// M3 (after the payload transfer): new local set = stayers + arrivals
+ab_status mig_assemble(ab_engine* e) {
+  cudaStream_t st = e->st;
+  const int nstay = e->NX, n0 = e->nr[0], n1 = e->nr[1];
+  const int Nn = nstay + n0 + n1;
+  CK(e->pos_tmp.ensure((size_t)Nn + 64));
+  CK(e->vel_tmp.ensure(3 * (size_t)Nn + 3));
+  CK(e->gid_tmp.ensure((size_t)Nn + 64));
+  k_mig_assemble<<<nblk(Nn, 256), 256, 0, st>>>(nstay, e->idx[0].p, e->pos.p, e->vel.p, e->gid.p, n0,
+                                                reinterpret_cast<const double*>(e->rb[0].p), n1,
+                                                reinterpret_cast<const double*>(e->rb[1].p), e->pos_tmp.p,
+                                                e->vel_tmp.p, e->gid_tmp.p);
+  CKL();
+  // the assembled arrays become the state (no buffer is freed under a pending kernel)
+  std::swap(e->pos, e->pos_tmp);
+  std::swap(e->vel, e->vel_tmp);
+  std::swap(e->gid, e->gid_tmp);
+  e->N = Nn;
+  CK(e->F.ensure(3 * (size_t)Nn + 3));
+  return AB_OK;
+}
+
+// H1 (locals sorted): halo send lists, counts into sb[c]
+ab_status halo_select(ab_engine* e) {
+  const int N = e->N;
+  cudaStream_t st = e->st;
+  for (int c = 0; c < 2; ++c) {
+    CK(e->fl[c].ensure(N));
+    CK(e->sendl[c].ensure(N));
+  }
+  TRY(ensure_xbufs(e, 4, 4, 4, 4));
+  k_halo_flags<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->xlo, e->xhi, e->halo, e->fl[0].p, e->fl[1].p);
+  CKL();
+  for (int c = 0; c < 2; ++c)
+    TRY(select_flagged(e, N, e->fl[c].p, e->sendl[c].p, reinterpret_cast<int*>(e->sb[c].p)));
+  return AB_OK;
+}
+
+// per step (and H2): positions of the halo atoms into sb[c]
+ab_status halo_pack(ab_engine* e) {
+  TRY(ensure_xbufs(e, 32 * (size_t)e->ns[0], 32 * (size_t)e->ns[1], 32 * (size_t)e->nr[0], 32 * (size_t)e->nr[1]));
+  k_halo_pack<<<nblk(e->ns[0] + e->ns[1], 128), 128, 0, e->st>>>(
+      e->ns[0], e->sendl[0].p, e->ns[1], e->sendl[1].p, e->pos.p, reinterpret_cast<double4*>(e->sb[0].p),
+      reinterpret_cast<double4*>(e->sb[1].p));
+  CKL();
+  return AB_OK;
+}
+
+// H2 (after the count transfer): read the halo sizes, size the ghost slots, pack positions
+ab_status halo_size(ab_engine* e) {
+  cudaStream_t st = e->st;
+  int v[4];
+  CK(cudaMemcpyAsync(&v[0], e->sb[0].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&v[1], e->sb[1].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&v[2], e->rb[0].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&v[3], e->rb[1].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  e->ns[0] = v[0], e->ns[1] = v[1], e->nr[0] = v[2], e->nr[1] = v[3];
+  e->NX = e->N + v[2] + v[3];
+  return halo_pack(e);
+}
+
+// per step: received halo positions into the x-ghost slots
+ab_status halo_unpack(ab_engine* e) {
+  k_halo_unpack<<<nblk(e->nr[0] + e->nr[1], 128), 128, 0, e->st>>>(
+      e->N, e->nr[0], reinterpret_cast<const double4*>(e->rb[0].p), chan_sx(e, 0), e->nr[1],
+      reinterpret_cast<const double4*>(e->rb[1].p), chan_sx(e, 1), e->pos.p);
+  CKL();
+  return AB_OK;
+}
+
+// H3 (after the payload transfer): x-ghosts in place, then images, binning and lists
+ab_status halo_finish(ab_engine* e) {
+  const int NX = e->NX;
+  TRY(grow_keep(e, e->pos, (size_t)NX + 64, e->N));
+  TRY(grow_keep(e, e->gid, (size_t)NX + 64, e->N));
+  TRY(grow_keep(e, e->owner, (size_t)NX + 64, 0));
+  TRY(grow_keep(e, e->shift, (size_t)NX + 64, 0));
+  TRY(grow_keep(e, e->rshift, (size_t)NX + 64, 0));
+  TRY(halo_unpack(e));
+  k_xghost_meta<<<nblk(e->nr[0] + e->nr[1], 128), 128, 0, e->st>>>(e->N, e->nr[0], chan_sx(e, 0), e->nr[1],
+                                                                   chan_sx(e, 1), e->pos.p, e->owner.p, e->gid.p,
+                                                                   e->shift.p, e->rshift.p);
+  CKL();
+  return images_and_lists(e);
+}
+
+ab_status rebuild_all(ab_engine* e) {
+  prof_begin(e, 5);
+  auto D = doms(e);
+  if (!slabbed(e)) {
+    auto t0 = std::chrono::steady_clock::now();
+    setup_grid(e);
+    TRY(sort_locals(e));
+    e->rb_ms[0] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    e->NX = e->N;
+    TRY(images_and_lists(e));
+    ++e->rb_n;
+  } else {
+    for (ab_engine* d : D) setup_grid(d);
+    for (ab_engine* d : D) TRYD(d, mig_select(d));
+    TRY(xfer(e));  // migrant counts
+    for (ab_engine* d : D) TRYD(d, mig_pack(d));
+    TRY(xfer(e));  // migrant records
+    for (ab_engine* d : D) TRYD(d, mig_assemble(d));
+    for (ab_engine* d : D) TRYD(d, sort_locals(d));
+    for (ab_engine* d : D) TRYD(d, halo_select(d));
+    TRY(xfer(e));  // halo counts
+    for (ab_engine* d : D) TRYD(d, halo_size(d));
+    TRY(xfer(e));  // halo positions
+    for (ab_engine* d : D) TRYD(d, halo_finish(d));
+    if (e != D[0]) ++e->rebuilds;
+  }
+  e->lists_valid = true;
+  prof_end(e);
+  return AB_OK;
+}
+
+// ghosts follow the owned atoms (every step without a rebuild)
+ab_status refresh_ghosts_all(ab_engine* e) {
+  auto D = doms(e);
+  if (slabbed(e)) {
+    for (ab_engine* d : D) TRYD(d, halo_pack(d));
+    TRY(xfer(e));
+    for (ab_engine* d : D) TRYD(d, halo_unpack(d));
+  }
+  for (ab_engine* d : D)
+    if (d->NT > d->NX) {
+      k_image_update<<<nblk(d->NT - d->NX, 256), 256, 0, d->st>>>(d->NX, d->NT, d->pos.p, d->owner.p, d->rshift.p);
+      ++d->launches;
+      cudaError_t ce = cudaGetLastError();
+      if (ce != cudaSuccess) {
+        e->err = std::string("CUDA launch error: ") + cudaGetErrorString(ce);
+        return AB_E_CUDA;
+      }
+    }
+  return AB_OK;
+}
+
+// ---------------------------------------------------------------- force evaluation
 template <typename R>
-ab_status forces_impl(ab_engine* e, bool sync_host) {
+ab_status enqueue_forces(ab_engine* e) {
   const int N = e->N, NT = e->NT;
   cudaStream_t st = e->st;
   StageBuf sb0{nullptr, nullptr, 0}, sb1{nullptr, nullptr, 0};
@@ -477,59 +901,83 @@ ab_status forces_impl(ab_engine* e, bool sync_host) {
       CK(e->q_M.ensure(e->capQ));
     }
   }
-  for (int attempt = 0; attempt < 3; ++attempt) {
-    CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * N, st));
-    CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
-    ShortList<R> S = short_view<R>(e);
-    // grids and the per-block partial rows of the energy / virial / counter reduction
-    const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
-    const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4, g_slow = e->nsm;
-    const int nrows = g_short + g_rebo + g_near + g_far + g_bstar + 2 * g_slow;
-    CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
-    CK(e->ovf_q.ensure(e->capQ));
-    CK(e->red_d.ensure((size_t)ACC_N * nrows));
-    CK(e->red_u.ensure((size_t)CT_N * nrows));
-    RedRows RR{e->red_d.p, e->red_u.p, nrows, 0};
-    prof_begin(e, 0);
+  CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * e->NX, st));
+  CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
+  ShortList<R> S = short_view<R>(e);
+  // grids and the per-block partial rows of the energy / virial / counter reduction
+  const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
+  const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4, g_slow = e->nsm;
+  const int nrows = g_short + g_rebo + g_near + g_far + g_bstar + 2 * g_slow;
+  CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
+  CK(e->ovf_q.ensure(e->capQ));
+  CK(e->red_d.ensure((size_t)ACC_N * nrows));
+  CK(e->red_u.ensure((size_t)CT_N * nrows));
+  RedRows RR{e->red_d.p, e->red_u.p, nrows, 0};
+  // Kernel DAG of one evaluation (the 32k-atom kernels each fill only part of the GPU, so the
+  // independent ones run concurrently): the far LJ pairs need only the skinned lists and start
+  // at once on aux[1]; REBO + torsion (aux[0]) and the near LJ pairs -> b* batch (main stream)
+  // need the short list.  Partial rows of the reduction are disjoint per kernel; F takes fp64
+  // atomics from all of them.
+  const cudaStream_t s_rebo = e->aux[0], s_far = e->aux[1];
+  CK(cudaEventRecord(e->ev_fork[1], st));
+  CK(cudaStreamWaitEvent(s_far, e->ev_fork[1], 0));
+  const int row_far = g_short + g_rebo + g_slow + g_near;
+  BstarQueue Qu{e->q_item.p, e->q_M.p, e->small_i.p + 1, e->capQ};
+  LJArgs A;
+  A.N = N;
+  A.pos = e->pos.p;
+  for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
+  {
+    cudaEvent_t t = prof_start(e, s_far);
+    RedRows R6 = RR;
+    R6.row0 = row_far;
+    if (e->want_virial)
+      k_lj_far<R, true><<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, R6);
+    else
+      k_lj_far<R, false><<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, R6);
+    CKL();
+    prof_stop(e, 6, s_far, t);
+  }
+  CK(cudaEventRecord(e->ev_join[1], s_far));
+  {
+    cudaEvent_t t = prof_start(e, st);
     k_short<R><<<g_short, 128, 0, st>>>(N, NT, e->pos.p, e->in_cnt.p, e->in_nbr.p, e->capI, S, e->gid.p,
                                         e->shift.p, e->bonds.p, e->small_i.p, e->ct.p, RR);
     CKL();
-    prof_end(e);
-    RR.row0 += g_short;
-    prof_begin(e, 1);
-    k_rebo<R, NB_FAST><<<g_rebo, 128, 0, st>>>(e->bonds.p, e->small_i.p, nullptr, e->ovf_bond.p, e->small_i.p + 8,
-                                               S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb0, RR);
+    prof_stop(e, 0, st, t);
+  }
+  CK(cudaEventRecord(e->ev_fork[0], st));
+  CK(cudaStreamWaitEvent(s_rebo, e->ev_fork[0], 0));
+  {
+    cudaEvent_t t = prof_start(e, s_rebo);
+    RedRows R1 = RR;
+    R1.row0 = g_short;
+    k_rebo<R, NB_FAST><<<g_rebo, 128, 0, s_rebo>>>(e->bonds.p, e->small_i.p, nullptr, e->ovf_bond.p,
+                                                   e->small_i.p + 8, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p,
+                                                   e->F.p, sb0, R1);
     CKL();
-    RR.row0 += g_rebo;
-    k_rebo<R, NBMAX><<<g_slow, 128, 0, st>>>(e->bonds.p, e->small_i.p, e->ovf_bond.p, nullptr, e->small_i.p + 8, S,
-                                             e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb0, RR);
+    R1.row0 += g_rebo;
+    k_rebo<R, NBMAX><<<g_slow, 128, 0, s_rebo>>>(e->bonds.p, e->small_i.p, e->ovf_bond.p, nullptr, e->small_i.p + 8,
+                                                 S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb0, R1);
     CKL();
-    RR.row0 += g_slow;
-    prof_end(e);
-    BstarQueue Qu{e->q_item.p, e->q_M.p, e->small_i.p + 1, e->capQ};
-    LJArgs A;
-    A.N = N;
-    A.pos = e->pos.p;
-    for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
-    prof_begin(e, 2);
+    prof_stop(e, 1, s_rebo, t);
+  }
+  CK(cudaEventRecord(e->ev_join[0], s_rebo));
+  RR.row0 = g_short + g_rebo + g_slow;
+  {
+    cudaEvent_t t = prof_start(e, st);
     if (e->want_virial)
-      k_lj_near<R, true><<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                                                     e->acc.p, e->ct.p, Qu, sb1, RR);
+      k_lj_near<R, true><<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p,
+                                                                     e->F.p, e->acc.p, e->ct.p, Qu, sb1, RR);
     else
-      k_lj_near<R, false><<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                                                      e->acc.p, e->ct.p, Qu, sb1, RR);
+      k_lj_near<R, false><<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p,
+                                                                      e->F.p, e->acc.p, e->ct.p, Qu, sb1, RR);
     CKL();
-    prof_end(e);
-    RR.row0 += g_near;
-    prof_begin(e, 6);
-    if (e->want_virial)
-      k_lj_far<R, true><<<g_far, 128, 0, st>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, RR);
-    else
-      k_lj_far<R, false><<<g_far, 128, 0, st>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, RR);
-    CKL();
-    prof_end(e);
-    RR.row0 += g_far;
-    prof_begin(e, 3);
+    prof_stop(e, 2, st, t);
+  }
+  RR.row0 = row_far + g_far;
+  {
+    cudaEvent_t t = prof_start(e, st);
     k_bstar<R, NB_FAST, false><<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->pos.p, S,
                                                         e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
     CKL();
@@ -537,97 +985,429 @@ ab_status forces_impl(ab_engine* e, bool sync_host) {
     k_bstar<R, NBMAX, true><<<g_slow, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, e->pos.p, S, e->typ.p,
                                                     e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
     CKL();
-    prof_end(e);
-    RR.row0 = 0;
-    k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows, e->acc.p, e->ct.p);
-    CKL();
-    if (!sync_host) {  // NVE steps: results stay on the device until somebody needs them
-      e->host_stale = true;
-      e->forces_valid = true;
-      return AB_OK;
-    }
-    CK(cudaMemcpyAsync(e->h_ct, e->ct.p, sizeof(unsigned long long) * CT_N, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(e->h_acc, e->acc.p, sizeof(double) * ACC_N, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    prof_collect(e);
-    if (e->h_ct[CT_OVF_SHORT]) {
-      e->err = "an atom has more than 16 REBO short-list neighbours (NBMAX); unsupported geometry";
-      return AB_E_STATE;
-    }
-    if (e->h_ct[CT_OVF_QUEUE]) {  // grow the b* queue and redo the evaluation
-      int need = (int)(e->h_ct[CT_BSTAR] + e->h_ct[CT_OVF_QUEUE]);
-      e->capQ = std::max(2 * e->capQ, need + need / 4 + 1024);
-      CK(e->q_item.ensure(e->capQ));
-      CK(e->q_M.ensure(e->capQ));
-      ++e->retries;
-      continue;
-    }
-    break;
+    prof_stop(e, 3, st, t);
   }
-  std::memcpy(e->last_ct, e->h_ct, sizeof(e->last_ct));
-  for (int c = 0; c < 3; ++c) e->E3[c] = e->h_acc[ACC_EREBO + c];
-  for (int c = 0; c < 6; ++c) e->W6[c] = e->h_acc[ACC_W + c];
+  CK(cudaStreamWaitEvent(st, e->ev_join[0], 0));
+  CK(cudaStreamWaitEvent(st, e->ev_join[1], 0));
+  RR.row0 = 0;
+  k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows, e->acc.p, e->ct.p);
+  CKL();
+  return AB_OK;
+}
+
+// reverse communication: forces on x-ghosts go home and are added to the owned atoms
+ab_status force_pack(ab_engine* e) {
+  TRY(ensure_xbufs(e, 32 * (size_t)e->nr[0], 32 * (size_t)e->nr[1], 32 * (size_t)e->ns[0], 32 * (size_t)e->ns[1]));
+  k_force_pack<<<nblk(e->nr[0] + e->nr[1], 128), 128, 0, e->st>>>(e->N, e->nr[0], e->nr[1], e->F.p,
+                                                                  reinterpret_cast<double4*>(e->sb[0].p),
+                                                                  reinterpret_cast<double4*>(e->sb[1].p));
+  CKL();
+  return AB_OK;
+}
+ab_status force_unpack(ab_engine* e) {
+  for (int c = 0; c < 2; ++c) {
+    k_force_unpack<<<nblk(e->ns[c], 128), 128, 0, e->st>>>(e->ns[c], e->sendl[c].p,
+                                                           reinterpret_cast<const double4*>(e->rb[c].p), e->F.p);
+    CKL();
+  }
+  return AB_OK;
+}
+
+ab_status nonfinite_or_ovf(ab_engine* e) {
+  if (e->last_ct[CT_OVF_SHORT]) {
+    e->err = "an atom has more than 16 REBO short-list neighbours (NBMAX); unsupported geometry";
+    return AB_E_STATE;
+  }
   if (!std::isfinite(e->E3[0] + e->E3[1] + e->E3[2])) {
     e->err = "non-finite energy";
     return AB_E_NONFINITE;
   }
-  e->forces_valid = true;
+  return AB_OK;
+}
+
+inline bool ct_max_col(int c) { return c == CT_MAXSHORT || c == CT_MAXREACH; }
+
+// energies / virial / counters of the last evaluation, summed over all domains and ranks
+ab_status collect(ab_engine* e) {
+  auto D = doms(e);
+  double acc[ACC_N] = {0};
+  unsigned long long ct[CT_N] = {0};
+  if (e->comm) {
+    NcclApi& NC = nccl(e->err);
+    if (!NC.ok) return AB_E_NCCL;
+    const size_t bd = sizeof(double) * ACC_N, bu = sizeof(unsigned long long) * CT_N;
+    CK(e->redx.ensure(bd + 2 * bu));
+    unsigned char* x = e->redx.p;
+    CK(cudaMemcpyAsync(x, e->acc.p, bd, cudaMemcpyDeviceToDevice, e->st));
+    CK(cudaMemcpyAsync(x + bd, e->ct.p, bu, cudaMemcpyDeviceToDevice, e->st));
+    CK(cudaMemcpyAsync(x + bd + bu, e->ct.p, bu, cudaMemcpyDeviceToDevice, e->st));
+    CKN(NC.groupStart());
+    CKN(NC.allReduce(x, x, ACC_N, ncclFloat64, ncclSum, e->comm, e->st));
+    CKN(NC.allReduce(x + bd, x + bd, CT_N, ncclUint64, ncclSum, e->comm, e->st));
+    CKN(NC.allReduce(x + bd + bu, x + bd + bu, CT_N, ncclUint64, ncclMax, e->comm, e->st));
+    CKN(NC.groupEnd());
+    unsigned long long mx[CT_N];
+    CK(cudaMemcpyAsync(acc, x, bd, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(ct, x + bd, bu, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(mx, x + bd + bu, bu, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaStreamSynchronize(e->st));
+    for (int c = 0; c < CT_N; ++c)
+      if (ct_max_col(c)) ct[c] = mx[c];
+  } else {
+    for (ab_engine* d : D) {
+      CK(cudaMemcpyAsync(d->h_ct, d->ct.p, sizeof(unsigned long long) * CT_N, cudaMemcpyDeviceToHost, e->st));
+      CK(cudaMemcpyAsync(d->h_acc, d->acc.p, sizeof(double) * ACC_N, cudaMemcpyDeviceToHost, e->st));
+    }
+    CK(cudaStreamSynchronize(e->st));
+    for (ab_engine* d : D) {  // fixed domain order: deterministic sums
+      for (int c = 0; c < ACC_N; ++c) acc[c] += d->h_acc[c];
+      for (int c = 0; c < CT_N; ++c) ct[c] = ct_max_col(c) ? std::max(ct[c], d->h_ct[c]) : ct[c] + d->h_ct[c];
+    }
+  }
+  for (ab_engine* d : D) prof_collect(d);
+  if (e != D[0]) prof_collect(e);
+  std::memcpy(e->last_ct, ct, sizeof(ct));
+  for (int c = 0; c < 3; ++c) e->E3[c] = acc[ACC_EREBO + c];
+  for (int c = 0; c < 6; ++c) e->W6[c] = acc[ACC_W + c];
   e->host_stale = false;
   return AB_OK;
 }
 
-ab_status forces(ab_engine* e, bool sync_host = true) {
-  return e->prec == AB_FP64 ? forces_impl<double>(e, sync_host) : forces_impl<float>(e, sync_host);
+ab_status forces_all(ab_engine* e, bool sync_host = true) {
+  auto D = doms(e);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    for (ab_engine* d : D) TRYD(d, d->prec == AB_FP64 ? enqueue_forces<double>(d) : enqueue_forces<float>(d));
+    if (slabbed(e)) {
+      for (ab_engine* d : D) TRYD(d, force_pack(d));
+      TRY(xfer(e));
+      for (ab_engine* d : D) TRYD(d, force_unpack(d));
+    }
+    e->forces_valid = true;
+    if (!sync_host) {  // NVE steps: results stay on the device until somebody needs them
+      e->host_stale = true;
+      return AB_OK;
+    }
+    TRY(collect(e));
+    if (e->last_ct[CT_OVF_QUEUE] && !e->last_ct[CT_OVF_SHORT]) {  // grow the b* queue and redo
+      for (ab_engine* d : D) {
+        long long need = (long long)(e->last_ct[CT_BSTAR] + e->last_ct[CT_OVF_QUEUE]);
+        d->capQ = (int)std::min<long long>(std::max<long long>(2ll * d->capQ, need + need / 4 + 1024), 1ll << 30);
+        TRYD(d, d->q_item.ensure(d->capQ) == cudaSuccess && d->q_M.ensure(d->capQ) == cudaSuccess ? AB_OK : AB_E_OOM);
+        ++d->retries;
+      }
+      continue;
+    }
+    break;
+  }
+  return nonfinite_or_ovf(e);
 }
 
 // bring energies / virial / counters of the last (asynchronous) evaluation to the host
 ab_status pull_results(ab_engine* e) {
   if (!e->host_stale) return AB_OK;
-  CK(cudaMemcpyAsync(e->h_ct, e->ct.p, sizeof(unsigned long long) * CT_N, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaMemcpyAsync(e->h_acc, e->acc.p, sizeof(double) * ACC_N, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaStreamSynchronize(e->st));
-  prof_collect(e);
-  e->host_stale = false;
-  if (e->h_ct[CT_OVF_SHORT]) {
-    e->err = "an atom has more than 16 REBO short-list neighbours (NBMAX); unsupported geometry";
-    return AB_E_STATE;
+  TRY(collect(e));
+  return nonfinite_or_ovf(e);
+}
+
+// max displacement^2 since the last build over all domains / ranks (d2 slot ct[CT_N]) plus the
+// short-list overflow flag: enqueue the read-back into e->h_flag (valid after a sync)
+ab_status enqueue_flags(ab_engine* e) {
+  auto D = doms(e);
+  if (e->comm) {
+    NcclApi& NC = nccl(e->err);
+    if (!NC.ok) return AB_E_NCCL;
+    CK(e->redx.ensure(64));
+    unsigned long long* f = reinterpret_cast<unsigned long long*>(e->redx.p);
+    k_flags2<<<1, 1, 0, e->st>>>(e->ct.p, CT_OVF_SHORT, CT_N, f);
+    CKL();
+    CKN(NC.allReduce(f, f, 2, ncclUint64, ncclMax, e->comm, e->st));
+    CK(cudaMemcpyAsync(e->h_flag, f, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->st));
+    return AB_OK;
   }
-  std::memcpy(e->last_ct, e->h_ct, sizeof(e->last_ct));
-  for (int c = 0; c < 3; ++c) e->E3[c] = e->h_acc[ACC_EREBO + c];
-  for (int c = 0; c < 6; ++c) e->W6[c] = e->h_acc[ACC_W + c];
-  if (!std::isfinite(e->E3[0] + e->E3[1] + e->E3[2])) {
-    e->err = "non-finite energy";
-    return AB_E_NONFINITE;
-  }
+  for (ab_engine* d : D)
+    CK(cudaMemcpyAsync(d->h_ct, d->ct.p, sizeof(unsigned long long) * (CT_N + 1), cudaMemcpyDeviceToHost, e->st));
   return AB_OK;
+}
+// after the sync: combine into h_flag
+void read_flags(ab_engine* e) {
+  if (e->comm) return;
+  e->h_flag[0] = e->h_flag[1] = 0;
+  for (ab_engine* d : doms(e)) {
+    e->h_flag[0] = std::max(e->h_flag[0], d->h_ct[CT_N]);
+    e->h_flag[1] = std::max(e->h_flag[1], d->h_ct[CT_OVF_SHORT]);
+  }
+}
+double flag_d2(const ab_engine* e) {
+  double d2;
+  std::memcpy(&d2, &e->h_flag[0], sizeof(d2));
+  return d2;
 }
 
 // make lists valid for the current positions (rebuild if needed, else move the ghosts)
-ab_status prepare(ab_engine* e, bool check_disp) {
-  if (!e->lists_valid) return rebuild(e);
+ab_status prepare_all(ab_engine* e, bool check_disp) {
+  if (!e->lists_valid) return rebuild_all(e);
   if (check_disp) {
-    CK(cudaMemsetAsync(e->ct.p + CT_N, 0, sizeof(unsigned long long), e->st));
-    k_maxdisp<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->pos.p, e->xref.p, e->ct.p + CT_N);
-    CKL();
-    unsigned long long bits;
-    CK(cudaMemcpyAsync(&bits, e->ct.p + CT_N, sizeof(bits), cudaMemcpyDeviceToHost, e->st));
+    for (ab_engine* d : doms(e)) {
+      CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), e->st));
+      k_maxdisp<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->pos.p, d->xref.p, d->ct.p + CT_N);
+      CKL();
+    }
+    TRY(enqueue_flags(e));
     CK(cudaStreamSynchronize(e->st));
-    double d2;
-    std::memcpy(&d2, &bits, sizeof(d2));
+    read_flags(e);
     double half = 0.5 * e->hp.skin;
-    if (d2 > half * half) return rebuild(e);
+    if (flag_d2(e) > half * half) return rebuild_all(e);
   }
-  if (e->NT > e->N) {
-    k_ghost_update<<<nblk(e->NT - e->N, 256), 256, 0, e->st>>>(e->N, e->NT, e->pos.p, e->owner.p, e->shift.p);
-    CKL();
-  }
-  return AB_OK;
+  return refresh_ghosts_all(e);
 }
 
 bool bad_ptr(ab_engine* e, const void* p, const char* what) {
   if (p) return false;
   e->err = std::string("NULL pointer: ") + what;
   return true;
+}
+
+// ---- engine construction (shared by the three modes)
+ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision prec, int device) {
+  std::string perr = parse_host_params(text, len, e->hp);
+  if (!perr.empty()) {
+    e->err = perr;
+    return AB_E_PARAM;
+  }
+  e->prec = prec;
+  e->dev = device;
+  cudaDeviceProp prop;
+  if (cudaSetDevice(device) != cudaSuccess || cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    e->err = "no CUDA device " + std::to_string(device);
+    cudaGetLastError();
+    return AB_E_CUDA;
+  }
+  if (prop.major != 10) {
+    e->err = std::string("device is not sm_100 (Blackwell): ") + prop.name;
+    return AB_E_CUDA;
+  }
+  std::snprintf(e->devname, sizeof(e->devname), "%s", prop.name);
+  e->nsm = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking) != cudaSuccess) {
+    e->err = "cudaStreamCreate failed";
+    return AB_E_CUDA;
+  }
+  e->st = e->own;
+  for (int c = 0; c < 2; ++c)
+    if (cudaStreamCreateWithFlags(&e->aux[c], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_fork[c], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&e->ev_join[c], cudaEventDisableTiming) != cudaSuccess) {
+      e->err = "cudaStreamCreate / cudaEventCreate failed";
+      return AB_E_CUDA;
+    }
+  fill_tab(e->hp, e->td);
+  fill_tab(e->hp, e->tf);
+  geo_fields(e);
+  bool ok = e->scratch.ensure(SCRATCH_BYTES) == cudaSuccess &&
+            cudaMemset(e->scratch.p, 0, SCRATCH_BYTES) == cudaSuccess &&
+            cudaMallocHost(&e->h_ct, sizeof(unsigned long long) * (CT_N + 1)) == cudaSuccess &&
+            cudaMallocHost(&e->h_acc, sizeof(double) * ACC_N) == cudaSuccess &&
+            cudaMallocHost(&e->h_small, sizeof(int) * 8) == cudaSuccess;
+  static_assert(sizeof(double) * ACC_N <= SCRATCH_CT, "scratch layout");
+  static_assert(SCRATCH_CT + sizeof(unsigned long long) * (CT_N + 1) <= SCRATCH_SMALL, "scratch layout");
+  if (ok) {  // views into the scratch block (not separately allocated)
+    e->acc.p = reinterpret_cast<double*>(e->scratch.p), e->acc.n = ACC_N;
+    e->ct.p = reinterpret_cast<unsigned long long*>(e->scratch.p + SCRATCH_CT), e->ct.n = CT_N + 1;
+    e->small_i.p = reinterpret_cast<int*>(e->scratch.p + SCRATCH_SMALL), e->small_i.n = 16;
+  }
+  if (!ok) {
+    e->err = std::string("CUDA init failed: ") + cudaGetErrorString(cudaGetLastError());
+    return AB_E_CUDA;
+  }
+  return AB_OK;
+}
+
+void free_engine(ab_engine* e) {
+  if (!e) return;
+  if (e->host_steps && std::getenv("AB_HOST_TIMING"))
+    std::fprintf(stderr,
+                 "[airebo_b200] host ms/step over %lld NVE steps: integrate1+flags %.4f, speculative enqueue %.4f, "
+                 "wait %.4f, rebuild path %.4f, integrate2 %.4f\n",
+                 e->host_steps, e->host_ms[0] / e->host_steps, e->host_ms[1] / e->host_steps,
+                 e->host_ms[2] / e->host_steps, e->host_ms[3] / e->host_steps, e->host_ms[4] / e->host_steps);
+  if (e->rb_n && std::getenv("AB_HOST_TIMING"))
+    std::fprintf(stderr, "[airebo_b200] host ms/rebuild over %lld: sort %.3f, image count+sync %.3f, fill+bin %.3f, lists %.3f (retries %lld)\n",
+                 e->rb_n, e->rb_ms[0] / e->rb_n, e->rb_ms[1] / e->rb_n, e->rb_ms[2] / e->rb_n, e->rb_ms[3] / e->rb_n,
+                 e->retries);
+  cudaSetDevice(e->dev);
+  if (e->st) cudaStreamSynchronize(e->st);
+  for (int c = 0; c < 2; ++c)
+    if (e->aux[c]) cudaStreamSynchronize(e->aux[c]);
+  for (ab_engine* s : e->subs) free_engine(s);
+  e->subs.clear();
+  if (g_const_owner == e) g_const_owner = nullptr;
+  if (e->comm) {
+    std::string tmp;
+    NcclApi& NC = nccl(tmp);
+    if (NC.ok) NC.commDestroy(e->comm);
+    e->comm = nullptr;
+  }
+  DBuf<double4>* b4[] = {&e->pos, &e->pos_tmp, &e->xref};
+  for (auto* b : b4) b->release();
+  e->acc.p = nullptr, e->ct.p = nullptr, e->small_i.p = nullptr;  // views into scratch
+  e->scratch.release();
+  DBuf<double>* bd[] = {&e->vel, &e->vel_tmp, &e->F, &e->io, &e->q_M, &e->stage0, &e->stage1, &e->gio};
+  for (auto* b : bd) b->release();
+  DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->key2, &e->val, &e->val2, &e->cell_start,
+                     &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
+                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_q,
+                     &e->sendl[0], &e->sendl[1], &e->fl[0], &e->fl[1], &e->fl[2], &e->idx[0], &e->idx[1],
+                     &e->idx[2], &e->cnt_d};
+  for (auto* b : bi) b->release();
+  DBuf<unsigned char>* bu[] = {&e->s_dr, &e->s_w, &e->s_N, &e->cub_tmp, &e->sb[0], &e->sb[1], &e->rb[0], &e->rb[1],
+                               &e->redx};
+  for (auto* b : bu) b->release();
+  e->shift.release();
+  e->rshift.release();
+  e->typ.release();
+  e->bonds.release();
+  e->q_item.release();
+  e->red_d.release();
+  e->red_u.release();
+  if (e->h_ct) cudaFreeHost(e->h_ct);
+  if (e->h_acc) cudaFreeHost(e->h_acc);
+  if (e->h_small) cudaFreeHost(e->h_small);
+  if (e->ev_disp) cudaEventDestroy(e->ev_disp);
+  for (auto& p : e->pending) cudaEventDestroy(p.a), cudaEventDestroy(p.b);
+  for (auto& x : e->pool) cudaEventDestroy(x);
+  for (int c = 0; c < 2; ++c) {
+    if (e->aux[c]) cudaStreamDestroy(e->aux[c]);
+    if (e->ev_fork[c]) cudaEventDestroy(e->ev_fork[c]);
+    if (e->ev_join[c]) cudaEventDestroy(e->ev_join[c]);
+  }
+  if (e->own) cudaStreamDestroy(e->own);
+  delete e;
+}
+
+// host copy of the device wrap (same IEEE operations; host code is built with -ffp-contract=off)
+double wrap_host(double x, double L) {
+  double y = x - L * std::floor(x / L);
+  if (y >= L) y = y - L;
+  if (y < 0.0) y = y + L;
+  return y;
+}
+
+// load one domain with the atoms `sel` of the caller arrays (velocities zero)
+ab_status load_domain(ab_engine* e, const std::vector<int64_t>& sel, const int32_t* type, const double* xyz,
+                      int64_t nglob) {
+  const int64_t n = (int64_t)sel.size();
+  std::vector<double4> p(n);
+  std::vector<int> g(n);
+  for (int64_t q = 0; q < n; ++q) {
+    int64_t i = sel[q];
+    long long key = make_key((int)i, 0, 0, 0, type[i]);
+    double kd;
+    std::memcpy(&kd, &key, sizeof(kd));
+    p[q] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], kd);
+    g[q] = (int)i;
+  }
+  e->N = (int)n;
+  e->NT = e->NX = (int)n;
+  e->Nglob = (int)nglob;
+  CK(e->pos.ensure((size_t)n + n / 4 + 64));
+  CK(e->gid.ensure((size_t)n + n / 4 + 64));
+  CK(e->vel.ensure(3 * (size_t)n + 3));
+  CK(e->F.ensure(3 * (size_t)n + 3));
+  if (!e->root) CK(e->io.ensure(3 * (size_t)nglob));  // virtual domains use the handle's array
+  if (n) {
+    CK(cudaMemcpyAsync(e->pos.p, p.data(), sizeof(double4) * n, cudaMemcpyHostToDevice, e->st));
+    CK(cudaMemcpyAsync(e->gid.p, g.data(), sizeof(int) * n, cudaMemcpyHostToDevice, e->st));
+    CK(cudaMemsetAsync(e->vel.p, 0, sizeof(double) * 3 * n, e->st));
+  }
+  CK(cudaStreamSynchronize(e->st));
+  e->have_atoms = true;
+  e->lists_valid = false;
+  e->forces_valid = false;
+  e->capL[0] = e->capL[1] = e->capL[2] = e->capI = 0;
+  return AB_OK;
+}
+
+// caller-order global array <-> domains.  to_caller: which = 0 positions, 1 velocities, 2 forces.
+ab_status to_caller(ab_engine* e, int which, double* host) {
+  auto D = doms(e);
+  const size_t bytes = sizeof(double) * 3 * (size_t)e->Nglob;
+  double* buf = nullptr;
+  if (!slabbed(e)) {
+    buf = e->io.p;
+  } else {
+    CK(e->gio.ensure(3 * (size_t)e->Nglob));
+    buf = e->gio.p;
+    if (e->comm) CK(cudaMemsetAsync(buf, 0, bytes, e->st));
+  }
+  for (ab_engine* d : D) {
+    if (which == 0)
+      k_scatter_caller_pos<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->gid.p, d->pos.p, buf);
+    else
+      k_to_caller_vec<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->gid.p, which == 1 ? d->vel.p : d->F.p, buf);
+    ++d->launches;
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) {
+      e->err = std::string("CUDA launch error: ") + cudaGetErrorString(ce);
+      return AB_E_CUDA;
+    }
+  }
+  if (e->comm) {  // each entry has exactly one non-zero contributor: the sum is exact
+    NcclApi& NC = nccl(e->err);
+    if (!NC.ok) return AB_E_NCCL;
+    CKN(NC.allReduce(buf, buf, 3 * (size_t)e->Nglob, ncclFloat64, ncclSum, e->comm, e->st));
+  }
+  CK(cudaMemcpyAsync(host, buf, bytes, cudaMemcpyDeviceToHost, e->st));
+  CK(cudaStreamSynchronize(e->st));
+  return AB_OK;
+}
+
+ab_status from_caller_vel(ab_engine* e, const double* host) {
+  auto D = doms(e);
+  double* buf = e->io.p;
+  if (!e->subs.empty()) {
+    CK(e->gio.ensure(3 * (size_t)e->Nglob));
+    buf = e->gio.p;
+  }
+  CK(cudaMemcpyAsync(buf, host, sizeof(double) * 3 * (size_t)e->Nglob, cudaMemcpyHostToDevice, e->st));
+  for (ab_engine* d : D) {
+    k_from_caller_vec<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->gid.p, buf, d->vel.p);
+    ++d->launches;
+  }
+  CK(cudaGetLastError());
+  return AB_OK;
+}
+
+ab_status set_atoms_impl(ab_engine* e, int64_t n, const int32_t* type, const double* xyz) {
+  if (!slabbed(e)) {
+    std::vector<int64_t> sel(n);
+    for (int64_t i = 0; i < n; ++i) sel[i] = i;
+    TRY(load_domain(e, sel, type, xyz, n));
+  } else {
+    auto D = doms(e);
+    std::vector<std::vector<int64_t>> sel(e->nranks);
+    for (int64_t i = 0; i < n; ++i) sel[slab_of(wrap_host(xyz[3 * i], e->L[0]), e->nranks, e->L[0])].push_back(i);
+    for (ab_engine* d : D) TRYD(d, load_domain(d, sel[d->rank], type, xyz, n));
+  }
+  e->Nglob = (int)n;
+  e->N = slabbed(e) && !e->subs.empty() ? (int)n : e->N;
+  e->have_atoms = true;
+  e->lists_valid = false;
+  e->forces_valid = false;
+  if (!e->subs.empty()) e->rebuilds = 0;
+  return AB_OK;
+}
+
+ab_status check_slab_box(ab_engine* e) {
+  if (!slabbed(e)) return AB_OK;
+  double w = e->L[0] / e->nranks;
+  if (w < e->halo) {
+    char b[256];
+    std::snprintf(b, sizeof(b), "slab width L_x/n = %.4f A is below the halo width %.4f A (r_c,max + skin) for %d ranks",
+                  w, e->halo, e->nranks);
+    e->err = b;
+    return AB_E_BOX;
+  }
+  return AB_OK;
 }
 
 }  // namespace
@@ -642,96 +1422,103 @@ ab_status ab_create(const char* text, size_t len, ab_precision prec, int device,
   }
   *out = nullptr;
   ab_engine* e = new ab_engine();
-  std::string perr = parse_host_params(text, len, e->hp);
-  if (!perr.empty()) {
-    g_create_error = perr;
-    delete e;
-    return AB_E_PARAM;
-  }
-  e->prec = prec;
-  e->dev = device;
-  cudaDeviceProp prop;
-  if (cudaSetDevice(device) != cudaSuccess || cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
-    g_create_error = "no CUDA device " + std::to_string(device);
-    cudaGetLastError();
-    delete e;
-    return AB_E_CUDA;
-  }
-  if (prop.major != 10) {
-    g_create_error = std::string("device is not sm_100 (Blackwell): ") + prop.name;
-    delete e;
-    return AB_E_CUDA;
-  }
-  std::snprintf(e->devname, sizeof(e->devname), "%s", prop.name);
-  e->nsm = prop.multiProcessorCount;
-  if (cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking) != cudaSuccess) {
-    g_create_error = "cudaStreamCreate failed";
-    delete e;
-    return AB_E_CUDA;
-  }
-  e->st = e->own;
-  Tab<double> td;
-  Tab<float> tf;
-  fill_tab(e->hp, td);
-  fill_tab(e->hp, tf);
-  bool ok = cudaMemcpyToSymbol(c_tabd, &td, sizeof(td)) == cudaSuccess &&
-            cudaMemcpyToSymbol(c_tabf, &tf, sizeof(tf)) == cudaSuccess &&
-            e->scratch.ensure(SCRATCH_BYTES) == cudaSuccess &&
-            cudaMemset(e->scratch.p, 0, SCRATCH_BYTES) == cudaSuccess &&
-            cudaMallocHost(&e->h_ct, sizeof(unsigned long long) * (CT_N + 1)) == cudaSuccess &&
-            cudaMallocHost(&e->h_acc, sizeof(double) * ACC_N) == cudaSuccess &&
-            cudaMallocHost(&e->h_small, sizeof(int) * 8) == cudaSuccess;
-  static_assert(sizeof(double) * ACC_N <= SCRATCH_CT, "scratch layout");
-  static_assert(SCRATCH_CT + sizeof(unsigned long long) * (CT_N + 1) <= SCRATCH_SMALL, "scratch layout");
-  if (ok) {  // views into the scratch block (not separately allocated)
-    e->acc.p = reinterpret_cast<double*>(e->scratch.p), e->acc.n = ACC_N;
-    e->ct.p = reinterpret_cast<unsigned long long*>(e->scratch.p + SCRATCH_CT), e->ct.n = CT_N + 1;
-    e->small_i.p = reinterpret_cast<int*>(e->scratch.p + SCRATCH_SMALL), e->small_i.n = 16;
-  }
-  if (!ok) {
-    g_create_error = std::string("CUDA init failed: ") + cudaGetErrorString(cudaGetLastError());
-    ab_destroy(e);
-    return AB_E_CUDA;
+  ab_status s = init_engine(e, text, len, prec, device);
+  if (s != AB_OK) {
+    g_create_error = e->err;
+    free_engine(e);
+    return s;
   }
   *out = e;
   return AB_OK;
 }
 
-void ab_destroy(ab_engine* e) {
-  if (!e) return;
-  cudaSetDevice(e->dev);
-  if (e->st) cudaStreamSynchronize(e->st);
-  DBuf<double4>* b4[] = {&e->pos, &e->pos_tmp, &e->xref};
-  for (auto* b : b4) b->release();
-  e->acc.p = nullptr, e->ct.p = nullptr, e->small_i.p = nullptr;  // views into scratch
-  e->scratch.release();
-  DBuf<double>* bd[] = {&e->vel, &e->vel_tmp, &e->F, &e->io, &e->q_M, &e->stage0, &e->stage1};
-  for (auto* b : bd) b->release();
-  DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->key2, &e->val, &e->val2, &e->cell_start,
-                     &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
-                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr,
-                     &e->small_i, &e->ovf_bond, &e->ovf_q};
-  for (auto* b : bi) b->release();
-  e->shift.release();
-  e->typ.release();
-  e->s_dr.release();
-  e->s_w.release();
-  e->s_N.release();
-  e->bonds.release();
-  e->q_item.release();
-  e->ct.release();
-  e->red_d.release();
-  e->red_u.release();
-  e->cub_tmp.release();
-  if (e->h_ct) cudaFreeHost(e->h_ct);
-  if (e->h_acc) cudaFreeHost(e->h_acc);
-  if (e->h_small) cudaFreeHost(e->h_small);
-  if (e->ev_disp) cudaEventDestroy(e->ev_disp);
-  for (auto& p : e->pending) cudaEventDestroy(p.a), cudaEventDestroy(p.b);
-  for (auto& x : e->pool) cudaEventDestroy(x);
-  if (e->own) cudaStreamDestroy(e->own);
-  delete e;
+ab_status ab_create_virtual(const char* text, size_t len, ab_precision prec, int device, int nranks,
+                            ab_engine** out) {
+  if (!out || nranks < 1 || nranks > 64) {
+    g_create_error = "ab_create_virtual: bad argument (nranks in [1, 64])";
+    return AB_E_ARG;
+  }
+  TRY(ab_create(text, len, prec, device, out));
+  ab_engine* e = *out;
+  if (nranks == 1) return AB_OK;
+  e->nranks = nranks;
+  for (int r = 0; r < nranks; ++r) {
+    ab_engine* d = nullptr;
+    ab_status s = ab_create(text, len, prec, device, &d);
+    if (s != AB_OK) {
+      free_engine(e);
+      *out = nullptr;
+      return s;
+    }
+    d->root = e;
+    d->rank = r;
+    d->nranks = nranks;
+    d->st = e->st;
+    e->subs.push_back(d);
+  }
+  return AB_OK;
 }
+
+ab_status ab_nccl_unique_id(void* id128) {
+  if (!id128) return AB_E_ARG;
+  NcclApi& NC = nccl(g_create_error);
+  if (!NC.ok) return AB_E_NCCL;
+  ncclUniqueId id;
+  ncclResult_t r = NC.getUniqueId(&id);
+  if (r != ncclSuccess) {
+    g_create_error = std::string("ncclGetUniqueId: ") + NC.errStr(r);
+    return AB_E_NCCL;
+  }
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+  std::memcpy(id128, &id, 128);
+  return AB_OK;
+}
+
+ab_status ab_create_dist(const char* text, size_t len, ab_precision prec, int device, int rank, int nranks,
+                         const void* id128, ab_engine** out) {
+  if (!out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) {
+    g_create_error = "ab_create_dist: bad argument";
+    return AB_E_ARG;
+  }
+  TRY(ab_create(text, len, prec, device, out));
+  ab_engine* e = *out;
+  e->rank = rank;
+  e->nranks = nranks;
+  if (nranks == 1) return AB_OK;
+  NcclApi& NC = nccl(e->err);
+  if (!NC.ok) {
+    g_create_error = e->err;
+    free_engine(e);
+    *out = nullptr;
+    return AB_E_NCCL;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, id128, 128);
+  ncclResult_t r = NC.commInitRank(&e->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    g_create_error = std::string("ncclCommInitRank: ") + NC.errStr(r);
+    e->comm = nullptr;
+    free_engine(e);
+    *out = nullptr;
+    return AB_E_NCCL;
+  }
+  return AB_OK;
+}
+
+ab_status ab_slab_info(const double L[3], double halo, int nranks, int rank, double* xlo, double* xhi) {
+  if (!L || nranks < 1 || rank < 0 || rank >= nranks || !(L[0] > 0)) return AB_E_ARG;
+  if (xlo) *xlo = slab_lo(rank, nranks, L[0]);
+  if (xhi) *xhi = slab_lo(rank + 1, nranks, L[0]);
+  if (nranks > 1 && L[0] / nranks < halo) return AB_E_BOX;
+  return AB_OK;
+}
+
+int ab_slab_of(double x, double Lx, int nranks) {
+  if (!(Lx > 0) || nranks < 1) return -1;
+  return slab_of(wrap_host(x, Lx), nranks, Lx);
+}
+
+void ab_destroy(ab_engine* e) { free_engine(e); }
 
 const char* ab_last_error(const ab_engine* e) { return e ? e->err.c_str() : g_create_error.c_str(); }
 
@@ -740,6 +1527,7 @@ ab_status ab_set_stream(ab_engine* e, void* stream) {
   cudaSetDevice(e->dev);
   CK(cudaStreamSynchronize(e->st));
   e->st = stream ? (cudaStream_t)stream : e->own;
+  for (ab_engine* d : e->subs) d->st = e->st;
   return AB_OK;
 }
 
@@ -752,11 +1540,19 @@ ab_status ab_set_box(ab_engine* e, const double L[3]) {
       return AB_E_BOX;
     }
   cudaSetDevice(e->dev);
+  for (ab_engine* d : doms(e)) {
+    for (int c = 0; c < 3; ++c) d->L[c] = L[c];
+    d->xlo = slab_lo(d->rank, d->nranks, L[0]);
+    d->xhi = slab_lo(d->rank + 1, d->nranks, L[0]);
+    d->have_box = true;
+    d->lists_valid = d->forces_valid = false;
+  }
   for (int c = 0; c < 3; ++c) e->L[c] = L[c];
   e->have_box = true;
-  e->lists_valid = false;
-  e->forces_valid = false;
-  return upload_geo(e);
+  e->lists_valid = e->forces_valid = false;
+  TRY(check_slab_box(e));
+  if (g_const_owner == e) g_const_owner = nullptr;  // box changed: reload the constants
+  return bind_consts(e);
 }
 
 ab_status ab_set_atoms(ab_engine* e, int64_t n, const int32_t* type, const double* xyz) {
@@ -771,8 +1567,6 @@ ab_status ab_set_atoms(ab_engine* e, int64_t n, const int32_t* type, const doubl
     return AB_E_STATE;
   }
   cudaSetDevice(e->dev);
-  std::vector<double4> p(n);
-  std::vector<int> g(n);
   for (int64_t i = 0; i < n; ++i) {
     if (type[i] != 0 && type[i] != 1) {
       e->err = "type[" + std::to_string(i) + "] must be 0 (C) or 1 (H)";
@@ -783,28 +1577,9 @@ ab_status ab_set_atoms(ab_engine* e, int64_t n, const int32_t* type, const doubl
         e->err = "non-finite coordinate of atom " + std::to_string(i);
         return AB_E_NONFINITE;
       }
-    long long key = make_key((int)i, 0, 0, 0, type[i]);
-    double kd;
-    std::memcpy(&kd, &key, sizeof(kd));
-    p[i] = make_double4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], kd);
-    g[i] = (int)i;
   }
-  e->N = (int)n;
-  e->NT = (int)n;
-  CK(e->pos.ensure((size_t)n + n / 4 + 64));
-  CK(e->gid.ensure((size_t)n + n / 4 + 64));
-  CK(e->vel.ensure(3 * (size_t)n));
-  CK(e->F.ensure(3 * (size_t)n));
-  CK(e->io.ensure(3 * (size_t)n));
-  CK(cudaMemcpyAsync(e->pos.p, p.data(), sizeof(double4) * n, cudaMemcpyHostToDevice, e->st));
-  CK(cudaMemcpyAsync(e->gid.p, g.data(), sizeof(int) * n, cudaMemcpyHostToDevice, e->st));
-  CK(cudaMemsetAsync(e->vel.p, 0, sizeof(double) * 3 * n, e->st));
-  CK(cudaStreamSynchronize(e->st));
-  e->have_atoms = true;
-  e->lists_valid = false;
-  e->forces_valid = false;
-  e->capL[0] = e->capL[1] = e->capL[2] = e->capI = 0;
-  return AB_OK;
+  TRY(bind_consts(e));
+  return set_atoms_impl(e, n, type, xyz);
 }
 
 static ab_status need_atoms(ab_engine* e) {
@@ -814,32 +1589,66 @@ static ab_status need_atoms(ab_engine* e) {
     return AB_E_STATE;
   }
   cudaSetDevice(e->dev);
-  return AB_OK;
+  return bind_consts(e);
 }
 
 ab_status ab_set_positions(ab_engine* e, const double* xyz) {
   TRY(need_atoms(e));
   if (bad_ptr(e, xyz, "xyz")) return AB_E_ARG;
-  CK(cudaMemcpyAsync(e->io.p, xyz, sizeof(double) * 3 * e->N, cudaMemcpyHostToDevice, e->st));
-  k_from_caller_pos<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->gid.p, e->io.p, e->pos.p);
-  CKL();
-  e->forces_valid = false;
-  return AB_OK;
+  if (!slabbed(e)) {
+    CK(cudaMemcpyAsync(e->io.p, xyz, sizeof(double) * 3 * e->N, cudaMemcpyHostToDevice, e->st));
+    k_from_caller_pos<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->gid.p, e->io.p, e->pos.p);
+    CKL();
+    e->forces_valid = false;
+    return AB_OK;
+  }
+  // slab domains: atoms may change owner arbitrarily -> redistribute (velocities kept)
+  const int64_t n = e->Nglob;
+  std::vector<double> v(3 * n);
+  std::vector<int32_t> t(n);
+  TRY(to_caller(e, 1, v.data()));
+  {  // species from the instance keys of the owned atoms
+    std::vector<double> buf(3 * n, 0.0);
+    for (ab_engine* d : doms(e)) {
+      std::vector<double4> p(d->N);
+      std::vector<int> g(d->N);
+      if (d->N) {
+        CK(cudaMemcpy(p.data(), d->pos.p, sizeof(double4) * d->N, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(g.data(), d->gid.p, sizeof(int) * d->N, cudaMemcpyDeviceToHost));
+      }
+      for (int q = 0; q < d->N; ++q) {
+        long long k;
+        std::memcpy(&k, &p[q].w, sizeof(k));
+        buf[g[q]] = (double)(k & 3) + 1.0;
+      }
+    }
+    if (e->comm) {
+      NcclApi& NC = nccl(e->err);
+      if (!NC.ok) return AB_E_NCCL;
+      CK(e->gio.ensure(3 * (size_t)n));
+      CK(cudaMemcpyAsync(e->gio.p, buf.data(), sizeof(double) * n, cudaMemcpyHostToDevice, e->st));
+      CKN(NC.allReduce(e->gio.p, e->gio.p, n, ncclFloat64, ncclSum, e->comm, e->st));
+      CK(cudaMemcpyAsync(buf.data(), e->gio.p, sizeof(double) * n, cudaMemcpyDeviceToHost, e->st));
+      CK(cudaStreamSynchronize(e->st));
+    }
+    for (int64_t i = 0; i < n; ++i) t[i] = (int32_t)buf[i] - 1;
+  }
+  TRY(set_atoms_impl(e, n, t.data(), xyz));
+  return from_caller_vel(e, v.data());
 }
 
 ab_status ab_set_velocities(ab_engine* e, const double* v) {
   TRY(need_atoms(e));
   if (bad_ptr(e, v, "v")) return AB_E_ARG;
-  CK(cudaMemcpyAsync(e->io.p, v, sizeof(double) * 3 * e->N, cudaMemcpyHostToDevice, e->st));
-  k_from_caller_vec<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->gid.p, e->io.p, e->vel.p);
-  CKL();
-  return AB_OK;
+  return from_caller_vel(e, v);
 }
+
+ab_status ab_get_forces(ab_engine* e, double* f);
 
 ab_status ab_compute(ab_engine* e, double* f, double* energy, double virial[6], double terms[3]) {
   TRY(need_atoms(e));
-  TRY(prepare(e, true));
-  TRY(forces(e));
+  TRY(prepare_all(e, true));
+  TRY(forces_all(e));
   if (energy) *energy = e->E3[0] + e->E3[1] + e->E3[2];
   if (terms)
     for (int c = 0; c < 3; ++c) terms[c] = e->E3[c];
@@ -855,9 +1664,9 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
 // compiled out of the LJ kernel for these steps (ab_compute always evaluates it).
 ab_status ab_run_nve(ab_engine* e, int64_t nsteps, double dt, int64_t every, double* thermo) {
   TRY(need_atoms(e));
-  e->want_virial = false;
+  for (ab_engine* d : doms(e)) d->want_virial = false;
   ab_status s = run_nve_impl(e, nsteps, dt, every, thermo);
-  e->want_virial = true;
+  for (ab_engine* d : doms(e)) d->want_virial = true;
   return s;
 }
 
@@ -867,69 +1676,104 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     return AB_E_ARG;
   }
   cudaStream_t st = e->st;
-  const int N = e->N;
+  auto D = doms(e);
   if (!e->forces_valid) {
-    TRY(prepare(e, true));
-    TRY(forces(e));
+    TRY(prepare_all(e, true));
+    TRY(forces_all(e));
   }
   const HostParams& hp = e->hp;
   double dtf0 = 0.5 * dt * hp.ftm2v / hp.mass[0], dtf1 = 0.5 * dt * hp.ftm2v / hp.mass[1];
   int row = 0;
   auto record = [&](int64_t step) -> ab_status {
-    CK(cudaMemsetAsync(e->acc.p + ACC_KE, 0, sizeof(double), st));
-    k_ke<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->vel.p, hp.mass[0], hp.mass[1], e->acc.p);
-    CKL();
-    double ke;
-    CK(cudaMemcpyAsync(&ke, e->acc.p + ACC_KE, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    double ke = 0;
+    for (ab_engine* d : D) {
+      CK(cudaMemsetAsync(d->acc.p + ACC_KE, 0, sizeof(double), st));
+      k_ke<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, hp.mass[0], hp.mass[1], d->acc.p);
+      CKL();
+    }
+    if (e->comm) {
+      NcclApi& NC = nccl(e->err);
+      if (!NC.ok) return AB_E_NCCL;
+      CK(e->redx.ensure(64));
+      double* x = reinterpret_cast<double*>(e->redx.p);
+      CKN(NC.allReduce(e->acc.p + ACC_KE, x, 1, ncclFloat64, ncclSum, e->comm, st));
+      CK(cudaMemcpyAsync(&ke, x, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    } else {
+      std::vector<double> kd(D.size());
+      for (size_t q = 0; q < D.size(); ++q)
+        CK(cudaMemcpyAsync(&kd[q], D[q]->acc.p + ACC_KE, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (double k : kd) ke += k;
+    }
     ke *= hp.mvv2e;
     double pe = e->E3[0] + e->E3[1] + e->E3[2];
     double* t = thermo + 4 * row++;
     t[0] = (double)step, t[1] = pe, t[2] = ke, t[3] = pe + ke;
     return AB_OK;
   };
-  if (thermo && every > 0) TRY(record(0));
+  if (thermo && every > 0) {
+    TRY(pull_results(e));
+    TRY(record(0));
+  }
   // The rebuild decision (max displacement) is the only per-step host round trip and
   // it is hidden: after the drift the force kernels are enqueued speculatively on the current
   // lists (they only write F, the scratch block and the b* queue), the host then waits for the
   // displacement read-back alone and, if a rebuild is needed (rare), rebuilds and re-enqueues
   // the forces before the second half-kick.  Energies and counters stay on the device except on
   // thermo steps; the b* queue is sized so it cannot overflow, and the short-list overflow flag
-  // of step s is read at step s+1.
+  // of step s is read at step s+1.  Slab domains: the displacement and overflow flags are
+  // max-reduced over all ranks first, so every rank takes the same rebuild decision.
   if (!e->ev_disp) CK(cudaEventCreateWithFlags(&e->ev_disp, cudaEventDisableTiming));
+  using clk = std::chrono::steady_clock;
+  auto ms_since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
   for (int64_t s = 1; s <= nsteps; ++s) {
     const bool th = thermo && every > 0 && s % every == 0;
-    CK(cudaMemsetAsync(e->ct.p + CT_N, 0, sizeof(unsigned long long), st));
+    auto t0 = clk::now();
     prof_begin(e, 4);
-    k_integrate1<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->vel.p, e->F.p, dtf0, dtf1, dt, e->xref.p,
-                                                e->ct.p + CT_N);
-    CKL();
+    for (ab_engine* d : D) {
+      CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), st));
+      k_integrate1<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt, d->xref.p,
+                                                    d->ct.p + CT_N);
+      CKL();
+    }
     prof_end(e);
-    CK(cudaMemcpyAsync(e->h_ct, e->ct.p, sizeof(unsigned long long) * (CT_N + 1), cudaMemcpyDeviceToHost, st));
+    TRY(enqueue_flags(e));
     CK(cudaEventRecord(e->ev_disp, st));
+    e->host_ms[0] += ms_since(t0);
+    t0 = clk::now();
     bool speculated = false;
     if (e->lists_valid && !th) {
-      TRY(prepare(e, false));
-      TRY(forces(e, false));
+      TRY(refresh_ghosts_all(e));
+      TRY(forces_all(e, false));
       speculated = true;
     }
+    e->host_ms[1] += ms_since(t0);
+    t0 = clk::now();
     CK(cudaEventSynchronize(e->ev_disp));
-    if (e->h_ct[CT_OVF_SHORT]) {
+    e->host_ms[2] += ms_since(t0);
+    t0 = clk::now();
+    read_flags(e);
+    if (e->h_flag[1]) {
       e->err = "an atom has more than 16 REBO short-list neighbours (NBMAX); unsupported geometry";
       return AB_E_STATE;
     }
-    double d2;
-    std::memcpy(&d2, &e->h_ct[CT_N], sizeof(d2));
     double half = 0.5 * hp.skin;
-    if (d2 > half * half) e->lists_valid = false, speculated = false;
+    if (flag_d2(e) > half * half) e->lists_valid = false, speculated = false;
     if (!speculated) {
-      TRY(prepare(e, false));
-      TRY(forces(e, th));
+      TRY(prepare_all(e, false));
+      TRY(forces_all(e, th));
     }
+    e->host_ms[3] += ms_since(t0);
+    t0 = clk::now();
     prof_begin(e, 4);
-    k_integrate2<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->vel.p, e->F.p, dtf0, dtf1);
-    CKL();
+    for (ab_engine* d : D) {
+      k_integrate2<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
+      CKL();
+    }
     prof_end(e);
+    e->host_ms[4] += ms_since(t0);
+    ++e->host_steps;
     ++e->steps;
     if (th) TRY(record(s));
   }
@@ -942,21 +1786,13 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
 ab_status ab_get_positions(ab_engine* e, double* xyz) {
   TRY(need_atoms(e));
   if (bad_ptr(e, xyz, "xyz")) return AB_E_ARG;
-  k_to_caller_pos<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->gid.p, e->pos.p, e->io.p);
-  CKL();
-  CK(cudaMemcpyAsync(xyz, e->io.p, sizeof(double) * 3 * e->N, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaStreamSynchronize(e->st));
-  return AB_OK;
+  return to_caller(e, 0, xyz);
 }
 
 ab_status ab_get_velocities(ab_engine* e, double* v) {
   TRY(need_atoms(e));
   if (bad_ptr(e, v, "v")) return AB_E_ARG;
-  k_to_caller_vec<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->gid.p, e->vel.p, e->io.p);
-  CKL();
-  CK(cudaMemcpyAsync(v, e->io.p, sizeof(double) * 3 * e->N, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaStreamSynchronize(e->st));
-  return AB_OK;
+  return to_caller(e, 1, v);
 }
 
 ab_status ab_get_forces(ab_engine* e, double* f) {
@@ -966,43 +1802,34 @@ ab_status ab_get_forces(ab_engine* e, double* f) {
     e->err = "no force evaluation at the current positions";
     return AB_E_STATE;
   }
-  k_to_caller_vec<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->gid.p, e->F.p, e->io.p);
-  CKL();
-  CK(cudaMemcpyAsync(f, e->io.p, sizeof(double) * 3 * e->N, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaStreamSynchronize(e->st));
-  return AB_OK;
+  return to_caller(e, 2, f);
 }
 
-ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows) {
-  TRY(need_atoms(e));
-  if (bad_ptr(e, count, "count")) return AB_E_ARG;
-  if (which != AB_LIST_SHORT && which != AB_LIST_BONDS && which != AB_LIST_LJ) {
-    e->err = "unknown list";
-    return AB_E_ARG;
-  }
-  if (!e->forces_valid) {
-    TRY(prepare(e, true));
-    TRY(forces(e));
-  }
-  const int N = e->N, NT = e->NT;
+// rows of one domain's list (canonical rows only for bonds / LJ)
+static ab_status list_rows(ab_engine* e, ab_engine* d, ab_list which, std::vector<std::array<int64_t, 5>>& out) {
+  const int N = d->N, NT = d->NT;
   std::vector<int> gid(NT);
   std::vector<char4> sh(NT);
   std::vector<double4> pos(NT);
-  CK(cudaMemcpyAsync(gid.data(), e->gid.p, sizeof(int) * NT, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaMemcpyAsync(sh.data(), e->shift.p, sizeof(char4) * NT, cudaMemcpyDeviceToHost, e->st));
-  CK(cudaMemcpyAsync(pos.data(), e->pos.p, sizeof(double4) * NT, cudaMemcpyDeviceToHost, e->st));
+  if (NT) {
+    CK(cudaMemcpyAsync(gid.data(), d->gid.p, sizeof(int) * NT, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(sh.data(), d->shift.p, sizeof(char4) * NT, cudaMemcpyDeviceToHost, e->st));
+    CK(cudaMemcpyAsync(pos.data(), d->pos.p, sizeof(double4) * NT, cudaMemcpyDeviceToHost, e->st));
+  }
   // (count, neighbour) tables of the requested list(s)
   int nl = which == AB_LIST_LJ ? 3 : 1;
   std::vector<int> cnt[3], nbr[3];
   int cap[3];
   for (int c = 0; c < nl; ++c) {
-    cap[c] = which == AB_LIST_LJ ? e->capL[c] : e->capS;
-    const int* dc = which == AB_LIST_LJ ? e->ljc[c].p : e->s_cnt.p;
-    const int* dn = which == AB_LIST_LJ ? e->ljn[c].p : e->s_nbr.p;
+    cap[c] = which == AB_LIST_LJ ? d->capL[c] : d->capS;
+    const int* dc = which == AB_LIST_LJ ? d->ljc[c].p : d->s_cnt.p;
+    const int* dn = which == AB_LIST_LJ ? d->ljn[c].p : d->s_nbr.p;
     cnt[c].resize(N);
     nbr[c].resize((size_t)N * cap[c]);
-    CK(cudaMemcpyAsync(cnt[c].data(), dc, sizeof(int) * N, cudaMemcpyDeviceToHost, e->st));
-    CK(cudaMemcpyAsync(nbr[c].data(), dn, sizeof(int) * N * (size_t)cap[c], cudaMemcpyDeviceToHost, e->st));
+    if (N) {
+      CK(cudaMemcpyAsync(cnt[c].data(), dc, sizeof(int) * N, cudaMemcpyDeviceToHost, e->st));
+      CK(cudaMemcpyAsync(nbr[c].data(), dn, sizeof(int) * N * (size_t)cap[c], cudaMemcpyDeviceToHost, e->st));
+    }
   }
   CK(cudaStreamSynchronize(e->st));
   auto type_h = [&](int a) {
@@ -1010,7 +1837,6 @@ ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows
     std::memcpy(&k, &pos[a].w, sizeof(k));
     return (int)(k & 3);
   };
-  std::vector<std::array<int64_t, 5>> out;
   for (int c = 0; c < nl; ++c)
     for (int i = 0; i < N; ++i)
       for (int q = 0; q < cnt[c][i]; ++q) {
@@ -1024,11 +1850,27 @@ ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows
           volatile double a = dx * dx, b = dy * dy, cc = dz * dz;
           volatile double ab = a + b;
           double r2 = ab + cc;
-          double rc = e->hp.pr[type_h(i) + type_h(J)].rc;
+          double rc = d->hp.pr[type_h(i) + type_h(J)].rc;
           if (!(r2 <= rc * rc)) continue;
         }
         out.push_back({gid[i], gid[J], s.x, s.y, s.z});
       }
+  return AB_OK;
+}
+
+ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows) {
+  TRY(need_atoms(e));
+  if (bad_ptr(e, count, "count")) return AB_E_ARG;
+  if (which != AB_LIST_SHORT && which != AB_LIST_BONDS && which != AB_LIST_LJ) {
+    e->err = "unknown list";
+    return AB_E_ARG;
+  }
+  if (!e->forces_valid) {
+    TRY(prepare_all(e, true));
+    TRY(forces_all(e));
+  }
+  std::vector<std::array<int64_t, 5>> out;
+  for (ab_engine* d : doms(e)) TRY(list_rows(e, d, which, out));
   std::sort(out.begin(), out.end());
   *count = (int64_t)out.size();
   if (rows)
@@ -1045,9 +1887,17 @@ ab_status ab_get_stats(ab_engine* e, ab_stats* s) {
   s->n_short = c[CT_SHORT], s->n_bonds = c[CT_BONDS], s->n_quads = c[CT_QUADS], s->n_lj = c[CT_LJ];
   s->n_C0 = c[CT_C0], s->n_bstar = c[CT_BSTAR], s->n_sb_trans = c[CT_SBTRANS], s->max_short = c[CT_MAXSHORT];
   s->max_reach = c[CT_MAXREACH], s->n_badarg = c[CT_BADARG];
-  s->n_atoms = e->N, s->n_ghosts = e->G, s->n_rebuilds = e->rebuilds, s->n_steps = e->steps;
-  s->n_overflow_retries = e->retries + c[CT_OVF_REACH];
-  s->lj_capacity = e->capL[0] + e->capL[1] + e->capL[2], s->inter_capacity = e->capI;
+  s->n_atoms = slabbed(e) ? e->Nglob : e->N;
+  s->n_ghosts = 0, s->n_rebuilds = e->rebuilds, s->n_steps = e->steps;
+  s->n_overflow_retries = c[CT_OVF_REACH];
+  s->lj_capacity = 0, s->inter_capacity = 0;
+  for (ab_engine* d : doms(e)) {
+    s->n_ghosts += d->G;
+    s->n_overflow_retries += d->retries;
+    s->lj_capacity = std::max<int64_t>(s->lj_capacity, d->capL[0] + d->capL[1] + d->capL[2]);
+    s->inter_capacity = std::max<int64_t>(s->inter_capacity, d->capI);
+  }
+  if (!e->subs.empty()) s->n_rebuilds = e->rebuilds;
   s->n_lj_entries = c[CT_LJENT], s->n_angles = c[CT_ANGLES];
   s->n_lj_far = c[CT_LJFAR], s->n_lj_entries_far = c[CT_LJENTFAR];
   return AB_OK;
@@ -1055,6 +1905,7 @@ ab_status ab_get_stats(ab_engine* e, ab_stats* s) {
 
 ab_status ab_record_stages(ab_engine* e, int on) {
   if (!e) return AB_E_ARG;
+  for (ab_engine* d : doms(e)) d->record = on != 0;
   e->record = on != 0;
   e->forces_valid = false;
   return AB_OK;
@@ -1067,15 +1918,19 @@ ab_status ab_get_stage(ab_engine* e, int stage, int64_t* count, double* out) {
     e->err = "stage must be 0 or 1, recording on (ab_record_stages) and forces evaluated";
     return AB_E_STATE;
   }
-  int n[2];
-  CK(cudaMemcpyAsync(n, e->small_i.p + 6, 2 * sizeof(int), cudaMemcpyDeviceToHost, e->st));
-  CK(cudaStreamSynchronize(e->st));
-  int width = stage == 0 ? 13 : 7;
-  int rows = n[stage];
-  *count = rows;
-  if (out && rows)
-    CK(cudaMemcpy(out, stage == 0 ? e->stage0.p : e->stage1.p, sizeof(double) * width * rows,
-                  cudaMemcpyDeviceToHost));
+  const int width = stage == 0 ? 13 : 7;
+  int64_t total = 0;
+  for (ab_engine* d : doms(e)) {
+    int n[2];
+    CK(cudaMemcpyAsync(n, d->small_i.p + 6, 2 * sizeof(int), cudaMemcpyDeviceToHost, e->st));
+    CK(cudaStreamSynchronize(e->st));
+    int rows = n[stage];
+    if (out && rows)
+      CK(cudaMemcpy(out + total * width, stage == 0 ? d->stage0.p : d->stage1.p, sizeof(double) * width * rows,
+                    cudaMemcpyDeviceToHost));
+    total += rows;
+  }
+  *count = total;
   return AB_OK;
 }
 
@@ -1083,6 +1938,11 @@ ab_status ab_set_profiling(ab_engine* e, int on) {
   if (!e) return AB_E_ARG;
   cudaSetDevice(e->dev);
   CK(cudaStreamSynchronize(e->st));
+  for (ab_engine* d : doms(e)) {
+    prof_collect(d);
+    d->prof = on != 0;
+    for (int q = 0; q < AB_NPHASE; ++q) d->phase_ms[q] = 0, d->phase_n[q] = 0;
+  }
   prof_collect(e);
   e->prof = on != 0;
   for (int q = 0; q < AB_NPHASE; ++q) e->phase_ms[q] = 0, e->phase_n[q] = 0;
@@ -1093,8 +1953,13 @@ ab_status ab_get_phase_ms(ab_engine* e, double ms[AB_NPHASE], int64_t n[AB_NPHAS
   if (!e || !ms || !n) return AB_E_ARG;
   cudaSetDevice(e->dev);
   CK(cudaStreamSynchronize(e->st));
-  prof_collect(e);
-  for (int q = 0; q < AB_NPHASE; ++q) ms[q] = e->phase_ms[q], n[q] = e->phase_n[q];
+  for (int q = 0; q < AB_NPHASE; ++q) ms[q] = 0, n[q] = 0;
+  auto D = doms(e);
+  if (D[0] != e) D.push_back(e);
+  for (ab_engine* d : D) {
+    prof_collect(d);
+    for (int q = 0; q < AB_NPHASE; ++q) ms[q] += d->phase_ms[q], n[q] += d->phase_n[q];
+  }
   return AB_OK;
 }
 
@@ -1133,7 +1998,11 @@ ab_status ab_device_info(ab_engine* e, int* device, char* name, size_t name_len,
   if (!e) return AB_E_ARG;
   if (device) *device = e->dev;
   if (name && name_len) std::snprintf(name, name_len, "%s", e->devname);
-  if (launches) *launches = e->launches;
+  if (launches) {
+    int64_t n = e->launches;
+    for (ab_engine* d : e->subs) n += d->launches;
+    *launches = n;
+  }
   return AB_OK;
 }
 

@@ -63,72 +63,7 @@ __global__ void k_permute(int N, const int* perm, const double4* pos_in, double4
   gid_out[i] = gid_in[o];
 }
 
-// image position u = x + s L evaluated as t = s*L; u = x + t (bitwise as the oracle)
-__device__ __forceinline__ double img(double x, int s, double L) { return __dadd_rn(x, __dmul_rn((double)s, L)); }
-
-__device__ __forceinline__ bool in_padded(double u, double L, double h) { return u >= -h && u < L + h; }
-
-// ghosts: every image (s != 0) of a local atom inside [-h, L+h)^3 (explicit images)
-__global__ void k_ghost_count(int N, const double4* pos, int3 smax, double h, int* cnt) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  double4 p = pos[i];
-  int c = 0;
-  for (int sx = -smax.x; sx <= smax.x; ++sx) {
-    double ux = img(p.x, sx, c_geo.L[0]);
-    if (!in_padded(ux, c_geo.L[0], h)) continue;
-    for (int sy = -smax.y; sy <= smax.y; ++sy) {
-      double uy = img(p.y, sy, c_geo.L[1]);
-      if (!in_padded(uy, c_geo.L[1], h)) continue;
-      for (int sz = -smax.z; sz <= smax.z; ++sz) {
-        if (sx == 0 && sy == 0 && sz == 0) continue;
-        double uz = img(p.z, sz, c_geo.L[2]);
-        if (in_padded(uz, c_geo.L[2], h)) ++c;
-      }
-    }
-  }
-  cnt[i] = c;
-}
-
-__global__ void k_ghost_fill(int N, double4* pos, int3 smax, double h, const int* off, int* owner, int* gid,
-                             char4* shift) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  double4 p = pos[i];
-  int w = N + off[i];
-  owner[i] = i;
-  shift[i] = make_char4(0, 0, 0, 0);
-  for (int sx = -smax.x; sx <= smax.x; ++sx) {
-    double ux = img(p.x, sx, c_geo.L[0]);
-    if (!in_padded(ux, c_geo.L[0], h)) continue;
-    for (int sy = -smax.y; sy <= smax.y; ++sy) {
-      double uy = img(p.y, sy, c_geo.L[1]);
-      if (!in_padded(uy, c_geo.L[1], h)) continue;
-      for (int sz = -smax.z; sz <= smax.z; ++sz) {
-        if (sx == 0 && sy == 0 && sz == 0) continue;
-        double uz = img(p.z, sz, c_geo.L[2]);
-        if (!in_padded(uz, c_geo.L[2], h)) continue;
-        long long key = key_of(p) + ((long long)sx << 18) + ((long long)sy << 10) + ((long long)sz << 2);
-        pos[w] = make_double4(ux, uy, uz, __longlong_as_double(key));
-        owner[w] = i;
-        gid[w] = gid[i];
-        shift[w] = make_char4((signed char)sx, (signed char)sy, (signed char)sz, 0);
-        ++w;
-      }
-    }
-  }
-}
-
-// per step: ghost image positions follow their owners (same IEEE ops as at creation)
-__global__ void k_ghost_update(int N, int NT, double4* pos, const int* owner, const char4* shift) {
-  int g = N + blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= NT) return;
-  double4 p = pos[owner[g]];
-  char4 s = shift[g];
-  long long key = key_of(p) + ((long long)s.x << 18) + ((long long)s.y << 10) + ((long long)s.z << 2);
-  pos[g] = make_double4(img(p.x, s.x, c_geo.L[0]), img(p.y, s.y, c_geo.L[1]), img(p.z, s.z, c_geo.L[2]),
-                        __longlong_as_double(key));
-}
+// periodic images / slab halo ghosts: k_dist.cuh (k_image_*, k_halo_*)
 
 __global__ void k_cell_keys(int NT, const double4* pos, Grid g, int* key, int* val) {
   int a = blockIdx.x * blockDim.x + threadIdx.x;

@@ -40,7 +40,8 @@ class ABStats(C.Structure):
 EXPORTS = ["ab_create", "ab_destroy", "ab_last_error", "ab_set_stream", "ab_set_box", "ab_set_atoms",
            "ab_set_positions", "ab_set_velocities", "ab_compute", "ab_run_nve", "ab_get_positions",
            "ab_get_velocities", "ab_get_forces", "ab_get_list", "ab_get_stats", "ab_record_stages", "ab_get_stage",
-           "ab_set_profiling", "ab_get_phase_ms", "ab_peak_flops", "ab_device_info"]
+           "ab_set_profiling", "ab_get_phase_ms", "ab_peak_flops", "ab_device_info", "ab_nccl_unique_id",
+           "ab_create_dist", "ab_create_virtual", "ab_slab_info", "ab_slab_of"]
 
 _lib = None
 
@@ -77,6 +78,12 @@ def load(path: str = LIB_PATH):
     L.ab_set_profiling.argtypes = [vp, C.c_int]
     L.ab_get_phase_ms.argtypes = [vp, dp, i64p]
     L.ab_peak_flops.argtypes = [vp, C.c_int, dp]
+    L.ab_nccl_unique_id.argtypes = [C.c_char_p]
+    L.ab_create_dist.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]
+    L.ab_create_virtual.argtypes = [C.c_char_p, C.c_size_t, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    L.ab_slab_info.argtypes = [dp, C.c_double, C.c_int, C.c_int, dp, dp]
+    L.ab_slab_of.argtypes = [C.c_double, C.c_double, C.c_int]
+    L.ab_slab_of.restype = C.c_int
     _lib = L
     return L
 
@@ -85,17 +92,54 @@ def _dp(a):
     return a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None
 
 
-class Engine:
-    """One engine (one GPU, one precision).  Arrays in and out are in the caller's atom order."""
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for ab_create_dist (create on one rank, broadcast to all)."""
+    L = load()
+    buf = C.create_string_buffer(128)
+    rc = L.ab_nccl_unique_id(buf)
+    if rc != 0:
+        raise ABError(rc, L.ab_last_error(None).decode())
+    return buf.raw
 
-    def __init__(self, precision: str = "fp64", device: int = 0, params: bytes | None = None):
+
+def slab_info(box, halo, nranks, rank):
+    """(xlo, xhi, ok) of slab `rank` (host-only library call, no GPU)."""
+    L = load()
+    b = np.ascontiguousarray(box, dtype=np.float64)
+    lo, hi = C.c_double(), C.c_double()
+    rc = L.ab_slab_info(_dp(b), halo, nranks, rank, C.byref(lo), C.byref(hi))
+    if rc not in (0, -3):
+        raise ABError(rc, "ab_slab_info")
+    return lo.value, hi.value, rc == 0
+
+
+def slab_of(x, Lx, nranks):
+    return load().ab_slab_of(float(x), float(Lx), int(nranks))
+
+
+class Engine:
+    """One engine handle (one precision).  Arrays in and out are in the caller's atom order.
+
+    ranks=None: one GPU, whole box.  ranks=("virtual", n): n slab domains on this GPU exchanging
+    their halo by device copies.  ranks=("nccl", rank, n, uid): slab `rank` of an n-process job
+    (collective calls; uid from nccl_unique_id() on one rank)."""
+
+    def __init__(self, precision: str = "fp64", device: int = 0, params: bytes | None = None, ranks=None):
         self.L = load()
         if params is None:
             with open(PARAMS, "rb") as f:
                 params = f.read()
         h = C.c_void_p()
         prec = {"fp64": AB_FP64, "mixed": AB_MIXED}[precision]
-        rc = self.L.ab_create(params, len(params), prec, device, C.byref(h))
+        if ranks is None:
+            rc = self.L.ab_create(params, len(params), prec, device, C.byref(h))
+        elif ranks[0] == "virtual":
+            rc = self.L.ab_create_virtual(params, len(params), prec, device, int(ranks[1]), C.byref(h))
+        elif ranks[0] == "nccl":
+            _, rank, n, uid = ranks
+            rc = self.L.ab_create_dist(params, len(params), prec, device, int(rank), int(n), uid, C.byref(h))
+        else:
+            raise ValueError(ranks)
         if rc != 0:
             raise ABError(rc, self.L.ab_last_error(None).decode())
         self.h = h
@@ -193,9 +237,9 @@ class Engine:
         return dict(device=dev.value, name=name.value.decode(), kernel_launches=n.value)
 
 
-def make(system, precision="fp64", device=0):
+def make(system, precision="fp64", device=0, ranks=None):
     """Engine loaded with an inputs.System (box, types, positions, velocities)."""
-    e = Engine(precision, device)
+    e = Engine(precision, device, ranks=ranks)
     e.set_box(system.box)
     e.set_atoms(system.types, system.x)
     if system.v is not None:

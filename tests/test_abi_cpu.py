@@ -4,6 +4,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -63,3 +64,28 @@ def test_param_errors_reported_by_library(lib, params_text):
     bad = b"1.0 2.0\n" + params_text
     rc = lib.ab_create(bad, len(bad), 0, 0, C.byref(h))
     assert rc == -2 and b"line 1" in lib.ab_last_error(None)
+
+
+def test_slab_geometry_host_calls(lib):
+    """ab_slab_info / ab_slab_of need no GPU: slabs tile [0, L_x), the owner of x is the slab that
+    contains wrap(x), and a slab narrower than the halo is reported (AB_E_BOX)."""
+    from paper_1810_07026_b200 import engine
+    L = [89.04, 79.2, 35.56]
+    for n in (1, 2, 3, 7):
+        b = [engine.slab_info(L, 11.2, n, r) for r in range(n)]
+        assert b[0][0] == 0.0 and b[-1][1] == L[0] and all(ok for _, _, ok in b)
+        for r in range(n - 1):
+            assert b[r][1] == b[r + 1][0]
+        for x in np.linspace(-L[0], 2 * L[0], 301):
+            r = engine.slab_of(x, L[0], n)
+            xw = x - L[0] * np.floor(x / L[0])
+            assert b[r][0] <= xw < b[r][1] or (xw == L[0] and r == 0)
+    assert not engine.slab_info(L, 11.2, 8, 0)[2]  # 11.13 A < 11.2 A
+
+
+def test_nccl_resolves_at_run_time(lib):
+    """The distributed mode dlopens libnccl.so.2 and creates the 128-byte unique id that the
+    ranks share (no GPU needed for the id)."""
+    from paper_1810_07026_b200 import engine
+    a, b = engine.nccl_unique_id(), engine.nccl_unique_id()
+    assert len(a) == 128 and a != b
