@@ -116,8 +116,11 @@ void ab_destroy(ab_engine* e);
 /* Text of the last error on this engine (or of the last failed ab_create if e == NULL). */
 const char* ab_last_error(const ab_engine* e);
 
-/* Use an external CUDA stream (cudaStream_t passed as void*; NULL = the engine's own stream)
- * for every subsequent kernel and copy.  The caller keeps ownership of the stream. */
+/* Use an external CUDA stream (cudaStream_t passed as void*; NULL = the engine's own stream,
+ * which is non-blocking: pass cudaStreamLegacy ((void*)1) to order with the legacy default
+ * stream) for every subsequent kernel and copy.  The caller keeps ownership of the stream.
+ * Independent force kernels fork onto two engine-owned streams and join back before the call's
+ * last operation on this stream, so events recorded on it bracket all of the engine's work. */
 ab_status ab_set_stream(ab_engine* e, void* cuda_stream);
 
 /* Orthorhombic periodic box, edge lengths L[3] in Angstrom (periodic in x, y, z).  Any edge

@@ -47,11 +47,12 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
-  // grows with 25 % slack: atom / ghost counts drift between list rebuilds, and a reallocation
-  // (cudaFree synchronises the device) in every rebuild would cost milliseconds
+  // allocates with 25 % slack: atom / ghost / list counts drift between list rebuilds, and a
+  // reallocation inside the NVE loop (cudaFree synchronises the device, large cudaMalloc maps
+  // pages) costs tens of milliseconds -- measured 77 ms for the first in-loop rebuild of cfg2
   cudaError_t ensure(size_t cnt) {
     if (cnt <= n && p) return cudaSuccess;
-    size_t c = std::max<size_t>(p ? cnt + cnt / 4 : cnt, 1);
+    size_t c = std::max<size_t>(cnt + cnt / 4, 1);
     if (p) cudaFree(p);
     p = nullptr;
     n = 0;
@@ -136,6 +137,7 @@ struct ab_engine {
   cudaStream_t own = nullptr, st = nullptr;
   cudaStream_t aux[2] = {nullptr, nullptr};     // concurrent force kernels (REBO, LJ far)
   cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
+  bool serial = false;  // AB_SERIAL_KERNELS=1: the whole DAG on one stream (isolated kernel timing)
   bool have_box = false, have_atoms = false, lists_valid = false, forces_valid = false;
   bool record = false;
   double L[3] = {0, 0, 0};
@@ -208,6 +210,8 @@ struct ab_engine {
   DBuf<unsigned char> redx;          // all-reduce staging
   DBuf<double> gio;                  // caller-order global array (3 Nglob) of a handle
   unsigned long long h_flag[2] = {0, 0};
+  double* h_th = nullptr;  // pinned staging of thermo rows
+  size_t h_th_cap = 0;
   // host-side time breakdown of the NVE loop (AB_HOST_TIMING=1: printed by ab_destroy)
   double host_ms[6] = {0, 0, 0, 0, 0, 0};  // integrate1+flags, speculative enqueue, wait, rebuild path, integrate2
   long long host_steps = 0;
@@ -658,6 +662,11 @@ ab_status images_and_lists(ab_engine* e) {
     }
     CK(e->in_nbr.ensure((size_t)NT * e->capI));
     CK(cudaMemsetAsync(e->small_i.p + 2, 0, 4 * sizeof(int), st));
+    const bool dbg = std::getenv("AB_HOST_TIMING") && std::getenv("AB_HOST_TIMING")[0] == '2';
+    cudaEvent_t dbg_ev[3] = {nullptr, nullptr, nullptr};
+    if (dbg)
+      for (auto& x : dbg_ev) cudaEventCreate(&x), cudaEventRecord(x, st);
+    double t_pre = tms(tq);
     k_build_lj<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
                                                               e->nrLJ, Lg, e->small_i.p + 2);
     CKL();
@@ -665,9 +674,18 @@ ab_status images_and_lists(ab_engine* e) {
                                                                   e->nrI, e->capI, e->in_cnt.p, e->in_nbr.p,
                                                                   e->small_i.p + 5);
     CKL();
+    if (dbg) cudaEventRecord(dbg_ev[2], st);
     int mx[4];
     CK(cudaMemcpyAsync(mx, e->small_i.p + 2, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    auto tw = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
+    if (dbg) {
+      float k1 = 0;
+      cudaEventElapsedTime(&k1, dbg_ev[1], dbg_ev[2]);
+      std::fprintf(stderr, "[airebo_b200] rebuild lists: host before kernels %.3f ms, build kernels %.3f ms, sync wait %.3f ms\n",
+                   t_pre, k1, tms(tw));
+      for (auto& x : dbg_ev) cudaEventDestroy(x);
+    }
     bool ok = true;
     for (int c = 0; c < 3; ++c)
       if (mx[c] > e->capL[c]) e->capL[c] = mx[c] + mx[c] / 8 + 32, ok = false;
@@ -676,7 +694,10 @@ ab_status images_and_lists(ab_engine* e) {
     ++e->retries;
   }
   e->capS = std::min(e->capI, 32);
+  auto te = std::chrono::steady_clock::now();
   TRY(ensure_short(e));
+  if (std::getenv("AB_HOST_TIMING") && std::getenv("AB_HOST_TIMING")[0] == '2')
+    std::fprintf(stderr, "[airebo_b200] rebuild ensure_short %.3f ms\n", tms(te));
   e->rb_ms[3] += tms(tq);
   CK(e->xref.ensure(N));
   k_copy_xref<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->xref.p);
@@ -918,7 +939,8 @@ ab_status enqueue_forces(ab_engine* e) {
   // at once on aux[1]; REBO + torsion (aux[0]) and the near LJ pairs -> b* batch (main stream)
   // need the short list.  Partial rows of the reduction are disjoint per kernel; F takes fp64
   // atomics from all of them.
-  const cudaStream_t s_rebo = e->aux[0], s_far = e->aux[1];
+  const bool serial = e->serial;
+  const cudaStream_t s_rebo = serial ? st : e->aux[0], s_far = serial ? st : e->aux[1];
   CK(cudaEventRecord(e->ev_fork[1], st));
   CK(cudaStreamWaitEvent(s_far, e->ev_fork[1], 0));
   const int row_far = g_short + g_rebo + g_slow + g_near;
@@ -1193,6 +1215,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
     return AB_E_CUDA;
   }
   e->st = e->own;
+  e->serial = std::getenv("AB_SERIAL_KERNELS") && std::getenv("AB_SERIAL_KERNELS")[0] == '1';
   for (int c = 0; c < 2; ++c)
     if (cudaStreamCreateWithFlags(&e->aux[c], cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_fork[c], cudaEventDisableTiming) != cudaSuccess ||
@@ -1272,6 +1295,7 @@ void free_engine(ab_engine* e) {
   if (e->h_ct) cudaFreeHost(e->h_ct);
   if (e->h_acc) cudaFreeHost(e->h_acc);
   if (e->h_small) cudaFreeHost(e->h_small);
+  if (e->h_th) cudaFreeHost(e->h_th);
   if (e->ev_disp) cudaEventDestroy(e->ev_disp);
   for (auto& p : e->pending) cudaEventDestroy(p.a), cudaEventDestroy(p.b);
   for (auto& x : e->pool) cudaEventDestroy(x);
@@ -1683,39 +1707,48 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
   }
   const HostParams& hp = e->hp;
   double dtf0 = 0.5 * dt * hp.ftm2v / hp.mass[0], dtf1 = 0.5 * dt * hp.ftm2v / hp.mass[1];
+  // Thermo rows are staged on the device stream (energies of the evaluation + KE after the
+  // second half-kick, copied into pinned host memory) and assembled after one synchronisation at
+  // the end of the call: thermo steps add no host round trip.
+  const int nrows = (thermo && every > 0) ? (int)(nsteps / every) + 1 : 0;
+  const int nd = e->comm ? 1 : (int)D.size();
+  if (nrows) {
+    size_t need = (size_t)nrows * nd * 4;
+    if (e->h_th_cap < need) {
+      if (e->h_th) cudaFreeHost(e->h_th);
+      e->h_th = nullptr;
+      e->h_th_cap = 0;
+      CK(cudaMallocHost(&e->h_th, sizeof(double) * (need + need / 2 + 64)));
+      e->h_th_cap = need + need / 2 + 64;
+    }
+  }
   int row = 0;
-  auto record = [&](int64_t step) -> ab_status {
-    double ke = 0;
+  auto stage_row = [&]() -> ab_status {
     for (ab_engine* d : D) {
       CK(cudaMemsetAsync(d->acc.p + ACC_KE, 0, sizeof(double), st));
       k_ke<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, hp.mass[0], hp.mass[1], d->acc.p);
       CKL();
     }
+    double* h = e->h_th + (size_t)row * nd * 4;
     if (e->comm) {
       NcclApi& NC = nccl(e->err);
       if (!NC.ok) return AB_E_NCCL;
       CK(e->redx.ensure(64));
       double* x = reinterpret_cast<double*>(e->redx.p);
-      CKN(NC.allReduce(e->acc.p + ACC_KE, x, 1, ncclFloat64, ncclSum, e->comm, st));
-      CK(cudaMemcpyAsync(&ke, x, sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpyAsync(x, e->acc.p + ACC_EREBO, 3 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(x + 3, e->acc.p + ACC_KE, sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CKN(NC.allReduce(x, x, 4, ncclFloat64, ncclSum, e->comm, st));
+      CK(cudaMemcpyAsync(h, x, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
     } else {
-      std::vector<double> kd(D.size());
-      for (size_t q = 0; q < D.size(); ++q)
-        CK(cudaMemcpyAsync(&kd[q], D[q]->acc.p + ACC_KE, sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      for (double k : kd) ke += k;
+      for (int q = 0; q < nd; ++q) {
+        CK(cudaMemcpyAsync(h + 4 * q, D[q]->acc.p + ACC_EREBO, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h + 4 * q + 3, D[q]->acc.p + ACC_KE, sizeof(double), cudaMemcpyDeviceToHost, st));
+      }
     }
-    ke *= hp.mvv2e;
-    double pe = e->E3[0] + e->E3[1] + e->E3[2];
-    double* t = thermo + 4 * row++;
-    t[0] = (double)step, t[1] = pe, t[2] = ke, t[3] = pe + ke;
+    ++row;
     return AB_OK;
   };
-  if (thermo && every > 0) {
-    TRY(pull_results(e));
-    TRY(record(0));
-  }
+  if (nrows) TRY(stage_row());
   // The rebuild decision (max displacement) is the only per-step host round trip and
   // it is hidden: after the drift the force kernels are enqueued speculatively on the current
   // lists (they only write F, the scratch block and the b* queue), the host then waits for the
@@ -1743,7 +1776,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     e->host_ms[0] += ms_since(t0);
     t0 = clk::now();
     bool speculated = false;
-    if (e->lists_valid && !th) {
+    if (e->lists_valid) {
       TRY(refresh_ghosts_all(e));
       TRY(forces_all(e, false));
       speculated = true;
@@ -1762,7 +1795,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     if (flag_d2(e) > half * half) e->lists_valid = false, speculated = false;
     if (!speculated) {
       TRY(prepare_all(e, false));
-      TRY(forces_all(e, th));
+      TRY(forces_all(e, false));
     }
     e->host_ms[3] += ms_since(t0);
     t0 = clk::now();
@@ -1775,7 +1808,21 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     e->host_ms[4] += ms_since(t0);
     ++e->host_steps;
     ++e->steps;
-    if (th) TRY(record(s));
+    if (th) TRY(stage_row());
+  }
+  if (nrows) {  // the one synchronisation of a thermo call
+    CK(cudaStreamSynchronize(st));
+    for (int r = 0; r < nrows; ++r) {
+      double ee = 0, ke = 0;
+      for (int q = 0; q < nd; ++q) {
+        const double* h = e->h_th + ((size_t)r * nd + q) * 4;
+        ee += h[0] + h[1] + h[2];
+        ke += h[3];
+      }
+      ke *= hp.mvv2e;
+      double* t = thermo + 4 * r;
+      t[0] = (double)(r * every), t[1] = ee, t[2] = ke, t[3] = ee + ke;
+    }
   }
   // no final synchronisation: the last step's kernels may still run; every call that returns
   // data (or the stream itself) orders after them

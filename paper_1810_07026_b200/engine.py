@@ -158,7 +158,14 @@ class Engine:
     __del__ = close
 
     def set_stream(self, stream_ptr: int | None):
-        self._ck(self.L.ab_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+        """Run on a caller's cudaStream_t (e.g. torch.cuda.Stream().cuda_stream).  None: the
+        engine's own stream.  0 (torch's legacy default stream) maps to cudaStreamLegacy, so the
+        engine's work is ordered with work on that stream."""
+        if stream_ptr is None:
+            ptr = 0
+        else:
+            ptr = 1 if stream_ptr == 0 else stream_ptr
+        self._ck(self.L.ab_set_stream(self.h, C.c_void_p(ptr)))
 
     def set_box(self, L):
         b = np.ascontiguousarray(L, dtype=np.float64)

@@ -15,8 +15,9 @@ from paper_1810_07026_b200 import inputs as I  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "2"
 s = I.config(int(cfg) if cfg.isdigit() else cfg)
 eng = E.make(s, "fp64")
-st = torch.cuda.current_stream()
+st = torch.cuda.Stream()
 eng.set_stream(st.cuda_stream)
+torch.cuda.set_stream(st)
 eng.run_nve(5, s.dt)
 torch.cuda.synchronize()
 eng.L.ab_set_profiling(eng.h, 1)
