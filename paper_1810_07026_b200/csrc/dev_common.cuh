@@ -133,6 +133,17 @@ __device__ __forceinline__ double rsqrt_fast(double a) {
 }
 __device__ __forceinline__ float rsqrt_fast(float a) { return rsqrtf(a); }
 
+// 1/a: hardware approximation + two Newton steps (y += y (1 - a y)), a > 0 and finite
+__device__ __forceinline__ double rcp_fast(double a) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  double e = fma(-a, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-a, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ float rcp_fast(float a) { return __frcp_rn(a); }
+
 // Branch-free half-cosine on t in [0, 1] (caller clamps): S = (1 + cos(pi t))/2 and dS/dt, from
 // x = pi (t - 1/2) in [-pi/2, pi/2]: cos(pi t) = -sin x, sin(pi t) = cos x, Taylor polynomials
 // truncated below the working precision (fp64: x^21 / x^20 terms, error < 3e-17; fp32: x^13 / x^12).

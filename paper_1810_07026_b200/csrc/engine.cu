@@ -147,6 +147,7 @@ struct ab_engine {
   Grid grid{};
   int ncell = 0, nrLJ = 1, nrI = 1;
   int capI = 0, capS = 0, capQ = 0;
+  int qcap[3] = {0, 0, 0}, qoff[3] = {0, 0, 0};  // b* candidate queue regions (build-time bounds)
   long long launches = 0, rebuilds = 0, steps = 0, retries = 0;
   // device state
   DBuf<double4> pos, pos_tmp, xref;
@@ -434,7 +435,7 @@ ab_status ensure_short(ab_engine* e) {
   CK(e->s_dr.ensure(ent * 4 * rs));
   CK(e->s_w.ensure(ent * 2 * rs));
   CK(e->s_N.ensure((size_t)e->NT * 3 * rs));
-  CK(e->bonds.ensure((size_t)e->N * e->capS + 1));
+  CK(e->bonds.ensure(3 * ((size_t)e->N * e->capS + 1)));
   return AB_OK;
 }
 
@@ -652,7 +653,12 @@ ab_status images_and_lists(ab_engine* e) {
   for (int p = 0; p < 3; ++p) {
     double b = e->hp.pr[p].rlo - skin;
     Lg.pure2[p] = b > rnear ? b * b : -1.0;
+    // a canonical pair can be queued as a window candidate (r^2 < (2^(1/6) sigma)^2 (1 + 1e-9))
+    // until the next build only if r_b <= 2^(1/6) sigma (1 + 1e-9) + skin now (pairs move < skin)
+    double q = e->hp.pr[p].sigma * 1.122462048309373 * (1.0 + 1e-9) + skin;
+    Lg.bq2[p] = q * q;
   }
+  Lg.bqcnt = e->small_i.p + 6;
   for (int attempt = 0; attempt < 4; ++attempt) {
     for (int c = 0; c < 3; ++c) {
       CK(e->ljn[c].ensure((size_t)N * e->capL[c]));
@@ -661,7 +667,7 @@ ab_status images_and_lists(ab_engine* e) {
       Lg.nbr[c] = e->ljn[c].p;
     }
     CK(e->in_nbr.ensure((size_t)NT * e->capI));
-    CK(cudaMemsetAsync(e->small_i.p + 2, 0, 4 * sizeof(int), st));
+    CK(cudaMemsetAsync(e->small_i.p + 2, 0, 7 * sizeof(int), st));
     const bool dbg = std::getenv("AB_HOST_TIMING") && std::getenv("AB_HOST_TIMING")[0] == '2';
     cudaEvent_t dbg_ev[3] = {nullptr, nullptr, nullptr};
     if (dbg)
@@ -675,8 +681,8 @@ ab_status images_and_lists(ab_engine* e) {
                                                                   e->small_i.p + 5);
     CKL();
     if (dbg) cudaEventRecord(dbg_ev[2], st);
-    int mx[4];
-    CK(cudaMemcpyAsync(mx, e->small_i.p + 2, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    int mx[7];
+    CK(cudaMemcpyAsync(mx, e->small_i.p + 2, 7 * sizeof(int), cudaMemcpyDeviceToHost, st));
     auto tw = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
     if (dbg) {
@@ -690,7 +696,14 @@ ab_status images_and_lists(ab_engine* e) {
     for (int c = 0; c < 3; ++c)
       if (mx[c] > e->capL[c]) e->capL[c] = mx[c] + mx[c] / 8 + 32, ok = false;
     if (mx[3] > e->capI) e->capI = mx[3] + 4, ok = false;
-    if (ok) break;
+    if (ok) {
+      int off = 0;
+      for (int t = 0; t < 3; ++t) e->qcap[t] = mx[4 + t] + 64, e->qoff[t] = off, off += e->qcap[t];
+      e->capQ = off;
+      CK(e->q_item.ensure(e->capQ));
+      CK(e->q_M.ensure(e->capQ));
+      break;
+    }
     ++e->retries;
   }
   e->capS = std::min(e->capI, 32);
@@ -913,15 +926,6 @@ ab_status enqueue_forces(ab_engine* e) {
     sb0 = StageBuf{e->stage0.p, e->small_i.p + 6, (int)n0};
     sb1 = StageBuf{e->stage1.p, e->small_i.p + 7, (int)n1};
   }
-  // b* queue: the canonical near-list pairs bound the queue, so it cannot overflow
-  {
-    long long qb = (long long)N * e->capL[0] / 2 + 1024;
-    if (e->capQ < qb) {
-      e->capQ = (int)std::min<long long>(qb, 1ll << 30);
-      CK(e->q_item.ensure(e->capQ));
-      CK(e->q_M.ensure(e->capQ));
-    }
-  }
   CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * e->NX, st));
   CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
   ShortList<R> S = short_view<R>(e);
@@ -944,7 +948,10 @@ ab_status enqueue_forces(ab_engine* e) {
   CK(cudaEventRecord(e->ev_fork[1], st));
   CK(cudaStreamWaitEvent(s_far, e->ev_fork[1], 0));
   const int row_far = g_short + g_rebo + g_slow + g_near;
-  BstarQueue Qu{e->q_item.p, e->q_M.p, e->small_i.p + 1, e->capQ};
+  BstarQueue Qu;
+  Qu.item = e->q_item.p, Qu.M = e->q_M.p, Qu.count = e->small_i.p + 13;
+  for (int t = 0; t < 3; ++t) Qu.cap[t] = e->qcap[t], Qu.off[t] = e->qoff[t];
+  const BondList BL{e->bonds.p, e->small_i.p + 10, e->N * e->capS + 1};
   LJArgs A;
   A.N = N;
   A.pos = e->pos.p;
@@ -964,7 +971,7 @@ ab_status enqueue_forces(ab_engine* e) {
   {
     cudaEvent_t t = prof_start(e, st);
     k_short<R><<<g_short, 128, 0, st>>>(N, NT, e->pos.p, e->in_cnt.p, e->in_nbr.p, e->capI, S, e->gid.p,
-                                        e->shift.p, e->bonds.p, e->small_i.p, e->ct.p, RR);
+                                        e->shift.p, BL, e->ct.p, RR);
     CKL();
     prof_stop(e, 0, st, t);
   }
@@ -974,12 +981,12 @@ ab_status enqueue_forces(ab_engine* e) {
     cudaEvent_t t = prof_start(e, s_rebo);
     RedRows R1 = RR;
     R1.row0 = g_short;
-    k_rebo<R, NB_FAST><<<g_rebo, 128, 0, s_rebo>>>(e->bonds.p, e->small_i.p, nullptr, e->ovf_bond.p,
+    k_rebo<R, NB_FAST><<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, e->ovf_bond.p,
                                                    e->small_i.p + 8, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p,
                                                    e->F.p, sb0, R1);
     CKL();
     R1.row0 += g_rebo;
-    k_rebo<R, NBMAX><<<g_slow, 128, 0, s_rebo>>>(e->bonds.p, e->small_i.p, e->ovf_bond.p, nullptr, e->small_i.p + 8,
+    k_rebo<R, NBMAX><<<g_slow, 128, 0, s_rebo>>>(BL, e->ovf_bond.p, nullptr, e->small_i.p + 8,
                                                  S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb0, R1);
     CKL();
     prof_stop(e, 1, s_rebo, t);
@@ -1110,10 +1117,11 @@ ab_status forces_all(ab_engine* e, bool sync_host = true) {
       return AB_OK;
     }
     TRY(collect(e));
-    if (e->last_ct[CT_OVF_QUEUE] && !e->last_ct[CT_OVF_SHORT]) {  // grow the b* queue and redo
+    if (e->last_ct[CT_OVF_QUEUE] && !e->last_ct[CT_OVF_SHORT]) {  // (bound violated) grow the b* queue, redo
       for (ab_engine* d : D) {
-        long long need = (long long)(e->last_ct[CT_BSTAR] + e->last_ct[CT_OVF_QUEUE]);
-        d->capQ = (int)std::min<long long>(std::max<long long>(2ll * d->capQ, need + need / 4 + 1024), 1ll << 30);
+        int off = 0;
+        for (int t = 0; t < 3; ++t) d->qcap[t] = 2 * d->qcap[t] + 1024, d->qoff[t] = off, off += d->qcap[t];
+        d->capQ = off;
         TRYD(d, d->q_item.ensure(d->capQ) == cudaSuccess && d->q_M.ensure(d->capQ) == cudaSuccess ? AB_OK : AB_E_OOM);
         ++d->retries;
       }

@@ -426,20 +426,22 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 // list = (i, slot) pairs; NB = NB_FAST: bonds with a larger side are appended to ovf (indices into
 // list) for the NB = NBMAX instantiation, which runs over ovf (list_idx != nullptr).
 template <typename R, int NB>
-__global__ void __launch_bounds__(128) k_rebo(const int2* bonds, const int* nbonds, const int* list_idx,
+__global__ void __launch_bounds__(128) k_rebo(BondList BL, const int* list_idx,
                                               int* ovf, int* novf, ShortList<R> S, const signed char* typ,
                                               const int* owner, const int* gid, const char4* shift, double* F,
                                               StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
   red_init(rs);
   const Tab<R>& T = tab<R>();
-  const int nb = list_idx ? *novf : *nbonds;
+  const int n0 = BL.cnt[0], n01 = n0 + BL.cnt[1];
+  const int nb = list_idx ? *novf : n01 + BL.cnt[2];
   double e[3 + 6] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long nq = 0, nbad = 0, ncount = 0, nang = 0;
   int stride = gridDim.x * blockDim.x;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += stride) {
-    int bidx = list_idx ? list_idx[t] : t;
-    int2 bd = bonds[bidx];
+    int bidx = list_idx ? list_idx[t]
+                        : (t < n0 ? t : (t < n01 ? BL.cap + (t - n0) : 2 * BL.cap + (t - n01)));
+    int2 bd = BL.b[bidx];
     int i = bd.x, q = bd.y;
     size_t e0 = (size_t)i * S.capS + q;
     int J = S.nbr[e0];
@@ -604,15 +606,18 @@ __device__ __forceinline__ R lj_v(int p, R r2, double r2d, R& dVr_over_r) {
   return V;
 }
 
+// window-candidate queue in three regions by species pair (region t: item[off[t] .. off[t] +
+// cap[t]), count[t] entries), sized from the build-time bound so it cannot overflow
 struct BstarQueue {
   int4* item;  // i, J, -, -
   double* M;
-  int* count;
-  int cap;
+  int* count;  // [3]
+  int cap[3], off[3];
 };
 
 // ---------------------------------------------------------------- deferred b* batch
-// E = (S_r S_b(b*) + 1 - S_r) C V for every canonical LJ pair with C != 0 and S_r != 0.
+// E = (S_r S_b(b*) + 1 - S_r) C V for every canonical LJ pair with C != 0 queued as a
+// window candidate (r^2 pre-filter); pairs with S_r == 0 reduce to the plain gated LJ C V.
 // FULL = false: NB_FAST, forward pass only; a pair whose S_b is in its transition (dS_b != 0),
 // whose C is fractional (0 < M) or whose side is too large is deferred to ovf for FULL = true.
 template <typename R, int NB, bool FULL>
@@ -623,12 +628,14 @@ __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_id
   __shared__ RedSmem rs;
   red_init(rs);
   const Tab<R>& T = tab<R>();
-  const int nq = FULL ? *novf : min(*Qu.count, Qu.cap);
+  const int q0 = min(Qu.count[0], Qu.cap[0]), q1 = min(Qu.count[1], Qu.cap[1]), q2 = min(Qu.count[2], Qu.cap[2]);
+  const int nq = FULL ? *novf : q0 + q1 + q2;
   double e[1 + 6] = {0, 0, 0, 0, 0, 0, 0};
   unsigned long long ntr = 0, nb = 0, nbad = 0;
   int stride = gridDim.x * blockDim.x;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += stride) {
-    int qi = FULL ? list_idx[t] : t;
+    int qi = FULL ? list_idx[t]
+                  : (t < q0 ? Qu.off[0] + t : (t < q0 + q1 ? Qu.off[1] + (t - q0) : Qu.off[2] + (t - q0 - q1)));
     int4 it = Qu.item[qi];
     int i = it.x, J = it.y;
     double Md = Qu.M[qi];
@@ -637,34 +644,41 @@ __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_id
       continue;
     }
     double4 pi = pos[i], pj = pos[J];
-    double dxd = pj.x - pi.x, dyd = pj.y - pi.y, dzd = pj.z - pi.z;
+    double dxd = __dsub_rn(pj.x, pi.x), dyd = __dsub_rn(pj.y, pi.y), dzd = __dsub_rn(pj.z, pi.z);
     double r2d = r2_exact(dxd, dyd, dzd);
     double rd = sqrt(r2d);
     int ti = typ[i], tj = typ[J], p = ti + tj;
+    // the queue holds window candidates: S_r(r) != 0 decided exactly in fp64 in both precision
+    // modes (reading A14); outside the window the pair is the plain gated LJ (Q = 1)
+    const bool win = (rd - c_tabd.sigma[p]) / (c_tabd.srhi[p] - c_tabd.sigma[p]) < 1.0;
     V3<R> d = mk3<R>((R)dxd, (R)dyd, (R)dzd);
     R r = (R)rd, ir = R(1) / r;
     R rho = T.rho[p];
-    V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
     BoState<R, NB> st;
-    bo_forward<R, false, NB, !FULL>(S, typ, i, J, ds, rho, st);
-    if (!FULL && st.overflow) {
-      list_append(ovf, novf, 1 << 30, qi);
-      continue;
+    R bs = 0, B = 1, dB = 0;
+    if (win) {
+      V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
+      bo_forward<R, false, NB, !FULL>(S, typ, i, J, ds, rho, st);
+      if (!FULL && st.overflow) {
+        list_append(ovf, novf, 1 << 30, qi);
+        continue;
+      }
+      bs = bo_value(st);
+      B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
+      if (!FULL && dB != R(0)) {  // S_b transition: the reverse pass of b* is needed
+        list_append(ovf, novf, 1 << 30, qi);
+        continue;
+      }
+    } else {
+      st.bad = false;
     }
-    R bs = bo_value(st);
-    R dB;
-    R B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
-    if (!FULL && dB != R(0)) {  // S_b transition: the reverse pass of b* is needed
-      list_append(ovf, novf, 1 << 30, qi);
-      continue;
-    }
-    R dP;
-    R P = sw<R>(r, T.sigma[p], T.srhi[p], dP);
+    R dP = 0;
+    R P = win ? sw<R>(r, T.sigma[p], T.srhi[p], dP) : R(0);
     R dVr;
     R V = lj_v<R>(p, (R)r2d, r2d, dVr);
     R M = (R)Md, C = R(1) - M;
     R tb = (bs - T.bmin[p]) / (T.bmax[p] - T.bmin[p]);
-    if (tb > R(0) && tb < R(1)) ++ntr;
+    if (win && tb > R(0) && tb < R(1)) ++ntr;
     R Q = P * B + R(1) - P;
     R E = Q * C * V;
     V3<R> gd = ((C * (Q * dVr + V * (B - R(1)) * dP * ir))) * d;
@@ -686,8 +700,8 @@ __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_id
     atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
     vir_add(e + 1, d, gd);
     e[0] += (double)E;
-    ++nb;
-    nbad += st.bad;
+    nb += win;
+    nbad += win && st.bad;
     if (stage.rows) {
       double* row = stage_row(stage, 7);
       if (row) {

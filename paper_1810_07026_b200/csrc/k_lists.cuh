@@ -103,6 +103,8 @@ struct LJLists {
   int* nbr[3];
   double near2;    // (3 r_max,max + skin)^2
   double pure2[3]; // (r_lo(p) - skin)^2, or -1 if that band is empty
+  double bq2[3];   // (2^(1/6) sigma_p (1 + 1e-9) + skin)^2: canonical pairs that can become b*
+  int* bqcnt;      // [3] per species pair: bound of the b* candidate queue until the next build
 };
 
 __device__ __forceinline__ void warp_append(bool take, int* row, int cap, int& n, int b) {
@@ -126,6 +128,8 @@ __global__ void k_build_lj(int N, const double4* pos, Grid g, const int* cell_st
   int cz = cell_coord(p.z, g.lo[2], g.cs[2], g.nc[2]);
   int z0 = max(0, cz - nr), z1 = min(g.nc[2] - 1, cz + nr);
   int n[3] = {0, 0, 0};
+  int nq[3] = {0, 0, 0};
+  const long long ka = key_of(p);
   int* row[3];
   for (int c = 0; c < 3; ++c) row[c] = Lg.nbr[c] + (size_t)a * Lg.cap[c];
   for (int ax = max(0, cx - nr); ax <= min(g.nc[0] - 1, cx + nr); ++ax)
@@ -151,12 +155,16 @@ __global__ void k_build_lj(int N, const double4* pos, Grid g, const int* cell_st
         warp_append(nearp, row[0], Lg.cap[0], n[0], b);
         warp_append(purep, row[1], Lg.cap[1], n[1], b);
         warp_append(bandp, row[2], Lg.cap[2], n[2], b);
+        const bool bq = nearp && r2 <= Lg.bq2[pr] && ka < key_of(pos[b]);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) nq[t] += __popc(__ballot_sync(0xffffffffu, bq && pr == t));
       }
     }
   if (lane == 0) {
     for (int c = 0; c < 3; ++c) {
       Lg.cnt[c][a] = n[c];
       atomicMax(maxcnt + c, n[c]);
+      if (nq[c]) atomicAdd(Lg.bqcnt + c, nq[c]);
     }
   }
 }
@@ -219,18 +227,26 @@ __device__ __forceinline__ V3<R> sl_d(const ShortList<R>& S, int a, int n, R& r)
   return mk3<R>(v.x, v.y, v.z);
 }
 
+// REBO half bonds in three regions by species pair (CC, CH, HH), so that the warps of the bond
+// kernel run uniform neighbour loops (species-sorted bond batches).
+struct BondList {
+  int2* b;    // region t at b + t * cap: (i, slot in N(i))
+  int* cnt;   // [3]
+  int cap;    // per region (>= canonical short-list entries of the owned atoms)
+};
+
 // Exact short list every step: filter the intermediate list at r <= r_max
 // (closed boundary), store d, r, w = S(r; r_min, r_max), dw/dr; N^C, N^H per atom.
-// Local atoms also append their canonical entries to the REBO bond list.
+// Local atoms also append their canonical entries to the REBO bond list of the species pair.
 template <typename R>
 __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, const int* in_nbr, int capI,
-                        ShortList<R> S, const int* gid, const char4* shift, int2* bonds, int* nbonds,
-                        unsigned long long* ct, RedRows RR) {
+                        ShortList<R> S, const int* gid, const char4* shift, BondList BL, unsigned long long* ct,
+                        RedRows RR) {
   __shared__ RedSmem rs;
   red_init(rs);
   int a = blockIdx.x * blockDim.x + threadIdx.x;
   bool live = a < NT;
-  int nloc = 0, nbond = 0;
+  int nloc = 0, nbond[3] = {0, 0, 0};
   if (live) {
     const Tab<R>& T = tab<R>();
     double4 p = pos[a];
@@ -257,7 +273,7 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
           S.w[base + n] = {w, dw};
           if (tb == 0) nc += w;
           else nh += w;
-          if (a < N && ka < key_of(pb)) ++nbond;
+          if (a < N && ka < key_of(pb)) ++nbond[pr];
         }
         ++n;
       }
@@ -270,25 +286,36 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
     S.Ntot[a] = nc + nh;
     if (a < N) nloc = n;
   }
-  // bond list compaction (warp-aggregated atomics) -- order is irrelevant to the physics
+  // bond list compaction per species pair (warp-aggregated atomics; order within a region is
+  // irrelevant to the physics)
   unsigned lane = threadIdx.x & 31;
-  int incl = nbond;
+  int w[3];
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= (unsigned)o) incl += v;
+  for (int t = 0; t < 3; ++t) {
+    int incl = nbond[t];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= (unsigned)o) incl += v;
+    }
+    int total = __shfl_sync(0xffffffffu, incl, 31);
+    int basew = 0;
+    if (lane == 31 && total) basew = atomicAdd(BL.cnt + t, total);
+    basew = __shfl_sync(0xffffffffu, basew, 31);
+    w[t] = basew + incl - nbond[t];
   }
-  int total = __shfl_sync(0xffffffffu, incl, 31);
-  int basew = 0;
-  if (lane == 31 && total) basew = atomicAdd(nbonds, total);
-  basew = __shfl_sync(0xffffffffu, basew, 31);
-  int w = basew + incl - nbond;
-  if (live && a < N && nbond) {
+  if (live && a < N && (nbond[0] | nbond[1] | nbond[2])) {
     size_t base = (size_t)a * S.capS;
     int n = S.cnt[a];
+    const long long ka = key_of(pos[a]);
+    const int ta = type_of(pos[a]);
     for (int q = 0; q < n; ++q) {
       int b = S.nbr[base + q];
-      if (key_of(pos[a]) < key_of(pos[b])) bonds[w++] = make_int2(a, q);
+      const double4 pb = pos[b];
+      if (ka < key_of(pb)) {
+        int t = ta + type_of(pb);
+        BL.b[(size_t)t * BL.cap + w[t]++] = make_int2(a, q);
+      }
     }
   }
   red_add_u(rs, CT_SHORT, (unsigned long long)nloc);

@@ -155,18 +155,28 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
   __syncwarp();
   const bool ovf = s.ovf != 0;
 
-  // 2. pairs
+  // 2. pairs.  The next entry's index and position are loaded before the current one is
+  // processed (two gathers in flight per lane).  Pairs that may lie in the S_r window
+  // (r^2 < (2^(1/6) sigma)^2 (1 + 1e-9), a superset of S_r != 0) are not evaluated here: the
+  // canonical side queues them and the b* batch takes the exact fp64 window decision and
+  // evaluates the whole pair (b* if S_r != 0, else the plain gated LJ) for both atoms.
   double fx = 0, fy = 0, fz = 0, en = 0;
   double W[6] = {0, 0, 0, 0, 0, 0};
-  unsigned long long nlj = 0, nc0 = 0;
+  unsigned nlj = 0, nc0 = 0;
   if (cntN > 0) {
     const double4 pi = A.pos[i];
     const int ti = type_of(pi);
     const long long ki = key_of(pi);
     const int* row = A.nbr[0] + (size_t)i * A.cap[0];
+    int Jn = gl < cntN ? row[gl] : i;
+    double4 pjn = A.pos[Jn];
     for (int q = gl; q < cntN; q += NEAR_GROUP) {
-      const int J = row[q];
-      const double4 pj = A.pos[J];
+      const int J = Jn;
+      const double4 pj = pjn;
+      if (q + NEAR_GROUP < cntN) {
+        Jn = row[q + NEAR_GROUP];
+        pjn = A.pos[Jn];
+      }
       const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
       const double r2 = r2_exact(dx, dy, dz);
       const int p = ti + type_of(pj);
@@ -175,13 +185,8 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
       double Md = 0.0;
       if (inr && r2 <= c_geo.reach2) Md = ovf ? (double)path_search(S, i, J).M : reach_lookup_fast(s, J);
       const bool c0 = Md == 1.0;  // C_ij == 0 (Alg. 3 "continue")
-      // S_r(r) != 0 decided exactly in fp64 in both precision modes (reading A14); r^2 pre-filter
-      bool bst = false;
-      if (inr && !c0 && r2 < c_geo.srhi2_hi[p]) {
-        double rd = sqrt(r2);
-        bst = (rd - c_tabd.sigma[p]) / (c_tabd.srhi[p] - c_tabd.sigma[p]) < 1.0;
-      }
-      const bool norm = inr && !c0 && !bst;
+      const bool cand = inr && !c0 && r2 < c_geo.srhi2_hi[p];  // possible S_r != 0: b* batch
+      const bool norm = inr && !c0 && !cand;
       nlj += inr && canon;
       nc0 += c0 && canon;
       // LJ for every lane (weight 0 unless norm)
@@ -206,16 +211,17 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
         vir_add(W, dd, (R(0.5) * fr) * dd);
       }
       // rare work last
-      if (bst && canon) {  // deferred b* batch: the whole pair is evaluated once by the canonical side
+      if (cand && canon) {  // deferred to the b* batch: the whole pair, once, by the canonical side
         unsigned am = __activemask();
-        int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+        unsigned grp = __match_any_sync(am, p);  // one aggregated append per species pair
+        int lane = threadIdx.x & 31, leader = __ffs(grp) - 1;
         int base = 0;
-        if (lane == leader) base = atomicAdd(Qu.count, __popc(am));
+        if (lane == leader) base = atomicAdd(Qu.count + p, __popc(grp));
         base = __shfl_sync(am, base, leader);
-        int k = base + __popc(am & ((1u << lane) - 1u));
-        if (k < Qu.cap) {
-          Qu.item[k] = make_int4(i, J, 0, 0);
-          Qu.M[k] = Md;
+        int k = base + __popc(grp & ((1u << lane) - 1u));
+        if (k < Qu.cap[p]) {
+          Qu.item[Qu.off[p] + k] = make_int4(i, J, 0, 0);
+          Qu.M[Qu.off[p] + k] = Md;
         } else {
           atomicAdd(ct + CT_OVF_QUEUE, 1ull);
         }
@@ -227,7 +233,8 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
         if (VIRIAL)
           for (int c = 0; c < 6; ++c) W[c] += Wp[c];
       }
-      if (stage.rows && canon && inr && !bst) stage_lj_row(stage, gid[i], gid[J], shift[J], c0 ? 0.0 : (double)C, 0.0);
+      if (stage.rows && canon && inr && norm) stage_lj_row(stage, gid[i], gid[J], shift[J], (double)C, 0.0);
+      if (stage.rows && canon && inr && c0) stage_lj_row(stage, gid[i], gid[J], shift[J], 0.0, 0.0);
     }
   }
 
@@ -239,8 +246,8 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
   red_add_d(rs, ACC_ELJ, 0.5 * en);
   if (VIRIAL)
     for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, W[c]);
-  red_add_u(rs, CT_LJ, nlj);
-  red_add_u(rs, CT_C0, nc0);
+  red_add_u(rs, CT_LJ, (unsigned long long)nlj);
+  red_add_u(rs, CT_C0, (unsigned long long)nc0);
   red_max_u(rs, CT_MAXREACH, gl == 0 ? (unsigned long long)s.nins : 0ull);
   red_add_u(rs, CT_OVF_REACH, gl == 0 && ovf ? 1ull : 0ull);
   red_add_u(rs, CT_LJENT, gl == 0 ? (unsigned long long)cntN : 0ull);
@@ -253,7 +260,7 @@ constexpr int FAR_UNROLL = 4;
 template <typename R, bool VIRIAL, bool BAND>
 __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, double4 pi, int ti, long long ki,
                                          const int* gid, const char4* shift, StageBuf stage, double& fx, double& fy,
-                                         double& fz, double& en, double (&W)[6], unsigned long long& nlj) {
+                                         double& fz, double& en, double (&W)[6], unsigned& nlj) {
   const Tab<R>& T = tab<R>();
   const int lane = threadIdx.x & 31;
   const int cnt = A.cnt[list][i];
@@ -281,14 +288,15 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
       const bool valid = J[u] >= 0;
       const bool hj = type_of(pj[u]) != 0;
       double dx = __dsub_rn(pj[u].x, pi.x), dy = __dsub_rn(pj[u].y, pi.y), dz = __dsub_rn(pj[u].z, pi.z);
-      double r2 = r2_exact(dx, dy, dz);
-      // pure entries are inside r_lo <= r_c by construction; band entries: exact cutoff decision
+      // pure entries are inside r_lo <= r_c by construction (no decision: r^2 may be fused);
+      // band entries: exact (un-fused) cutoff decision, as the oracle's
+      double r2 = BAND ? r2_exact(dx, dy, dz) : fma(dz, dz, fma(dy, dy, dx * dx));
       bool in = valid && (!BAND || r2 <= (hj ? rcb : rca));
       nlj += (in && ki < key_of(pj[u]));
       R rr2 = in ? (R)r2 : R(1);
-      R y = rsqrt_fast(rr2);  // 1/r
+      R y = BAND ? rsqrt_fast(rr2) : R(0);  // 1/r (taper only)
       R dVr;
-      R V = lj_plain<R>(hj ? e4b : e4a, hj ? s2b : s2a, y * y, dVr);
+      R V = lj_plain<R>(hj ? e4b : e4a, hj ? s2b : s2a, BAND ? y * y : rcp_fast(rr2), dVr);
       if (BAND) {  // taper S(r; r_lo, r_c) (reading A10), branch-free
         R r = rr2 * y;
         R iv = hj ? ivb : iva;
@@ -329,7 +337,8 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   double en = 0;
   double W[6] = {0, 0, 0, 0, 0, 0};
-  unsigned long long nlj = 0, ne = 0;
+  unsigned nlj = 0;
+  unsigned long long ne = 0;
   // grid-stride over atoms: a resident grid, one warp per atom at a time
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < A.N; i += nwarps) {
     const double4 pi = A.pos[i];
@@ -347,8 +356,8 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
   red_add_d(rs, ACC_ELJ, 0.5 * en);
   if (VIRIAL)
     for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, W[c]);
-  red_add_u(rs, CT_LJ, nlj);
-  red_add_u(rs, CT_LJFAR, nlj);
+  red_add_u(rs, CT_LJ, (unsigned long long)nlj);
+  red_add_u(rs, CT_LJFAR, (unsigned long long)nlj);
   red_add_u(rs, CT_LJENT, ne);
   red_add_u(rs, CT_LJENTFAR, ne);
   red_flush(rs, RR);

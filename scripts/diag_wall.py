@@ -46,6 +46,15 @@ for serial in ("0", "1", "0", "1"):
         ts.append(a.elapsed_time(b))
     nb2 = eng.stats()["n_rebuilds"] - nb
     ts.sort()
+    import ctypes as C
+    eng.L.ab_set_profiling(eng.h, 1)
+    eng.run_nve(50, s.dt)
+    ms = (C.c_double * 8)()
+    cnt = (C.c_int64 * 8)()
+    eng.L.ab_get_phase_ms(eng.h, ms, cnt)
+    eng.L.ab_set_profiling(eng.h, 0)
+    ph = {n: round(ms[q] / max(cnt[q], 1), 4) for q, n in enumerate(["short", "rebo", "near", "bstar", "integ", "rebuild", "far"])}
+    print(ph)
     print(f"serial={serial}: long run {K} steps ({nb1} rebuilds): device {dev:.4f} ms/step, wall {wall:.4f} | "
           f"per-step flushed 100 steps ({nb2} rebuilds): mean {sum(ts) / len(ts):.4f} median {ts[50]:.4f} max {ts[-1]:.3f}")
     eng.close()

@@ -38,5 +38,6 @@ for r in rows:
 tot = sum(v[0] for v in agg.values()) or 1
 toti = sum(v[1] for v in agg.values()) or 1
 print('samples', tot, 'warp-inst', toti)
-for k, v in sorted(agg.items(), key=lambda x: -x[1][0])[:int(sys.argv[3]) if len(sys.argv) > 3 else 40]:
+key = 1 if len(sys.argv) > 4 and sys.argv[4] == "inst" else 0
+for k, v in sorted(agg.items(), key=lambda x: -x[1][key])[:int(sys.argv[3]) if len(sys.argv) > 3 else 40]:
     print(f"{100*v[0]/tot:5.1f}% smp {100*v[1]/toti:5.1f}% inst  act={v[2]/max(v[1],1):4.1f}  {k[0]}:{k[1]}  {k[2]}")
