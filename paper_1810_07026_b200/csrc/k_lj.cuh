@@ -25,10 +25,15 @@
 
 namespace ab {
 
-constexpr int NEAR_GROUP = 8;                    // lanes per atom
-constexpr int NEAR_ATOMS = 16;                   // atoms per 128-thread block
-constexpr int NEAR_SLOTS = 64;                   // reach table slots per atom
-constexpr int NEAR_TWO = 64;                     // 2-hop frontier capacity per atom
+#ifndef AB_NEAR_GROUP
+#define AB_NEAR_GROUP 8
+#endif
+#ifndef AB_NEAR_SLOTS
+#define AB_NEAR_SLOTS 64
+#endif
+constexpr int NEAR_GROUP = AB_NEAR_GROUP;        // lanes per atom (measured: 8 beats 16 and 32)
+constexpr int NEAR_ATOMS = 128 / NEAR_GROUP;     // atoms per 128-thread block
+constexpr int NEAR_SLOTS = AB_NEAR_SLOTS;        // reach table slots per atom (measured: 64 beats 128)
 
 struct ReachSmem {
   int keys[NEAR_SLOTS];
@@ -36,7 +41,10 @@ struct ReachSmem {
   int nins, ovf;
 };
 
-__device__ __forceinline__ unsigned reach_hash(int key) { return ((unsigned)key * 2654435761u) >> 26; }
+__host__ __device__ constexpr int log2i(int v) { return v <= 1 ? 0 : 1 + log2i(v / 2); }
+__device__ __forceinline__ unsigned reach_hash(int key) {
+  return ((unsigned)key * 2654435761u) >> (32 - log2i(NEAR_SLOTS));
+}
 
 __device__ __forceinline__ void reach_insert(ReachSmem& s, int key, double M) {
   unsigned h = reach_hash(key);
@@ -115,8 +123,17 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
                                                                     BstarQueue Qu, StageBuf stage, RedRows RR) {
   __shared__ ReachSmem sm_all[NEAR_ATOMS];
   __shared__ RedSmem rs;
-  red_init(rs);
+  // per-pair parameters indexed by the species pair p, which differs between the lanes of a
+  // warp: shared-memory copies (an indexed __constant__ load serialises per distinct address)
+  __shared__ double pd[9];  // r_c^2, S_r window pre-filter, r_lo^2
+  __shared__ R pr_[12];     // 4 eps, sigma^2, r_lo, r_c
   const Tab<R>& T = tab<R>();
+  if (threadIdx.x < 3) {
+    const int t = threadIdx.x;
+    pd[t] = c_geo.rc2[t], pd[3 + t] = c_geo.srhi2_hi[t], pd[6 + t] = c_geo.rlo2[t];
+    pr_[t] = R(4) * T.eps[t], pr_[3 + t] = T.sigma2[t], pr_[6 + t] = T.rlo[t], pr_[9 + t] = T.rc[t];
+  }
+  red_init(rs);
   const int grp = threadIdx.x / NEAR_GROUP, gl = threadIdx.x % NEAR_GROUP;
   ReachSmem& s = sm_all[grp];
   const int i = blockIdx.x * NEAR_ATOMS + grp;
@@ -131,7 +148,11 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
   if (gl == 0) s.nins = 0, s.ovf = 0;
   __syncwarp();
   const size_t bi = (size_t)(active ? i : 0) * S.capS;
+#ifdef AB_ABL_NOREACH
+  const int ni = 0;  // ablation (timing experiments only): no reach set
+#else
   const int ni = cntN > 0 ? S.cnt[i] : 0;
+#endif
   for (int t = gl; t < ni; t += NEAR_GROUP) {
     int k = S.nbr[bi + t];
     R w1 = S.w[bi + t].x;
@@ -180,12 +201,14 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
       const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
       const double r2 = r2_exact(dx, dy, dz);
       const int p = ti + type_of(pj);
-      const bool inr = r2 <= c_geo.rc2[p];
+      const bool inr = r2 <= pd[p];
       const bool canon = ki < key_of(pj);
       double Md = 0.0;
+#ifndef AB_ABL_NOLOOKUP
       if (inr && r2 <= c_geo.reach2) Md = ovf ? (double)path_search(S, i, J).M : reach_lookup_fast(s, J);
+#endif
       const bool c0 = Md == 1.0;  // C_ij == 0 (Alg. 3 "continue")
-      const bool cand = inr && !c0 && r2 < c_geo.srhi2_hi[p];  // possible S_r != 0: b* batch
+      const bool cand = inr && !c0 && r2 < pd[3 + p];  // possible S_r != 0: b* batch
       const bool norm = inr && !c0 && !cand;
       nlj += inr && canon;
       nc0 += c0 && canon;
@@ -193,10 +216,10 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, S
       R rr2 = norm ? (R)r2 : R(1);
       R y = rsqrt_fast(rr2);
       R dVr;
-      R V = lj_plain<R>(R(4) * T.eps[p], T.sigma2[p], y * y, dVr);
-      if (norm && r2 > c_geo.rlo2[p]) {  // taper S(r; r_lo, r_c) (reading A10): rare in the near list
+      R V = lj_plain<R>(pr_[p], pr_[3 + p], y * y, dVr);
+      if (norm && r2 > pd[6 + p]) {  // taper S(r; r_lo, r_c) (reading A10): rare in the near list
         R r = rr2 * y, dsw;
-        R sv = sw<R>(r, T.rlo[p], T.rc[p], dsw);
+        R sv = sw<R>(r, pr_[6 + p], pr_[9 + p], dsw);
         dVr = dVr * sv + V * dsw * y;
         V = V * sv;
       }
