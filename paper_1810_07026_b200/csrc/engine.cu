@@ -162,7 +162,7 @@ struct ab_engine {
   DBuf<unsigned char> s_dr, s_w, s_N;  // typed by precision at use
   DBuf<int2> bonds;
   DBuf<int4> q_item;
-  DBuf<int> ovf_bond, ovf_q;  // overflow (large side / full b*) index lists
+  DBuf<int> ovf_bond, ovf_q, ovf_q2;  // overflow (large side / full b*) index lists
   DBuf<double> q_M;
   // one small device scratch block, zeroed with a single memset per evaluation:
   //   acc (ACC_N doubles) at 0, ct (CT_N + 1 u64; [CT_N] = max displacement^2) at 128,
@@ -931,10 +931,11 @@ ab_status enqueue_forces(ab_engine* e) {
   ShortList<R> S = short_view<R>(e);
   // grids and the per-block partial rows of the energy / virial / counter reduction
   const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
-  const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4, g_slow = e->nsm;
-  const int nrows = g_short + g_rebo + g_near + g_far + g_bstar + 2 * g_slow;
+  const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4, g_slow = e->nsm * 2;
+  const int nrows = g_short + g_rebo + g_near + g_far + 2 * g_bstar + 2 * g_slow;
   CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
   CK(e->ovf_q.ensure(e->capQ));
+  CK(e->ovf_q2.ensure(e->capQ));
   CK(e->red_d.ensure((size_t)ACC_N * nrows));
   CK(e->red_u.ensure((size_t)CT_N * nrows));
   RedRows RR{e->red_d.p, e->red_u.p, nrows, 0};
@@ -1007,12 +1008,21 @@ ab_status enqueue_forces(ab_engine* e) {
   RR.row0 = row_far + g_far;
   {
     cudaEvent_t t = prof_start(e, st);
-    k_bstar<R, NB_FAST, false><<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->pos.p, S,
-                                                        e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+    // forward-only fast path; pairs needing the reverse pass / path forces -> ovf_q (NB_FAST
+    // sides, count small_i[9]), pairs with a large side -> ovf_q2 (NBMAX, count small_i[1])
+    k_bstar<R, NB_FAST, false><<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p,
+                                                        e->small_i.p + 1, e->pos.p, S, e->typ.p, e->owner.p,
+                                                        e->gid.p, e->shift.p, e->F.p, sb1, RR);
     CKL();
     RR.row0 += g_bstar;
-    k_bstar<R, NBMAX, true><<<g_slow, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, e->pos.p, S, e->typ.p,
-                                                    e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+    k_bstar<R, NB_FAST, true><<<g_bstar, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, nullptr, nullptr,
+                                                       e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p,
+                                                       sb1, RR);
+    CKL();
+    RR.row0 += g_bstar;
+    k_bstar<R, NBMAX, true><<<g_slow, 128, 0, st>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr,
+                                                    e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p,
+                                                    sb1, RR);
     CKL();
     prof_stop(e, 3, st, t);
   }
@@ -1286,7 +1296,7 @@ void free_engine(ab_engine* e) {
   for (auto* b : bd) b->release();
   DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->key2, &e->val, &e->val2, &e->cell_start,
                      &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
-                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_q,
+                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_q, &e->ovf_q2,
                      &e->sendl[0], &e->sendl[1], &e->fl[0], &e->fl[1], &e->fl[2], &e->idx[0], &e->idx[1],
                      &e->idx[2], &e->cnt_d};
   for (auto* b : bi) b->release();

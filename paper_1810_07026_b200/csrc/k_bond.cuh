@@ -618,11 +618,12 @@ struct BstarQueue {
 // ---------------------------------------------------------------- deferred b* batch
 // E = (S_r S_b(b*) + 1 - S_r) C V for every canonical LJ pair with C != 0 queued as a
 // window candidate (r^2 pre-filter); pairs with S_r == 0 reduce to the plain gated LJ C V.
-// FULL = false: NB_FAST, forward pass only; a pair whose S_b is in its transition (dS_b != 0),
-// whose C is fractional (0 < M) or whose side is too large is deferred to ovf for FULL = true.
+// FULL = false: NB_FAST, forward pass only; a pair whose S_b is in its transition (dS_b != 0) or
+// whose C is fractional (0 < M) is deferred to ovf for FULL = true with NB_FAST register sides,
+// a pair with a side larger than NB_FAST to ovf2 for FULL = true with NB = NBMAX.
 template <typename R, int NB, bool FULL>
-__global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf,
-                                               const double4* pos, ShortList<R> S, const signed char* typ,
+__global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf, int* ovf2,
+                                               int* novf2, const double4* pos, ShortList<R> S, const signed char* typ,
                                                const int* owner, const int* gid, const char4* shift, double* F,
                                                StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
@@ -639,10 +640,6 @@ __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_id
     int4 it = Qu.item[qi];
     int i = it.x, J = it.y;
     double Md = Qu.M[qi];
-    if (!FULL && Md > 0.0) {  // fractional C_ij: forces along the path -> full kernel
-      list_append(ovf, novf, 1 << 30, qi);
-      continue;
-    }
     double4 pi = pos[i], pj = pos[J];
     double dxd = __dsub_rn(pj.x, pi.x), dyd = __dsub_rn(pj.y, pi.y), dzd = __dsub_rn(pj.z, pi.z);
     double r2d = r2_exact(dxd, dyd, dzd);
@@ -658,19 +655,19 @@ __global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_id
     R bs = 0, B = 1, dB = 0;
     if (win) {
       V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
-      bo_forward<R, false, NB, !FULL>(S, typ, i, J, ds, rho, st);
-      if (!FULL && st.overflow) {
-        list_append(ovf, novf, 1 << 30, qi);
+      bo_forward<R, false, NB, !FULL || NB <= NB_FAST>(S, typ, i, J, ds, rho, st);
+      if (!FULL && st.overflow) {  // a side larger than NB_FAST: the NBMAX kernel
+        list_append(ovf2, novf2, 1 << 30, qi);
         continue;
       }
       bs = bo_value(st);
       B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
-      if (!FULL && dB != R(0)) {  // S_b transition: the reverse pass of b* is needed
-        list_append(ovf, novf, 1 << 30, qi);
-        continue;
-      }
     } else {
       st.bad = false;
+    }
+    if (!FULL && (dB != R(0) || Md > 0.0)) {  // S_b transition or fractional C_ij: reverse pass /
+      list_append(ovf, novf, 1 << 30, qi);  // path forces in the full kernel (NB_FAST sides)
+      continue;
     }
     R dP = 0;
     R P = win ? sw<R>(r, T.sigma[p], T.srhi[p], dP) : R(0);
