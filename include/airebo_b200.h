@@ -179,6 +179,13 @@ ab_status ab_get_stage(ab_engine* e, int stage, int64_t* count, double* out);
 ab_status ab_set_profiling(ab_engine* e, int on);
 ab_status ab_get_phase_ms(ab_engine* e, double ms[AB_NPHASE], int64_t n[AB_NPHASE]);
 
+/* Kernel concurrency inside one force evaluation (default on): the far-LJ kernel and the REBO
+ * kernel run on two engine-owned streams beside the near-LJ -> b* chain.  on = 0 runs the whole
+ * evaluation on the engine stream, one kernel at a time (isolated per-kernel timing; the
+ * environment variable AB_SERIAL_KERNELS=1 sets the default at ab_create).  Results are the same
+ * up to the order of fp64 atomic additions. */
+ab_status ab_set_concurrency(ab_engine* e, int on);
+
 /* FP64 (prec = AB_FP64) or FP32 (AB_MIXED) FMA-throughput microbenchmark on the engine's GPU:
  * all SMs, 8 independent FMA chains per thread; returns the achieved TFLOP/s (2 flops per FMA).
  * Used as the measured ALU roofline denominator by bench.py. */

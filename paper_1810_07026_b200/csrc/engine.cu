@@ -2014,6 +2014,15 @@ ab_status ab_set_profiling(ab_engine* e, int on) {
   return AB_OK;
 }
 
+ab_status ab_set_concurrency(ab_engine* e, int on) {
+  if (!e) return AB_E_ARG;
+  cudaSetDevice(e->dev);
+  CK(cudaStreamSynchronize(e->st));
+  e->serial = on == 0;
+  for (ab_engine* d : doms(e)) d->serial = on == 0;
+  return AB_OK;
+}
+
 ab_status ab_get_phase_ms(ab_engine* e, double ms[AB_NPHASE], int64_t n[AB_NPHASE]) {
   if (!e || !ms || !n) return AB_E_ARG;
   cudaSetDevice(e->dev);

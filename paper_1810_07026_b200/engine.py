@@ -41,7 +41,7 @@ EXPORTS = ["ab_create", "ab_destroy", "ab_last_error", "ab_set_stream", "ab_set_
            "ab_set_positions", "ab_set_velocities", "ab_compute", "ab_run_nve", "ab_get_positions",
            "ab_get_velocities", "ab_get_forces", "ab_get_list", "ab_get_stats", "ab_record_stages", "ab_get_stage",
            "ab_set_profiling", "ab_get_phase_ms", "ab_peak_flops", "ab_device_info", "ab_nccl_unique_id",
-           "ab_create_dist", "ab_create_virtual", "ab_slab_info", "ab_slab_of"]
+           "ab_create_dist", "ab_create_virtual", "ab_slab_info", "ab_slab_of", "ab_set_concurrency"]
 
 _lib = None
 
@@ -84,6 +84,7 @@ def load(path: str = LIB_PATH):
     L.ab_slab_info.argtypes = [dp, C.c_double, C.c_int, C.c_int, dp, dp]
     L.ab_slab_of.argtypes = [C.c_double, C.c_double, C.c_int]
     L.ab_slab_of.restype = C.c_int
+    L.ab_set_concurrency.argtypes = [vp, C.c_int]
     _lib = L
     return L
 
@@ -166,6 +167,9 @@ class Engine:
         else:
             ptr = 1 if stream_ptr == 0 else stream_ptr
         self._ck(self.L.ab_set_stream(self.h, C.c_void_p(ptr)))
+
+    def set_concurrency(self, on: bool):
+        self._ck(self.L.ab_set_concurrency(self.h, int(on)))
 
     def set_box(self, L):
         b = np.ascontiguousarray(L, dtype=np.float64)
