@@ -256,6 +256,24 @@ __device__ __forceinline__ int gridw(R x, R lo, int n, R w[4], R dw[4]) {
   return i - 1;  // knot index of weight 0
 }
 
+// x exactly on a knot of the integer grid (or clamped to an end): the Hermite weights are the
+// unit vector (0, 1, 0, 0), so a tensor-product sum has a single non-zero value term and only
+// the derivative weights of the other directions contribute -- the same sums with the exact
+// zero terms left out (bitwise identical results).  Saturated hydrocarbons have integer
+// coordination numbers, so this is the common case of P, pi^rc and T.
+template <typename R>
+__device__ __forceinline__ bool on_knot(R x, R lo, int n) {
+  if (x <= lo || x >= lo + R(n - 1)) return true;
+  return x == floor(x);
+}
+// the knot an on-knot (or clamped) coordinate sits on
+template <typename R>
+__device__ __forceinline__ int knot_of(R x, R lo, int n) {
+  if (x <= lo) return 0;
+  if (x >= lo + R(n - 1)) return n - 1;
+  return (int)(x - lo);
+}
+
 // P_ij(N^C, N^H) for a C centre (table index = partner species); value and gradient
 template <typename R>
 __device__ __forceinline__ R pspline(int tj, R x, R y, R& dx, R& dy) {
@@ -263,6 +281,18 @@ __device__ __forceinline__ R pspline(int tj, R x, R y, R& dx, R& dy) {
   R wx[4], dwx[4], wy[4], dwy[4];
   int ax = gridw(x, R(0), 5, wx, dwx);
   int ay = gridw(y, R(0), 5, wy, dwy);
+  if (on_knot(x, R(0), 5) && on_knot(y, R(0), 5)) {  // value: 1 term; gradient: 4 + 4 terms
+    const int kx = knot_of(x, R(0), 5), ky = knot_of(y, R(0), 5);
+    R fx = 0, fy = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      int ka = ax + a, kb = ay + a;
+      if (ka >= 0 && ka <= 4) fx += dwx[a] * T.P[tj][ka * 5 + ky];
+      if (kb >= 0 && kb <= 4) fy += dwy[a] * T.P[tj][kx * 5 + kb];
+    }
+    dx = fx, dy = fy;
+    return T.P[tj][kx * 5 + ky];
+  }
   R f = 0, fx = 0, fy = 0;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
@@ -291,6 +321,19 @@ __device__ __forceinline__ R rtspline(int which, int p, R x, R y, R z, R& gx, R&
   int ax = gridw(x, R(0), 5, wx, dwx);
   int ay = gridw(y, R(0), 5, wy, dwy);
   int az = gridw(z, R(1), 9, wz, dwz);
+  if (on_knot(x, R(0), 5) && on_knot(y, R(0), 5) && on_knot(z, R(1), 9)) {  // 1 + 4 + 4 + 4 terms
+    const int kx = knot_of(x, R(0), 5), ky = knot_of(y, R(0), 5), kz = knot_of(z, R(1), 9);
+    R fx = 0, fy = 0, fz = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      int ka = ax + a, kb = ay + a, kc = az + a;
+      if (ka >= 0 && ka <= 4) fx += dwx[a] * tb[(ka * 5 + ky) * 9 + kz];
+      if (kb >= 0 && kb <= 4) fy += dwy[a] * tb[(kx * 5 + kb) * 9 + kz];
+      if (kc >= 0 && kc <= 8) fz += dwz[a] * tb[(kx * 5 + ky) * 9 + kc];
+    }
+    gx = fx, gy = fy, gz = fz;
+    return tb[(kx * 5 + ky) * 9 + kz];
+  }
   R f = 0, fx = 0, fy = 0, fz = 0;
 #pragma unroll
   for (int a = 0; a < 4; ++a) {

@@ -425,8 +425,14 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 // ---------------------------------------------------------------- REBO + torsion, one thread per bond
 // list = (i, slot) pairs; NB = NB_FAST: bonds with a larger side are appended to ovf (indices into
 // list) for the NB = NBMAX instantiation, which runs over ovf (list_idx != nullptr).
+#ifndef AB_REBO_MINBLOCKS
+#define AB_REBO_MINBLOCKS 1
+#endif
+#ifndef AB_BSTAR_MINBLOCKS
+#define AB_BSTAR_MINBLOCKS 1
+#endif
 template <typename R, int NB>
-__global__ void __launch_bounds__(128) k_rebo(BondList BL, const int* list_idx,
+__global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_rebo(BondList BL, const int* list_idx,
                                               int* ovf, int* novf, ShortList<R> S, const signed char* typ,
                                               const int* owner, const int* gid, const char4* shift, double* F,
                                               StageBuf stage, RedRows RR) {
@@ -622,7 +628,7 @@ struct BstarQueue {
 // whose C is fractional (0 < M) is deferred to ovf for FULL = true with NB_FAST register sides,
 // a pair with a side larger than NB_FAST to ovf2 for FULL = true with NB = NBMAX.
 template <typename R, int NB, bool FULL>
-__global__ void __launch_bounds__(128) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf, int* ovf2,
+__global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBLOCKS : 1) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf, int* ovf2,
                                                int* novf2, const double4* pos, ShortList<R> S, const signed char* typ,
                                                const int* owner, const int* gid, const char4* shift, double* F,
                                                StageBuf stage, RedRows RR) {

@@ -117,7 +117,10 @@ __device__ __forceinline__ double reach_lookup_fast(const ReachSmem& s, int key)
 }
 
 template <typename R, bool VIRIAL>
-__global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS) k_lj_near(LJArgs A, ShortList<R> S, const int* owner,
+#ifndef AB_NEAR_MINBLOCKS
+#define AB_NEAR_MINBLOCKS 7  // measured: 7 blocks (73 regs) beat 6 (80 regs) and 8 (64 regs, spills)
+#endif
+__global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_lj_near(LJArgs A, ShortList<R> S, const int* owner,
                                                                     const int* gid, const char4* shift, double* F,
                                                                     double* acc, unsigned long long* ct,
                                                                     BstarQueue Qu, StageBuf stage, RedRows RR) {
