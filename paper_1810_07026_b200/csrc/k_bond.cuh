@@ -624,9 +624,10 @@ struct BstarQueue {
 // ---------------------------------------------------------------- deferred b* batch
 // E = (S_r S_b(b*) + 1 - S_r) C V for every canonical LJ pair with C != 0 queued as a
 // window candidate (r^2 pre-filter); pairs with S_r == 0 reduce to the plain gated LJ C V.
-// FULL = false: NB_FAST, forward pass only; a pair whose S_b is in its transition (dS_b != 0) or
-// whose C is fractional (0 < M) is deferred to ovf for FULL = true with NB_FAST register sides,
-// a pair with a side larger than NB_FAST to ovf2 for FULL = true with NB = NBMAX.
+// FULL = false: NB_FAST, forward pass of b* (+ the path forces of a fractional C); a pair whose
+// S_b is in its transition (dS_b != 0: the reverse pass of b* is needed) is deferred to ovf for
+// FULL = true with NB_FAST register sides, a pair with a side larger than NB_FAST to ovf2 for
+// FULL = true with NB = NBMAX.
 template <typename R, int NB, bool FULL>
 __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBLOCKS : 1) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf, int* ovf2,
                                                int* novf2, const double4* pos, ShortList<R> S, const signed char* typ,
@@ -671,8 +672,8 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
     } else {
       st.bad = false;
     }
-    if (!FULL && (dB != R(0) || Md > 0.0)) {  // S_b transition or fractional C_ij: reverse pass /
-      list_append(ovf, novf, 1 << 30, qi);  // path forces in the full kernel (NB_FAST sides)
+    if (!FULL && dB != R(0)) {  // S_b transition: the reverse pass of b* in the full kernel
+      list_append(ovf, novf, 1 << 30, qi);  // (NB_FAST sides)
       continue;
     }
     R dP = 0;
@@ -694,10 +695,10 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
         V3<R> u = ir * d;
         addto(gd, (rho * ir) * (gs - dot3(u, gs) * u));
       }
-      if (M > R(0)) {
-        PathRes<R> pr = path_search(S, i, J);
-        path_forces(S, owner, pr, -Q * V, F, e + 1);
-      }
+    }
+    if (M > R(0)) {  // fractional C_ij: dC along the maximising path
+      PathRes<R> pr = path_search(S, i, J);
+      path_forces(S, owner, pr, -Q * V, F, e + 1);
     }
     atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
     atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
