@@ -35,11 +35,22 @@ constexpr int NEAR_GROUP = AB_NEAR_GROUP;        // lanes per atom (measured: 8 
 constexpr int NEAR_ATOMS = 128 / NEAR_GROUP;     // atoms per 128-thread block
 constexpr int NEAR_SLOTS = AB_NEAR_SLOTS;        // reach table slots per atom (measured: 64 beats 128)
 
+#ifndef AB_NEAR_BLOOM
+#define AB_NEAR_BLOOM 16 // 32-bit words of the per-atom Bloom filter in front of the table (0: none)
+#endif
 struct ReachSmem {
   int keys[NEAR_SLOTS];
   unsigned long long mbits[NEAR_SLOTS];
   int nins, ovf;
+#if AB_NEAR_BLOOM
+  unsigned bloom[AB_NEAR_BLOOM];  // one bit per inserted key: a clear bit proves M = 0
+#endif
 };
+#if AB_NEAR_BLOOM
+__device__ __forceinline__ unsigned bloom_bit(int key) {  // bits independent of the table slot
+  return (((unsigned)key * 0x9E3779B1u) >> 7) & (32u * AB_NEAR_BLOOM - 1u);
+}
+#endif
 
 __host__ __device__ constexpr int log2i(int v) { return v <= 1 ? 0 : 1 + log2i(v / 2); }
 __device__ __forceinline__ unsigned reach_hash(int key) {
@@ -51,7 +62,13 @@ __device__ __forceinline__ void reach_insert(ReachSmem& s, int key, double M) {
   for (int probe = 0; probe < NEAR_SLOTS; ++probe) {
     int old = atomicCAS(&s.keys[h], REACH_EMPTY, key);
     if (old == REACH_EMPTY || old == key) {
-      if (old == REACH_EMPTY) atomicAdd(&s.nins, 1);
+      if (old == REACH_EMPTY) {
+        atomicAdd(&s.nins, 1);
+#if AB_NEAR_BLOOM
+        const unsigned b = bloom_bit(key);
+        atomicOr(&s.bloom[b >> 5], 1u << (b & 31u));
+#endif
+      }
       atomicMax(&s.mbits[h], (unsigned long long)__double_as_longlong(M));
       return;
     }
@@ -105,6 +122,10 @@ __device__ __forceinline__ double group_sum(double v) {
 // pair loop is branch-light (the rare b* / fractional-C / stage work sits at the end of the
 // body) so the group stays converged through the LJ arithmetic.
 __device__ __forceinline__ double reach_lookup_fast(const ReachSmem& s, int key) {
+#if AB_NEAR_BLOOM
+  const unsigned b = bloom_bit(key);
+  if (!((s.bloom[b >> 5] >> (b & 31u)) & 1u)) return 0.0;  // not in the reach set: M = 0
+#endif
   unsigned h = reach_hash(key);
 #pragma unroll
   for (int probe = 0; probe < 4; ++probe) {
@@ -149,6 +170,9 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
     s.mbits[q] = 0ull;
   }
   if (gl == 0) s.nins = 0, s.ovf = 0;
+#if AB_NEAR_BLOOM
+  for (int q = gl; q < AB_NEAR_BLOOM; q += NEAR_GROUP) s.bloom[q] = 0u;
+#endif
   __syncwarp();
   const size_t bi = (size_t)(active ? i : 0) * S.capS;
 #ifdef AB_ABL_NOREACH
