@@ -178,9 +178,18 @@ def run_ours(args, ws, rank, local):
     def max_over_ranks(x):
         return reduce_max(x, ws, dev)
 
+    params = open(E.PARAMS, "rb").read()
+    if args.potential != "airebo":  # the paper's REBO / AIREBO-M variants
+        params = params.replace(b"potential airebo\n", b"potential " + args.potential.encode() + b"\n")
+
     def make_engine(precision):
         ranks = ("nccl", rank, ws, uid) if ws > 1 else None
-        return E.make(s, precision, device=local, ranks=ranks)
+        e = E.Engine(precision, local, params=params, ranks=ranks)
+        e.set_box(s.box)
+        e.set_atoms(s.types, s.x)
+        if s.v is not None:
+            e.set_velocities(s.v)
+        return e
 
     def timed_steps(eng, K):
         """K NVE steps, each bracketed by CUDA events on the engine's stream, L2 flushed before
@@ -330,7 +339,7 @@ def run_ours(args, ws, rank, local):
             "config": {"workload": s.name + (" (BASELINE configs[1]: PE 12x16x14 cells, 32,256 atoms, 300 K, "
                                              "dt 0.5 fs, NVE, LJ cutoff 3 sigma, torsion on)" if ws == 1 else
                                              f" (cfg2 block per GPU along x, {ws} slabs)"),
-                       "atoms": n_atoms, "dt_fs": s.dt, "precision": args.precision,
+                       "atoms": n_atoms, "dt_fs": s.dt, "precision": args.precision, "potential": args.potential,
                        "parallelism": "single GPU" if ws == 1 else f"slab{ws} (x slabs, NCCL halo send/recv)",
                        "l2": "flushed between timed steps (256 MiB write)",
                        "timed_step": "ab_run_nve(1): integrate, rebuild check, forces, integrate"},
@@ -401,6 +410,7 @@ def main():
     ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
     ap.add_argument("--config", default=2, type=lambda v: int(v) if v.isdigit() else v)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--potential", default="airebo", choices=["airebo", "rebo", "airebo-m"])
     ap.add_argument("--no-mixed", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

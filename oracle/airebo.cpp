@@ -20,6 +20,9 @@
 //   LJ (i<j): E = (S_r S_b(b*) + 1 - S_r) C_ij V_LJ(r)                  P:467, Alg.3
 //   C_ij = 1 - max{w_ij, w_ik w_kj, w_ik w_kl w_lj}  (nested search)
 //   b*: bond order with d_ij -> rho d_ij/|d_ij|                         P:488-494, reading A8
+// Variants (param key `potential`): REBO = the REBO bond terms only (no
+// torsion, no LJ); AIREBO-M = V_LJ replaced by eps_m [e^{-2a(r-re)} - 2 e^{-a(r-re)}]
+// with every gate, switch and the taper kept (reading A31).
 // Functional forms and spline rules: SURVEY A2, A5-A11.
 #include <algorithm>
 #include <array>
@@ -389,7 +392,7 @@ inline void build_lists(const Params& P, const Sys& S, bool brute, bool want_lj,
     });
     std::sort(Lo.shortl[i].begin(), Lo.shortl[i].end(), nb_less);
   }
-  if (!want_lj) return;
+  if (!want_lj || P.potential == POT_REBO) return;  // REBO: no inter-molecular term
   Finder fl(S, rcmax, brute);
 #pragma omp parallel for schedule(dynamic, 64)
   for (int i = 0; i < S.n; ++i) {
@@ -629,9 +632,10 @@ void eval_bond(const Params& P, const Sys& S, const Lists& Lo, int i, const Nb& 
   BondInfo bi;
   T b = bond_order(P, ti, tj, d, I, J, &bi);
   T Erebo = VR + b * VA;
-  // torsion (reading A9: guard G on both angles; A12: eps keyed K I J L)
+  // torsion (reading A9: guard G on both angles; A12: eps keyed K I J L); none in REBO
   T Etors(0.0);
-  for (size_t k = 0; k < I.tk.size(); ++k) {
+  const size_t nk_tors = P.potential == POT_REBO ? 0 : I.tk.size();
+  for (size_t k = 0; k < nk_tors; ++k) {
     T ck = clamp1(dot(d, I.dk[k]) / (r * I.rk[k]));
     T Gk = Gguard(P, ck);
     if (val(Gk) == 0.0) continue;
@@ -765,11 +769,18 @@ void eval_lj(const Params& P, const Sys& S, const Lists& Lo, int i, const Nb& e,
         Sw(norm(cx.pos[qj] - cx.pos[ql]), p3.rmin, p3.rmax);
   }
   T C = 1.0 - M;
-  // V_LJ(r) = 4 eps [(s/r)^12 - (s/r)^6] S(r; rlo, rc)   (reading A10)
-  T sr = pp.sigma / r;
-  T sr2 = sr * sr;
-  T sr6 = (sr2 * sr2) * sr2;
-  T V = (4.0 * pp.eps * (sr6 * sr6 - sr6)) * Sw(r, pp.rlo, pp.rc);
+  // V_LJ(r) = 4 eps [(s/r)^12 - (s/r)^6] S(r; rlo, rc)   (reading A10); AIREBO-M:
+  // the Morse form eps_m [e^{-2a(r-re)} - 2 e^{-a(r-re)}] under the same taper
+  T V;
+  if (P.potential == POT_AIREBO_M) {
+    T x = exp(-pp.m_a * (r - pp.m_re));
+    V = (pp.m_eps * (x * x - 2.0 * x)) * Sw(r, pp.rlo, pp.rc);
+  } else {
+    T sr = pp.sigma / r;
+    T sr2 = sr * sr;
+    T sr6 = (sr2 * sr2) * sr2;
+    V = (4.0 * pp.eps * (sr6 * sr6 - sr6)) * Sw(r, pp.rlo, pp.rc);
+  }
   T Q(1.0);
   if (needP) {
     acc.cnt[CNT_BSTAR] += 1;
@@ -847,7 +858,8 @@ inline void compute(const Params& P, const Sys& S, const Lists& Lo, const Opts& 
     if (o.owners && !(*o.owners)[i]) continue;
     acc.cnt[CNT_SHORT] += (long long)Lo.shortl[i].size();
     acc.cnt[CNT_MAXSHORT] = std::max(acc.cnt[CNT_MAXSHORT], (long long)Lo.shortl[i].size());
-    acc.cnt[CNT_MAXREACH] = std::max(acc.cnt[CNT_MAXREACH], reach_size(Lo, i));
+    if (P.potential != POT_REBO)  // the C_ij reach map belongs to the LJ term; REBO has none
+      acc.cnt[CNT_MAXREACH] = std::max(acc.cnt[CNT_MAXREACH], reach_size(Lo, i));
     if (o.rebo)
       for (const Nb& e : Lo.shortl[i]) {
         if (!canonical(i, e.j, e.s)) continue;

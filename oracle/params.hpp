@@ -23,9 +23,15 @@ struct PairParams {
   double rmin, rmax, Q, alpha, A, B[3], beta[3];
   // LJ
   double eps, sigma, rc, rlo, bmin, bmax, rho;
+  // Morse radial form of AIREBO-M: eps_m [e^{-2a(r-re)} - 2 e^{-a(r-re)}]
+  double m_eps = 0, m_a = 0, m_re = 0;
 };
 
+// the method applies to AIREBO, to REBO (no inter-molecular forces) and to AIREBO-M
+enum Potential { POT_AIREBO = 0, POT_REBO = 1, POT_AIREBO_M = 2 };
+
 struct Params {
+  Potential potential = POT_AIREBO;
   double mass[2], kB, mvv2e, ftm2v, skin;
   PairParams pair[2][2];  // symmetric [t_i][t_j]
   Spline1 g[2];           // g_C, g_H (centre species)
@@ -101,6 +107,14 @@ inline std::string parse_params(const std::string& text, Params& p) {
   p.mvv2e = one("const.mvv2e");
   p.ftm2v = one("const.ftm2v");
   p.skin = one("neigh.skin");
+  if (kv.count("potential")) {
+    const auto& v = kv["potential"];
+    std::string name = v.size() == 1 ? v[0] : std::string("?");
+    if (name == "airebo") p.potential = POT_AIREBO;
+    else if (name == "rebo") p.potential = POT_REBO;
+    else if (name == "airebo-m") p.potential = POT_AIREBO_M;
+    else if (err.empty()) err = "key potential: expected airebo, rebo or airebo-m";
+  }
   for (int q = 0; q < 3; ++q) {
     PairParams pp;
     std::string b = std::string("pair.") + PK[q] + ".";
@@ -119,6 +133,12 @@ inline std::string parse_params(const std::string& text, Params& p) {
     pp.bmin = one(l + "bmin");
     pp.bmax = one(l + "bmax");
     pp.rho = one(l + "rho");
+    if (p.potential == POT_AIREBO_M) {
+      std::string m = std::string("morse.") + PK[q] + ".";
+      pp.m_eps = one(m + "eps");
+      pp.m_a = one(m + "alpha");
+      pp.m_re = one(m + "re");
+    }
     if (err.empty()) {
       if (!(pp.rmin < pp.rmax)) err = b + "rmin >= " + b + "rmax";
       else if (!(pp.rlo < pp.rc)) err = l + "rlo >= " + l + "rc";

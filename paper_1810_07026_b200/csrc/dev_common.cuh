@@ -22,6 +22,7 @@ struct Tab {
   R rmin[3], rmax[3], Q[3], alpha[3], A[3], B[3][3], beta[3][3];
   R eps[3], sigma[3], sigma2[3], rc[3], rlo[3], bmin[3], bmax[3], rho[3], srhi[3];
   R inv_taper[3];  // 1 / (r_c - r_lo)
+  R meps[3], malpha[3], mre[3];  // AIREBO-M Morse radial form
   R explam[2][2][2];  // e^{lambda_{jik}} [t_j][t_i][t_k]
   int gn[2];
   R gx[2][16], gy[2][16], gm[2][16];
@@ -35,6 +36,7 @@ struct Geo {  // double-only quantities: exact list / gate decisions, box, integ
   double srhi2_hi[3];  // (2^(1/6) sigma)^2 (1 + 1e-9): pre-filter of the exact S_r window test
   double L[3];
   double mass[2], ftm2v, mvv2e;
+  int potential;  // 0 AIREBO, 1 REBO, 2 AIREBO-M
 };
 
 __constant__ Tab<double> c_tabd;

@@ -369,7 +369,10 @@ void fill_tab(const HostParams& hp, Tab<R>& t) {
   for (int k = 0; k < 2; ++k)
     for (int i = 0; i < 2; ++i)
       for (int j = 0; j < 2; ++j)
-        for (int l = 0; l < 2; ++l) t.tors[k][i][j][l] = (R)hp.tors[k][i][j][l];
+        for (int l = 0; l < 2; ++l)  // REBO has no torsion term
+          t.tors[k][i][j][l] = hp.potential == kREBO ? R(0) : (R)hp.tors[k][i][j][l];
+  for (int p = 0; p < 3; ++p)
+    t.meps[p] = (R)hp.pr[p].meps, t.malpha[p] = (R)hp.pr[p].malpha, t.mre[p] = (R)hp.pr[p].mre;
 }
 
 // host-side geometry of the engine (cutoffs, halo); no device work
@@ -403,6 +406,7 @@ ab_status bind_consts(ab_engine* e) {
   g.reach2 = (3 * rmm) * (3 * rmm);
   for (int c = 0; c < 3; ++c) g.L[c] = e->L[c];
   g.mass[0] = hp.mass[0], g.mass[1] = hp.mass[1], g.ftm2v = hp.ftm2v, g.mvv2e = hp.mvv2e;
+  g.potential = hp.potential;
   CK(cudaMemcpyToSymbolAsync(c_geo, &g, sizeof(Geo), 0, cudaMemcpyHostToDevice, e->st));
   CK(cudaMemcpyToSymbolAsync(c_tabd, &e->td, sizeof(e->td), 0, cudaMemcpyHostToDevice, e->st));
   CK(cudaMemcpyToSymbolAsync(c_tabf, &e->tf, sizeof(e->tf), 0, cudaMemcpyHostToDevice, e->st));
@@ -636,6 +640,7 @@ ab_status images_and_lists(ab_engine* e) {
   CK(e->in_cnt.ensure(NT));
   const double skin = e->hp.skin;
   const double rnear = 3 * e->rmaxmax + skin;
+  if (e->capL[0] == 0 && e->hp.potential == kREBO) e->capL[0] = e->capL[1] = e->capL[2] = 1;
   if (e->capL[0] == 0) {  // first build: capacities from the mean density (grown on overflow)
     double vol = e->L[0] * e->L[1] * e->L[2];
     if (slabbed(e)) vol = (e->xhi - e->xlo) * e->L[1] * e->L[2];
@@ -673,9 +678,14 @@ ab_status images_and_lists(ab_engine* e) {
     if (dbg)
       for (auto& x : dbg_ev) cudaEventCreate(&x), cudaEventRecord(x, st);
     double t_pre = tms(tq);
-    k_build_lj<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
-                                                              e->nrLJ, Lg, e->small_i.p + 2);
-    CKL();
+    if (e->hp.potential != kREBO) {  // REBO has no inter-molecular term: no LJ lists
+      k_build_lj<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
+                                                                e->nrLJ, Lg, e->small_i.p + 2);
+      CKL();
+    } else {
+      for (int c = 0; c < 3; ++c)
+        if (N) CK(cudaMemsetAsync(e->ljc[c].p, 0, sizeof(int) * N, st));
+    }
     k_build_inter<<<nblk((long long)NT * 32, 128), 128, 0, st>>>(NT, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
                                                                   e->nrI, e->capI, e->in_cnt.p, e->in_nbr.p,
                                                                   e->small_i.p + 5);
@@ -945,9 +955,13 @@ ab_status enqueue_forces(ab_engine* e) {
   // need the short list.  Partial rows of the reduction are disjoint per kernel; F takes fp64
   // atomics from all of them.
   const bool serial = e->serial;
+  const bool lj = e->hp.potential != kREBO, morse = e->hp.potential == kAIREBOM;
+  const int nrows_used = lj ? nrows : g_short + g_rebo + g_slow;  // REBO: short + bond kernels only
   const cudaStream_t s_rebo = serial ? st : e->aux[0], s_far = serial ? st : e->aux[1];
-  CK(cudaEventRecord(e->ev_fork[1], st));
-  CK(cudaStreamWaitEvent(s_far, e->ev_fork[1], 0));
+  if (lj) {
+    CK(cudaEventRecord(e->ev_fork[1], st));
+    CK(cudaStreamWaitEvent(s_far, e->ev_fork[1], 0));
+  }
   const int row_far = g_short + g_rebo + g_slow + g_near;
   BstarQueue Qu;
   Qu.item = e->q_item.p, Qu.M = e->q_M.p, Qu.count = e->small_i.p + 13;
@@ -957,18 +971,17 @@ ab_status enqueue_forces(ab_engine* e) {
   A.N = N;
   A.pos = e->pos.p;
   for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
-  {
+  if (lj) {
     cudaEvent_t t = prof_start(e, s_far);
     RedRows R6 = RR;
     R6.row0 = row_far;
-    if (e->want_virial)
-      k_lj_far<R, true><<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, R6);
-    else
-      k_lj_far<R, false><<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, R6);
+    auto far = [&](auto kern) { kern<<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, R6); };
+    if (e->want_virial) morse ? far(k_lj_far<R, true, true>) : far(k_lj_far<R, true, false>);
+    else morse ? far(k_lj_far<R, false, true>) : far(k_lj_far<R, false, false>);
     CKL();
     prof_stop(e, 6, s_far, t);
+    CK(cudaEventRecord(e->ev_join[1], s_far));
   }
-  CK(cudaEventRecord(e->ev_join[1], s_far));
   {
     cudaEvent_t t = prof_start(e, st);
     k_short<R><<<g_short, 128, 0, st>>>(N, NT, e->pos.p, e->in_cnt.p, e->in_nbr.p, e->capI, S, e->gid.p,
@@ -994,19 +1007,19 @@ ab_status enqueue_forces(ab_engine* e) {
   }
   CK(cudaEventRecord(e->ev_join[0], s_rebo));
   RR.row0 = g_short + g_rebo + g_slow;
-  {
+  if (lj) {
     cudaEvent_t t = prof_start(e, st);
-    if (e->want_virial)
-      k_lj_near<R, true><<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p,
-                                                                     e->F.p, e->acc.p, e->ct.p, Qu, sb1, RR);
-    else
-      k_lj_near<R, false><<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p,
-                                                                      e->F.p, e->acc.p, e->ct.p, Qu, sb1, RR);
+    auto near = [&](auto kern) {
+      kern<<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p, e->acc.p,
+                                                       e->ct.p, Qu, sb1, RR);
+    };
+    if (e->want_virial) morse ? near(k_lj_near<R, true, true>) : near(k_lj_near<R, true, false>);
+    else morse ? near(k_lj_near<R, false, true>) : near(k_lj_near<R, false, false>);
     CKL();
     prof_stop(e, 2, st, t);
   }
   RR.row0 = row_far + g_far;
-  {
+  if (lj) {
     cudaEvent_t t = prof_start(e, st);
     // forward-only fast path; pairs needing the reverse pass / path forces -> ovf_q (NB_FAST
     // sides, count small_i[9]), pairs with a large side -> ovf_q2 (NBMAX, count small_i[1])
@@ -1027,9 +1040,9 @@ ab_status enqueue_forces(ab_engine* e) {
     prof_stop(e, 3, st, t);
   }
   CK(cudaStreamWaitEvent(st, e->ev_join[0], 0));
-  CK(cudaStreamWaitEvent(st, e->ev_join[1], 0));
+  if (lj) CK(cudaStreamWaitEvent(st, e->ev_join[1], 0));
   RR.row0 = 0;
-  k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows, e->acc.p, e->ct.p);
+  k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows_used, e->acc.p, e->ct.p);
   CKL();
   return AB_OK;
 }

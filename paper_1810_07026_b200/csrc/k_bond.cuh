@@ -596,11 +596,19 @@ __device__ void path_forces(const ShortList<R>& S, const int* owner, const PathR
 template <typename R>
 __device__ __forceinline__ R lj_v(int p, R r2, double r2d, R& dVr_over_r) {
   const Tab<R>& T = tab<R>();
-  R sr2 = T.sigma2[p] / r2;
-  R sr6 = sr2 * sr2 * sr2;
-  R e4 = R(4) * T.eps[p];
-  R V = e4 * (sr6 * sr6 - sr6);
-  R dv = -e4 * (R(12) * sr6 * sr6 - R(6) * sr6) / r2;  // (dV0/dr)/r
+  R V, dv;
+  if (c_geo.potential == 2) {  // AIREBO-M: Morse radial form
+    R r = sqr_t(r2);
+    R x = ex(-T.malpha[p] * (r - T.mre[p]));
+    V = T.meps[p] * (x * x - R(2) * x);
+    dv = R(2) * T.malpha[p] * T.meps[p] * x * (R(1) - x) / r;
+  } else {
+    R sr2 = T.sigma2[p] / r2;
+    R sr6 = sr2 * sr2 * sr2;
+    R e4 = R(4) * T.eps[p];
+    V = e4 * (sr6 * sr6 - sr6);
+    dv = -e4 * (R(12) * sr6 * sr6 - R(6) * sr6) / r2;  // (dV0/dr)/r
+  }
   if (r2d > c_tabd.rlo[p] * c_tabd.rlo[p]) {
     R r = sqr_t(r2);
     R ds;

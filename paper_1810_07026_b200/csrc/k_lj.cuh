@@ -97,6 +97,15 @@ __device__ __forceinline__ R lj_plain(R e4, R sig2, R inv_r2, R& dVr) {
   return e4 * (sr6 * sr6 - sr6);
 }
 
+// AIREBO-M radial form: V_M = eps_m [x^2 - 2 x], x = e^{-a (r - r_e)};
+// returns V_M and (dV_M/dr)/r = 2 a eps_m x (1 - x) / r
+template <typename R>
+__device__ __forceinline__ R morse_plain(R em, R a, R re, R r, R ir, R& dVr) {
+  R x = ex(-a * (r - re));
+  dVr = R(2) * a * em * x * (R(1) - x) * ir;
+  return em * (x * x - R(2) * x);
+}
+
 struct LJArgs {
   int N;
   const double4* pos;
@@ -137,7 +146,7 @@ __device__ __forceinline__ double reach_lookup_fast(const ReachSmem& s, int key)
   return reach_lookup(s, key);  // long probe chain: rare
 }
 
-template <typename R, bool VIRIAL>
+template <typename R, bool VIRIAL, bool MORSE>
 #ifndef AB_NEAR_MINBLOCKS
 #define AB_NEAR_MINBLOCKS 7  // measured: 7 blocks (73 regs) beat 6 (80 regs) and 8 (64 regs, spills)
 #endif
@@ -150,13 +159,16 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   // per-pair parameters indexed by the species pair p, which differs between the lanes of a
   // warp: shared-memory copies (an indexed __constant__ load serialises per distinct address)
   __shared__ double pd[9];  // r_c^2, S_r window pre-filter, r_lo^2
-  __shared__ R pr_[12];     // 4 eps, sigma^2, r_lo, r_c
+  __shared__ R pr_[12];     // 4 eps, sigma^2, r_lo, r_c  (Morse: eps_m, a, r_e, -)
   const Tab<R>& T = tab<R>();
   if (threadIdx.x < 3) {
     const int t = threadIdx.x;
     pd[t] = c_geo.rc2[t], pd[3 + t] = c_geo.srhi2_hi[t], pd[6 + t] = c_geo.rlo2[t];
-    pr_[t] = R(4) * T.eps[t], pr_[3 + t] = T.sigma2[t], pr_[6 + t] = T.rlo[t], pr_[9 + t] = T.rc[t];
+    pr_[t] = MORSE ? T.meps[t] : R(4) * T.eps[t], pr_[3 + t] = MORSE ? T.malpha[t] : T.sigma2[t];
+    pr_[6 + t] = T.rlo[t], pr_[9 + t] = T.rc[t];
   }
+  __shared__ R pm_[3];  // Morse r_e
+  if (MORSE && threadIdx.x < 3) pm_[threadIdx.x] = T.mre[threadIdx.x];
   red_init(rs);
   const int grp = threadIdx.x / NEAR_GROUP, gl = threadIdx.x % NEAR_GROUP;
   ReachSmem& s = sm_all[grp];
@@ -305,7 +317,8 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       R rr2 = norm ? (R)r2 : R(1);
       R y = rsqrt_fast(rr2);
       R dVr;
-      R V = lj_plain<R>(pr_[p], pr_[3 + p], y * y, dVr);
+      R V = MORSE ? morse_plain<R>(pr_[p], pr_[3 + p], pm_[p], rr2 * y, y, dVr)
+                  : lj_plain<R>(pr_[p], pr_[3 + p], y * y, dVr);
       if (norm && r2 > pd[6 + p]) {  // taper S(r; r_lo, r_c) (reading A10): rare in the near list
         R r = rr2 * y, dsw;
         R sv = sw<R>(r, pr_[6 + p], pr_[9 + p], dsw);
@@ -369,7 +382,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 // ---------------------------------------------------------------------------------- far pairs
 constexpr int FAR_UNROLL = 4;
 
-template <typename R, bool VIRIAL, bool BAND>
+template <typename R, bool VIRIAL, bool BAND, bool MORSE>
 __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, double4 pi, int ti, long long ki,
                                          const int* gid, const char4* shift, StageBuf stage, double& fx, double& fy,
                                          double& fz, double& en, double (&W)[6], unsigned& nlj) {
@@ -379,8 +392,9 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
   const int* row = A.nbr[list] + (size_t)i * A.cap[list];
   // t_i is warp-uniform, so a pair is one of two species pairs: hold both parameter sets in
   // registers and select (no divergent constant-cache loads in the loop)
-  const R e4a = R(4) * T.eps[ti], e4b = R(4) * T.eps[ti + 1];
-  const R s2a = T.sigma2[ti], s2b = T.sigma2[ti + 1];
+  const R e4a = MORSE ? T.meps[ti] : R(4) * T.eps[ti], e4b = MORSE ? T.meps[ti + 1] : R(4) * T.eps[ti + 1];
+  const R s2a = MORSE ? T.malpha[ti] : T.sigma2[ti], s2b = MORSE ? T.malpha[ti + 1] : T.sigma2[ti + 1];
+  const R rea = MORSE ? T.mre[ti] : R(0), reb = MORSE ? T.mre[ti + 1] : R(0);
   const R rloa = T.rlo[ti], rlob = T.rlo[ti + 1];
   const R iva = T.inv_taper[ti], ivb = T.inv_taper[ti + 1];
   const double rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
@@ -406,9 +420,10 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
       bool in = valid && (!BAND || r2 <= (hj ? rcb : rca));
       nlj += (in && ki < key_of(pj[u]));
       R rr2 = in ? (R)r2 : R(1);
-      R y = BAND ? rsqrt_fast(rr2) : R(0);  // 1/r (taper only)
+      R y = (BAND || MORSE) ? rsqrt_fast(rr2) : R(0);  // 1/r (taper / Morse only)
       R dVr;
-      R V = lj_plain<R>(hj ? e4b : e4a, hj ? s2b : s2a, BAND ? y * y : rcp_fast(rr2), dVr);
+      R V = MORSE ? morse_plain<R>(hj ? e4b : e4a, hj ? s2b : s2a, hj ? reb : rea, rr2 * y, y, dVr)
+                  : lj_plain<R>(hj ? e4b : e4a, hj ? s2b : s2a, BAND ? y * y : rcp_fast(rr2), dVr);
       if (BAND) {  // taper S(r; r_lo, r_c) (reading A10), branch-free
         R r = rr2 * y;
         R iv = hj ? ivb : iva;
@@ -437,7 +452,7 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
   }
 }
 
-template <typename R, bool VIRIAL>
+template <typename R, bool VIRIAL, bool MORSE>
 #ifndef AB_FAR_MINBLOCKS
 #define AB_FAR_MINBLOCKS 4
 #endif
@@ -457,8 +472,8 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     const int ti = type_of(pi);
     const long long ki = key_of(pi);
     double fx = 0, fy = 0, fz = 0;
-    far_list<R, VIRIAL, false>(A, 1, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
-    far_list<R, VIRIAL, true>(A, 2, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
+    far_list<R, VIRIAL, false, MORSE>(A, 1, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
+    far_list<R, VIRIAL, true, MORSE>(A, 2, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
     fx = warp_sum(fx);
     fy = warp_sum(fy);
     fz = warp_sum(fz);

@@ -121,6 +121,15 @@ std::string parse_host_params(const char* text, size_t len, HostParams& hp) {
   hp.mvv2e = t.val("const.mvv2e");
   hp.ftm2v = t.val("const.ftm2v");
   hp.skin = t.val("neigh.skin");
+  hp.potential = kAIREBO;  // `potential` is optional (default AIREBO)
+  auto pot = t.recs.find("potential");
+  if (t.error.empty() && pot != t.recs.end()) {
+    const auto& w = pot->second.words;
+    if (w.size() == 1 && w[0] == "airebo") hp.potential = kAIREBO;
+    else if (w.size() == 1 && w[0] == "rebo") hp.potential = kREBO;
+    else if (w.size() == 1 && w[0] == "airebo-m") hp.potential = kAIREBOM;
+    else t.error = "param line " + std::to_string(pot->second.line) + ": potential must be airebo, rebo or airebo-m";
+  }
   for (int p = 0; p < 3; ++p) {
     PairSet& s = hp.pr[p];
     const std::string a = std::string("pair.") + PN[p] + ".", l = std::string("lj.") + PN[p] + ".";
@@ -141,6 +150,14 @@ std::string parse_host_params(const char* text, size_t len, HostParams& hp) {
     s.bmin = t.val(l + "bmin");
     s.bmax = t.val(l + "bmax");
     s.rho = t.val(l + "rho");
+    if (hp.potential == kAIREBOM) {  // the Morse block is read (and required) for AIREBO-M only
+      const std::string m = std::string("morse.") + PN[p] + ".";
+      s.meps = t.val(m + "eps");
+      s.malpha = t.val(m + "alpha");
+      s.mre = t.val(m + "re");
+      if (t.error.empty() && !(s.malpha > 0.0 && s.mre > 0.0 && s.meps >= 0.0))
+        t.error = m + "alpha and " + m + "re must be > 0, " + m + "eps >= 0";
+    }
     if (t.error.empty()) {
       if (!(s.rmin > 0.0)) t.error = a + "rmin must be > 0";
       else if (!(s.rmin < s.rmax)) t.error = a + "rmin >= " + a + "rmax (invariant r_min < r_max)";

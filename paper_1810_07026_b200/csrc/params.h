@@ -12,9 +12,15 @@ inline int pair_index(int ta, int tb) { return ta + tb; }  // CC 0, CH 1, HH 2
 struct PairSet {
   double rmin, rmax, Q, alpha, A, B[3], beta[3];      // REBO f_R / f_A
   double eps, sigma, rc, rlo, bmin, bmax, rho;        // LJ, S_r, S_b, fictitious distance
+  double meps = 0, malpha = 0, mre = 0;               // Morse radial form of AIREBO-M
 };
 
+// potential variants of the paper's section 2.1: AIREBO, REBO (no inter-molecular
+// LJ term, no torsion), AIREBO-M (LJ radial form replaced by Morse, every gate kept)
+enum { kAIREBO = 0, kREBO = 1, kAIREBOM = 2 };
+
 struct HostParams {
+  int potential = kAIREBO;
   double mass[2] = {0, 0}, kB = 0, mvv2e = 0, ftm2v = 0, skin = 0;
   PairSet pr[3];
   std::vector<double> gknot[2], gval[2];  // g_C, g_H knots (cos theta) and values
