@@ -262,17 +262,25 @@ def run_ours(args, ws, rank, local):
         achieved = flops[dom] / avg_s / 1e12 if avg_s > 0 else 0.0
         clk = r["clocks"]["sm_mhz"] or 1965.0
         peak = fp64_peak_tflops(clk) if precision == "fp64" else fp32_peak_tflops(clk)
-        traffic = None
+        traffic, hw = None, None
         if os.path.exists(PROFILE_SUMMARY):
             try:
                 summ = json.load(open(PROFILE_SUMMARY))
-                traffic = summ.get(precision, {}).get(KERNEL_OF[dom], {}).get("dram_bytes_per_launch")
+                ks = summ.get(precision, {}).get(KERNEL_OF[dom], {})
+                traffic = summ.get("fp64", {}).get(KERNEL_OF[dom], {}).get("dram_bytes_per_launch") \
+                    if precision == "fp64" else ks.get("dram_bytes_per_launch")
+                if ks.get("hw_flops_per_launch") and avg_s > 0:
+                    # SURVEY §8(d) fraction (i): executed FP64 (FP32) flops of the kernel, counted by ncu
+                    # (2 DFMA + DMUL + DADD thread instructions per launch), over the live duration
+                    hw_tf = ks["hw_flops_per_launch"] / avg_s / 1e12
+                    hw = {"flops_per_launch": ks["hw_flops_per_launch"], "tflops": round(hw_tf, 4),
+                          "frac": round(hw_tf / peak, 5), "source": os.path.basename(PROFILE_SUMMARY)}
             except (ValueError, OSError):
                 traffic = None
         step_flops = sum(flops.values())
         step_s = r["total_ms"] / K * 1e-3
         return {"bound": "alu", "kernel": KERNEL_OF[dom], "achieved": round(achieved, 4), "peak": round(peak, 3),
-                "unit": "TFLOP/s", "frac": round(achieved / peak, 5), "traffic": traffic,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 5), "traffic": traffic, "hw": hw,
                 "peak_basis": f"{'FP64' if precision == 'fp64' else 'FP32'} FMA units x 2 x median SM clock "
                               f"{clk:.0f} MHz under load (no FP64 entry in MEASURED_PEAKS.json)",
                 "algorithmic_flops_per_launch": flops[dom], "avg_launch_ms": round(avg_s * 1e3, 5),

@@ -1,9 +1,12 @@
 """Turn ncu outputs from gpurun_out/ into the committed summaries under profiles/.
 
 usage: python scripts/make_profile_summary.py <launch_list.csv> <full.ncu-rep> <round tag>
+                                             [<fp64 flops.csv> <mixed flops.csv>]
 Writes profiles/launches_<tag>.csv (copy), profiles/launch_shares_<tag>.txt,
 profiles/ncu_full_<tag>.txt and profiles/ncu_summary_<tag>.json (per-kernel DRAM bytes per
-launch, read by bench.py as roofline.traffic).
+launch, read by bench.py as roofline.traffic; with the optional metric-pass CSVs also the
+hardware FP64 / FP32 flop counts per launch, 2 DFMA + DMUL + DADD (FFMA ...) thread
+instructions, read by bench.py as roofline.hw -- SURVEY §8(d) fraction (i)).
 """
 import csv
 import json
@@ -71,6 +74,45 @@ for e in summ["fp64"].values():
     e["dram_bytes_per_launch"] = e["dram_bytes"] / max(e["launches"], 1)
 summ["_note"] = ("ncu --set full capture (cache flushed between replays, i.e. cold-cache DRAM traffic per "
                  "launch) of scripts/prof_step.py on cfg2, fp64")
+
+
+def flops_pass(path, prec):
+    """per kernel: hardware flops per launch from a --metrics pass CSV (long format)"""
+    rows = list(csv.reader(open(path)))
+    h = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    idx = {n: i for i, n in enumerate(rows[h])}
+    per = {}
+    for r in rows[h + 1:]:
+        if len(r) < len(rows[h]):
+            continue
+        kname = re.sub(r"<.*|\(.*", "", r[idx["Kernel Name"]]).replace("void ", "").replace("ab::", "").strip()
+        launch = (kname, r[idx["ID"]])
+        v = float(r[idx["Metric Value"]].replace(",", ""))
+        per.setdefault(launch, {})[r[idx["Metric Name"]]] = v
+    out = {}
+    for (kname, _), m in per.items():
+        if prec == "fp64":
+            fl = 2 * m.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", 0) + \
+                m.get("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0) + \
+                m.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0)
+        else:
+            fl = 2 * m.get("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum", 0) + \
+                m.get("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum", 0) + \
+                m.get("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum", 0)
+        e = out.setdefault(kname, {"launches": 0, "hw_flops": 0.0})
+        e["launches"] += 1
+        e["hw_flops"] += fl
+    for e in out.values():
+        e["hw_flops_per_launch"] = e["hw_flops"] / max(e["launches"], 1)
+    return out
+
+
+if len(sys.argv) > 5:
+    for prec, path in (("fp64", sys.argv[4]), ("mixed", sys.argv[5])):
+        for k, v in flops_pass(path, prec).items():
+            summ.setdefault(prec, {}).setdefault(k, {}).update(v)
+    summ["_note_hw"] = ("hw_flops_per_launch: ncu --metrics pass (smsp__sass_thread_inst_executed_op_{d,f}{fma,mul,add}"
+                        "_pred_on.sum; 2 per FMA) of scripts/prof_step.py on cfg2 in each precision")
 json.dump(summ, open(os.path.join(prof, f"ncu_summary_{tag}.json"), "w"), indent=1)
 print(open(os.path.join(prof, f"launch_shares_{tag}.txt")).read())
 print(json.dumps(summ, indent=1))
