@@ -429,7 +429,7 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 #define AB_REBO_MINBLOCKS 1
 #endif
 #ifndef AB_BSTAR_MINBLOCKS
-#define AB_BSTAR_MINBLOCKS 1
+#define AB_BSTAR_MINBLOCKS 3  // measured (cfg2): 3 blocks (170 regs) 56 us vs 64 us at 2 blocks
 #endif
 template <typename R, int NB>
 __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_rebo(BondList BL, const int* list_idx,
