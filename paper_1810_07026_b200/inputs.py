@@ -18,6 +18,9 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+import hashlib
+import os
+
 import numpy as np
 
 # unit constants, same values as params/toy_ch.param; used only to draw velocities
@@ -165,13 +168,25 @@ def random_insertion(n, box, dmin, seed):
     return pts
 
 
+RELAXED_CFG3 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "cfg3_relaxed.npz")
+
+
 def amorphous(n_c=21334, n_h=42668, L=82.038, dmin=1.0, seed_x=103, seed_t=303, seed_v=203, T=1500.0,
-              name="a-CH2") -> System:
+              name="a-CH2", relaxed=False) -> System:
+    """Random sequential insertion (SURVEY §8(d) cfg 3).  relaxed=True: positions from the frozen
+    file written by scripts/relax_cfg3.py (200 capped steepest-descent iterations with oracle
+    forces, SURVEY reading A22), checked against its SHA-256."""
     n = n_c + n_h
     box = np.array([L, L, L])
-    xyz = wrap(random_insertion(n, box, dmin, seed_x), box)
     types = np.full(n, H, dtype=np.int32)
     types[np.random.default_rng(seed_t).permutation(n)[:n_c]] = C
+    if relaxed:
+        f = np.load(RELAXED_CFG3)
+        xyz = np.ascontiguousarray(f["x"], dtype=np.float64)
+        if hashlib.sha256(xyz.tobytes()).hexdigest() != str(f["sha256"]) or not np.array_equal(f["types"], types):
+            raise RuntimeError(f"{RELAXED_CFG3}: checksum / species mismatch")
+    else:
+        xyz = wrap(random_insertion(n, box, dmin, seed_x), box)
     v = maxwell(types, T, seed_v) if seed_v is not None else None
     return System(name, types, xyz, box, v, dt=0.25)
 

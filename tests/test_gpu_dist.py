@@ -143,3 +143,20 @@ def test_virtual_stage_rows(eng_mod):
     assert len(key0) == len(rb)
     for row, ref in zip(rb, B_o):
         assert np.allclose(key0[tuple(int(v) for v in row)], ref, rtol=1e-12, atol=1e-13)
+
+
+def test_empty_slab_domain(eng_mod):
+    """A small cluster in a 40 A box cut into 3 slabs leaves a slab without atoms (and a neighbour
+    whose halo is empty): every kernel of the empty domain must launch cleanly and the result
+    still equal the oracle's."""
+    s = I.random_cluster(40, 8, box_len=40.0, spread=6.0, dmin=1.0, name="small-cluster")
+    owners = {eng_mod.slab_of(x, s.box[0], 3) for x in s.x[:, 0]}
+    assert len(owners) < 3
+    o = O.compute(s.types, s.x, s.box)
+    e = eng_mod.make(s, "fp64", ranks=("virtual", 3))
+    g = e.compute()
+    check_fp64(g, o, "empty-slab")
+    e.set_velocities(np.zeros_like(s.x))
+    e.run_nve(5, 0.25)
+    x = e.get_positions()
+    assert np.abs(e.compute()["F"] - O.compute(s.types, x, s.box)["F"]).max() <= 1e-9
