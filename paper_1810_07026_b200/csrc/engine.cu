@@ -1719,7 +1719,8 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
 // compiled out of the LJ kernel for these steps (ab_compute always evaluates it).
 ab_status ab_run_nve(ab_engine* e, int64_t nsteps, double dt, int64_t every, double* thermo) {
   TRY(need_atoms(e));
-  for (ab_engine* d : doms(e)) d->want_virial = false;
+  // the analysis instantiations (virial, stage rows) run only when stage recording is on
+  for (ab_engine* d : doms(e)) d->want_virial = e->record;
   ab_status s = run_nve_impl(e, nsteps, dt, every, thermo);
   for (ab_engine* d : doms(e)) d->want_virial = true;
   return s;

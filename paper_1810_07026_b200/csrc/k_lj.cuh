@@ -358,8 +358,8 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
         if (VIRIAL)
           for (int c = 0; c < 6; ++c) W[c] += Wp[c];
       }
-      if (stage.rows && canon && inr && norm) stage_lj_row(stage, gid[i], gid[J], shift[J], (double)C, 0.0);
-      if (stage.rows && canon && inr && c0) stage_lj_row(stage, gid[i], gid[J], shift[J], 0.0, 0.0);
+      if (VIRIAL && stage.rows && canon && inr && norm) stage_lj_row(stage, gid[i], gid[J], shift[J], (double)C, 0.0);
+      if (VIRIAL && stage.rows && canon && inr && c0) stage_lj_row(stage, gid[i], gid[J], shift[J], 0.0, 0.0);
     }
   }
 
@@ -447,7 +447,7 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
         V3<R> dd = mk3<R>(rx, ry, rz);
         vir_add(W, dd, (R(0.5) * dVr) * dd);
       }
-      if (stage.rows && in && ki < key_of(pj[u])) stage_lj_row(stage, gid[i], gid[J[u]], shift[J[u]], 1.0, 0.0);
+      if (VIRIAL && stage.rows && in && ki < key_of(pj[u])) stage_lj_row(stage, gid[i], gid[J[u]], shift[J[u]], 1.0, 0.0);
     }
   }
 }
