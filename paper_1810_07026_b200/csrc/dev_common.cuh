@@ -507,6 +507,7 @@ __device__ __forceinline__ void warp_acc(double (&v)[K], double* acc) {
 // virial of a vector v = x_b - x_a with energy gradient g = dE/dv:  W -= v (x) g
 template <typename R>
 __device__ __forceinline__ void vir_add(double W[6], V3<R> v, V3<R> g) {
+  if (!W) return;  // NVE instantiations pass a literal nullptr: folded away after inlining
   W[0] -= (double)v.x * (double)g.x;
   W[1] -= (double)v.y * (double)g.y;
   W[2] -= (double)v.z * (double)g.z;

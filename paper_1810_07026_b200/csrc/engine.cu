@@ -995,13 +995,16 @@ ab_status enqueue_forces(ab_engine* e) {
     cudaEvent_t t = prof_start(e, s_rebo);
     RedRows R1 = RR;
     R1.row0 = g_short;
-    k_rebo<R, NB_FAST><<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, e->ovf_bond.p,
-                                                   e->small_i.p + 8, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p,
-                                                   e->F.p, sb0, R1);
-    CKL();
-    R1.row0 += g_rebo;
-    k_rebo<R, NBMAX><<<g_slow, 128, 0, s_rebo>>>(BL, e->ovf_bond.p, nullptr, e->small_i.p + 8,
-                                                 S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb0, R1);
+    auto rebo = [&](auto fast, auto slow) {
+      fast<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, e->ovf_bond.p, e->small_i.p + 8, S, e->typ.p, e->owner.p,
+                                       e->gid.p, e->shift.p, e->F.p, sb0, R1);
+      R1.row0 += g_rebo;
+      slow<<<g_slow, 128, 0, s_rebo>>>(BL, e->ovf_bond.p, nullptr, e->small_i.p + 8, S, e->typ.p, e->owner.p,
+                                       e->gid.p, e->shift.p, e->F.p, sb0, R1);
+    };
+    if (e->want_virial) rebo(k_rebo<R, NB_FAST, true>, k_rebo<R, NBMAX, true>);
+    else rebo(k_rebo<R, NB_FAST, false>, k_rebo<R, NBMAX, false>);
+    ++e->launches;  // + the CKL below: two launches
     CKL();
     prof_stop(e, 1, s_rebo, t);
   }
@@ -1023,19 +1026,21 @@ ab_status enqueue_forces(ab_engine* e) {
     cudaEvent_t t = prof_start(e, st);
     // forward-only fast path; pairs needing the reverse pass / path forces -> ovf_q (NB_FAST
     // sides, count small_i[9]), pairs with a large side -> ovf_q2 (NBMAX, count small_i[1])
-    k_bstar<R, NB_FAST, false><<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p,
-                                                        e->small_i.p + 1, e->pos.p, S, e->typ.p, e->owner.p,
-                                                        e->gid.p, e->shift.p, e->F.p, sb1, RR);
-    CKL();
-    RR.row0 += g_bstar;
-    k_bstar<R, NB_FAST, true><<<g_bstar, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, nullptr, nullptr,
-                                                       e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                                       sb1, RR);
-    CKL();
-    RR.row0 += g_bstar;
-    k_bstar<R, NBMAX, true><<<g_slow, 128, 0, st>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr,
-                                                    e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p,
-                                                    sb1, RR);
+    auto bstar = [&](auto fast, auto full, auto big) {
+      fast<<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p, e->small_i.p + 1,
+                                    e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+      RR.row0 += g_bstar;
+      full<<<g_bstar, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, nullptr, nullptr, e->pos.p, S,
+                                    e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+      RR.row0 += g_bstar;
+      big<<<g_slow, 128, 0, st>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr, e->pos.p, S,
+                                  e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+    };
+    if (e->want_virial)
+      bstar(k_bstar<R, NB_FAST, false, true>, k_bstar<R, NB_FAST, true, true>, k_bstar<R, NBMAX, true, true>);
+    else
+      bstar(k_bstar<R, NB_FAST, false, false>, k_bstar<R, NB_FAST, true, false>, k_bstar<R, NBMAX, true, false>);
+    e->launches += 2;  // + the CKL below: three launches
     CKL();
     prof_stop(e, 3, st, t);
   }

@@ -431,7 +431,8 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 #ifndef AB_BSTAR_MINBLOCKS
 #define AB_BSTAR_MINBLOCKS 3  // measured (cfg2): 3 blocks (170 regs) 56 us vs 64 us at 2 blocks
 #endif
-template <typename R, int NB>
+// VIR = false (NVE steps): no virial accumulation and no stage rows (compiled out)
+template <typename R, int NB, bool VIR>
 __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_rebo(BondList BL, const int* list_idx,
                                               int* ovf, int* novf, ShortList<R> S, const signed char* typ,
                                               const int* owner, const int* gid, const char4* shift, double* F,
@@ -478,19 +479,19 @@ __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_
     R dVA = -dw * sb + w * sbb;
     R b = bo_value(st);
     V3<R> gd, fi, fj;
-    bo_reverse<R, true, NB>(S, typ, owner, st, VA, w, F, e + 3, gd, fi, fj);
+    bo_reverse<R, true, NB>(S, typ, owner, st, VA, w, F, VIR ? e + 3 : nullptr, gd, fi, fj);
     R dEdr = dVR + b * dVA + dw * st.Tsum;
     addto(gd, (dEdr * ir) * d);
     atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
     atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
-    vir_add(e + 3, d, gd);
+    vir_add(VIR ? e + 3 : nullptr, d, gd);
     e[0] += (double)(VR + b * VA);
     e[1] += (double)(w * st.Tsum);
     nq += st.nquads;
     nbad += st.bad;
     ncount += 1;
     nang += st.nI + st.nJ;
-    if (stage.rows) {
+    if (VIR && stage.rows) {
       double* row = stage_row(stage, 13);
       if (row) {
         char4 s = shift[J];
@@ -569,7 +570,7 @@ __device__ PathRes<R> path_search(const ShortList<R>& S, int i, int J) {
 
 // forces of E = f(M) along the maximising path: dE/dM = cM
 template <typename R>
-__device__ void path_forces(const ShortList<R>& S, const int* owner, const PathRes<R>& pr, R cM, double* F,
+__device__ __forceinline__ void path_forces(const ShortList<R>& S, const int* owner, const PathRes<R>& pr, R cM, double* F,
                             double W[6]) {
   int at[3] = {pr.a0, pr.a1, pr.a2}, sl[3] = {pr.q0, pr.q1, pr.q2};
   R w[3], dw[3];
@@ -636,7 +637,7 @@ struct BstarQueue {
 // S_b is in its transition (dS_b != 0: the reverse pass of b* is needed) is deferred to ovf for
 // FULL = true with NB_FAST register sides, a pair with a side larger than NB_FAST to ovf2 for
 // FULL = true with NB = NBMAX.
-template <typename R, int NB, bool FULL>
+template <typename R, int NB, bool FULL, bool VIR>
 __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBLOCKS : 1) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf, int* ovf2,
                                                int* novf2, const double4* pos, ShortList<R> S, const signed char* typ,
                                                const int* owner, const int* gid, const char4* shift, double* F,
@@ -698,7 +699,7 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
     if (FULL) {
       if (dB != R(0)) {
         V3<R> gs;
-        bo_reverse<R, false, NB>(S, typ, owner, st, C * V * P * dB, R(0), F, e + 1, gs, fi, fj);
+        bo_reverse<R, false, NB>(S, typ, owner, st, C * V * P * dB, R(0), F, VIR ? e + 1 : nullptr, gs, fi, fj);
         // chain through d* = rho d / |d|: dE/dd = (rho/r) (I - u u^T) dE/dd*
         V3<R> u = ir * d;
         addto(gd, (rho * ir) * (gs - dot3(u, gs) * u));
@@ -706,15 +707,15 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
     }
     if (M > R(0)) {  // fractional C_ij: dC along the maximising path
       PathRes<R> pr = path_search(S, i, J);
-      path_forces(S, owner, pr, -Q * V, F, e + 1);
+      path_forces(S, owner, pr, -Q * V, F, VIR ? e + 1 : nullptr);
     }
     atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
     atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
-    vir_add(e + 1, d, gd);
+    vir_add(VIR ? e + 1 : nullptr, d, gd);
     e[0] += (double)E;
     nb += win;
     nbad += win && st.bad;
-    if (stage.rows) {
+    if (VIR && stage.rows) {
       double* row = stage_row(stage, 7);
       if (row) {
         char4 s = shift[J];
