@@ -160,6 +160,7 @@ struct ab_engine {
   bool want_virial = true;
   DBuf<int> s_cnt, s_nbr;
   DBuf<unsigned char> s_dr, s_w, s_N;  // typed by precision at use
+  DBuf<double> s_wd;                   // fp64 switch weights of the short list (C_ij gate)
   DBuf<int2> bonds;
   DBuf<int4> q_item;
   DBuf<int> ovf_bond, ovf_q, ovf_q2;  // overflow (large side / full b*) index lists
@@ -422,6 +423,7 @@ ShortList<R> short_view(ab_engine* e) {
   S.nbr = e->s_nbr.p;
   S.dr = reinterpret_cast<decltype(S.dr)>(e->s_dr.p);
   S.w = reinterpret_cast<decltype(S.w)>(e->s_w.p);
+  S.wd = e->s_wd.p;
   R* base = reinterpret_cast<R*>(e->s_N.p);
   S.Ntot = base;
   S.NC = base + e->NT;
@@ -438,6 +440,7 @@ ab_status ensure_short(ab_engine* e) {
   CK(e->s_nbr.ensure(ent));
   CK(e->s_dr.ensure(ent * 4 * rs));
   CK(e->s_w.ensure(ent * 2 * rs));
+  CK(e->s_wd.ensure(ent));
   CK(e->s_N.ensure((size_t)e->NT * 3 * rs));
   CK(e->bonds.ensure(3 * ((size_t)e->N * e->capS + 1)));
   return AB_OK;
@@ -1310,7 +1313,7 @@ void free_engine(ab_engine* e) {
   for (auto* b : b4) b->release();
   e->acc.p = nullptr, e->ct.p = nullptr, e->small_i.p = nullptr;  // views into scratch
   e->scratch.release();
-  DBuf<double>* bd[] = {&e->vel, &e->vel_tmp, &e->F, &e->io, &e->q_M, &e->stage0, &e->stage1, &e->gio};
+  DBuf<double>* bd[] = {&e->vel, &e->vel_tmp, &e->F, &e->io, &e->q_M, &e->stage0, &e->stage1, &e->gio, &e->s_wd};
   for (auto* b : bd) b->release();
   DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->key2, &e->val, &e->val2, &e->cell_start,
                      &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],

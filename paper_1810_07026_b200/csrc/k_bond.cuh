@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_
 // used when 0 < C_ij < 1 (forces along the path) or when the per-atom reach table overflowed.
 template <typename R>
 struct PathRes {
-  R M;
+  double M;  // from the fp64 weights S.wd (gate, reading A14)
   int hops;
   int a0, q0, a1, q1, a2, q2;  // (atom, slot) of each path edge in the short list
 };
@@ -530,37 +530,37 @@ __device__ PathRes<R> path_search(const ShortList<R>& S, int i, int J) {
   int ni = S.cnt[i];
   for (int a = 0; a < ni; ++a)
     if (S.nbr[bi + a] == J) {
-      R c = S.w[bi + a].x;
+      double c = S.wd[bi + a];
       if (c > pr.M) pr.M = c, pr.hops = 1, pr.a0 = i, pr.q0 = a;
     }
   for (int a = 0; a < ni; ++a) {
     int k = S.nbr[bi + a];
     if (k == J) continue;
-    R w1 = S.w[bi + a].x;
+    double w1 = S.wd[bi + a];
     size_t bk = (size_t)k * S.capS;
     int nk = S.cnt[k];
     for (int b = 0; b < nk; ++b) {
       int l = S.nbr[bk + b];
       if (l != J) continue;
-      R c = w1 * S.w[bk + b].x;
+      double c = w1 * S.wd[bk + b];
       if (c > pr.M) pr.M = c, pr.hops = 2, pr.a0 = i, pr.q0 = a, pr.a1 = k, pr.q1 = b;
     }
   }
   for (int a = 0; a < ni; ++a) {
     int k = S.nbr[bi + a];
     if (k == J) continue;
-    R w1 = S.w[bi + a].x;
+    double w1 = S.wd[bi + a];
     size_t bk = (size_t)k * S.capS;
     int nk = S.cnt[k];
     for (int b = 0; b < nk; ++b) {
       int l = S.nbr[bk + b];
       if (l == i || l == J) continue;
-      R w2 = S.w[bk + b].x;
+      double w2 = S.wd[bk + b];
       size_t bl = (size_t)l * S.capS;
       int nl = S.cnt[l];
       for (int c2 = 0; c2 < nl; ++c2) {
         if (S.nbr[bl + c2] != J) continue;
-        R c = (w1 * w2) * S.w[bl + c2].x;
+        double c = (w1 * w2) * S.wd[bl + c2];
         if (c > pr.M) pr.M = c, pr.hops = 3, pr.a0 = i, pr.q0 = a, pr.a1 = k, pr.q1 = b, pr.a2 = l, pr.q2 = c2;
       }
     }
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
     R P = win ? sw<R>(r, T.sigma[p], T.srhi[p], dP) : R(0);
     R dVr;
     R V = lj_v<R>(p, (R)r2d, r2d, dVr);
-    R M = (R)Md, C = R(1) - M;
+    R C = (R)(1.0 - Md);  // 1 - M in fp64: M may sit within an fp32 ulp of 1 (gate, reading A14)
     R tb = (bs - T.bmin[p]) / (T.bmax[p] - T.bmin[p]);
     if (win && tb > R(0) && tb < R(1)) ++ntr;
     R Q = P * B + R(1) - P;
@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
         addto(gd, (rho * ir) * (gs - dot3(u, gs) * u));
       }
     }
-    if (M > R(0)) {  // fractional C_ij: dC along the maximising path
+    if (Md > 0.0) {  // fractional C_ij: dC along the maximising path
       PathRes<R> pr = path_search(S, i, J);
       path_forces(S, owner, pr, -Q * V, F, VIR ? e + 1 : nullptr);
     }

@@ -215,6 +215,8 @@ struct ShortList {
   int* nbr;
   typename std::conditional<sizeof(R) == 8, double4, float4>::type* dr;  // d.x d.y d.z r
   typename std::conditional<sizeof(R) == 8, double2, float2>::type* w;   // w, dw/dr
+  double* wd;  // w in fp64 in both modes: the C_ij gate (M = max path product, C = 1 - M) is a
+               // gate decision (reading A14); near w = 1 an fp32 w would round M to 1
   R* Ntot;  // N_a = N^C_a + N^H_a
   R* NC;
   R* NH;
@@ -268,6 +270,8 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
           double r = sqrt(r2);
           R dw;
           R w = sw<R>((R)r, T.rmin[pr], T.rmax[pr], dw);
+          double dwd;
+          S.wd[base + n] = sizeof(R) == 8 ? (double)w : sw<double>(r, c_tabd.rmin[pr], c_tabd.rmax[pr], dwd);
           S.nbr[base + n] = b;
           S.dr[base + n] = {(R)dx, (R)dy, (R)dz, (R)r};
           S.w[base + n] = {w, dw};

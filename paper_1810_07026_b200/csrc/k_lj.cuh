@@ -198,16 +198,16 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   // bitwise that of the serial walk (the fallback for large neighbourhoods).
   constexpr int L2MAX = 4;  // (k, l) pairs per lane
   int k1 = -1, n1 = 0;
-  R w1 = 0;
+  double w1 = 0;
   if (gl < ni && gl < NEAR_GROUP) {
     k1 = S.nbr[bi + gl];
-    w1 = S.w[bi + gl].x;
+    w1 = S.wd[bi + gl];
     n1 = S.cnt[k1];
-    reach_insert(s, k1, (double)w1);
+    reach_insert(s, k1, w1);
   }
   const unsigned gmask = (NEAR_GROUP == 32 ? 0xffffffffu : ((1u << NEAR_GROUP) - 1u)) << (threadIdx.x & 31 & ~(NEAR_GROUP - 1));
   int kk[NEAR_GROUP], pp[NEAR_GROUP + 1];
-  R ww[NEAR_GROUP];
+  double ww[NEAR_GROUP];
   pp[0] = 0;
 #pragma unroll
   for (int t = 0; t < NEAR_GROUP; ++t) {
@@ -218,22 +218,22 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   const int T2 = pp[NEAR_GROUP];
   if (ni <= NEAR_GROUP && T2 <= NEAR_GROUP * L2MAX) {
     int l2[L2MAX];
-    R w2[L2MAX];
+    double w2[L2MAX];
     int n2 = 0;
     for (int e = gl; e < T2; e += NEAR_GROUP) {
       int t = 0;
 #pragma unroll
       for (int u = 1; u < NEAR_GROUP; ++u) t += (e >= pp[u]);
       int k = 0, b = 0;
-      R wk = 0;
+      double wk = 0;
 #pragma unroll
       for (int u = 0; u < NEAR_GROUP; ++u)
         if (u == t) k = kk[u], wk = ww[u], b = e - pp[u];
       const size_t ek = (size_t)k * S.capS + b;
       const int l = S.nbr[ek];
       if (l == i) continue;
-      const R w12 = wk * S.w[ek].x;
-      reach_insert(s, l, (double)w12);
+      const double w12 = wk * S.wd[ek];
+      reach_insert(s, l, w12);
 #pragma unroll
       for (int u = 0; u < L2MAX; ++u)
         if (u == n2) l2[u] = l, w2[u] = w12;
@@ -243,33 +243,33 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
     for (int u = 0; u < L2MAX; ++u) {
       if (u >= n2) break;
       const int l = l2[u];
-      const R w12 = w2[u];
+      const double w12 = w2[u];
       const size_t bl = (size_t)l * S.capS;
       const int nl = S.cnt[l];
       for (int c = 0; c < nl; ++c) {
         const int m = S.nbr[bl + c];
         if (m == i) continue;
-        reach_insert(s, m, (double)(w12 * S.w[bl + c].x));
+        reach_insert(s, m, w12 * S.wd[bl + c]);
       }
     }
   } else {  // large neighbourhood: one lane per k walks its paths (the nested enumeration)
     for (int t = gl; t < ni; t += NEAR_GROUP) {
       int k = S.nbr[bi + t];
-      R w1t = S.w[bi + t].x;
-      if (t >= NEAR_GROUP) reach_insert(s, k, (double)w1t);
+      double w1t = S.wd[bi + t];
+      if (t >= NEAR_GROUP) reach_insert(s, k, w1t);
       size_t bk = (size_t)k * S.capS;
       int nk = S.cnt[k];
       for (int b = 0; b < nk; ++b) {
         int l = S.nbr[bk + b];
         if (l == i) continue;
-        R w12 = w1t * S.w[bk + b].x;
-        reach_insert(s, l, (double)w12);
+        double w12 = w1t * S.wd[bk + b];
+        reach_insert(s, l, w12);
         size_t bl = (size_t)l * S.capS;
         int nl = S.cnt[l];
         for (int c = 0; c < nl; ++c) {
           int m = S.nbr[bl + c];
           if (m == i) continue;
-          reach_insert(s, m, (double)(w12 * S.w[bl + c].x));
+          reach_insert(s, m, w12 * S.wd[bl + c]);
         }
       }
     }
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
         dVr = dVr * sv + V * dsw * y;
         V = V * sv;
       }
-      R C = norm ? R(1) - (R)Md : R(0);
+      R C = norm ? (R)(1.0 - Md) : R(0);  // 1 - M in fp64 (gate, reading A14)
       R fr = C * dVr;  // F_i += fr d  (E(d), d = x_j - x_i)
       fx += (double)(fr * (R)dx);
       fy += (double)(fr * (R)dy);

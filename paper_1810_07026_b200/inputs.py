@@ -213,7 +213,7 @@ def config(idx: int, n_rep: int = 1) -> System:
     elif idx == 2:
         s = polyethylene((12, 16, 14), 0.02, 102, 202, name="cfg2-pe-32k")
     elif idx == 3:
-        s = amorphous(name="cfg3-aCH2-64k")
+        s = amorphous(name="cfg3-aCH2-64k", relaxed=True)  # SURVEY reading A22 (scripts/relax_cfg3.py)
         s.steps = 100
         return s
     elif idx == 4:
