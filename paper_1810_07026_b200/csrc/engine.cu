@@ -667,6 +667,7 @@ ab_status images_and_lists(ab_engine* e) {
     Lg.bq2[p] = q * q;
   }
   Lg.bqcnt = e->small_i.p + 6;
+  Lg.reach = (e->rcmax + skin) * (1.0 + 1e-9) + 1e-9;
   for (int attempt = 0; attempt < 4; ++attempt) {
     for (int c = 0; c < 3; ++c) {
       CK(e->ljn[c].ensure((size_t)N * e->capL[c]));
@@ -690,7 +691,8 @@ ab_status images_and_lists(ab_engine* e) {
         if (N) CK(cudaMemsetAsync(e->ljc[c].p, 0, sizeof(int) * N, st));
     }
     k_build_inter<<<nblk((long long)NT * 32, 128), 128, 0, st>>>(NT, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
-                                                                  e->nrI, e->capI, e->in_cnt.p, e->in_nbr.p,
+                                                                  e->nrI, (e->rmaxmax + skin) * (1.0 + 1e-9) + 1e-9,
+                                                                  e->capI, e->in_cnt.p, e->in_nbr.p,
                                                                   e->small_i.p + 5);
     CKL();
     if (dbg) cudaEventRecord(dbg_ev[2], st);

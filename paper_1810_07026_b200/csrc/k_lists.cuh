@@ -105,7 +105,23 @@ struct LJLists {
   double pure2[3]; // (r_lo(p) - skin)^2, or -1 if that band is empty
   double bq2[3];   // (2^(1/6) sigma_p (1 + 1e-9) + skin)^2: canonical pairs that can become b*
   int* bqcnt;      // [3] per species pair: bound of the b* candidate queue until the next build
+  double reach;    // (r_c,max + skin) with a rounding margin: stencil culling radius
 };
+
+// Stencil culling: a column (ax, ay) of cells is scanned only over the z-range of cells that
+// intersect the sphere of radius R around p (the full (2 nr + 1)^3 cube scans ~3x the sphere).
+// Conservative: R carries a margin, so no cell holding a partner within the list cutoff is missed.
+__device__ __forceinline__ bool column_range(const Grid& g, double4 p, int ax, int ay, double R, int& z0, int& z1) {
+  const double x0 = g.lo[0] + ax * g.cs[0], y0 = g.lo[1] + ay * g.cs[1];
+  const double dx = p.x < x0 ? x0 - p.x : (p.x > x0 + g.cs[0] ? p.x - (x0 + g.cs[0]) : 0.0);
+  const double dy = p.y < y0 ? y0 - p.y : (p.y > y0 + g.cs[1] ? p.y - (y0 + g.cs[1]) : 0.0);
+  const double d2 = dx * dx + dy * dy;
+  if (d2 > R * R) return false;
+  const double hz = sqrt(R * R - d2);
+  z0 = cell_coord(p.z - hz, g.lo[2], g.cs[2], g.nc[2]);
+  z1 = cell_coord(p.z + hz, g.lo[2], g.cs[2], g.nc[2]);
+  return true;
+}
 
 __device__ __forceinline__ void warp_append(bool take, int* row, int cap, int& n, int b) {
   unsigned m = __ballot_sync(0xffffffffu, take);
@@ -134,8 +150,11 @@ __global__ void k_build_lj(int N, const double4* pos, Grid g, const int* cell_st
   for (int c = 0; c < 3; ++c) row[c] = Lg.nbr[c] + (size_t)a * Lg.cap[c];
   for (int ax = max(0, cx - nr); ax <= min(g.nc[0] - 1, cx + nr); ++ax)
     for (int ay = max(0, cy - nr); ay <= min(g.nc[1] - 1, cy + nr); ++ay) {
+      int zc0, zc1;
+      if (!column_range(g, p, ax, ay, Lg.reach, zc0, zc1)) continue;
+      zc0 = max(zc0, z0), zc1 = min(zc1, z1);
       int c0 = (ax * g.nc[1] + ay) * g.nc[2];
-      int beg = cell_start[c0 + z0], end = cell_start[c0 + z1 + 1];
+      int beg = cell_start[c0 + zc0], end = cell_start[c0 + zc1 + 1];
       for (int base = beg; base < end; base += 32) {
         int q = base + lane;
         bool ok = q < end;
@@ -171,7 +190,7 @@ __global__ void k_build_lj(int N, const double4* pos, Grid g, const int* cell_st
 
 // intermediate REBO list: all atoms (locals + ghosts), r_b <= r_max(p) + skin
 __global__ void k_build_inter(int NT, const double4* pos, Grid g, const int* cell_start, const int* cell_atoms,
-                              int nr, int cap, int* cnt, int* nbr, int* maxcnt) {
+                              int nr, double reach, int cap, int* cnt, int* nbr, int* maxcnt) {
   int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= NT) return;
   int lane = threadIdx.x & 31;
@@ -185,8 +204,11 @@ __global__ void k_build_inter(int NT, const double4* pos, Grid g, const int* cel
   int* row = nbr + (size_t)a * cap;
   for (int ax = max(0, cx - nr); ax <= min(g.nc[0] - 1, cx + nr); ++ax)
     for (int ay = max(0, cy - nr); ay <= min(g.nc[1] - 1, cy + nr); ++ay) {
+      int zc0, zc1;
+      if (!column_range(g, p, ax, ay, reach, zc0, zc1)) continue;
+      zc0 = max(zc0, z0), zc1 = min(zc1, z1);
       int c0 = (ax * g.nc[1] + ay) * g.nc[2];
-      int beg = cell_start[c0 + z0], end = cell_start[c0 + z1 + 1];
+      int beg = cell_start[c0 + zc0], end = cell_start[c0 + zc1 + 1];
       for (int base = beg; base < end; base += 32) {
         int q = base + lane;
         bool ok = q < end;
