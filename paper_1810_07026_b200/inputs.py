@@ -130,6 +130,55 @@ def diamond(reps, jitter=0.0, seed_x=None, seed_v=None, T=1000.0, a=DIAMOND_A, n
     return System(name, types, xyz, box, v)
 
 
+# ---------------------------------------------------------------- carbon nanotube
+def nanotube(n, m, reps, bond=1.42, vacuum=12.0, jitter=0.0, seed_x=None, seed_v=None, T=300.0,
+             name=None) -> System:
+    """All-carbon (n, m) single-wall nanotube along z, periodic in z (reps translational unit
+    cells), isolated in x/y by `vacuum` A of empty space.  The paper's second workload is a custom
+    CNT ("contains no hydrogen, and stresses all the dihedral terms"; its geometry is
+    not in the container), so it is generated here: the graphene sheet (C-C distance `bond`) is
+    rolled along the chiral vector C_h = n a1 + m a2 with the translation vector
+    T = ((2m+n) a1 - (2n+m) a2) / gcd(2m+n, 2n+m).  Geometry only; no method arithmetic."""
+    if n < 1 or m < 0 or m > n:
+        raise ValueError("need n >= 1, 0 <= m <= n")
+    a = bond * math.sqrt(3.0)
+    a1 = np.array([a, 0.0])
+    a2 = np.array([a / 2.0, a * math.sqrt(3.0) / 2.0])
+    ch = n * a1 + m * a2
+    dr = math.gcd(2 * m + n, 2 * n + m)
+    t1, t2 = (2 * m + n) // dr, -(2 * n + m) // dr
+    tv = t1 * a1 + t2 * a2
+    lc, lt = float(np.linalg.norm(ch)), float(np.linalg.norm(tv))
+    nhex = 2 * (n * n + n * m + m * m) // dr  # hexagons (2 atoms each) per translational cell
+    basis = [np.zeros(2), (a1 + a2) / 3.0]  # the two graphene sublattices
+    pts = []
+    rng_i = range(-abs(t1) - n - abs(t2) - m - 2, abs(t1) + n + abs(t2) + m + 3)
+    for i in rng_i:
+        for j in rng_i:
+            for b in basis:
+                p = i * a1 + j * a2 + b
+                u, w = float(p @ ch) / lc ** 2, float(p @ tv) / lt ** 2  # fractional coordinates
+                if -1e-9 <= u < 1 - 1e-9 and -1e-9 <= w < 1 - 1e-9:
+                    pts.append((u, w))
+    if len(pts) != 2 * nhex:
+        raise RuntimeError(f"nanotube({n},{m}): {len(pts)} sites, expected {2 * nhex}")
+    radius = lc / (2.0 * math.pi)
+    side = 2.0 * radius + 2.0 * vacuum
+    box = np.array([side, side, lt * reps])
+    xyz = []
+    for k in range(reps):
+        for u, w in pts:
+            ph = 2.0 * math.pi * u
+            xyz.append((side / 2 + radius * math.cos(ph), side / 2 + radius * math.sin(ph), (w + k) * lt))
+    xyz = np.array(xyz)
+    types = np.zeros(len(xyz), dtype=np.int32)
+    if jitter > 0:
+        xyz = xyz + np.random.default_rng(seed_x).uniform(-jitter, jitter, xyz.shape)
+    xyz = wrap(xyz, box)
+    v = maxwell(types, T, seed_v) if seed_v is not None else None
+    return System(name or f"cnt-{n}-{m}-x{reps}", types, xyz, box, v)
+
+
 # ---------------------------------------------------------------- amorphous CH2
 def random_insertion(n, box, dmin, seed):
     """Random sequential insertion, uniform in the periodic box, reject if any distance < dmin."""

@@ -438,3 +438,23 @@ def test_nve_energy_drift_dt2_scaling():
     d1 = np.abs(th1[:, 3] - th1[0, 3]).max()
     d2 = np.abs(th2[:, 3] - th2[0, 3]).max()
     assert 3.0 <= d1 / d2 <= 5.0, (d1, d2)
+
+
+@pytest.mark.parametrize("nm", [(10, 10), (12, 0), (8, 4), (6, 1)])
+def test_nanotube_generator(nm):
+    """The CNT generator (no method arithmetic) against graphene geometry: every atom has exactly
+    three neighbours within r_max, nearest-neighbour distances are the C-C bond shortened only by
+    the curvature, the radius is a sqrt(n^2 + nm + m^2) / (2 pi), and the atom count per
+    translational cell is 4 (n^2 + nm + m^2) / gcd(2m + n, 2n + m)."""
+    n, m = nm
+    s = I.nanotube(n, m, 2, vacuum=10.0)
+    rows = O.get_list(s.types, s.x, s.box, 0)
+    assert np.all(np.bincount(rows[:, 0], minlength=s.n) == 3)
+    d = s.x[rows[:, 1]] + rows[:, 2:] * s.box - s.x[rows[:, 0]]
+    r = np.sqrt((d ** 2).sum(1))
+    assert r.max() <= 1.42 + 1e-9 and r.min() >= 1.42 * 0.97
+    a = 1.42 * math.sqrt(3.0)
+    R = a * math.sqrt(n * n + n * m + m * m) / (2 * math.pi)
+    rad = np.sqrt((s.x[:, 0] - s.box[0] / 2) ** 2 + (s.x[:, 1] - s.box[1] / 2) ** 2)
+    assert np.abs(rad - R).max() <= 1e-9
+    assert s.n == 2 * 4 * (n * n + n * m + m * m) // math.gcd(2 * m + n, 2 * n + m)
