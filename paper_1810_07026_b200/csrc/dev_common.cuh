@@ -29,6 +29,12 @@ struct Tab {
   R P[2][25], Rt[3][225], Tt[3][225];
   R conj_lo, conj_hi, s2lo, s2hi;
   R tors[2][2][2][2];
+  // global-memory copies of the spline tables, read through L1 (__ldg): the knot indices differ
+  // between the lanes of a warp when coordination numbers are fractional, and an indexed
+  // __constant__ load serialises per distinct address (set by the engine)
+  const R* gRT;  // [2][3][225]: pi^rc (which 0) and T (which 1) per species pair
+  const R* gP;   // [2][25]
+  const R* gG;   // [3][2][16]: g knots, values, knot slopes per centre species
 };
 
 struct Geo {  // double-only quantities: exact list / gate decisions, box, integrator
@@ -203,22 +209,25 @@ __device__ __forceinline__ void halfcos_poly(float t, float& S, float& dSdt) {
 template <typename R>
 __device__ __forceinline__ R gspline(int sp, R c, R& dg) {
   const Tab<R>& T = tab<R>();
-  int n = T.gn[sp];
-  if (c <= T.gx[sp][0]) {
+  const int n = T.gn[sp];
+  const R* gx = T.gG + sp * 16;
+  const R* gy = T.gG + 32 + sp * 16;
+  const R* gm = T.gG + 64 + sp * 16;
+  if (c <= __ldg(gx)) {
     dg = R(0);
-    return T.gy[sp][0];
+    return __ldg(gy);
   }
-  if (c >= T.gx[sp][n - 1]) {
+  if (c >= __ldg(gx + n - 1)) {
     dg = R(0);
-    return T.gy[sp][n - 1];
+    return __ldg(gy + n - 1);
   }
   int i = 0;
 #pragma unroll 1
-  while (i < n - 2 && T.gx[sp][i + 1] <= c) ++i;
-  R h = T.gx[sp][i + 1] - T.gx[sp][i];
-  R t = (c - T.gx[sp][i]) / h;
+  while (i < n - 2 && __ldg(gx + i + 1) <= c) ++i;
+  R h = __ldg(gx + i + 1) - __ldg(gx + i);
+  R t = (c - __ldg(gx + i)) / h;
   R t2 = t * t, t3 = t2 * t;
-  R y0 = T.gy[sp][i], y1 = T.gy[sp][i + 1], m0 = h * T.gm[sp][i], m1 = h * T.gm[sp][i + 1];
+  R y0 = __ldg(gy + i), y1 = __ldg(gy + i + 1), m0 = h * __ldg(gm + i), m1 = h * __ldg(gm + i + 1);
   R v = (R(2) * t3 - R(3) * t2 + R(1)) * y0 + (t3 - R(2) * t2 + t) * m0 + (R(-2) * t3 + R(3) * t2) * y1 +
         (t3 - t2) * m1;
   R dvt = (R(6) * t2 - R(6) * t) * y0 + (R(3) * t2 - R(4) * t + R(1)) * m0 + (R(-6) * t2 + R(6) * t) * y1 +
@@ -289,11 +298,11 @@ __device__ __forceinline__ R pspline(int tj, R x, R y, R& dx, R& dy) {
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       int ka = ax + a, kb = ay + a;
-      if (ka >= 0 && ka <= 4) fx += dwx[a] * T.P[tj][ka * 5 + ky];
-      if (kb >= 0 && kb <= 4) fy += dwy[a] * T.P[tj][kx * 5 + kb];
+      if (ka >= 0 && ka <= 4) fx += dwx[a] * __ldg(T.gP + tj * 25 + ka * 5 + ky);
+      if (kb >= 0 && kb <= 4) fy += dwy[a] * __ldg(T.gP + tj * 25 + kx * 5 + kb);
     }
     dx = fx, dy = fy;
-    return T.P[tj][kx * 5 + ky];
+    return __ldg(T.gP + tj * 25 + kx * 5 + ky);
   }
   R f = 0, fx = 0, fy = 0;
 #pragma unroll
@@ -304,7 +313,7 @@ __device__ __forceinline__ R pspline(int tj, R x, R y, R& dx, R& dy) {
     for (int b = 0; b < 4; ++b) {
       int kb = ay + b;
       if (kb < 0 || kb > 4) continue;
-      R v = T.P[tj][ka * 5 + kb];
+      R v = __ldg(T.gP + tj * 25 + ka * 5 + kb);
       f += wx[a] * wy[b] * v;
       fx += dwx[a] * wy[b] * v;
       fy += wx[a] * dwy[b] * v;
@@ -318,7 +327,7 @@ __device__ __forceinline__ R pspline(int tj, R x, R y, R& dx, R& dy) {
 template <typename R>
 __device__ __forceinline__ R rtspline(int which, int p, R x, R y, R z, R& gx, R& gy, R& gz) {
   const Tab<R>& T = tab<R>();
-  const R* tb = which == 0 ? T.Rt[p] : T.Tt[p];
+  const R* tb = T.gRT + (which * 3 + p) * 225;
   R wx[4], dwx[4], wy[4], dwy[4], wz[4], dwz[4];
   int ax = gridw(x, R(0), 5, wx, dwx);
   int ay = gridw(y, R(0), 5, wy, dwy);
@@ -329,12 +338,12 @@ __device__ __forceinline__ R rtspline(int which, int p, R x, R y, R z, R& gx, R&
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       int ka = ax + a, kb = ay + a, kc = az + a;
-      if (ka >= 0 && ka <= 4) fx += dwx[a] * tb[(ka * 5 + ky) * 9 + kz];
-      if (kb >= 0 && kb <= 4) fy += dwy[a] * tb[(kx * 5 + kb) * 9 + kz];
-      if (kc >= 0 && kc <= 8) fz += dwz[a] * tb[(kx * 5 + ky) * 9 + kc];
+      if (ka >= 0 && ka <= 4) fx += dwx[a] * __ldg(tb + (ka * 5 + ky) * 9 + kz);
+      if (kb >= 0 && kb <= 4) fy += dwy[a] * __ldg(tb + (kx * 5 + kb) * 9 + kz);
+      if (kc >= 0 && kc <= 8) fz += dwz[a] * __ldg(tb + (kx * 5 + ky) * 9 + kc);
     }
     gx = fx, gy = fy, gz = fz;
-    return tb[(kx * 5 + ky) * 9 + kz];
+    return __ldg(tb + (kx * 5 + ky) * 9 + kz);
   }
   R f = 0, fx = 0, fy = 0, fz = 0;
 #pragma unroll
@@ -350,7 +359,7 @@ __device__ __forceinline__ R rtspline(int which, int p, R x, R y, R z, R& gx, R&
       for (int c = 0; c < 4; ++c) {
         int kc = az + c;
         if (kc < 0 || kc > 8) continue;
-        R v = tb[(ka * 5 + kb) * 9 + kc];
+        R v = __ldg(tb + (ka * 5 + kb) * 9 + kc);
         f += wab * wz[c] * v;
         fx += dxab * wz[c] * v;
         fy += dyab * wz[c] * v;

@@ -211,6 +211,7 @@ struct ab_engine {
   DBuf<int> cnt_d;                   // selection counts (device)
   DBuf<unsigned char> redx;          // all-reduce staging
   DBuf<double> gio;                  // caller-order global array (3 Nglob) of a handle
+  DBuf<unsigned char> gtab;          // global copies of the spline tables (Tab::gRT / gP / gG)
   unsigned long long h_flag[2] = {0, 0};
   double* h_th = nullptr;  // pinned staging of thermo rows
   size_t h_th_cap = 0;
@@ -1267,6 +1268,34 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   fill_tab(e->hp, e->td);
   fill_tab(e->hp, e->tf);
   geo_fields(e);
+  {  // global-memory spline tables (read through L1 with divergent knot indices)
+    const size_t nrt = 2 * 3 * 225, np = 2 * 25, ng = 3 * 2 * 16, nall = nrt + np + ng;
+    std::vector<double> hd(nall);
+    std::vector<float> hf(nall);
+    for (int w = 0; w < 2; ++w)
+      for (int p = 0; p < 3; ++p)
+        for (int q = 0; q < 225; ++q) hd[(w * 3 + p) * 225 + q] = w == 0 ? e->td.Rt[p][q] : e->td.Tt[p][q];
+    for (int a = 0; a < 2; ++a)
+      for (int q = 0; q < 25; ++q) hd[nrt + a * 25 + q] = e->td.P[a][q];
+    for (int c = 0; c < 2; ++c)
+      for (int q = 0; q < 16; ++q) {
+        hd[nrt + np + c * 16 + q] = e->td.gx[c][q];
+        hd[nrt + np + 32 + c * 16 + q] = e->td.gy[c][q];
+        hd[nrt + np + 64 + c * 16 + q] = e->td.gm[c][q];
+      }
+    for (size_t q = 0; q < nall; ++q) hf[q] = (float)hd[q];
+    if (e->gtab.ensure(nall * (sizeof(double) + sizeof(float))) != cudaSuccess ||
+        cudaMemcpy(e->gtab.p, hd.data(), nall * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(e->gtab.p + nall * sizeof(double), hf.data(), nall * sizeof(float), cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+      e->err = "spline table upload failed";
+      return AB_E_CUDA;
+    }
+    const double* dd = reinterpret_cast<const double*>(e->gtab.p);
+    const float* ff = reinterpret_cast<const float*>(e->gtab.p + nall * sizeof(double));
+    e->td.gRT = dd, e->td.gP = dd + nrt, e->td.gG = dd + nrt + np;
+    e->tf.gRT = ff, e->tf.gP = ff + nrt, e->tf.gG = ff + nrt + np;
+  }
   bool ok = e->scratch.ensure(SCRATCH_BYTES) == cudaSuccess &&
             cudaMemset(e->scratch.p, 0, SCRATCH_BYTES) == cudaSuccess &&
             cudaMallocHost(&e->h_ct, sizeof(unsigned long long) * (CT_N + 1)) == cudaSuccess &&
@@ -1323,7 +1352,7 @@ void free_engine(ab_engine* e) {
                      &e->sendl[0], &e->sendl[1], &e->fl[0], &e->fl[1], &e->fl[2], &e->idx[0], &e->idx[1],
                      &e->idx[2], &e->cnt_d};
   for (auto* b : bi) b->release();
-  DBuf<unsigned char>* bu[] = {&e->s_dr, &e->s_w, &e->s_N, &e->cub_tmp, &e->sb[0], &e->sb[1], &e->rb[0], &e->rb[1],
+  DBuf<unsigned char>* bu[] = {&e->s_dr, &e->s_w, &e->s_N, &e->gtab, &e->cub_tmp, &e->sb[0], &e->sb[1], &e->rb[0], &e->rb[1],
                                &e->redx};
   for (auto* b : bu) b->release();
   e->shift.release();
