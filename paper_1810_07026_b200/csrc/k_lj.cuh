@@ -315,11 +315,13 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       nc0 += c0 && canon;
       // LJ for every lane (weight 0 unless norm)
       R rr2 = norm ? (R)r2 : R(1);
-      R y = rsqrt_fast(rr2);
+      // 1/r^2 by a reciprocal for the 12-6 form (1/r only for Morse and the rare taper)
+      R y = MORSE ? rsqrt_fast(rr2) : R(0);
       R dVr;
       R V = MORSE ? morse_plain<R>(pr_[p], pr_[3 + p], pm_[p], rr2 * y, y, dVr)
-                  : lj_plain<R>(pr_[p], pr_[3 + p], y * y, dVr);
+                  : lj_plain<R>(pr_[p], pr_[3 + p], rcp_fast(rr2), dVr);
       if (norm && r2 > pd[6 + p]) {  // taper S(r; r_lo, r_c) (reading A10): rare in the near list
+        if (!MORSE) y = rsqrt_fast(rr2);
         R r = rr2 * y, dsw;
         R sv = sw<R>(r, pr_[6 + p], pr_[9 + p], dsw);
         dVr = dVr * sv + V * dsw * y;
