@@ -143,7 +143,7 @@ def algorithmic_flops(stats):
             "bstar": 1500 * stats["n_bstar"], "lj_far": 31 * far_in + 9 * max(0, far_ent - far_in)}
 
 
-PHASES = ["short", "rebo", "lj_near", "bstar", "integrate", "rebuild", "lj_far", "spare"]
+PHASES = ["short", "rebo", "lj_near", "bstar", "integrate", "rebuild", "lj_far", "comm"]
 KERNEL_OF = {"short": "k_short", "rebo": "k_rebo", "lj_near": "k_lj_near", "bstar": "k_bstar", "lj_far": "k_lj_far"}
 
 
@@ -301,7 +301,8 @@ def run_ours(args, ws, rank, local):
                                "value runs the concurrent DAG",
                 "whole_step_tflops": round(step_flops / step_s / 1e12, 4),
                 "whole_step_frac": round(step_flops / step_s / 1e12 / peak, 5),
-                "phase_ms_per_step": {p: round(v[0] / K, 5) for p, v in r["phase"].items()}}
+                "phase_ms_per_step": {p: round(v[0] / K, 5) for p, v in r["phase"].items()},
+                "comm_ms_per_step": round(r["phase"]["comm"][0] / K, 5) if ws > 1 else None}
 
     peak_meas = {}
     for p, code in (("fp64", E.AB_FP64), ("fp32", E.AB_MIXED)):

@@ -172,7 +172,8 @@ ab_status ab_get_stage(ab_engine* e, int stage, int64_t* count, double* out);
 
 /* Per-phase device timing with CUDA events on the engine's stream (the paper's profile labels,
  * P:359-360): phase 0 short list + N_i, 1 REBO + bond order + torsion, 2 LJ near
- * pairs + C_ij reach sets, 3 b* batch, 4 integrator, 5 list rebuild, 6 LJ far pairs, 7 spare.
+ * pairs + C_ij reach sets, 3 b* batch, 4 integrator, 5 list rebuild, 6 LJ far pairs, 7 slab transfers
+ * (halo positions, ghost forces, migration; multi-domain engines only).
  * ab_get_phase_ms returns accumulated milliseconds ms[AB_NPHASE] and launch counts n[AB_NPHASE]
  * since profiling was switched on (on != 0 resets them). */
 #define AB_NPHASE 8

@@ -218,6 +218,7 @@ struct ab_engine {
   long long graph_launches = 0;  // kernel launches per replay
   long long graph_epoch = -1;    // layout version the graph was captured at
   long long layout = 0;          // bumped whenever buffers / capacities / kernel choices change
+  double disp1 = -1.0, disp2 = -1.0;  // max displacement since the last build at the last two steps
   unsigned long long h_flag[2] = {0, 0};
   double* h_th = nullptr;  // pinned staging of thermo rows
   size_t h_th_cap = 0;
@@ -485,8 +486,17 @@ ab_status select_flagged(ab_engine* e, int n, const int* flags, int* out, int* n
 // left neighbour sends on its channel 1 arrives in my rb[0] and vice versa.  NCCL order per
 // rank: send(left) recv(right) send(right) recv(left) -- with two ranks (left == right) the pairs
 // match in issue order: my first send lands in the peer's first receive (its rb[1]).
+ab_status xfer_impl(ab_engine* e);
+// every transfer is timed as phase 7 (halo exchange / reverse communication, SURVEY §8(d):
+// "communication time per step") when profiling is on
 ab_status xfer(ab_engine* e) {
   if (!slabbed(e)) return AB_OK;
+  cudaEvent_t t = prof_start(e, e->st);
+  ab_status s = xfer_impl(e);
+  prof_stop(e, 7, e->st, t);
+  return s;
+}
+ab_status xfer_impl(ab_engine* e) {
   if (!e->subs.empty()) {
     const int n = (int)e->subs.size();
     for (int r = 0; r < n; ++r) {
@@ -1904,8 +1914,13 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     CK(cudaEventRecord(e->ev_disp, st));
     e->host_ms[0] += ms_since(t0);
     t0 = clk::now();
+    // Speculate unless the displacement trend predicts a rebuild at this step (linear
+    // extrapolation of the max displacement since the last build): in hot systems that rebuild
+    // every few steps a wasted speculative evaluation would sit in front of the rebuild.
     bool speculated = false;
-    if (e->lists_valid) {
+    const double half_skin = 0.5 * hp.skin;
+    const bool predict_rebuild = e->disp1 >= 0.0 && e->disp2 >= 0.0 && 2.0 * e->disp1 - e->disp2 > half_skin;
+    if (e->lists_valid && !predict_rebuild) {
       TRY(step_forces(e));
       speculated = true;
     }
@@ -1920,7 +1935,10 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
       return AB_E_STATE;
     }
     double half = 0.5 * hp.skin;
+    const double dnow = std::sqrt(std::max(flag_d2(e), 0.0));
     if (flag_d2(e) > half * half) e->lists_valid = false, speculated = false;
+    if (e->lists_valid) e->disp2 = e->disp1, e->disp1 = dnow;
+    else e->disp1 = 0.0, e->disp2 = -1.0;  // a rebuild: displacement 0 at the new build
     if (!speculated) {
       TRY(prepare_all(e, false));
       TRY(forces_all(e, false));
