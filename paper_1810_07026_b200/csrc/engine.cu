@@ -655,6 +655,9 @@ ab_status images_and_lists(ab_engine* e) {
   e->rb_ms[2] += tms(tq);
   tq = std::chrono::steady_clock::now();
   // 4. skinned lists: LJ (local atoms, full) and intermediate REBO (all atoms)
+  // cell edge >= (r_c,max + skin)/3 and >= r_max + skin (setup_grid): nrLJ <= 3, nrI <= 1
+  if ((2 * e->nrLJ + 1) * (2 * e->nrLJ + 1) > STENCIL_MAXCOL || (2 * e->nrI + 1) * (2 * e->nrI + 1) > STENCIL_MAXCOL)
+    return AB_E_STATE;
   CK(e->small_i.ensure(8));
   for (int c = 0; c < 3; ++c) CK(e->ljc[c].ensure(N));
   CK(e->in_cnt.ensure(NT));

@@ -132,53 +132,99 @@ __device__ __forceinline__ void warp_append(bool take, int* row, int cap, int& n
   n += __popc(m);
 }
 
-__global__ void k_build_lj(int N, const double4* pos, Grid g, const int* cell_start, const int* cell_atoms, int nr,
-                           LJLists Lg, int* maxcnt) {
+// The culled stencil of atom p flattened for one warp: column k (x-major, then y -- the scan
+// order of the lists) holds candidates [cb[k], cb[k] + pre[k+1] - pre[k]) of the cell-sorted
+// index.  The column bounds are computed 32 columns at a time (independent loads), instead of
+// one dependent cell_start read per column, and candidates are then streamed in full chunks of
+// 32 across column boundaries.  Returns the candidate count; needs (2 nr + 1)^2 <= STENCIL_MAXCOL.
+constexpr int STENCIL_MAXCOL = 128;
+__device__ __forceinline__ int stencil_columns(const Grid& g, double4 p, int nr, double R, const int* cell_start,
+                                               int* cb, int* pre) {
+  const int lane = threadIdx.x & 31;
+  const int cx = cell_coord(p.x, g.lo[0], g.cs[0], g.nc[0]);
+  const int cy = cell_coord(p.y, g.lo[1], g.cs[1], g.nc[1]);
+  const int cz = cell_coord(p.z, g.lo[2], g.cs[2], g.nc[2]);
+  const int z0 = max(0, cz - nr), z1 = min(g.nc[2] - 1, cz + nr);
+  const int side = 2 * nr + 1, ncol = side * side;
+  int run = 0;
+  for (int c0 = 0; c0 < ncol; c0 += 32) {
+    const int col = c0 + lane;
+    int beg = 0, len = 0;
+    if (col < ncol) {
+      const int ax = cx - nr + col / side, ay = cy - nr + col % side;
+      int zc0, zc1;
+      if (ax >= 0 && ax < g.nc[0] && ay >= 0 && ay < g.nc[1] && column_range(g, p, ax, ay, R, zc0, zc1)) {
+        zc0 = max(zc0, z0), zc1 = min(zc1, z1);
+        const int c = (ax * g.nc[1] + ay) * g.nc[2];
+        beg = cell_start[c + zc0];
+        len = max(cell_start[c + zc1 + 1] - beg, 0);
+      }
+    }
+    int v = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (col < ncol) cb[col] = beg, pre[col] = run + v - len;
+    run += __shfl_sync(0xffffffffu, v, 31);
+  }
+  if (lane == 0) pre[ncol] = run;
+  __syncwarp();
+  return run;
+}
+
+// candidate f of the flattened stencil, scanning forward from column k (k <= f's column)
+__device__ __forceinline__ int stencil_at(const int* cb, const int* pre, const int* cell_atoms, int f, int& k) {
+  while (pre[k + 1] <= f) ++k;
+  return cell_atoms[cb[k] + f - pre[k]];
+}
+
+__global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, Grid g, const int* cell_start,
+                                                  const int* cell_atoms, int nr, LJLists Lg, int* maxcnt) {
+  __shared__ int s_cb[4][STENCIL_MAXCOL], s_pre[4][STENCIL_MAXCOL + 1];
   int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= N) return;
-  int lane = threadIdx.x & 31;
-  double4 p = pos[a];
-  int ta = type_of(p);
-  int cx = cell_coord(p.x, g.lo[0], g.cs[0], g.nc[0]);
-  int cy = cell_coord(p.y, g.lo[1], g.cs[1], g.nc[1]);
-  int cz = cell_coord(p.z, g.lo[2], g.cs[2], g.nc[2]);
-  int z0 = max(0, cz - nr), z1 = min(g.nc[2] - 1, cz + nr);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double4 p = pos[a];
+  const int ta = type_of(p);
   int n[3] = {0, 0, 0};
   int nq[3] = {0, 0, 0};
   const long long ka = key_of(p);
   int* row[3];
   for (int c = 0; c < 3; ++c) row[c] = Lg.nbr[c] + (size_t)a * Lg.cap[c];
-  for (int ax = max(0, cx - nr); ax <= min(g.nc[0] - 1, cx + nr); ++ax)
-    for (int ay = max(0, cy - nr); ay <= min(g.nc[1] - 1, cy + nr); ++ay) {
-      int zc0, zc1;
-      if (!column_range(g, p, ax, ay, Lg.reach, zc0, zc1)) continue;
-      zc0 = max(zc0, z0), zc1 = min(zc1, z1);
-      int c0 = (ax * g.nc[1] + ay) * g.nc[2];
-      int beg = cell_start[c0 + zc0], end = cell_start[c0 + zc1 + 1];
-      for (int base = beg; base < end; base += 32) {
-        int q = base + lane;
-        bool ok = q < end;
-        int b = ok ? cell_atoms[q] : -1;
-        ok = ok && b != a;
-        double r2 = 1e300;
-        int pr = 0;
-        if (ok) {
-          double4 pb = pos[b];
-          r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
-          pr = ta + type_of(pb);
-        }
-        bool in = ok && r2 <= c_geo.rc_s2[pr];
-        bool nearp = in && r2 <= Lg.near2;
-        bool purep = in && !nearp && r2 <= Lg.pure2[pr];
-        bool bandp = in && !nearp && !purep;
-        warp_append(nearp, row[0], Lg.cap[0], n[0], b);
-        warp_append(purep, row[1], Lg.cap[1], n[1], b);
-        warp_append(bandp, row[2], Lg.cap[2], n[2], b);
-        const bool bq = nearp && r2 <= Lg.bq2[pr] && ka < key_of(pos[b]);
-#pragma unroll
-        for (int t = 0; t < 3; ++t) nq[t] += __popc(__ballot_sync(0xffffffffu, bq && pr == t));
-      }
+  int* cb = s_cb[w];
+  int* pre = s_pre[w];
+  const int total = stencil_columns(g, p, nr, Lg.reach, cell_start, cb, pre);
+  int k = 0;  // column of the chunk's first candidate (warp-uniform)
+  // software pipeline: the next chunk's index and position loads are in flight while this
+  // chunk is classified and appended
+  int b = lane < total ? stencil_at(cb, pre, cell_atoms, lane, k) : -1;
+  double4 pb = b >= 0 ? pos[b] : make_double4(0, 0, 0, 0);
+  for (int base = 0; base < total; base += 32) {
+    int kn = __shfl_sync(0xffffffffu, k, 31);
+    const int fn = base + 32 + lane;
+    const int bn = fn < total ? stencil_at(cb, pre, cell_atoms, fn, kn) : -1;
+    const double4 pbn = bn >= 0 ? pos[bn] : make_double4(0, 0, 0, 0);
+    const bool ok = b >= 0 && b != a;
+    double r2 = 1e300;
+    int pr = 0;
+    if (ok) {
+      r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
+      pr = ta + type_of(pb);
     }
+    const bool in = ok && r2 <= c_geo.rc_s2[pr];
+    const bool nearp = in && r2 <= Lg.near2;
+    const bool purep = in && !nearp && r2 <= Lg.pure2[pr];
+    const bool bandp = in && !nearp && !purep;
+    warp_append(nearp, row[0], Lg.cap[0], n[0], b);
+    warp_append(purep, row[1], Lg.cap[1], n[1], b);
+    warp_append(bandp, row[2], Lg.cap[2], n[2], b);
+    const bool bq = nearp && r2 <= Lg.bq2[pr] && ka < key_of(pb);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) nq[t] += __popc(__ballot_sync(0xffffffffu, bq && pr == t));
+    b = bn, pb = pbn, k = kn;
+  }
   if (lane == 0) {
     for (int c = 0; c < 3; ++c) {
       Lg.cnt[c][a] = n[c];
@@ -189,40 +235,33 @@ __global__ void k_build_lj(int N, const double4* pos, Grid g, const int* cell_st
 }
 
 // intermediate REBO list: all atoms (locals + ghosts), r_b <= r_max(p) + skin
-__global__ void k_build_inter(int NT, const double4* pos, Grid g, const int* cell_start, const int* cell_atoms,
-                              int nr, double reach, int cap, int* cnt, int* nbr, int* maxcnt) {
+__global__ void __launch_bounds__(128) k_build_inter(int NT, const double4* pos, Grid g, const int* cell_start,
+                                                     const int* cell_atoms, int nr, double reach, int cap, int* cnt,
+                                                     int* nbr, int* maxcnt) {
+  __shared__ int s_cb[4][STENCIL_MAXCOL], s_pre[4][STENCIL_MAXCOL + 1];
   int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= NT) return;
-  int lane = threadIdx.x & 31;
-  double4 p = pos[a];
-  int ta = type_of(p);
-  int cx = cell_coord(p.x, g.lo[0], g.cs[0], g.nc[0]);
-  int cy = cell_coord(p.y, g.lo[1], g.cs[1], g.nc[1]);
-  int cz = cell_coord(p.z, g.lo[2], g.cs[2], g.nc[2]);
-  int z0 = max(0, cz - nr), z1 = min(g.nc[2] - 1, cz + nr);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double4 p = pos[a];
+  const int ta = type_of(p);
   int n = 0;
   int* row = nbr + (size_t)a * cap;
-  for (int ax = max(0, cx - nr); ax <= min(g.nc[0] - 1, cx + nr); ++ax)
-    for (int ay = max(0, cy - nr); ay <= min(g.nc[1] - 1, cy + nr); ++ay) {
-      int zc0, zc1;
-      if (!column_range(g, p, ax, ay, reach, zc0, zc1)) continue;
-      zc0 = max(zc0, z0), zc1 = min(zc1, z1);
-      int c0 = (ax * g.nc[1] + ay) * g.nc[2];
-      int beg = cell_start[c0 + zc0], end = cell_start[c0 + zc1 + 1];
-      for (int base = beg; base < end; base += 32) {
-        int q = base + lane;
-        bool ok = q < end;
-        int b = ok ? cell_atoms[q] : -1;
-        ok = ok && b != a;
-        bool in = false;
-        if (ok) {
-          double4 pb = pos[b];
-          double r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
-          in = r2 <= c_geo.rmax_s2[ta + type_of(pb)];
-        }
-        warp_append(in, row, cap, n, b);
-      }
+  int* cb = s_cb[w];
+  int* pre = s_pre[w];
+  const int total = stencil_columns(g, p, nr, reach, cell_start, cb, pre);
+  int k = 0;
+  for (int base = 0; base < total; base += 32) {
+    const int f = base + lane;
+    const int b = f < total ? stencil_at(cb, pre, cell_atoms, f, k) : -1;
+    bool in = false;
+    if (b >= 0 && b != a) {
+      const double4 pb = pos[b];
+      const double r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
+      in = r2 <= c_geo.rmax_s2[ta + type_of(pb)];
     }
+    warp_append(in, row, cap, n, b);
+    k = __shfl_sync(0xffffffffu, k, 31);
+  }
   if (lane == 0) {
     cnt[a] = n;
     atomicMax(maxcnt, n);
