@@ -382,7 +382,10 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 }
 
 // ---------------------------------------------------------------------------------- far pairs
-constexpr int FAR_UNROLL = 4;
+#ifndef AB_FAR_UNROLL
+#define AB_FAR_UNROLL 4
+#endif
+constexpr int FAR_UNROLL = AB_FAR_UNROLL;
 
 template <typename R, bool VIRIAL, bool BAND, bool MORSE>
 __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, double4 pi, int ti, long long ki,
@@ -400,16 +403,26 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
   const R rloa = T.rlo[ti], rlob = T.rlo[ti + 1];
   const R iva = T.inv_taper[ti], ivb = T.inv_taper[ti + 1];
   const double rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
+  // the next chunk's list indices are loaded one iteration ahead: the position gathers of a
+  // chunk then wait on one memory latency, not on two dependent ones
+  int Jn[FAR_UNROLL];
+#pragma unroll
+  for (int u = 0; u < FAR_UNROLL; ++u) {
+    int q = u * 32 + lane;
+    Jn[u] = q < cnt ? row[q] : -1;
+  }
   for (int base = 0; base < cnt; base += 32 * FAR_UNROLL) {
     int J[FAR_UNROLL];
     double4 pj[FAR_UNROLL];
 #pragma unroll
-    for (int u = 0; u < FAR_UNROLL; ++u) {
-      int q = base + u * 32 + lane;
-      J[u] = q < cnt ? row[q] : -1;
-    }
+    for (int u = 0; u < FAR_UNROLL; ++u) J[u] = Jn[u];
 #pragma unroll
     for (int u = 0; u < FAR_UNROLL; ++u) pj[u] = A.pos[J[u] >= 0 ? J[u] : i];
+#pragma unroll
+    for (int u = 0; u < FAR_UNROLL; ++u) {
+      int q = base + 32 * FAR_UNROLL + u * 32 + lane;
+      Jn[u] = q < cnt ? row[q] : -1;
+    }
     // branch-free bodies: every lane evaluates, invalid / out-of-cutoff lanes are weighted by 0
 #pragma unroll
     for (int u = 0; u < FAR_UNROLL; ++u) {
