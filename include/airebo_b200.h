@@ -43,8 +43,13 @@ typedef enum {
 
 typedef enum {
   AB_FP64 = 0,  /* IEEE binary64 throughout */
-  AB_MIXED = 1  /* fp64 positions/displacements/list decisions/accumulators; fp32 term arithmetic
+  AB_MIXED = 1, /* fp64 positions/displacements/list decisions/accumulators; fp32 term arithmetic
                    after the displacement vector (SURVEY reading A14) */
+  AB_SINGLE = 2 /* the paper's "single" mode for the precision study (SURVEY
+                   8(f) F2): AB_MIXED with every accumulation in fp32 -- per-thread force / energy
+                   / virial sums, the warp reductions and the per-atom force array (fp32 atomics)
+                   -- so the accumulator precision is the only difference to AB_MIXED (reading
+                   A32).  Positions, velocities and the integrator stay fp64. */
 } ab_precision;
 
 typedef enum {

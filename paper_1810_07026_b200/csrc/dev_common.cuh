@@ -372,15 +372,32 @@ __device__ __forceinline__ R rtspline(int which, int p, R x, R y, R z, R& gx, R&
 }
 
 // ------------------------------------------------------------------ atomics and reductions
+// AB_SINGLE (kernels instantiated with SG = true) accumulates in fp32: a running sum is rounded
+// to binary32 after every addition (both operands are binary32 values, so this is the fp32 sum
+// up to a rare double rounding)
+template <bool SG = false>
+__device__ __forceinline__ double acc_round(double a) { return SG ? (double)(float)a : a; }
+
+// With SG the force array handed to the kernels is an fp32 array (engine.cu: Ff), summed with
+// fp32 atomics and widened into F after the evaluation.
+template <bool SG = false>
 __device__ __forceinline__ void atomic_add3(double* F, int a, double x, double y, double z) {
+  if (SG) {
+    float* f = reinterpret_cast<float*>(F);
+    atomicAdd(f + 3 * a + 0, (float)x);
+    atomicAdd(f + 3 * a + 1, (float)y);
+    atomicAdd(f + 3 * a + 2, (float)z);
+    return;
+  }
   atomicAdd(F + 3 * a + 0, x);
   atomicAdd(F + 3 * a + 1, y);
   atomicAdd(F + 3 * a + 2, z);
 }
 
+template <bool SG = false>
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v = acc_round<SG>(v + __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 __device__ __forceinline__ unsigned long long warp_sum_u(unsigned long long v) {

@@ -152,6 +152,7 @@ struct ab_engine {
   // device state
   DBuf<double4> pos, pos_tmp, xref;
   DBuf<double> vel, vel_tmp, F, io;
+  DBuf<float> Ff;  // AB_SINGLE: fp32 force accumulation array of an evaluation
   DBuf<int> gid, gid_tmp, owner, key, key2, val, val2, cell_start, gcnt, goff;
   DBuf<char4> shift, rshift;
   DBuf<signed char> typ;
@@ -956,7 +957,8 @@ ab_status refresh_ghosts_all(ab_engine* e) {
 }
 
 // ---------------------------------------------------------------- force evaluation
-template <typename R>
+// SG: AB_SINGLE (fp32 accumulation: fp32 force array, fp32 running sums), only with R = float
+template <typename R, bool SG = false>
 ab_status enqueue_forces(ab_engine* e) {
   const int N = e->N, NT = e->NT;
   cudaStream_t st = e->st;
@@ -969,6 +971,12 @@ ab_status enqueue_forces(ab_engine* e) {
     sb1 = StageBuf{e->stage1.p, e->small_i.p + 7, (int)n1};
   }
   CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * e->NX, st));
+  // AB_SINGLE: the kernels sum forces into an fp32 array (atomic_add3), widened into F below
+  if (SG) {
+    CK(e->Ff.ensure(3 * (size_t)e->NX + 3));
+    CK(cudaMemsetAsync(e->Ff.p, 0, sizeof(float) * 3 * e->NX, st));
+  }
+  double* const Fk = SG ? reinterpret_cast<double*>(e->Ff.p) : e->F.p;
   CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
   ShortList<R> S = short_view<R>(e);
   // grids and the per-block partial rows of the energy / virial / counter reduction
@@ -1007,9 +1015,9 @@ ab_status enqueue_forces(ab_engine* e) {
     cudaEvent_t t = prof_start(e, s_far);
     RedRows R6 = RR;
     R6.row0 = row_far;
-    auto far = [&](auto kern) { kern<<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, e->F.p, e->acc.p, e->ct.p, sb1, R6); };
-    if (e->want_virial) morse ? far(k_lj_far<R, true, true>) : far(k_lj_far<R, true, false>);
-    else morse ? far(k_lj_far<R, false, true>) : far(k_lj_far<R, false, false>);
+    auto far = [&](auto kern) { kern<<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, Fk, e->acc.p, e->ct.p, sb1, R6); };
+    if (e->want_virial) morse ? far(k_lj_far<R, true, true, SG>) : far(k_lj_far<R, true, false, SG>);
+    else morse ? far(k_lj_far<R, false, true, SG>) : far(k_lj_far<R, false, false, SG>);
     CKL();
     prof_stop(e, 6, s_far, t);
     CK(cudaEventRecord(e->ev_join[1], s_far));
@@ -1029,13 +1037,13 @@ ab_status enqueue_forces(ab_engine* e) {
     R1.row0 = g_short;
     auto rebo = [&](auto fast, auto slow) {
       fast<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, e->ovf_bond.p, e->small_i.p + 8, S, e->typ.p, e->owner.p,
-                                       e->gid.p, e->shift.p, e->F.p, sb0, R1);
+                                       e->gid.p, e->shift.p, Fk, sb0, R1);
       R1.row0 += g_rebo;
       slow<<<g_slow, 128, 0, s_rebo>>>(BL, e->ovf_bond.p, nullptr, e->small_i.p + 8, S, e->typ.p, e->owner.p,
-                                       e->gid.p, e->shift.p, e->F.p, sb0, R1);
+                                       e->gid.p, e->shift.p, Fk, sb0, R1);
     };
-    if (e->want_virial) rebo(k_rebo<R, NB_FAST, true>, k_rebo<R, NBMAX, true>);
-    else rebo(k_rebo<R, NB_FAST, false>, k_rebo<R, NBMAX, false>);
+    if (e->want_virial) rebo(k_rebo<R, NB_FAST, true, SG>, k_rebo<R, NBMAX, true, SG>);
+    else rebo(k_rebo<R, NB_FAST, false, SG>, k_rebo<R, NBMAX, false, SG>);
     ++e->launches;  // + the CKL below: two launches
     CKL();
     prof_stop(e, 1, s_rebo, t);
@@ -1045,11 +1053,11 @@ ab_status enqueue_forces(ab_engine* e) {
   if (lj) {
     cudaEvent_t t = prof_start(e, st);
     auto near = [&](auto kern) {
-      kern<<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, e->F.p, e->acc.p,
+      kern<<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, Fk, e->acc.p,
                                                        e->ct.p, Qu, sb1, RR);
     };
-    if (e->want_virial) morse ? near(k_lj_near<R, true, true>) : near(k_lj_near<R, true, false>);
-    else morse ? near(k_lj_near<R, false, true>) : near(k_lj_near<R, false, false>);
+    if (e->want_virial) morse ? near(k_lj_near<R, true, true, SG>) : near(k_lj_near<R, true, false, SG>);
+    else morse ? near(k_lj_near<R, false, true, SG>) : near(k_lj_near<R, false, false, SG>);
     CKL();
     prof_stop(e, 2, st, t);
   }
@@ -1060,18 +1068,18 @@ ab_status enqueue_forces(ab_engine* e) {
     // sides, count small_i[9]), pairs with a large side -> ovf_q2 (NBMAX, count small_i[1])
     auto bstar = [&](auto fast, auto full, auto big) {
       fast<<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p, e->small_i.p + 1,
-                                    e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+                                    e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
       RR.row0 += g_bstar;
       full<<<g_bstar, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, nullptr, nullptr, e->pos.p, S,
-                                    e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+                                    e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
       RR.row0 += g_bstar;
       big<<<g_slow, 128, 0, st>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr, e->pos.p, S,
-                                  e->typ.p, e->owner.p, e->gid.p, e->shift.p, e->F.p, sb1, RR);
+                                  e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
     };
     if (e->want_virial)
-      bstar(k_bstar<R, NB_FAST, false, true>, k_bstar<R, NB_FAST, true, true>, k_bstar<R, NBMAX, true, true>);
+      bstar(k_bstar<R, NB_FAST, false, true, SG>, k_bstar<R, NB_FAST, true, true, SG>, k_bstar<R, NBMAX, true, true, SG>);
     else
-      bstar(k_bstar<R, NB_FAST, false, false>, k_bstar<R, NB_FAST, true, false>, k_bstar<R, NBMAX, true, false>);
+      bstar(k_bstar<R, NB_FAST, false, false, SG>, k_bstar<R, NB_FAST, true, false, SG>, k_bstar<R, NBMAX, true, false, SG>);
     e->launches += 2;  // + the CKL below: three launches
     CKL();
     prof_stop(e, 3, st, t);
@@ -1081,7 +1089,17 @@ ab_status enqueue_forces(ab_engine* e) {
   RR.row0 = 0;
   k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows_used, e->acc.p, e->ct.p);
   CKL();
+  if (SG) {
+    k_widen<<<nblk(3LL * e->NX, 256), 256, 0, st>>>(3 * e->NX, e->Ff.p, e->F.p);
+    CKL();
+  }
   return AB_OK;
+}
+
+ab_status enqueue_forces_any(ab_engine* e) {
+  if (e->prec == AB_FP64) return enqueue_forces<double>(e);
+  if (e->prec == AB_SINGLE) return enqueue_forces<float, true>(e);
+  return enqueue_forces<float>(e);
 }
 
 // reverse communication: forces on x-ghosts go home and are added to the owned atoms
@@ -1165,7 +1183,7 @@ ab_status collect(ab_engine* e) {
 ab_status forces_all(ab_engine* e, bool sync_host = true) {
   auto D = doms(e);
   for (int attempt = 0; attempt < 3; ++attempt) {
-    for (ab_engine* d : D) TRYD(d, d->prec == AB_FP64 ? enqueue_forces<double>(d) : enqueue_forces<float>(d));
+    for (ab_engine* d : D) TRYD(d, enqueue_forces_any(d));
     if (slabbed(e)) {
       for (ab_engine* d : D) TRYD(d, force_pack(d));
       TRY(xfer(e));
@@ -1383,6 +1401,7 @@ void free_engine(ab_engine* e) {
   DBuf<unsigned char>* bu[] = {&e->s_dr, &e->s_w, &e->s_N, &e->gtab, &e->cub_tmp, &e->sb[0], &e->sb[1], &e->rb[0], &e->rb[1],
                                &e->redx};
   for (auto* b : bu) b->release();
+  e->Ff.release();
   e->shift.release();
   e->rshift.release();
   e->typ.release();
@@ -1538,7 +1557,7 @@ ab_status check_slab_box(ab_engine* e) {
 extern "C" {
 
 ab_status ab_create(const char* text, size_t len, ab_precision prec, int device, ab_engine** out) {
-  if (!text || !out || (prec != AB_FP64 && prec != AB_MIXED)) {
+  if (!text || !out || (prec != AB_FP64 && prec != AB_MIXED && prec != AB_SINGLE)) {
     g_create_error = "ab_create: bad argument";
     return AB_E_ARG;
   }

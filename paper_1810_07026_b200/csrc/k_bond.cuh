@@ -224,15 +224,15 @@ __device__ __forceinline__ R bo_value(const BoState<R, NB>& st) {
   return R(0.5) * (st.pij + st.pji) + st.Rv + st.Tv * st.D;
 }
 
-template <typename R>
+template <typename R, bool SG = false>
 __device__ __forceinline__ void scatter_vec(double* F, const int* owner, int a_to, int a_from, V3<R> g) {
   // vector v = x_to - x_from with gradient g: F_to -= g, F_from += g
-  atomic_add3(F, owner[a_to], -(double)g.x, -(double)g.y, -(double)g.z);
-  atomic_add3(F, owner[a_from], (double)g.x, (double)g.y, (double)g.z);
+  atomic_add3<SG>(F, owner[a_to], -(double)g.x, -(double)g.y, -(double)g.z);
+  atomic_add3<SG>(F, owner[a_from], (double)g.x, (double)g.y, (double)g.z);
 }
 
 // N^conj chain: N_c = sum_m w_cm (m != excluded) -> forces on every m with dw != 0
-template <typename R>
+template <typename R, bool SG = false>
 __device__ __forceinline__ void conj_chain(const ShortList<R>& S, const int* owner, int c, int excl, R chain,
                                            double* F, double W[6]) {
   size_t bc = (size_t)c * S.capS;
@@ -245,7 +245,7 @@ __device__ __forceinline__ void conj_chain(const ShortList<R>& S, const int* own
     R rcm;
     V3<R> dcm = sl_d(S, c, q2, rcm);
     V3<R> g = (chain * dw / rcm) * dcm;
-    scatter_vec(F, owner, m, c, g);
+    scatter_vec<R, SG>(F, owner, m, c, g);
     vir_add(W, dcm, g);
   }
 }
@@ -254,7 +254,7 @@ __device__ __forceinline__ void conj_chain(const ShortList<R>& S, const int* own
 // cb = dE/db.  wij: weight of the bond for the merged torsion term (TORS only).
 // Output gd = dE/d(d) through the bond-order (and torsion) terms; fi / fj = force contributions
 // on i / J from the k and l vectors (the forces on k, l, m, n are scattered here).
-template <typename R, bool TORS, int NB, bool UNROLL = false>
+template <typename R, bool TORS, int NB, bool UNROLL = false, bool SG = false>
 __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const int* owner, const BoState<R, NB>& st,
                            R cb, R wij, double* F, double W[6], V3<R>& gd, V3<R>& fi, V3<R>& fj) {
   const Tab<R>& T = tab<R>();
@@ -366,10 +366,10 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     addto(gk, (Ck * irk) * (u - ck * uk));
     addto(gd, (Ck * ir) * (uk - ck * u));
     // force on k now; the +gk on i is accumulated in fi (one atomic per bond for i)
-    atomic_add3(F, owner[k], -(double)gk.x, -(double)gk.y, -(double)gk.z);
+    atomic_add3<SG>(F, owner[k], -(double)gk.x, -(double)gk.y, -(double)gk.z);
     addto(fi, gk);
     vir_add(W, dk, gk);
-    if (chain != R(0)) conj_chain(S, owner, k, i, chain, F, W);
+    if (chain != R(0)) conj_chain<R, SG>(S, owner, k, i, chain, F, W);
   }
 #pragma unroll(Unr<NB, UNROLL>::v)
   for (int c = 0; c < NB; ++c) {
@@ -387,14 +387,14 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     addto(g, (Wl[c] * dwl) * ul);
     addto(g, (Cl[c] * irl) * (mk3(-u.x, -u.y, -u.z) - cl * ul));
     addto(gd, (-Cl[c] * ir) * (ul + cl * u));
-    atomic_add3(F, owner[l], -(double)g.x, -(double)g.y, -(double)g.z);
+    atomic_add3<SG>(F, owner[l], -(double)g.x, -(double)g.y, -(double)g.z);
     addto(fj, g);
     vir_add(W, dl, g);
     if (tl == 0) {
       R dF;
       F_conj<R>(S.Ntot[l] - wl, dF);
       R chain = dNc * R(2) * st.Sj * wl * dF;
-      if (chain != R(0)) conj_chain(S, owner, l, J, chain, F, W);
+      if (chain != R(0)) conj_chain<R, SG>(S, owner, l, J, chain, F, W);
     }
   }
 }
@@ -432,7 +432,7 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 #define AB_BSTAR_MINBLOCKS 3  // measured (cfg2): 3 blocks (170 regs) 56 us vs 64 us at 2 blocks
 #endif
 // VIR = false (NVE steps): no virial accumulation and no stage rows (compiled out)
-template <typename R, int NB, bool VIR>
+template <typename R, int NB, bool VIR, bool SG = false>
 __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_rebo(BondList BL, const int* list_idx,
                                               int* ovf, int* novf, ShortList<R> S, const signed char* typ,
                                               const int* owner, const int* gid, const char4* shift, double* F,
@@ -479,14 +479,14 @@ __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_
     R dVA = -dw * sb + w * sbb;
     R b = bo_value(st);
     V3<R> gd, fi, fj;
-    bo_reverse<R, true, NB>(S, typ, owner, st, VA, w, F, VIR ? e + 3 : nullptr, gd, fi, fj);
+    bo_reverse<R, true, NB, false, SG>(S, typ, owner, st, VA, w, F, VIR ? e + 3 : nullptr, gd, fi, fj);
     R dEdr = dVR + b * dVA + dw * st.Tsum;
     addto(gd, (dEdr * ir) * d);
-    atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
-    atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
+    atomic_add3<SG>(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
+    atomic_add3<SG>(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
     vir_add(VIR ? e + 3 : nullptr, d, gd);
-    e[0] += (double)(VR + b * VA);
-    e[1] += (double)(w * st.Tsum);
+    e[0] = acc_round<SG>(e[0] + (double)(VR + b * VA));
+    e[1] = acc_round<SG>(e[1] + (double)(w * st.Tsum));
     nq += st.nquads;
     nbad += st.bad;
     ncount += 1;
@@ -569,7 +569,7 @@ __device__ PathRes<R> path_search(const ShortList<R>& S, int i, int J) {
 }
 
 // forces of E = f(M) along the maximising path: dE/dM = cM
-template <typename R>
+template <typename R, bool SG = false>
 __device__ __forceinline__ void path_forces(const ShortList<R>& S, const int* owner, const PathRes<R>& pr, R cM, double* F,
                             double W[6]) {
   int at[3] = {pr.a0, pr.a1, pr.a2}, sl[3] = {pr.q0, pr.q1, pr.q2};
@@ -588,7 +588,7 @@ __device__ __forceinline__ void path_forces(const ShortList<R>& S, const int* ow
     V3<R> v = sl_d(S, at[h], sl[h], rr);
     int to = S.nbr[(size_t)at[h] * S.capS + sl[h]];
     V3<R> g = (cM * others * dw[h] / rr) * v;
-    scatter_vec(F, owner, to, at[h], g);
+    scatter_vec<R, SG>(F, owner, to, at[h], g);
     vir_add(W, v, g);
   }
 }
@@ -637,7 +637,7 @@ struct BstarQueue {
 // S_b is in its transition (dS_b != 0: the reverse pass of b* is needed) is deferred to ovf for
 // FULL = true with NB_FAST register sides, a pair with a side larger than NB_FAST to ovf2 for
 // FULL = true with NB = NBMAX.
-template <typename R, int NB, bool FULL, bool VIR>
+template <typename R, int NB, bool FULL, bool VIR, bool SG = false>
 __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBLOCKS : 1) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf, int* ovf2,
                                                int* novf2, const double4* pos, ShortList<R> S, const signed char* typ,
                                                const int* owner, const int* gid, const char4* shift, double* F,
@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
     if (FULL) {
       if (dB != R(0)) {
         V3<R> gs;
-        bo_reverse<R, false, NB>(S, typ, owner, st, C * V * P * dB, R(0), F, VIR ? e + 1 : nullptr, gs, fi, fj);
+        bo_reverse<R, false, NB, false, SG>(S, typ, owner, st, C * V * P * dB, R(0), F, VIR ? e + 1 : nullptr, gs, fi, fj);
         // chain through d* = rho d / |d|: dE/dd = (rho/r) (I - u u^T) dE/dd*
         V3<R> u = ir * d;
         addto(gd, (rho * ir) * (gs - dot3(u, gs) * u));
@@ -707,12 +707,12 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
     }
     if (Md > 0.0) {  // fractional C_ij: dC along the maximising path
       PathRes<R> pr = path_search(S, i, J);
-      path_forces(S, owner, pr, -Q * V, F, VIR ? e + 1 : nullptr);
+      path_forces<R, SG>(S, owner, pr, -Q * V, F, VIR ? e + 1 : nullptr);
     }
-    atomic_add3(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
-    atomic_add3(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
+    atomic_add3<SG>(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
+    atomic_add3<SG>(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
     vir_add(VIR ? e + 1 : nullptr, d, gd);
-    e[0] += (double)E;
+    e[0] = acc_round<SG>(e[0] + (double)E);
     nb += win;
     nbad += win && st.bad;
     if (VIR && stage.rows) {

@@ -119,10 +119,10 @@ __device__ __forceinline__ void stage_lj_row(StageBuf stage, int gi, int gj, cha
   if (rw) rw[0] = gi, rw[1] = gj, rw[2] = sh.x, rw[3] = sh.y, rw[4] = sh.z, rw[5] = C, rw[6] = bs;
 }
 
-template <int W>
+template <int W, bool SG = false>
 __device__ __forceinline__ double group_sum(double v) {
 #pragma unroll
-  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = W / 2; o > 0; o >>= 1) v = acc_round<SG>(v + __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
@@ -146,7 +146,7 @@ __device__ __forceinline__ double reach_lookup_fast(const ReachSmem& s, int key)
   return reach_lookup(s, key);  // long probe chain: rare
 }
 
-template <typename R, bool VIRIAL, bool MORSE>
+template <typename R, bool VIRIAL, bool MORSE, bool SG = false>
 #ifndef AB_NEAR_MINBLOCKS
 #define AB_NEAR_MINBLOCKS 7  // measured: 7 blocks (73 regs) beat 6 (80 regs) and 8 (64 regs, spills)
 #endif
@@ -329,10 +329,10 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       }
       R C = norm ? (R)(1.0 - Md) : R(0);  // 1 - M in fp64 (gate, reading A14)
       R fr = C * dVr;  // F_i += fr d  (E(d), d = x_j - x_i)
-      fx += (double)(fr * (R)dx);
-      fy += (double)(fr * (R)dy);
-      fz += (double)(fr * (R)dz);
-      en += (double)(C * V);
+      fx = acc_round<SG>(fx + (double)(fr * (R)dx));
+      fy = acc_round<SG>(fy + (double)(fr * (R)dy));
+      fz = acc_round<SG>(fz + (double)(fr * (R)dz));
+      en = acc_round<SG>(en + (double)(C * V));
       if (VIRIAL) {
         V3<R> dd = mk3<R>((R)dx, (R)dy, (R)dz);
         vir_add(W, dd, (R(0.5) * fr) * dd);
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       if (norm && canon && Md > 0.0) {  // 0 < C < 1: dC/dx along the maximising path, once per pair
         PathRes<R> pr = path_search(S, i, J);
         double Wp[6] = {0, 0, 0, 0, 0, 0};
-        path_forces(S, owner, pr, -V, F, Wp);
+        path_forces<R, SG>(S, owner, pr, -V, F, Wp);
         if (VIRIAL)
           for (int c = 0; c < 6; ++c) W[c] += Wp[c];
       }
@@ -366,10 +366,10 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   }
 
   // 3. reductions (8-lane groups, then one partial row per block)
-  fx = group_sum<NEAR_GROUP>(fx);
-  fy = group_sum<NEAR_GROUP>(fy);
-  fz = group_sum<NEAR_GROUP>(fz);
-  if (gl == 0 && cntN > 0) atomic_add3(F, i, fx, fy, fz);
+  fx = group_sum<NEAR_GROUP, SG>(fx);
+  fy = group_sum<NEAR_GROUP, SG>(fy);
+  fz = group_sum<NEAR_GROUP, SG>(fz);
+  if (gl == 0 && cntN > 0) atomic_add3<SG>(F, i, fx, fy, fz);
   red_add_d(rs, ACC_ELJ, 0.5 * en);
   if (VIRIAL)
     for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, W[c]);
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 #endif
 constexpr int FAR_UNROLL = AB_FAR_UNROLL;
 
-template <typename R, bool VIRIAL, bool BAND, bool MORSE>
+template <typename R, bool VIRIAL, bool BAND, bool MORSE, bool SG = false>
 __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, double4 pi, int ti, long long ki,
                                          const int* gid, const char4* shift, StageBuf stage, double& fx, double& fy,
                                          double& fz, double& en, double (&W)[6], unsigned& nlj) {
@@ -454,10 +454,10 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
       dVr *= wgt;
       V *= wgt;
       R rx = (R)dx, ry = (R)dy, rz = (R)dz;
-      fx += (double)(dVr * rx);
-      fy += (double)(dVr * ry);
-      fz += (double)(dVr * rz);
-      en += (double)V;
+      fx = acc_round<SG>(fx + (double)(dVr * rx));
+      fy = acc_round<SG>(fy + (double)(dVr * ry));
+      fz = acc_round<SG>(fz + (double)(dVr * rz));
+      en = acc_round<SG>(en + (double)V);
       if (VIRIAL) {
         V3<R> dd = mk3<R>(rx, ry, rz);
         vir_add(W, dd, (R(0.5) * dVr) * dd);
@@ -467,7 +467,7 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
   }
 }
 
-template <typename R, bool VIRIAL, bool MORSE>
+template <typename R, bool VIRIAL, bool MORSE, bool SG = false>
 #ifndef AB_FAR_MINBLOCKS
 #define AB_FAR_MINBLOCKS 4
 #endif
@@ -487,12 +487,12 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     const int ti = type_of(pi);
     const long long ki = key_of(pi);
     double fx = 0, fy = 0, fz = 0;
-    far_list<R, VIRIAL, false, MORSE>(A, 1, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
-    far_list<R, VIRIAL, true, MORSE>(A, 2, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
-    fx = warp_sum(fx);
-    fy = warp_sum(fy);
-    fz = warp_sum(fz);
-    if (lane == 0) atomic_add3(F, i, fx, fy, fz);
+    far_list<R, VIRIAL, false, MORSE, SG>(A, 1, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
+    far_list<R, VIRIAL, true, MORSE, SG>(A, 2, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
+    fx = warp_sum<SG>(fx);
+    fy = warp_sum<SG>(fy);
+    fz = warp_sum<SG>(fz);
+    if (lane == 0) atomic_add3<SG>(F, i, fx, fy, fz);
     if (lane == 0) ne += (unsigned long long)(A.cnt[1][i] + A.cnt[2][i]);
   }
   red_add_d(rs, ACC_ELJ, 0.5 * en);

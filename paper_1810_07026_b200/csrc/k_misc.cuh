@@ -42,6 +42,12 @@ __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, do
   block_max_atomic(d2, maxd2);
 }
 
+// AB_SINGLE: the fp32 force sums of an evaluation widened into the fp64 force array
+__global__ void k_widen(int n, const float* Ff, double* F) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) F[t] = (double)Ff[t];
+}
+
 __global__ void k_integrate2(int N, const double4* pos, double* v, const double* F, double dtf0, double dtf1) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
