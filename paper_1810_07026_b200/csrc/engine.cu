@@ -168,7 +168,8 @@ struct ab_engine {
   DBuf<double> q_M;
   // one small device scratch block, zeroed with a single memset per evaluation:
   //   acc (ACC_N doubles) at 0, ct (CT_N + 1 u64; [CT_N] = max displacement^2) at 128,
-  //   small_i (16 ints: nbonds, qcount, list maxima x4, stage counts x2, overflow counts x2) at 512
+  //   small_i (16 ints: nbonds, qcount, list maxima x4, stage counts x2, overflow counts x2,
+  //   b* queue counts x3 at 13..15) at 512
   DBuf<unsigned char> scratch;
   DBuf<int> small_i;
   DBuf<double> acc;
@@ -1048,7 +1049,7 @@ ab_status enqueue_forces(ab_engine* e) {
     CKL();
     prof_stop(e, 1, s_rebo, t);
   }
-  CK(cudaEventRecord(e->ev_join[0], s_rebo));
+  if (!lj) CK(cudaEventRecord(e->ev_join[0], s_rebo));
   RR.row0 = g_short + g_rebo + g_slow;
   if (lj) {
     cudaEvent_t t = prof_start(e, st);
@@ -1069,19 +1070,30 @@ ab_status enqueue_forces(ab_engine* e) {
     auto bstar = [&](auto fast, auto full, auto big) {
       fast<<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p, e->small_i.p + 1,
                                     e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
+      // the two deferred batches are independent: the NBMAX one (few pairs, long threads) runs
+      // on aux stream 0 (REBO is done or finishing there) beside the NB_FAST reverse-pass batch
+      RedRows Rb = RR;
+      Rb.row0 += 2 * g_bstar;
+      if (!serial) {
+        CK(cudaEventRecord(e->ev_fork[0], st));
+        CK(cudaStreamWaitEvent(s_rebo, e->ev_fork[0], 0));
+      }
+      big<<<g_slow, 128, 0, s_rebo>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr, e->pos.p, S,
+                                      e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, Rb);
       RR.row0 += g_bstar;
       full<<<g_bstar, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, nullptr, nullptr, e->pos.p, S,
                                     e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
-      RR.row0 += g_bstar;
-      big<<<g_slow, 128, 0, st>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr, e->pos.p, S,
-                                  e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
+      return AB_OK;
     };
     if (e->want_virial)
-      bstar(k_bstar<R, NB_FAST, false, true, SG>, k_bstar<R, NB_FAST, true, true, SG>, k_bstar<R, NBMAX, true, true, SG>);
+      TRY(bstar(k_bstar<R, NB_FAST, false, true, SG>, k_bstar<R, NB_FAST, true, true, SG>,
+                k_bstar<R, NBMAX, true, true, SG>));
     else
-      bstar(k_bstar<R, NB_FAST, false, false, SG>, k_bstar<R, NB_FAST, true, false, SG>, k_bstar<R, NBMAX, true, false, SG>);
+      TRY(bstar(k_bstar<R, NB_FAST, false, false, SG>, k_bstar<R, NB_FAST, true, false, SG>,
+                k_bstar<R, NBMAX, true, false, SG>));
     e->launches += 2;  // + the CKL below: three launches
     CKL();
+    CK(cudaEventRecord(e->ev_join[0], s_rebo));
     prof_stop(e, 3, st, t);
   }
   CK(cudaStreamWaitEvent(st, e->ev_join[0], 0));

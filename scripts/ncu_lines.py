@@ -4,7 +4,9 @@ import subprocess
 import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
-out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'cuda,sass', '-k', 'regex:' + kern],
+# optional 5th argument: launch index among the matching kernels (--launch-skip N --launch-count 1)
+extra = ['--launch-skip', sys.argv[5], '--launch-count', '1'] if len(sys.argv) > 5 else []
+out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'cuda,sass', '-k', 'regex:' + kern] + extra,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 agg = {}
