@@ -354,7 +354,8 @@ def run_ours(args, ws, rank, local):
             "metric": METRIC, "value": value, "unit": "atom-steps/s", "n_gpus": ws, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if (ws > 1 and args.scaling == "strong") else "weak",
-            "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32+f64acc",
+            "vs_baseline": None,
+            "dtype": {"fp64": "f64", "mixed": "f32+f64acc", "single": "f32"}[args.precision],
             "data": "synthetic (seeded generator, paper_1810_07026_b200/inputs.py)",
             "config": {"workload": s.name + (" (BASELINE configs[1]: PE 12x16x14 cells, 32,256 atoms, 300 K, "
                                              "dt 0.5 fs, NVE, LJ cutoff 3 sigma, torsion on)" if ws == 1 else
@@ -427,7 +428,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed", "single"])
     ap.add_argument("--config", default=2, type=lambda v: int(v) if v.isdigit() else v)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--potential", default="airebo", choices=["airebo", "rebo", "airebo-m"])
