@@ -165,14 +165,18 @@ def run_ours(args, ws, rank, local):
 
     if rank == 0:
         B.build()
-    uid = None
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+
+    def fresh_uid():
+        """A new NCCL unique id for each distributed engine (an id is single-use: NCCL's bootstrap
+        root serves one communicator); collective over the ranks."""
+        import torch.distributed as dist
         obj = [E.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-        dist.barrier()
+        return obj[0]
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     s = workload(args.config, ws, args.scaling)
@@ -194,7 +198,7 @@ def run_ours(args, ws, rank, local):
         params = params.replace(b"potential airebo\n", b"potential " + args.potential.encode() + b"\n")
 
     def make_engine(precision):
-        ranks = ("nccl", rank, ws, uid) if ws > 1 else None
+        ranks = ("nccl", rank, ws, fresh_uid()) if ws > 1 else None
         e = E.Engine(precision, local, params=params, ranks=ranks)
         e.set_box(s.box)
         e.set_atoms(s.types, s.x)

@@ -97,7 +97,8 @@ ab_status ab_create(const char* param_text, size_t len, ab_precision prec, int c
  * energies, virial and counters are sums over all ranks.
  *
  * ab_create_dist: one process per GPU.  All ranks call it collectively with the same 128-byte
- * NCCL unique id (from ab_nccl_unique_id on one rank, broadcast by the caller).  The halo and
+ * NCCL unique id (from ab_nccl_unique_id on one rank, broadcast by the caller); an id is
+ * single-use (NCCL's bootstrap root serves one communicator), so each engine needs a fresh one.  The halo and
  * force exchanges are ncclSend / ncclRecv between slab neighbours on the engine's stream, the
  * rebuild decision and results are NCCL all-reduces; libnccl.so.2 is loaded at run time.
  * Every call on a distributed engine is collective (all ranks, same order).  ab_get_list

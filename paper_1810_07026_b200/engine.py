@@ -123,7 +123,7 @@ class Engine:
 
     ranks=None: one GPU, whole box.  ranks=("virtual", n): n slab domains on this GPU exchanging
     their halo by device copies.  ranks=("nccl", rank, n, uid): slab `rank` of an n-process job
-    (collective calls; uid from nccl_unique_id() on one rank)."""
+    (collective calls; uid from nccl_unique_id() on one rank, a fresh one per engine: single-use)."""
 
     def __init__(self, precision: str = "fp64", device: int = 0, params: bytes | None = None, ranks=None):
         self.L = load()

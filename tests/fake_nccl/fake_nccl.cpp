@@ -38,6 +38,7 @@ struct World {
   std::mutex mu;
   std::condition_variable cv;
   std::map<std::pair<int, int>, std::deque<std::shared_ptr<Msg>>> box;  // (src, dst) FIFO
+  int inits = 0;  // ncclCommInitRank calls on this id: an id is single-use, as NCCL's
   // all-reduce rendezvous
   int arrived = 0, generation = 0;
   std::vector<std::vector<unsigned char>> data;
@@ -150,6 +151,7 @@ ncclResult_t ncclCommInitRank(ncclComm_t* comm, int nranks, ncclUniqueId id, int
       slot->n = nranks;
       slot->data.resize(nranks);
     }
+    if (++slot->inits > nranks) return ncclInvalidUsage;  // a reused unique id
     w = slot;
   }
   *comm = reinterpret_cast<ncclComm_t>(new Comm{w, rank});
