@@ -147,6 +147,7 @@ struct ab_engine {
   Grid grid{};
   int ncell = 0, nrLJ = 1, nrI = 1;
   int capI = 0, capS = 0, capQ = 0;
+  int far_at = 0;  // enqueue_forces: fork point of the far-LJ kernel (AB_FAR_AT)
   int qcap[3] = {0, 0, 0}, qoff[3] = {0, 0, 0};  // b* candidate queue regions (build-time bounds)
   long long launches = 0, rebuilds = 0, steps = 0, retries = 0;
   // device state
@@ -999,10 +1000,6 @@ ab_status enqueue_forces(ab_engine* e) {
   const bool lj = e->hp.potential != kREBO, morse = e->hp.potential == kAIREBOM;
   const int nrows_used = lj ? nrows : g_short + g_rebo + g_slow;  // REBO: short + bond kernels only
   const cudaStream_t s_rebo = serial ? st : e->aux[0], s_far = serial ? st : e->aux[1];
-  if (lj) {
-    CK(cudaEventRecord(e->ev_fork[1], st));
-    CK(cudaStreamWaitEvent(s_far, e->ev_fork[1], 0));
-  }
   const int row_far = g_short + g_rebo + g_slow + g_near;
   BstarQueue Qu;
   Qu.item = e->q_item.p, Qu.M = e->q_M.p, Qu.count = e->small_i.p + 13;
@@ -1012,7 +1009,12 @@ ab_status enqueue_forces(ab_engine* e) {
   A.N = N;
   A.pos = e->pos.p;
   for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
-  if (lj) {
+  // the far kernel forks from the engine stream at e->far_at: 0 = at once, 1 = after the short
+  // list, 2 = after the near kernel (it then fills the GPU beside the b* batch)
+  auto launch_far = [&]() -> ab_status {
+    if (!lj) return AB_OK;
+    CK(cudaEventRecord(e->ev_fork[1], st));
+    CK(cudaStreamWaitEvent(s_far, e->ev_fork[1], 0));
     cudaEvent_t t = prof_start(e, s_far);
     RedRows R6 = RR;
     R6.row0 = row_far;
@@ -1022,7 +1024,9 @@ ab_status enqueue_forces(ab_engine* e) {
     CKL();
     prof_stop(e, 6, s_far, t);
     CK(cudaEventRecord(e->ev_join[1], s_far));
-  }
+    return AB_OK;
+  };
+  if (e->far_at == 0) TRY(launch_far());
   {
     cudaEvent_t t = prof_start(e, st);
     k_short<R><<<g_short, 128, 0, st>>>(N, NT, e->pos.p, e->in_cnt.p, e->in_nbr.p, e->capI, S, e->gid.p,
@@ -1030,6 +1034,7 @@ ab_status enqueue_forces(ab_engine* e) {
     CKL();
     prof_stop(e, 0, st, t);
   }
+  if (e->far_at == 1) TRY(launch_far());
   CK(cudaEventRecord(e->ev_fork[0], st));
   CK(cudaStreamWaitEvent(s_rebo, e->ev_fork[0], 0));
   {
@@ -1062,6 +1067,7 @@ ab_status enqueue_forces(ab_engine* e) {
     CKL();
     prof_stop(e, 2, st, t);
   }
+  if (e->far_at == 2) TRY(launch_far());
   RR.row0 = row_far + g_far;
   if (lj) {
     cudaEvent_t t = prof_start(e, st);
@@ -1315,6 +1321,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   }
   e->st = e->own;
   e->serial = std::getenv("AB_SERIAL_KERNELS") && std::getenv("AB_SERIAL_KERNELS")[0] == '1';
+  if (const char* fa = std::getenv("AB_FAR_AT")) e->far_at = std::max(0, std::min(2, std::atoi(fa)));
   for (int c = 0; c < 2; ++c)
     if (cudaStreamCreateWithFlags(&e->aux[c], cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_fork[c], cudaEventDisableTiming) != cudaSuccess ||
