@@ -38,6 +38,16 @@ constexpr int NEAR_SLOTS = AB_NEAR_SLOTS;        // reach table slots per atom (
 #ifndef AB_NEAR_BLOOM
 #define AB_NEAR_BLOOM 16 // 32-bit words of the per-atom Bloom filter in front of the table (0: none)
 #endif
+#ifndef AB_NEAR_BLOCKQ
+#define AB_NEAR_BLOCKQ 1
+#endif
+constexpr int NEAR_BQ = 64;  // per species pair and block (16 atoms); beyond: direct global appends
+struct NearBlockQ {
+  int n[3], base[3];
+  int i[3][NEAR_BQ], j[3][NEAR_BQ];
+  double m[3][NEAR_BQ];
+};
+
 struct ReachSmem {
   int keys[NEAR_SLOTS];
   unsigned long long mbits[NEAR_SLOTS];
@@ -156,6 +166,10 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
                                                                     BstarQueue Qu, StageBuf stage, RedRows RR) {
   __shared__ ReachSmem sm_all[NEAR_ATOMS];
   __shared__ RedSmem rs;
+#if AB_NEAR_BLOCKQ
+  __shared__ NearBlockQ bq;
+  if (threadIdx.x < 3) bq.n[threadIdx.x] = 0;
+#endif
   // per-pair parameters indexed by the species pair p, which differs between the lanes of a
   // warp: shared-memory copies (an indexed __constant__ load serialises per distinct address)
   __shared__ double pd[9];  // r_c^2, S_r window pre-filter, r_lo^2
@@ -339,6 +353,22 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       }
       // rare work last
       if (cand && canon) {  // deferred to the b* batch: the whole pair, once, by the canonical side
+#if AB_NEAR_BLOCKQ
+        // staged in the block's shared-memory queue, flushed with one global atomic per species
+        // pair and block (global counters hit by every warp serialised in L2)
+        const int k = atomicAdd(&bq.n[p], 1);
+        if (k < NEAR_BQ) {
+          bq.i[p][k] = i, bq.j[p][k] = J, bq.m[p][k] = Md;
+        } else {
+          const int g = atomicAdd(Qu.count + p, 1);
+          if (g < Qu.cap[p]) {
+            Qu.item[Qu.off[p] + g] = make_int4(i, J, 0, 0);
+            Qu.M[Qu.off[p] + g] = Md;
+          } else {
+            atomicAdd(ct + CT_OVF_QUEUE, 1ull);
+          }
+        }
+#else
         unsigned am = __activemask();
         unsigned grp = __match_any_sync(am, p);  // one aggregated append per species pair
         int lane = threadIdx.x & 31, leader = __ffs(grp) - 1;
@@ -352,6 +382,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
         } else {
           atomicAdd(ct + CT_OVF_QUEUE, 1ull);
         }
+#endif
       }
       if (norm && canon && Md > 0.0) {  // 0 < C < 1: dC/dx along the maximising path, once per pair
         PathRes<R> pr = path_search(S, i, J);
@@ -370,6 +401,28 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   fy = group_sum<NEAR_GROUP, SG>(fy);
   fz = group_sum<NEAR_GROUP, SG>(fz);
   if (gl == 0 && cntN > 0) atomic_add3<SG>(F, i, fx, fy, fz);
+#if AB_NEAR_BLOCKQ
+  // flush the block's b* candidates: one global atomic per species pair
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int n = min(bq.n[threadIdx.x], NEAR_BQ);
+    bq.base[threadIdx.x] = n ? atomicAdd(Qu.count + threadIdx.x, n) : 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int pp = 0; pp < 3; ++pp) {
+    const int n = min(bq.n[pp], NEAR_BQ);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int g = bq.base[pp] + k;
+      if (g < Qu.cap[pp]) {
+        Qu.item[Qu.off[pp] + g] = make_int4(bq.i[pp][k], bq.j[pp][k], 0, 0);
+        Qu.M[Qu.off[pp] + g] = bq.m[pp][k];
+      } else {
+        atomicAdd(ct + CT_OVF_QUEUE, 1ull);
+      }
+    }
+  }
+#endif
   red_add_d(rs, ACC_ELJ, 0.5 * en);
   if (VIRIAL)
     for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, W[c]);
