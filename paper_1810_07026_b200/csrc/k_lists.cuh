@@ -306,10 +306,13 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
                         ShortList<R> S, const int* gid, const char4* shift, BondList BL, unsigned long long* ct,
                         RedRows RR) {
   __shared__ RedSmem rs;
+  __shared__ int s_bn[3], s_bb[3];  // block bond counts / global bases per species pair
+  if (threadIdx.x < 3) s_bn[threadIdx.x] = 0;
   red_init(rs);
   int a = blockIdx.x * blockDim.x + threadIdx.x;
   bool live = a < NT;
   int nloc = 0, nbond[3] = {0, 0, 0};
+  unsigned cmask = 0, hmask = 0;  // canonical entries / H partners by slot (capS <= NBMAX = 16)
   if (live) {
     const Tab<R>& T = tab<R>();
     double4 p = pos[a];
@@ -319,9 +322,19 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
     R nc = 0, nh = 0;
     int ci = in_cnt[a];
     size_t base = (size_t)a * S.capS;
+    const int* row = in_nbr + (size_t)a * capI;
+    // the next candidate's index and position are loaded while the current one is processed
+    int bn = ci > 0 ? row[0] : a;
+    double4 pbn = pos[bn];
+    int bnn = ci > 1 ? row[1] : a;
     for (int q = 0; q < ci; ++q) {
-      int b = in_nbr[(size_t)a * capI + q];
-      double4 pb = pos[b];
+      const int b = bn;
+      const double4 pb = pbn;
+      if (q + 1 < ci) {
+        bn = bnn;
+        pbn = pos[bn];
+        if (q + 2 < ci) bnn = row[q + 2];
+      }
       double dx = __dsub_rn(pb.x, p.x), dy = __dsub_rn(pb.y, p.y), dz = __dsub_rn(pb.z, p.z);
       double r2 = r2_exact(dx, dy, dz);
       int tb = type_of(pb);
@@ -338,7 +351,8 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
           S.w[base + n] = {w, dw};
           if (tb == 0) nc += w;
           else nh += w;
-          if (a < N && ka < key_of(pb)) ++nbond[pr];
+          if (a < N && ka < key_of(pb)) ++nbond[pr], cmask |= 1u << n;
+          if (tb != 0) hmask |= 1u << n;
         }
         ++n;
       }
@@ -351,8 +365,8 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
     S.Ntot[a] = nc + nh;
     if (a < N) nloc = n;
   }
-  // bond list compaction per species pair (warp-aggregated atomics; order within a region is
-  // irrelevant to the physics)
+  // bond list compaction per species pair: warp scan, one shared atomic per warp, one global
+  // atomic per block (order within a region is irrelevant to the physics)
   unsigned lane = threadIdx.x & 31;
   int w[3];
 #pragma unroll
@@ -365,22 +379,20 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
     }
     int total = __shfl_sync(0xffffffffu, incl, 31);
     int basew = 0;
-    if (lane == 31 && total) basew = atomicAdd(BL.cnt + t, total);
+    if (lane == 31 && total) basew = atomicAdd(&s_bn[t], total);
     basew = __shfl_sync(0xffffffffu, basew, 31);
     w[t] = basew + incl - nbond[t];
   }
-  if (live && a < N && (nbond[0] | nbond[1] | nbond[2])) {
-    size_t base = (size_t)a * S.capS;
-    int n = S.cnt[a];
-    const long long ka = key_of(pos[a]);
+  __syncthreads();
+  if (threadIdx.x < 3) s_bb[threadIdx.x] = s_bn[threadIdx.x] ? atomicAdd(BL.cnt + threadIdx.x, s_bn[threadIdx.x]) : 0;
+  __syncthreads();
+  if (cmask) {
     const int ta = type_of(pos[a]);
-    for (int q = 0; q < n; ++q) {
-      int b = S.nbr[base + q];
-      const double4 pb = pos[b];
-      if (ka < key_of(pb)) {
-        int t = ta + type_of(pb);
-        BL.b[(size_t)t * BL.cap + w[t]++] = make_int2(a, q);
-      }
+    for (int t = 0; t < 3; ++t) w[t] += s_bb[t];
+    for (unsigned m = cmask; m; m &= m - 1) {
+      const int q = __ffs(m) - 1;
+      const int t = ta + ((hmask >> q) & 1u);
+      BL.b[(size_t)t * BL.cap + w[t]++] = make_int2(a, q);
     }
   }
   red_add_u(rs, CT_SHORT, (unsigned long long)nloc);
