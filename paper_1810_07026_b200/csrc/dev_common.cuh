@@ -484,10 +484,10 @@ __device__ __forceinline__ void red_flush(const RedSmem& s, RedRows R) {
   for (int c = threadIdx.x; c < CT_N; c += blockDim.x) R.u[(size_t)c * R.stride + row] = s.u[c];
 }
 // one block per column: fixed-order sum (max for the max counters) over nrows partial rows
-__global__ void k_reduce(RedRows R, int nrows, double* acc, unsigned long long* ct) {
+__device__ __forceinline__ void reduce_column(const RedRows& R, int nrows, double* acc, unsigned long long* ct,
+                                              int c) {
   __shared__ double sd[32];
   __shared__ unsigned long long su[32];
-  int c = blockIdx.x;
   bool isd = c < ACC_N;
   int cc = isd ? c : c - ACC_N;
   bool mx = !isd && ct_is_max(cc);
@@ -517,6 +517,9 @@ __global__ void k_reduce(RedRows R, int nrows, double* acc, unsigned long long* 
     if (isd) acc[cc] += vd;  // acc may already hold direct contributions (KE)
     else ct[cc] = mx ? max(ct[cc], vu) : ct[cc] + vu;
   }
+}
+__global__ void k_reduce(RedRows R, int nrows, double* acc, unsigned long long* ct) {
+  reduce_column(R, nrows, acc, ct, blockIdx.x);
 }
 
 // warp-reduce an array of doubles and add lane 0's totals into global accumulators.

@@ -148,6 +148,10 @@ struct ab_engine {
   int ncell = 0, nrLJ = 1, nrI = 1;
   int capI = 0, capS = 0, capQ = 0;
   int far_at = 0;  // enqueue_forces: fork point of the far-LJ kernel (AB_FAR_AT)
+  // NVE steps: the reduction of the partial rows is fused into the second half-kick (k_post)
+  bool defer_reduce = false, post_pending = false;
+  RedRows post_rr{};
+  int post_rows = 0;
   int qcap[3] = {0, 0, 0}, qoff[3] = {0, 0, 0};  // b* candidate queue regions (build-time bounds)
   long long launches = 0, rebuilds = 0, steps = 0, retries = 0;
   // device state
@@ -189,11 +193,18 @@ struct ab_engine {
   unsigned long long last_ct[CT_N] = {0};
   // per-phase CUDA-event profiling (ab_set_profiling)
   bool prof = false;
+  // AB_TIMELINE=1 (with profiling on): per-phase start / end offsets from the start of each
+  // evaluation, averaged and printed at close (the concurrent DAG's timeline)
+  bool timeline = false;
+  cudaEvent_t tl_ref = nullptr;      // start of the current evaluation
+  std::vector<cudaEvent_t> tl_refs;  // the pending evaluations' start events (back to the pool)
+  double tl_sum[8][2] = {};
+  long long tl_n[8] = {};
   double phase_ms[AB_NPHASE] = {0};
   long long phase_n[AB_NPHASE] = {0};
   struct Pend {
     int phase;
-    cudaEvent_t a, b;
+    cudaEvent_t a, b, ref;  // ref: the evaluation's start (AB_TIMELINE), not owned
   };
   std::vector<Pend> pending;
   std::vector<cudaEvent_t> pool;
@@ -264,7 +275,7 @@ void prof_stop(ab_engine* e, int phase, cudaStream_t s, cudaEvent_t a) {
   if (!a) return;
   cudaEvent_t b = ev_get(e);
   cudaEventRecord(b, s);
-  e->pending.push_back({phase, a, b});
+  e->pending.push_back({phase, a, b, e->tl_ref});
 }
 void prof_begin(ab_engine* e, int phase) {
   e->open_phase = phase;
@@ -282,9 +293,16 @@ void prof_collect(ab_engine* e) {
       e->phase_ms[p.phase] += ms;
       e->phase_n[p.phase] += 1;
     }
+    float t0 = 0, t1 = 0;
+    if (e->timeline && p.ref && cudaEventElapsedTime(&t0, p.ref, p.a) == cudaSuccess &&
+        cudaEventElapsedTime(&t1, p.ref, p.b) == cudaSuccess && t0 >= 0) {
+      e->tl_sum[p.phase][0] += t0, e->tl_sum[p.phase][1] += t1, e->tl_n[p.phase] += 1;
+    }
     e->pool.push_back(p.a);
     e->pool.push_back(p.b);
   }
+  for (cudaEvent_t r : e->tl_refs) e->pool.push_back(r);
+  e->tl_refs.clear();
   e->pending.clear();
 }
 
@@ -974,6 +992,11 @@ ab_status enqueue_forces(ab_engine* e) {
   }
   CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * e->NX, st));
   // AB_SINGLE: the kernels sum forces into an fp32 array (atomic_add3), widened into F below
+  if (e->prof && e->timeline) {
+    e->tl_ref = ev_get(e);
+    e->tl_refs.push_back(e->tl_ref);
+    CK(cudaEventRecord(e->tl_ref, st));
+  }
   if (SG) {
     CK(e->Ff.ensure(3 * (size_t)e->NX + 3));
     CK(cudaMemsetAsync(e->Ff.p, 0, sizeof(float) * 3 * e->NX, st));
@@ -1105,8 +1128,12 @@ ab_status enqueue_forces(ab_engine* e) {
   CK(cudaStreamWaitEvent(st, e->ev_join[0], 0));
   if (lj) CK(cudaStreamWaitEvent(st, e->ev_join[1], 0));
   RR.row0 = 0;
-  k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows_used, e->acc.p, e->ct.p);
-  CKL();
+  if (e->defer_reduce) {  // NVE step: reduced by k_post together with the second half-kick
+    e->post_rr = RR, e->post_rows = nrows_used, e->post_pending = true;
+  } else {
+    k_reduce<<<ACC_N + CT_N, 256, 0, st>>>(RR, nrows_used, e->acc.p, e->ct.p);
+    CKL();
+  }
   if (SG) {
     k_widen<<<nblk(3LL * e->NX, 256), 256, 0, st>>>(3 * e->NX, e->Ff.p, e->F.p);
     CKL();
@@ -1321,6 +1348,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   }
   e->st = e->own;
   e->serial = std::getenv("AB_SERIAL_KERNELS") && std::getenv("AB_SERIAL_KERNELS")[0] == '1';
+  e->timeline = std::getenv("AB_TIMELINE") && std::getenv("AB_TIMELINE")[0] == '1';
   if (const char* fa = std::getenv("AB_FAR_AT")) e->far_at = std::max(0, std::min(2, std::atoi(fa)));
   for (int c = 0; c < 2; ++c)
     if (cudaStreamCreateWithFlags(&e->aux[c], cudaStreamNonBlocking) != cudaSuccess ||
@@ -1387,6 +1415,13 @@ void free_engine(ab_engine* e) {
                  "wait %.4f, rebuild path %.4f, integrate2 %.4f\n",
                  e->host_steps, e->host_ms[0] / e->host_steps, e->host_ms[1] / e->host_steps,
                  e->host_ms[2] / e->host_steps, e->host_ms[3] / e->host_steps, e->host_ms[4] / e->host_steps);
+  if (e->timeline) {
+    const char* nm[8] = {"short", "rebo", "near", "bstar", "integ", "rebuild", "far", "comm"};
+    for (int q = 0; q < 8; ++q)
+      if (e->tl_n[q])
+        std::fprintf(stderr, "[airebo_b200] timeline %-6s start %8.1f us  end %8.1f us  (n %lld)\n", nm[q],
+                     1e3 * e->tl_sum[q][0] / e->tl_n[q], 1e3 * e->tl_sum[q][1] / e->tl_n[q], e->tl_n[q]);
+  }
   if (e->rb_n && std::getenv("AB_HOST_TIMING"))
     std::fprintf(stderr, "[airebo_b200] host ms/rebuild over %lld: sort %.3f, image count+sync %.3f, fill+bin %.3f, lists %.3f (retries %lld)\n",
                  e->rb_n, e->rb_ms[0] / e->rb_n, e->rb_ms[1] / e->rb_n, e->rb_ms[2] / e->rb_n, e->rb_ms[3] / e->rb_n,
@@ -1868,6 +1903,7 @@ static ab_status step_forces(ab_engine* e) {
     e->graph_epoch = e->layout;
   }
   CK(cudaGraphLaunch(e->gexec, e->st));
+  if (e->defer_reduce) e->post_pending = true;  // the captured evaluation left its rows (post_rr)
   e->launches += e->graph_launches;
   e->forces_valid = true;
   e->host_stale = true;
@@ -1938,6 +1974,14 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
   // of step s is read at step s+1.  Slab domains: the displacement and overflow flags are
   // max-reduced over all ranks first, so every rank takes the same rebuild decision.
   if (!e->ev_disp) CK(cudaEventCreateWithFlags(&e->ev_disp, cudaEventDisableTiming));
+  // the step's evaluations leave their partial rows to k_post (reduction + second half-kick)
+  struct DeferGuard {
+    std::vector<ab_engine*> ds;
+    ~DeferGuard() {
+      for (ab_engine* d : ds) d->defer_reduce = false, d->post_pending = false;
+    }
+  } defer_guard{D};
+  for (ab_engine* d : D) d->defer_reduce = true;
   using clk = std::chrono::steady_clock;
   auto ms_since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
   for (int64_t s = 1; s <= nsteps; ++s) {
@@ -1988,7 +2032,13 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     t0 = clk::now();
     prof_begin(e, 4);
     for (ab_engine* d : D) {
-      k_integrate2<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
+      if (d->post_pending) {
+        k_post<<<ACC_N + CT_N + nblk(d->N, 256), 256, 0, st>>>(d->post_rr, d->post_rows, d->acc.p, d->ct.p, d->N,
+                                                               d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
+        d->post_pending = false;
+      } else {
+        k_integrate2<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
+      }
       CKL();
     }
     prof_end(e);

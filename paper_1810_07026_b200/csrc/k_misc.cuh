@@ -57,6 +57,22 @@ __global__ void k_integrate2(int N, const double4* pos, double* v, const double*
   v[3 * i + 2] += dtf * F[3 * i + 2];
 }
 
+// NVE second half-kick fused with the reduction of the evaluation's partial rows (the two are
+// independent): blocks [0, ACC_N + CT_N) reduce one column each, the rest kick 256 atoms each
+__global__ void k_post(RedRows R, int nrows, double* acc, unsigned long long* ct, int N, const double4* pos, double* v,
+                       const double* F, double dtf0, double dtf1) {
+  if (blockIdx.x < ACC_N + CT_N) {
+    reduce_column(R, nrows, acc, ct, blockIdx.x);
+    return;
+  }
+  int i = (blockIdx.x - (ACC_N + CT_N)) * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  double dtf = (type_of(pos[i]) == 0) ? dtf0 : dtf1;
+  v[3 * i + 0] += dtf * F[3 * i + 0];
+  v[3 * i + 1] += dtf * F[3 * i + 1];
+  v[3 * i + 2] += dtf * F[3 * i + 2];
+}
+
 __global__ void k_maxdisp(int N, const double4* pos, const double4* xref, unsigned long long* maxd2) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
