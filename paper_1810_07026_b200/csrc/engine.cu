@@ -150,6 +150,8 @@ struct ab_engine {
   int far_at = 0;  // enqueue_forces: fork point of the far-LJ kernel (AB_FAR_AT)
   // NVE steps: the reduction of the partial rows is fused into the second half-kick (k_post)
   bool defer_reduce = false, post_pending = false;
+  // set by k_integrate1_img (whole-box NVE): the image ghosts are current and F is zero
+  bool ghosts_fresh = false, f_zeroed = false;
   RedRows post_rr{};
   int post_rows = 0;
   int qcap[3] = {0, 0, 0}, qoff[3] = {0, 0, 0};  // b* candidate queue regions (build-time bounds)
@@ -920,6 +922,7 @@ ab_status halo_finish(ab_engine* e) {
 ab_status rebuild_all(ab_engine* e) {
   prof_begin(e, 5);
   auto D = doms(e);
+  for (ab_engine* d : D) d->ghosts_fresh = false;  // the rebuild regenerates the images
   if (!slabbed(e)) {
     auto t0 = std::chrono::steady_clock::now();
     setup_grid(e);
@@ -964,7 +967,9 @@ ab_status refresh_ghosts_all(ab_engine* e) {
     for (ab_engine* d : D) TRYD(d, halo_unpack(d));
   }
   for (ab_engine* d : D)
-    if (d->NT > d->NX) {
+    if (d->ghosts_fresh) {
+      d->ghosts_fresh = false;
+    } else if (d->NT > d->NX) {
       k_image_update<<<nblk(d->NT - d->NX, 256), 256, 0, d->st>>>(d->NX, d->NT, d->pos.p, d->owner.p, d->rshift.p);
       ++d->launches;
       cudaError_t ce = cudaGetLastError();
@@ -990,7 +995,8 @@ ab_status enqueue_forces(ab_engine* e) {
     sb0 = StageBuf{e->stage0.p, e->small_i.p + 6, (int)n0};
     sb1 = StageBuf{e->stage1.p, e->small_i.p + 7, (int)n1};
   }
-  CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * e->NX, st));
+  if (e->f_zeroed) e->f_zeroed = false;  // zeroed by k_integrate1_img
+  else CK(cudaMemsetAsync(e->F.p, 0, sizeof(double) * 3 * e->NX, st));
   // AB_SINGLE: the kernels sum forces into an fp32 array (atomic_add3), widened into F below
   if (e->prof && e->timeline) {
     e->tl_ref = ev_get(e);
@@ -1978,10 +1984,13 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
   struct DeferGuard {
     std::vector<ab_engine*> ds;
     ~DeferGuard() {
-      for (ab_engine* d : ds) d->defer_reduce = false, d->post_pending = false;
+      for (ab_engine* d : ds) d->defer_reduce = false, d->post_pending = false, d->ghosts_fresh = d->f_zeroed = false;
     }
   } defer_guard{D};
   for (ab_engine* d : D) d->defer_reduce = true;
+  // whole-box engines refresh their image ghosts and zero F inside the drift kernel (not with
+  // slab domains, whose x-ghosts arrive by exchange after the drift, nor under CUDA graphs)
+  const bool fuse_img = !slabbed(e) && e->subs.empty() && !(std::getenv("AB_GRAPH") && std::getenv("AB_GRAPH")[0] == '1');
   using clk = std::chrono::steady_clock;
   auto ms_since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
   for (int64_t s = 1; s <= nsteps; ++s) {
@@ -1990,8 +1999,15 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     prof_begin(e, 4);
     for (ab_engine* d : D) {
       CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), st));
-      k_integrate1<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt, d->xref.p,
-                                                    d->ct.p + CT_N);
+      if (fuse_img && d->lists_valid && d->NX == d->N) {
+        k_integrate1_img<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt,
+                                                          d->xref.p, d->ct.p + CT_N, d->NX, d->goff.p, d->gcnt.p,
+                                                          d->rshift.p);
+        d->ghosts_fresh = d->f_zeroed = true;
+      } else {
+        k_integrate1<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt, d->xref.p,
+                                                      d->ct.p + CT_N);
+      }
       CKL();
     }
     prof_end(e);

@@ -42,6 +42,40 @@ __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, do
   block_max_atomic(d2, maxd2);
 }
 
+// Whole-box NVE: k_integrate1 + the image-ghost refresh (k_image_update) + the zeroing of F
+// for the next evaluation in one pass.  Atom i writes its own periodic images, which the last
+// rebuild laid out contiguously at NB + goff[i] (k_image_fill), with k_image_update's operations.
+__global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, double dtf0, double dtf1, double dt,
+                                 const double4* xref, unsigned long long* maxd2, int NB, const int* goff,
+                                 const int* gcnt, const char4* rshift) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double d2 = 0.0;
+  if (i < N) {
+    double4 p = pos[i];
+    double dtf = (type_of(p) == 0) ? dtf0 : dtf1;
+    double vx = v[3 * i + 0] + dtf * F[3 * i + 0];
+    double vy = v[3 * i + 1] + dtf * F[3 * i + 1];
+    double vz = v[3 * i + 2] + dtf * F[3 * i + 2];
+    F[3 * i + 0] = 0.0, F[3 * i + 1] = 0.0, F[3 * i + 2] = 0.0;
+    v[3 * i + 0] = vx, v[3 * i + 1] = vy, v[3 * i + 2] = vz;
+    p.x += dt * vx, p.y += dt * vy, p.z += dt * vz;
+    pos[i] = p;
+    double4 r = xref[i];
+    double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
+    d2 = dx * dx + dy * dy + dz * dz;
+    const int g0 = NB + goff[i], ng = gcnt[i];
+    for (int k = 0; k < ng; ++k) {
+      const int g = g0 + k;
+      const char4 s = rshift[g];
+      const long long key = key_of(p) + ((long long)s.x << 18) + ((long long)s.y << 10) + ((long long)s.z << 2);
+      pos[g] = make_double4(__dadd_rn(p.x, __dmul_rn((double)s.x, c_geo.L[0])),
+                            __dadd_rn(p.y, __dmul_rn((double)s.y, c_geo.L[1])),
+                            __dadd_rn(p.z, __dmul_rn((double)s.z, c_geo.L[2])), __longlong_as_double(key));
+    }
+  }
+  block_max_atomic(d2, maxd2);
+}
+
 // AB_SINGLE: the fp32 force sums of an evaluation widened into the fp64 force array
 __global__ void k_widen(int n, const float* Ff, double* F) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
