@@ -71,6 +71,7 @@ struct DBuf {
 inline int nblk(long long n, int t) { return (int)std::max<long long>(1, (n + t - 1) / t); }
 
 constexpr size_t SCRATCH_BYTES = 1024, SCRATCH_CT = 128, SCRATCH_SMALL = 512, SCRATCH_ZERO_BYTES = 512 + 64;
+constexpr size_t SCRATCH_TICKET = 1016;  // k_integrate1_img's last-block ticket (never memset after init)
 
 // ---- NCCL, resolved at run time (only the distributed mode needs it)
 struct NcclApi {
@@ -151,7 +152,7 @@ struct ab_engine {
   // NVE steps: the reduction of the partial rows is fused into the second half-kick (k_post)
   bool defer_reduce = false, post_pending = false;
   // set by k_integrate1_img (whole-box NVE): the image ghosts are current and F is zero
-  bool ghosts_fresh = false, f_zeroed = false;
+  bool ghosts_fresh = false, f_zeroed = false, scratch_zeroed = false;
   RedRows post_rr{};
   int post_rows = 0;
   int qcap[3] = {0, 0, 0}, qoff[3] = {0, 0, 0};  // b* candidate queue regions (build-time bounds)
@@ -188,6 +189,7 @@ struct ab_engine {
   DBuf<unsigned char> cub_tmp;
   // pinned host mirror for small readbacks
   unsigned long long* h_ct = nullptr;
+  unsigned long long* h_ct_dev = nullptr;  // h_ct as seen by kernels (mapped pinned memory)
   double* h_acc = nullptr;
   int* h_small = nullptr;
   // results of the last evaluation (whole system: summed over domains / ranks)
@@ -200,13 +202,17 @@ struct ab_engine {
   bool timeline = false;
   cudaEvent_t tl_ref = nullptr;      // start of the current evaluation
   std::vector<cudaEvent_t> tl_refs;  // the pending evaluations' start events (back to the pool)
-  double tl_sum[8][2] = {};
-  long long tl_n[8] = {};
+  double tl_sum[10][2] = {};  // 0..7 = phases, 8 = first half-kick + drift, 9 = k_post
+  long long tl_n[10] = {};
+  int tl_sub = -1;            // timeline slot of the next prof_begin (-1: the phase's own)
+  double tl_period = 0;       // sum of start-to-start times of consecutive evaluations
+  long long tl_np = 0;
   double phase_ms[AB_NPHASE] = {0};
   long long phase_n[AB_NPHASE] = {0};
   struct Pend {
     int phase;
     cudaEvent_t a, b, ref;  // ref: the evaluation's start (AB_TIMELINE), not owned
+    int tl;                 // timeline slot
   };
   std::vector<Pend> pending;
   std::vector<cudaEvent_t> pool;
@@ -277,7 +283,8 @@ void prof_stop(ab_engine* e, int phase, cudaStream_t s, cudaEvent_t a) {
   if (!a) return;
   cudaEvent_t b = ev_get(e);
   cudaEventRecord(b, s);
-  e->pending.push_back({phase, a, b, e->tl_ref});
+  e->pending.push_back({phase, a, b, e->tl_ref, e->tl_sub >= 0 ? e->tl_sub : phase});
+  e->tl_sub = -1;
 }
 void prof_begin(ab_engine* e, int phase) {
   e->open_phase = phase;
@@ -298,10 +305,14 @@ void prof_collect(ab_engine* e) {
     float t0 = 0, t1 = 0;
     if (e->timeline && p.ref && cudaEventElapsedTime(&t0, p.ref, p.a) == cudaSuccess &&
         cudaEventElapsedTime(&t1, p.ref, p.b) == cudaSuccess && t0 >= 0) {
-      e->tl_sum[p.phase][0] += t0, e->tl_sum[p.phase][1] += t1, e->tl_n[p.phase] += 1;
+      e->tl_sum[p.tl][0] += t0, e->tl_sum[p.tl][1] += t1, e->tl_n[p.tl] += 1;
     }
     e->pool.push_back(p.a);
     e->pool.push_back(p.b);
+  }
+  for (size_t q = 1; q < e->tl_refs.size(); ++q) {
+    float dt = 0;
+    if (cudaEventElapsedTime(&dt, e->tl_refs[q - 1], e->tl_refs[q]) == cudaSuccess) e->tl_period += dt, ++e->tl_np;
   }
   for (cudaEvent_t r : e->tl_refs) e->pool.push_back(r);
   e->tl_refs.clear();
@@ -922,7 +933,7 @@ ab_status halo_finish(ab_engine* e) {
 ab_status rebuild_all(ab_engine* e) {
   prof_begin(e, 5);
   auto D = doms(e);
-  for (ab_engine* d : D) d->ghosts_fresh = false;  // the rebuild regenerates the images
+  for (ab_engine* d : D) d->ghosts_fresh = d->scratch_zeroed = false;  // the rebuild regenerates the images
   if (!slabbed(e)) {
     auto t0 = std::chrono::steady_clock::now();
     setup_grid(e);
@@ -1008,7 +1019,8 @@ ab_status enqueue_forces(ab_engine* e) {
     CK(cudaMemsetAsync(e->Ff.p, 0, sizeof(float) * 3 * e->NX, st));
   }
   double* const Fk = SG ? reinterpret_cast<double*>(e->Ff.p) : e->F.p;
-  CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
+  if (e->scratch_zeroed) e->scratch_zeroed = false;  // zeroed by k_integrate1_img's last block
+  else CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
   ShortList<R> S = short_view<R>(e);
   // grids and the per-block partial rows of the energy / virial / counter reduction
   const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
@@ -1401,6 +1413,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
             cudaMallocHost(&e->h_small, sizeof(int) * 8) == cudaSuccess;
   static_assert(sizeof(double) * ACC_N <= SCRATCH_CT, "scratch layout");
   static_assert(SCRATCH_CT + sizeof(unsigned long long) * (CT_N + 1) <= SCRATCH_SMALL, "scratch layout");
+  ok = ok && cudaHostGetDevicePointer((void**)&e->h_ct_dev, e->h_ct, 0) == cudaSuccess;
   if (ok) {  // views into the scratch block (not separately allocated)
     e->acc.p = reinterpret_cast<double*>(e->scratch.p), e->acc.n = ACC_N;
     e->ct.p = reinterpret_cast<unsigned long long*>(e->scratch.p + SCRATCH_CT), e->ct.n = CT_N + 1;
@@ -1422,8 +1435,11 @@ void free_engine(ab_engine* e) {
                  e->host_steps, e->host_ms[0] / e->host_steps, e->host_ms[1] / e->host_steps,
                  e->host_ms[2] / e->host_steps, e->host_ms[3] / e->host_steps, e->host_ms[4] / e->host_steps);
   if (e->timeline) {
-    const char* nm[8] = {"short", "rebo", "near", "bstar", "integ", "rebuild", "far", "comm"};
-    for (int q = 0; q < 8; ++q)
+    const char* nm[10] = {"short", "rebo", "near", "bstar", "integ", "rebuild", "far", "comm", "integ1", "post"};
+    if (e->tl_np)
+      std::fprintf(stderr, "[airebo_b200] timeline period %8.1f us between evaluation starts (n %lld)\n",
+                   1e3 * e->tl_period / e->tl_np, e->tl_np);
+    for (int q = 0; q < 10; ++q)
       if (e->tl_n[q])
         std::fprintf(stderr, "[airebo_b200] timeline %-6s start %8.1f us  end %8.1f us  (n %lld)\n", nm[q],
                      1e3 * e->tl_sum[q][0] / e->tl_n[q], 1e3 * e->tl_sum[q][1] / e->tl_n[q], e->tl_n[q]);
@@ -1984,7 +2000,8 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
   struct DeferGuard {
     std::vector<ab_engine*> ds;
     ~DeferGuard() {
-      for (ab_engine* d : ds) d->defer_reduce = false, d->post_pending = false, d->ghosts_fresh = d->f_zeroed = false;
+      for (ab_engine* d : ds)
+        d->defer_reduce = false, d->post_pending = false, d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = false;
     }
   } defer_guard{D};
   for (ab_engine* d : D) d->defer_reduce = true;
@@ -1996,14 +2013,22 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
   for (int64_t s = 1; s <= nsteps; ++s) {
     const bool th = thermo && every > 0 && s % every == 0;
     auto t0 = clk::now();
+    e->tl_sub = 8;
     prof_begin(e, 4);
+    bool flags_published = false;
     for (ab_engine* d : D) {
-      CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), st));
-      if (fuse_img && d->lists_valid && d->NX == d->N) {
+      const bool fused = fuse_img && d->lists_valid && d->NX == d->N;
+      // the fused kernel's last block leaves the displacement slot zero for the next step
+      if (!fused || s == 1) CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), st));
+      if (fused) {
+        FlagOut fo{d->h_ct_dev, reinterpret_cast<unsigned int*>(d->scratch.p + SCRATCH_TICKET),
+                   reinterpret_cast<unsigned long long*>(d->scratch.p), (int)(SCRATCH_ZERO_BYTES / 8), CT_OVF_SHORT,
+                   d->ct.p};
         k_integrate1_img<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt,
                                                           d->xref.p, d->ct.p + CT_N, d->NX, d->goff.p, d->gcnt.p,
-                                                          d->rshift.p);
-        d->ghosts_fresh = d->f_zeroed = true;
+                                                          d->rshift.p, fo);
+        d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = true;
+        flags_published = true;
       } else {
         k_integrate1<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt, d->xref.p,
                                                       d->ct.p + CT_N);
@@ -2011,7 +2036,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
       CKL();
     }
     prof_end(e);
-    TRY(enqueue_flags(e));
+    if (!flags_published) TRY(enqueue_flags(e));  // else written by k_integrate1_img into h_ct
     CK(cudaEventRecord(e->ev_disp, st));
     e->host_ms[0] += ms_since(t0);
     t0 = clk::now();
@@ -2046,6 +2071,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     }
     e->host_ms[3] += ms_since(t0);
     t0 = clk::now();
+    e->tl_sub = 9;
     prof_begin(e, 4);
     for (ab_engine* d : D) {
       if (d->post_pending) {

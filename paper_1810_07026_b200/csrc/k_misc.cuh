@@ -42,12 +42,45 @@ __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, do
   block_max_atomic(d2, maxd2);
 }
 
+// Rebuild flags straight to the host: the last block to finish (ticket) copies the maximal
+// displacement and the short-list overflow flag of the previous evaluation into mapped pinned
+// host memory, then zeroes the scratch block (energies, counters, small ints, the displacement)
+// for the next evaluation.  Replaces a memset before the kernel, a device-to-host copy and a
+// memset after it, all three serial steps on the engine stream.
+struct FlagOut {
+  unsigned long long* host;   // mapped pinned: [CT_N + 1] slots, only host[ovf] and host[CT_N] written
+  unsigned int* ticket;       // device counter, 0 between launches
+  unsigned long long* zero;   // scratch block to zero (device), nzero 64-bit words
+  int nzero, ovf;             // ovf: column of the overflow flag in ct
+  const unsigned long long* ct;
+};
+__device__ __forceinline__ void publish_flags(const FlagOut& fo, unsigned long long* maxd2) {
+  __shared__ bool last;
+  // thread 0 issued the block's atomicMax (block_max_atomic): it fences, then takes the ticket
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(fo.ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    volatile unsigned long long* h = fo.host;
+    h[CT_N] = *(volatile unsigned long long*)maxd2;
+    h[fo.ovf] = *(volatile const unsigned long long*)(fo.ct + fo.ovf);
+    *fo.ticket = 0u;
+    __threadfence_system();
+  }
+  __syncthreads();
+  for (int w = threadIdx.x; w < fo.nzero; w += blockDim.x) fo.zero[w] = 0ull;
+}
+
 // Whole-box NVE: k_integrate1 + the image-ghost refresh (k_image_update) + the zeroing of F
 // for the next evaluation in one pass.  Atom i writes its own periodic images, which the last
 // rebuild laid out contiguously at NB + goff[i] (k_image_fill), with k_image_update's operations.
 __global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, double dtf0, double dtf1, double dt,
                                  const double4* xref, unsigned long long* maxd2, int NB, const int* goff,
-                                 const int* gcnt, const char4* rshift) {
+                                 const int* gcnt, const char4* rshift, FlagOut fo) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (i < N) {
@@ -74,6 +107,7 @@ __global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, doub
     }
   }
   block_max_atomic(d2, maxd2);
+  if (fo.host) publish_flags(fo, maxd2);
 }
 
 // AB_SINGLE: the fp32 force sums of an evaluation widened into the fp64 force array
