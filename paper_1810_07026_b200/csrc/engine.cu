@@ -151,6 +151,11 @@ struct ab_engine {
   int far_at = 0;  // enqueue_forces: fork point of the far-LJ kernel (AB_FAR_AT)
   // NVE steps: the reduction of the partial rows is fused into the second half-kick (k_post)
   bool defer_reduce = false, post_pending = false;
+  // the last NVE step's partial rows, reduced only if energies / counters are read before the
+  // next evaluation overwrites them (collect); NVE steps without a thermo row skip the reduction
+  bool reduce_lazy = false;
+  RedRows lazy_rr{};
+  int lazy_rows = 0;
   // set by k_integrate1_img (whole-box NVE): the image ghosts are current and F is zero
   bool ghosts_fresh = false, f_zeroed = false, scratch_zeroed = false;
   RedRows post_rr{};
@@ -1019,6 +1024,7 @@ ab_status enqueue_forces(ab_engine* e) {
     CK(cudaMemsetAsync(e->Ff.p, 0, sizeof(float) * 3 * e->NX, st));
   }
   double* const Fk = SG ? reinterpret_cast<double*>(e->Ff.p) : e->F.p;
+  e->reduce_lazy = false;  // a new evaluation: the previous one's rows are overwritten
   if (e->scratch_zeroed) e->scratch_zeroed = false;  // zeroed by k_integrate1_img's last block
   else CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
   ShortList<R> S = short_view<R>(e);
@@ -1198,8 +1204,20 @@ ab_status nonfinite_or_ovf(ab_engine* e) {
 inline bool ct_max_col(int c) { return c == CT_MAXSHORT || c == CT_MAXREACH; }
 
 // energies / virial / counters of the last evaluation, summed over all domains and ranks
+// reduce the partial rows an NVE call left unreduced (its last step), before acc / ct are read
+ab_status flush_lazy(ab_engine* e) {
+  for (ab_engine* d : doms(e))
+    if (d->reduce_lazy) {
+      k_reduce<<<ACC_N + CT_N, 256, 0, e->st>>>(d->lazy_rr, d->lazy_rows, d->acc.p, d->ct.p);
+      CKL();
+      d->reduce_lazy = false;
+    }
+  return AB_OK;
+}
+
 ab_status collect(ab_engine* e) {
   auto D = doms(e);
+  TRY(flush_lazy(e));
   double acc[ACC_N] = {0};
   unsigned long long ct[CT_N] = {0};
   if (e->comm) {
@@ -1986,6 +2004,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     ++row;
     return AB_OK;
   };
+  TRY(flush_lazy(e));  // the first thermo row reads the previous evaluation's energies
   if (nrows) TRY(stage_row());
   // The rebuild decision (max displacement) is the only per-step host round trip and
   // it is hidden: after the drift the force kernels are enqueued speculatively on the current
@@ -2017,6 +2036,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     prof_begin(e, 4);
     bool flags_published = false;
     for (ab_engine* d : D) {
+      d->reduce_lazy = false;  // the drift starts a new evaluation (and may zero the scratch)
       const bool fused = fuse_img && d->lists_valid && d->NX == d->N;
       // the fused kernel's last block leaves the displacement slot zero for the next step
       if (!fused || s == 1) CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), st));
@@ -2074,11 +2094,13 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     e->tl_sub = 9;
     prof_begin(e, 4);
     for (ab_engine* d : D) {
-      if (d->post_pending) {
+      if (d->post_pending && th) {  // the thermo row needs the energies now
         k_post<<<ACC_N + CT_N + nblk(d->N, 256), 256, 0, st>>>(d->post_rr, d->post_rows, d->acc.p, d->ct.p, d->N,
                                                                d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
         d->post_pending = false;
       } else {
+        if (d->post_pending && s == nsteps) d->reduce_lazy = true, d->lazy_rr = d->post_rr, d->lazy_rows = d->post_rows;
+        d->post_pending = false;
         k_integrate2<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
       }
       CKL();
