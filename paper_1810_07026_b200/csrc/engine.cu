@@ -1386,8 +1386,18 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   e->serial = std::getenv("AB_SERIAL_KERNELS") && std::getenv("AB_SERIAL_KERNELS")[0] == '1';
   e->timeline = std::getenv("AB_TIMELINE") && std::getenv("AB_TIMELINE")[0] == '1';
   if (const char* fa = std::getenv("AB_FAR_AT")) e->far_at = std::max(0, std::min(2, std::atoi(fa)));
+  // AB_PRIO=<rebo>,<far>: stream priorities of the REBO and far-LJ branches (scheduling
+  // experiments; lower = higher priority, clamped to the device range; default 0 = the engine
+  // stream's)
+  int prio[2] = {0, 0};
+  if (const char* pe = std::getenv("AB_PRIO")) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    std::sscanf(pe, "%d,%d", &prio[0], &prio[1]);
+    for (int& q : prio) q = std::max(hi, std::min(lo, q));
+  }
   for (int c = 0; c < 2; ++c)
-    if (cudaStreamCreateWithFlags(&e->aux[c], cudaStreamNonBlocking) != cudaSuccess ||
+    if (cudaStreamCreateWithPriority(&e->aux[c], cudaStreamNonBlocking, prio[c]) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_fork[c], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&e->ev_join[c], cudaEventDisableTiming) != cudaSuccess) {
       e->err = "cudaStreamCreate / cudaEventCreate failed";

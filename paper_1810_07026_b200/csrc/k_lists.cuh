@@ -301,6 +301,10 @@ struct BondList {
 // Exact short list every step: filter the intermediate list at r <= r_max
 // (closed boundary), store d, r, w = S(r; r_min, r_max), dw/dr; N^C, N^H per atom.
 // Local atoms also append their canonical entries to the REBO bond list of the species pair.
+#ifndef AB_SHORT_BATCH
+#define AB_SHORT_BATCH 4  // measured (cfg2 k_short): 4 -> 20.0 us, 8 -> 24.9, 12 -> 31.2, 16 -> 32.7; 1-ahead pipeline 24.2
+#endif
+constexpr int SHORT_BATCH = AB_SHORT_BATCH;
 template <typename R>
 __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, const int* in_nbr, int capI,
                         ShortList<R> S, const int* gid, const char4* shift, BondList BL, unsigned long long* ct,
@@ -323,18 +327,21 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
     int ci = in_cnt[a];
     size_t base = (size_t)a * S.capS;
     const int* row = in_nbr + (size_t)a * capI;
-    // the next candidate's index and position are loaded while the current one is processed
-    int bn = ci > 0 ? row[0] : a;
-    double4 pbn = pos[bn];
-    int bnn = ci > 1 ? row[1] : a;
-    for (int q = 0; q < ci; ++q) {
-      const int b = bn;
-      const double4 pb = pbn;
-      if (q + 1 < ci) {
-        bn = bnn;
-        pbn = pos[bn];
-        if (q + 2 < ci) bnn = row[q + 2];
-      }
+    // candidates in batches of SHORT_BATCH: all indices, then all positions of a batch are in
+    // flight together (two memory latencies per batch instead of one per candidate); processed
+    // in list order, so the entries and the N sums are those of a serial walk
+    for (int q0 = 0; q0 < ci; q0 += SHORT_BATCH) {
+    int bq[SHORT_BATCH];
+    double4 pq[SHORT_BATCH];
+#pragma unroll
+    for (int u = 0; u < SHORT_BATCH; ++u) bq[u] = q0 + u < ci ? row[q0 + u] : a;
+#pragma unroll
+    for (int u = 0; u < SHORT_BATCH; ++u) pq[u] = pos[bq[u]];
+#pragma unroll
+    for (int u = 0; u < SHORT_BATCH; ++u) {
+      if (q0 + u >= ci) break;
+      const int b = bq[u];
+      const double4 pb = pq[u];
       double dx = __dsub_rn(pb.x, p.x), dy = __dsub_rn(pb.y, p.y), dz = __dsub_rn(pb.z, p.z);
       double r2 = r2_exact(dx, dy, dz);
       int tb = type_of(pb);
@@ -356,6 +363,7 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
         }
         ++n;
       }
+    }
     }
     if (n > S.capS) atomicAdd(ct + CT_OVF_SHORT, 1ull);
     n = min(n, S.capS);
