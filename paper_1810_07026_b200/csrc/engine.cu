@@ -137,6 +137,8 @@ struct ab_engine {
   int nsm = 148;
   cudaStream_t own = nullptr, st = nullptr;
   cudaStream_t aux[2] = {nullptr, nullptr};     // concurrent force kernels (REBO, LJ far)
+  cudaStream_t chain = nullptr;                  // AB_PRIO 3rd value: the short -> near -> b* chain's own stream
+  cudaEvent_t ev_chain[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork[2] = {nullptr, nullptr}, ev_join[2] = {nullptr, nullptr};
   bool serial = false;  // AB_SERIAL_KERNELS=1: the whole DAG on one stream (isolated kernel timing)
   bool have_box = false, have_atoms = false, lists_valid = false, forces_valid = false;
@@ -1003,6 +1005,11 @@ template <typename R, bool SG = false>
 ab_status enqueue_forces(ab_engine* e) {
   const int N = e->N, NT = e->NT;
   cudaStream_t st = e->st;
+  if (e->chain && !e->serial) {  // AB_PRIO experiment: the DAG's main branch on its own stream
+    CK(cudaEventRecord(e->ev_chain[0], e->st));
+    CK(cudaStreamWaitEvent(e->chain, e->ev_chain[0], 0));
+    st = e->chain;
+  }
   StageBuf sb0{nullptr, nullptr, 0}, sb1{nullptr, nullptr, 0};
   if (e->record) {
     size_t n0 = (size_t)N * e->capS + 16, n1 = (size_t)N * (e->capL[0] + e->capL[1] + e->capL[2]) + 16;
@@ -1161,6 +1168,10 @@ ab_status enqueue_forces(ab_engine* e) {
   if (SG) {
     k_widen<<<nblk(3LL * e->NX, 256), 256, 0, st>>>(3 * e->NX, e->Ff.p, e->F.p);
     CKL();
+  }
+  if (st != e->st) {
+    CK(cudaEventRecord(e->ev_chain[1], st));
+    CK(cudaStreamWaitEvent(e->st, e->ev_chain[1], 0));
   }
   return AB_OK;
 }
@@ -1389,12 +1400,19 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   // AB_PRIO=<rebo>,<far>: stream priorities of the REBO and far-LJ branches (scheduling
   // experiments; lower = higher priority, clamped to the device range; default 0 = the engine
   // stream's)
-  int prio[2] = {0, 0};
+  int prio[3] = {0, 0, 1};
   if (const char* pe = std::getenv("AB_PRIO")) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    std::sscanf(pe, "%d,%d", &prio[0], &prio[1]);
+    const int nv = std::sscanf(pe, "%d,%d,%d", &prio[0], &prio[1], &prio[2]);
     for (int& q : prio) q = std::max(hi, std::min(lo, q));
+    if (nv == 3 &&
+        (cudaStreamCreateWithPriority(&e->chain, cudaStreamNonBlocking, prio[2]) != cudaSuccess ||
+         cudaEventCreateWithFlags(&e->ev_chain[0], cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&e->ev_chain[1], cudaEventDisableTiming) != cudaSuccess)) {
+      e->err = "cudaStreamCreate / cudaEventCreate failed";
+      return AB_E_CUDA;
+    }
   }
   for (int c = 0; c < 2; ++c)
     if (cudaStreamCreateWithPriority(&e->aux[c], cudaStreamNonBlocking, prio[c]) != cudaSuccess ||
@@ -1525,6 +1543,9 @@ void free_engine(ab_engine* e) {
     if (e->ev_fork[c]) cudaEventDestroy(e->ev_fork[c]);
     if (e->ev_join[c]) cudaEventDestroy(e->ev_join[c]);
   }
+  if (e->chain) cudaStreamSynchronize(e->chain), cudaStreamDestroy(e->chain);
+  for (cudaEvent_t x : e->ev_chain)
+    if (x) cudaEventDestroy(x);
   if (e->own) cudaStreamDestroy(e->own);
   delete e;
 }
