@@ -150,7 +150,8 @@ struct ab_engine {
   Grid grid{};
   int ncell = 0, nrLJ = 1, nrI = 1;
   int capI = 0, capS = 0, capQ = 0;
-  int far_at = 0;  // enqueue_forces: fork point of the far-LJ kernel (AB_FAR_AT)
+  int far_at = 0;
+  int skip = 0;  // AB_SKIP bit mask (timing ablations only, results wrong): 1 REBO, 2 far, 4 near, 8 b*  // enqueue_forces: fork point of the far-LJ kernel (AB_FAR_AT)
   // NVE steps: the reduction of the partial rows is fused into the second half-kick (k_post)
   bool defer_reduce = false, post_pending = false;
   // the last NVE step's partial rows, reduced only if energies / counters are read before the
@@ -1072,7 +1073,9 @@ ab_status enqueue_forces(ab_engine* e) {
     cudaEvent_t t = prof_start(e, s_far);
     RedRows R6 = RR;
     R6.row0 = row_far;
-    auto far = [&](auto kern) { kern<<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, Fk, e->acc.p, e->ct.p, sb1, R6); };
+    auto far = [&](auto kern) {
+      if (!(e->skip & 2)) kern<<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, Fk, e->acc.p, e->ct.p, sb1, R6);
+    };
     if (e->want_virial) morse ? far(k_lj_far<R, true, true, SG>) : far(k_lj_far<R, true, false, SG>);
     else morse ? far(k_lj_far<R, false, true, SG>) : far(k_lj_far<R, false, false, SG>);
     CKL();
@@ -1096,6 +1099,7 @@ ab_status enqueue_forces(ab_engine* e) {
     RedRows R1 = RR;
     R1.row0 = g_short;
     auto rebo = [&](auto fast, auto slow) {
+      if (e->skip & 1) return;
       fast<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, e->ovf_bond.p, e->small_i.p + 8, S, e->typ.p, e->owner.p,
                                        e->gid.p, e->shift.p, Fk, sb0, R1);
       R1.row0 += g_rebo;
@@ -1113,7 +1117,7 @@ ab_status enqueue_forces(ab_engine* e) {
   if (lj) {
     cudaEvent_t t = prof_start(e, st);
     auto near = [&](auto kern) {
-      kern<<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, Fk, e->acc.p,
+      if (!(e->skip & 4)) kern<<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, Fk, e->acc.p,
                                                        e->ct.p, Qu, sb1, RR);
     };
     if (e->want_virial) morse ? near(k_lj_near<R, true, true, SG>) : near(k_lj_near<R, true, false, SG>);
@@ -1127,7 +1131,8 @@ ab_status enqueue_forces(ab_engine* e) {
     cudaEvent_t t = prof_start(e, st);
     // forward-only fast path; pairs needing the reverse pass / path forces -> ovf_q (NB_FAST
     // sides, count small_i[9]), pairs with a large side -> ovf_q2 (NBMAX, count small_i[1])
-    auto bstar = [&](auto fast, auto full, auto big) {
+    auto bstar = [&](auto fast, auto full, auto big) -> ab_status {
+      if (e->skip & 8) return AB_OK;
       fast<<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p, e->small_i.p + 1,
                                     e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
       // the two deferred batches are independent: the NBMAX one (few pairs, long threads) runs
@@ -1397,6 +1402,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   e->serial = std::getenv("AB_SERIAL_KERNELS") && std::getenv("AB_SERIAL_KERNELS")[0] == '1';
   e->timeline = std::getenv("AB_TIMELINE") && std::getenv("AB_TIMELINE")[0] == '1';
   if (const char* fa = std::getenv("AB_FAR_AT")) e->far_at = std::max(0, std::min(2, std::atoi(fa)));
+  if (const char* sk = std::getenv("AB_SKIP")) e->skip = std::atoi(sk);
   // AB_PRIO=<rebo>,<far>: stream priorities of the REBO and far-LJ branches (scheduling
   // experiments; lower = higher priority, clamped to the device range; default 0 = the engine
   // stream's)

@@ -217,3 +217,29 @@ def test_full_size_sampled_forces(eng_mod, cfg):
     gm = run_gpu(eng_mod, s, "mixed")
     rel = np.sqrt(((gm["F"][smp] - Fs) ** 2).sum()) / np.sqrt((Fs ** 2).sum())
     assert rel <= 1e-4
+
+
+def test_nve_last_step_energies_and_counters(eng_mod):
+    """Inside the NVE loop the partial-row reduction runs only on thermo steps; the call's last
+    step is reduced when energies / counters are read.  Both must equal the oracle at the
+    frames the GPU produced (thermo PE at the thermo step, counters of the last evaluation)."""
+    s = I.config(1)
+    e = eng_mod.make(s)
+    th = e.run_nve(7, 0.5, every=7)  # thermo row at step 7 (reduced with the second half-kick)
+    x7 = e.get_positions()
+    o7 = O.compute(s.types, x7, s.box)
+    assert abs(th[-1, 1] - o7["E"]) <= 1e-11 * abs(o7["E"])
+    e.run_nve(5, 0.5)  # no thermo row: the last step's rows stay unreduced until read
+    st = e.stats()
+    x12 = e.get_positions()
+    o12 = O.compute(s.types, x12, s.box)
+    for k in COUNTERS:
+        assert st[k] == o12["counters"][k], (k, st[k], o12["counters"][k])
+    g = e.compute()  # a fresh evaluation at the same frame: same energy as the oracle's
+    assert abs(g["E"] - o12["E"]) <= 1e-11 * abs(o12["E"])
+    # several calls of one step, each read back: every one is the oracle's at its frame
+    for _ in range(3):
+        th = e.run_nve(1, 0.5, every=1)
+        o = O.compute(s.types, e.get_positions(), s.box)
+        assert abs(th[-1, 1] - o["E"]) <= 1e-11 * abs(o["E"])
+        assert e.stats()["n_lj"] == o["counters"]["n_lj"]
