@@ -2081,7 +2081,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
         FlagOut fo{d->h_ct_dev, reinterpret_cast<unsigned int*>(d->scratch.p + SCRATCH_TICKET),
                    reinterpret_cast<unsigned long long*>(d->scratch.p), (int)(SCRATCH_ZERO_BYTES / 8), CT_OVF_SHORT,
                    d->ct.p};
-        k_integrate1_img<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt,
+        k_integrate1_img<<<nblk(d->N, 128), 128, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt,
                                                           d->xref.p, d->ct.p + CT_N, d->NX, d->goff.p, d->gcnt.p,
                                                           d->rshift.p, fo);
         d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = true;

@@ -68,8 +68,7 @@ __device__ __forceinline__ void publish_flags(const FlagOut& fo, unsigned long l
     volatile unsigned long long* h = fo.host;
     h[CT_N] = *(volatile unsigned long long*)maxd2;
     h[fo.ovf] = *(volatile const unsigned long long*)(fo.ct + fo.ovf);
-    *fo.ticket = 0u;
-    __threadfence_system();
+    *fo.ticket = 0u;  // (the host reads h after the kernel's completion event: no system fence)
   }
   __syncthreads();
   for (int w = threadIdx.x; w < fo.nzero; w += blockDim.x) fo.zero[w] = 0ull;
@@ -84,27 +83,37 @@ __global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, doub
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (i < N) {
+    // every load first (the stores below could alias them for the compiler): one memory
+    // latency for the atom and its first IMG_PRE image shifts instead of a dependent chain
+    constexpr int IMG_PRE = 4;
     double4 p = pos[i];
+    const double v0 = v[3 * i + 0], v1 = v[3 * i + 1], v2 = v[3 * i + 2];
+    const double f0 = F[3 * i + 0], f1 = F[3 * i + 1], f2 = F[3 * i + 2];
+    const double4 r = xref[i];
+    const int g0 = NB + goff[i], ng = gcnt[i];
+    char4 sh[IMG_PRE];
+#pragma unroll
+    for (int k = 0; k < IMG_PRE; ++k) sh[k] = k < ng ? rshift[g0 + k] : make_char4(0, 0, 0, 0);
     double dtf = (type_of(p) == 0) ? dtf0 : dtf1;
-    double vx = v[3 * i + 0] + dtf * F[3 * i + 0];
-    double vy = v[3 * i + 1] + dtf * F[3 * i + 1];
-    double vz = v[3 * i + 2] + dtf * F[3 * i + 2];
+    double vx = v0 + dtf * f0;
+    double vy = v1 + dtf * f1;
+    double vz = v2 + dtf * f2;
     F[3 * i + 0] = 0.0, F[3 * i + 1] = 0.0, F[3 * i + 2] = 0.0;
     v[3 * i + 0] = vx, v[3 * i + 1] = vy, v[3 * i + 2] = vz;
     p.x += dt * vx, p.y += dt * vy, p.z += dt * vz;
     pos[i] = p;
-    double4 r = xref[i];
     double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
     d2 = dx * dx + dy * dy + dz * dz;
-    const int g0 = NB + goff[i], ng = gcnt[i];
-    for (int k = 0; k < ng; ++k) {
-      const int g = g0 + k;
-      const char4 s = rshift[g];
+    auto image = [&](int g, char4 s) {
       const long long key = key_of(p) + ((long long)s.x << 18) + ((long long)s.y << 10) + ((long long)s.z << 2);
       pos[g] = make_double4(__dadd_rn(p.x, __dmul_rn((double)s.x, c_geo.L[0])),
                             __dadd_rn(p.y, __dmul_rn((double)s.y, c_geo.L[1])),
                             __dadd_rn(p.z, __dmul_rn((double)s.z, c_geo.L[2])), __longlong_as_double(key));
-    }
+    };
+#pragma unroll
+    for (int k = 0; k < IMG_PRE; ++k)
+      if (k < ng) image(g0 + k, sh[k]);
+    for (int k = IMG_PRE; k < ng; ++k) image(g0 + k, rshift[g0 + k]);
   }
   block_max_atomic(d2, maxd2);
   if (fo.host) publish_flags(fo, maxd2);

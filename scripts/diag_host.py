@@ -14,6 +14,8 @@ from paper_1810_07026_b200 import inputs as I  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "2"
 prec = sys.argv[2] if len(sys.argv) > 2 else "fp64"
 s = I.config(int(cfg) if cfg.isdigit() else cfg)
+if len(sys.argv) > 3:  # time step override (e.g. 1e-9 fs: frozen atoms, for AB_SKIP ablations)
+    s.dt = float(sys.argv[3])
 eng = E.make(s, prec)
 st = torch.cuda.Stream()
 eng.set_stream(st.cuda_stream)
