@@ -157,6 +157,11 @@ struct ab_engine {
   // the last NVE step's partial rows, reduced only if energies / counters are read before the
   // next evaluation overwrites them (collect); NVE steps without a thermo row skip the reduction
   bool reduce_lazy = false;
+  // whole-box NVE: the second half-kick of a step without a thermo row is deferred and applied by
+  // the next step's drift kernel (v += dtf_prev F; v += dtf F, the two roundings of the separate
+  // kernels), or by flush_kick before anything reads / replaces v or F (ab_get_velocities, ...)
+  bool kick_pending = false;
+  double kick_dtf[2] = {0, 0};
   RedRows lazy_rr{};
   int lazy_rows = 0;
   // set by k_integrate1_img (whole-box NVE): the image ghosts are current and F is zero
@@ -1231,6 +1236,20 @@ ab_status flush_lazy(ab_engine* e) {
   return AB_OK;
 }
 
+// apply a deferred second half-kick (v += dtf F with the forces it belongs to)
+ab_status flush_kick(ab_engine* e) {
+  for (ab_engine* d : doms(e))
+    if (d->kick_pending) {
+      d->kick_pending = false;
+      k_integrate2<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->pos.p, d->vel.p, d->F.p, d->kick_dtf[0], d->kick_dtf[1]);
+      CKL();
+    }
+  return AB_OK;
+}
+void drop_kick(ab_engine* e) {  // v is about to be replaced
+  for (ab_engine* d : doms(e)) d->kick_pending = false;
+}
+
 ab_status collect(ab_engine* e) {
   auto D = doms(e);
   TRY(flush_lazy(e));
@@ -1797,6 +1816,7 @@ const char* ab_last_error(const ab_engine* e) { return e ? e->err.c_str() : g_cr
 ab_status ab_set_stream(ab_engine* e, void* stream) {
   if (!e) return AB_E_ARG;
   cudaSetDevice(e->dev);
+  TRY(flush_kick(e));
   CK(cudaStreamSynchronize(e->st));
   e->st = stream ? (cudaStream_t)stream : e->own;
   for (ab_engine* d : e->subs) d->st = e->st;
@@ -1806,6 +1826,8 @@ ab_status ab_set_stream(ab_engine* e, void* stream) {
 ab_status ab_set_box(ab_engine* e, const double L[3]) {
   if (!e) return AB_E_ARG;
   if (bad_ptr(e, L, "L")) return AB_E_ARG;
+  cudaSetDevice(e->dev);
+  TRY(flush_kick(e));
   for (int c = 0; c < 3; ++c)
     if (!(L[c] > 0.0) || !std::isfinite(L[c])) {
       e->err = "box edge " + std::to_string(c) + " must be finite and > 0";
@@ -1830,6 +1852,7 @@ ab_status ab_set_box(ab_engine* e, const double L[3]) {
 
 ab_status ab_set_atoms(ab_engine* e, int64_t n, const int32_t* type, const double* xyz) {
   if (!e) return AB_E_ARG;
+  drop_kick(e);
   if (n < 1 || n > (1ll << 30)) {
     e->err = "n must be in [1, 2^30]";
     return AB_E_ARG;
@@ -1868,6 +1891,7 @@ static ab_status need_atoms(ab_engine* e) {
 ab_status ab_set_positions(ab_engine* e, const double* xyz) {
   TRY(need_atoms(e));
   if (bad_ptr(e, xyz, "xyz")) return AB_E_ARG;
+  TRY(flush_kick(e));
   if (!slabbed(e)) {
     CK(cudaMemcpyAsync(e->io.p, xyz, sizeof(double) * 3 * e->N, cudaMemcpyHostToDevice, e->st));
     k_from_caller_pos<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->gid.p, e->io.p, e->pos.p);
@@ -1913,6 +1937,7 @@ ab_status ab_set_positions(ab_engine* e, const double* xyz) {
 ab_status ab_set_velocities(ab_engine* e, const double* v) {
   TRY(need_atoms(e));
   if (bad_ptr(e, v, "v")) return AB_E_ARG;
+  drop_kick(e);
   return from_caller_vel(e, v);
 }
 
@@ -1920,6 +1945,7 @@ ab_status ab_get_forces(ab_engine* e, double* f);
 
 ab_status ab_compute(ab_engine* e, double* f, double* energy, double virial[6], double terms[3]) {
   TRY(need_atoms(e));
+  TRY(flush_kick(e));  // with the forces it belongs to, before they are recomputed
   TRY(prepare_all(e, true));
   TRY(forces_all(e));
   if (energy) *energy = e->E3[0] + e->E3[1] + e->E3[2];
@@ -1995,6 +2021,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
   cudaStream_t st = e->st;
   auto D = doms(e);
   if (!e->forces_valid) {
+    TRY(flush_kick(e));  // with the forces it belongs to, before they are recomputed
     TRY(prepare_all(e, true));
     TRY(forces_all(e));
   }
@@ -2042,7 +2069,10 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     return AB_OK;
   };
   TRY(flush_lazy(e));  // the first thermo row reads the previous evaluation's energies
-  if (nrows) TRY(stage_row());
+  if (nrows) {
+    TRY(flush_kick(e));  // the first row's KE reads v
+    TRY(stage_row());
+  }
   // The rebuild decision (max displacement) is the only per-step host round trip and
   // it is hidden: after the drift the force kernels are enqueued speculatively on the current
   // lists (they only write F, the scratch block and the b* queue), the host then waits for the
@@ -2075,13 +2105,17 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     for (ab_engine* d : D) {
       d->reduce_lazy = false;  // the drift starts a new evaluation (and may zero the scratch)
       const bool fused = fuse_img && d->lists_valid && d->NX == d->N;
+      if (!fused && d->kick_pending) TRY(flush_kick(d));
+      const bool pre = fused && d->kick_pending;  // the previous step's second half-kick, fused
+      const double pd0 = pre ? d->kick_dtf[0] : 0.0, pd1 = pre ? d->kick_dtf[1] : 0.0;
+      d->kick_pending = false;
       // the fused kernel's last block leaves the displacement slot zero for the next step
       if (!fused || s == 1) CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), st));
       if (fused) {
         FlagOut fo{d->h_ct_dev, reinterpret_cast<unsigned int*>(d->scratch.p + SCRATCH_TICKET),
                    reinterpret_cast<unsigned long long*>(d->scratch.p), (int)(SCRATCH_ZERO_BYTES / 8), CT_OVF_SHORT,
                    d->ct.p};
-        k_integrate1_img<<<nblk(d->N, 128), 128, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt,
+        k_integrate1_img<<<nblk(d->N, 128), 128, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, pre, pd0, pd1, dtf0, dtf1, dt,
                                                           d->xref.p, d->ct.p + CT_N, d->NX, d->goff.p, d->gcnt.p,
                                                           d->rshift.p, fo);
         d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = true;
@@ -2138,6 +2172,10 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
       } else {
         if (d->post_pending && s == nsteps) d->reduce_lazy = true, d->lazy_rr = d->post_rr, d->lazy_rows = d->post_rows;
         d->post_pending = false;
+        if (fuse_img && !th) {  // deferred to the next drift kernel (or flush_kick)
+          d->kick_pending = true, d->kick_dtf[0] = dtf0, d->kick_dtf[1] = dtf1;
+          continue;
+        }
         k_integrate2<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
       }
       CKL();
@@ -2177,6 +2215,7 @@ ab_status ab_get_positions(ab_engine* e, double* xyz) {
 ab_status ab_get_velocities(ab_engine* e, double* v) {
   TRY(need_atoms(e));
   if (bad_ptr(e, v, "v")) return AB_E_ARG;
+  TRY(flush_kick(e));
   return to_caller(e, 1, v);
 }
 
@@ -2290,6 +2329,8 @@ ab_status ab_get_stats(ab_engine* e, ab_stats* s) {
 
 ab_status ab_record_stages(ab_engine* e, int on) {
   if (!e) return AB_E_ARG;
+  cudaSetDevice(e->dev);
+  TRY(flush_kick(e));
   for (ab_engine* d : doms(e)) d->record = on != 0;
   e->record = on != 0;
   e->forces_valid = false;

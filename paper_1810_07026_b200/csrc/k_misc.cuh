@@ -77,7 +77,8 @@ __device__ __forceinline__ void publish_flags(const FlagOut& fo, unsigned long l
 // Whole-box NVE: k_integrate1 + the image-ghost refresh (k_image_update) + the zeroing of F
 // for the next evaluation in one pass.  Atom i writes its own periodic images, which the last
 // rebuild laid out contiguously at NB + goff[i] (k_image_fill), with k_image_update's operations.
-__global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, double dtf0, double dtf1, double dt,
+__global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, bool pre, double pd0, double pd1,
+                                 double dtf0, double dtf1, double dt,
                                  const double4* xref, unsigned long long* maxd2, int NB, const int* goff,
                                  const int* gcnt, const char4* rshift, FlagOut fo) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -95,9 +96,14 @@ __global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, doub
 #pragma unroll
     for (int k = 0; k < IMG_PRE; ++k) sh[k] = k < ng ? rshift[g0 + k] : make_char4(0, 0, 0, 0);
     double dtf = (type_of(p) == 0) ? dtf0 : dtf1;
-    double vx = v0 + dtf * f0;
-    double vy = v1 + dtf * f1;
-    double vz = v2 + dtf * f2;
+    double u0 = v0, u1 = v1, u2 = v2;
+    if (pre) {  // the previous step's deferred second half-kick (k_integrate2's operations)
+      const double pdtf = (type_of(p) == 0) ? pd0 : pd1;
+      u0 = v0 + pdtf * f0, u1 = v1 + pdtf * f1, u2 = v2 + pdtf * f2;
+    }
+    double vx = u0 + dtf * f0;
+    double vy = u1 + dtf * f1;
+    double vz = u2 + dtf * f2;
     F[3 * i + 0] = 0.0, F[3 * i + 1] = 0.0, F[3 * i + 2] = 0.0;
     v[3 * i + 0] = vx, v[3 * i + 1] = vy, v[3 * i + 2] = vz;
     p.x += dt * vx, p.y += dt * vy, p.z += dt * vz;

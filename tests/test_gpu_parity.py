@@ -243,3 +243,33 @@ def test_nve_last_step_energies_and_counters(eng_mod):
         o = O.compute(s.types, e.get_positions(), s.box)
         assert abs(th[-1, 1] - o["E"]) <= 1e-11 * abs(o["E"])
         assert e.stats()["n_lj"] == o["counters"]["n_lj"]
+
+
+def test_nve_deferred_half_kick_paths_agree(eng_mod):
+    """The second half-kick of a step without a thermo row is deferred into the next drift kernel
+    (or applied when v / F are read or replaced).  Every call pattern integrates the same
+    trajectory: thermo every step (no deferral), one call, one-step calls, and calls split by a
+    velocity read; up to fp64 atomic-order noise in F."""
+    s = I.config(1)
+
+    def run(pattern):
+        e = eng_mod.make(s)
+        for n, every, read_v in pattern:
+            e.run_nve(n, 0.5, every=every)
+            if read_v:
+                e.get_velocities()
+        return e.get_positions(), e.get_velocities(), e
+
+    ref_x, ref_v, _ = run([(10, 1, False)])
+    for pattern in ([(10, 0, False)], [(1, 0, False)] * 10, [(3, 0, True), (4, 0, False), (3, 0, True)],
+                    [(5, 0, False), (5, 5, False)]):
+        x, v, e = run(pattern)
+        assert np.abs(x - ref_x).max() <= 1e-10, pattern
+        assert np.abs(v - ref_v).max() <= 1e-12, pattern
+    # compute() after a deferred step: forces / energy at the current frame equal the oracle's,
+    # and the pending kick used the forces of that frame (velocities unchanged by compute)
+    x, v, e = run([(4, 0, False)])
+    g = e.compute()
+    o = O.compute(s.types, x, s.box)
+    assert np.abs(g["F"] - o["F"]).max() <= 1e-9
+    assert np.array_equal(e.get_velocities(), v)
