@@ -483,6 +483,16 @@ __device__ __forceinline__ void red_flush(const RedSmem& s, RedRows R) {
   for (int c = threadIdx.x; c < ACC_N; c += blockDim.x) R.d[(size_t)c * R.stride + row] = s.d[c];
   for (int c = threadIdx.x; c < CT_N; c += blockDim.x) R.u[(size_t)c * R.stride + row] = s.u[c];
 }
+// A block of a grid-stride kernel that gets no work item (blockIdx.x * blockDim.x >= nwork, the
+// same for all its threads) writes a zero partial row without barriers and leaves: the overflow
+// batches are launched with fixed grids and are usually empty.
+__device__ __forceinline__ bool red_idle_block(int nwork, const RedRows& R) {
+  if ((long long)blockIdx.x * blockDim.x < nwork) return false;
+  const int row = R.row0 + blockIdx.x;
+  for (int c = threadIdx.x; c < ACC_N; c += blockDim.x) R.d[(size_t)c * R.stride + row] = 0.0;
+  for (int c = threadIdx.x; c < CT_N; c += blockDim.x) R.u[(size_t)c * R.stride + row] = 0ull;
+  return true;
+}
 // one block per column: fixed-order sum (max for the max counters) over nrows partial rows
 __device__ __forceinline__ void reduce_column(const RedRows& R, int nrows, double* acc, unsigned long long* ct,
                                               int c) {

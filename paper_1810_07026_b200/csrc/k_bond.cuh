@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_
                                               const int* owner, const int* gid, const char4* shift, double* F,
                                               StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
+  if (red_idle_block(list_idx ? *novf : BL.cnt[0] + BL.cnt[1] + BL.cnt[2], RR)) return;
   red_init(rs);
   const Tab<R>& T = tab<R>();
   const int n0 = BL.cnt[0], n01 = n0 + BL.cnt[1];
@@ -643,10 +644,11 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
                                                const int* owner, const int* gid, const char4* shift, double* F,
                                                StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
-  red_init(rs);
-  const Tab<R>& T = tab<R>();
   const int q0 = min(Qu.count[0], Qu.cap[0]), q1 = min(Qu.count[1], Qu.cap[1]), q2 = min(Qu.count[2], Qu.cap[2]);
   const int nq = FULL ? *novf : q0 + q1 + q2;
+  if (red_idle_block(nq, RR)) return;
+  red_init(rs);
+  const Tab<R>& T = tab<R>();
   double e[1 + 6] = {0, 0, 0, 0, 0, 0, 0};
   unsigned long long ntr = 0, nb = 0, nbad = 0;
   int stride = gridDim.x * blockDim.x;
