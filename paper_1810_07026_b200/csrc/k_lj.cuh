@@ -32,7 +32,10 @@ namespace ab {
 #define AB_NEAR_SLOTS 64
 #endif
 constexpr int NEAR_GROUP = AB_NEAR_GROUP;        // lanes per atom (measured: 8 beats 16 and 32)
-constexpr int NEAR_ATOMS = 128 / NEAR_GROUP;     // atoms per 128-thread block
+#ifndef AB_NEAR_BLOCK
+#define AB_NEAR_BLOCK 128
+#endif
+constexpr int NEAR_ATOMS = AB_NEAR_BLOCK / NEAR_GROUP;  // atoms per block
 constexpr int NEAR_SLOTS = AB_NEAR_SLOTS;        // reach table slots per atom (measured: 64 beats 128)
 
 #ifndef AB_NEAR_BLOOM
