@@ -294,6 +294,24 @@ def run_ours(args, ws, rank, local):
                 traffic = None
         step_flops = sum(flops.values())
         step_s = r["total_ms"] / K * 1e-3
+        # DRAM bytes of one evaluation (ncu cold-cache bytes per launch x launches per
+        # NVE step: short 1, REBO 2, near 1, far 1, b* 3) against the measured HBM bandwidth
+        dram = None
+        try:
+            summ = json.load(open(PROFILE_SUMMARY)).get(precision, {})
+            per = {"k_short": 1, "k_rebo": 2, "k_lj_near": 1, "k_lj_far": 1, "k_bstar": 3}
+            if all(k in summ and summ[k].get("dram_bytes_per_launch") for k in per):
+                byts = sum(summ[k]["dram_bytes_per_launch"] * n for k, n in per.items())
+                hbm = None
+                mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+                if os.path.exists(mp):
+                    hbm = json.load(open(mp)).get("hbm_gbs")
+                gbs = byts / step_s / 1e9
+                dram = {"bytes_per_step": byts, "gbs_at_step_time": round(gbs, 1), "hbm_gbs": hbm,
+                        "frac": round(gbs / hbm, 4) if hbm else None,
+                        "source": os.path.basename(PROFILE_SUMMARY) + " (cold-cache per-launch bytes)"}
+        except (ValueError, OSError):
+            dram = None
         return {"bound": "alu", "kernel": KERNEL_OF[dom], "achieved": round(achieved, 4), "peak": round(peak, 3),
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 5), "traffic": traffic, "hw": hw,
                 "peak_basis": f"{'FP64' if precision == 'fp64' else 'FP32'} FMA units x 2 x median SM clock "
@@ -306,7 +324,8 @@ def run_ours(args, ws, rank, local):
                 "whole_step_tflops": round(step_flops / step_s / 1e12, 4),
                 "whole_step_frac": round(step_flops / step_s / 1e12 / peak, 5),
                 "phase_ms_per_step": {p: round(v[0] / K, 5) for p, v in r["phase"].items()},
-                "comm_ms_per_step": round(r["phase"]["comm"][0] / K, 5) if ws > 1 else None}
+                "comm_ms_per_step": round(r["phase"]["comm"][0] / K, 5) if ws > 1 else None,
+                "dram_per_step": dram}
 
     peak_meas = {}
     for p, code in (("fp64", E.AB_FP64), ("fp32", E.AB_MIXED)):
