@@ -151,6 +151,7 @@ struct ab_engine {
   int ncell = 0, nrLJ = 1, nrI = 1;
   int capI = 0, capS = 0, capQ = 0;
   int far_at = 0;
+  bool pdl = false;  // AB_PDL=1: programmatic dependent launch of the b* kernels
   int skip = 0;  // AB_SKIP bit mask (timing ablations only, results wrong): 1 REBO, 2 far, 4 near, 8 b*  // enqueue_forces: fork point of the far-LJ kernel (AB_FAR_AT)
   // NVE steps: the reduction of the partial rows is fused into the second half-kick (k_post)
   bool defer_reduce = false, post_pending = false;
@@ -1138,21 +1139,37 @@ ab_status enqueue_forces(ab_engine* e) {
     // sides, count small_i[9]), pairs with a large side -> ovf_q2 (NBMAX, count small_i[1])
     auto bstar = [&](auto fast, auto full, auto big) -> ab_status {
       if (e->skip & 8) return AB_OK;
-      fast<<<g_bstar, 128, 0, st>>>(Qu, nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p, e->small_i.p + 1,
-                                    e->pos.p, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
+      // AB_PDL=1: the fast and full b* kernels are launched as programmatic dependents of the
+      // kernel before them on the stream (their CTAs launch while it drains and wait in
+      // griddepcontrol.wait); the NBMAX batch then forks after the full kernel
+      cudaLaunchAttribute pdl[1];
+      pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      pdl[0].val.programmaticStreamSerializationAllowed = 1;
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(g_bstar), lc.blockDim = dim3(128), lc.dynamicSmemBytes = 0, lc.stream = st;
+      lc.attrs = pdl, lc.numAttrs = e->pdl ? 1 : 0;
+      CK(cudaLaunchKernelEx(&lc, fast, Qu, (const int*)nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p,
+                            e->small_i.p + 1, (const double4*)e->pos.p, S, (const signed char*)e->typ.p,
+                            (const int*)e->owner.p, (const int*)e->gid.p, (const char4*)e->shift.p, Fk, sb1, RR));
       // the two deferred batches are independent: the NBMAX one (few pairs, long threads) runs
       // on aux stream 0 (REBO is done or finishing there) beside the NB_FAST reverse-pass batch
       RedRows Rb = RR;
       Rb.row0 += 2 * g_bstar;
-      if (!serial) {
-        CK(cudaEventRecord(e->ev_fork[0], st));
-        CK(cudaStreamWaitEvent(s_rebo, e->ev_fork[0], 0));
-      }
-      big<<<g_slow, 128, 0, s_rebo>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr, e->pos.p, S,
-                                      e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, Rb);
+      auto fork_big = [&]() -> ab_status {
+        if (!serial) {
+          CK(cudaEventRecord(e->ev_fork[0], st));
+          CK(cudaStreamWaitEvent(s_rebo, e->ev_fork[0], 0));
+        }
+        big<<<g_slow, 128, 0, s_rebo>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr, e->pos.p, S,
+                                        e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, Rb);
+        return AB_OK;
+      };
+      if (!e->pdl) TRY(fork_big());
       RR.row0 += g_bstar;
-      full<<<g_bstar, 128, 0, st>>>(Qu, e->ovf_q.p, nullptr, e->small_i.p + 9, nullptr, nullptr, e->pos.p, S,
-                                    e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, RR);
+      CK(cudaLaunchKernelEx(&lc, full, Qu, (const int*)e->ovf_q.p, (int*)nullptr, e->small_i.p + 9, (int*)nullptr,
+                            (int*)nullptr, (const double4*)e->pos.p, S, (const signed char*)e->typ.p,
+                            (const int*)e->owner.p, (const int*)e->gid.p, (const char4*)e->shift.p, Fk, sb1, RR));
+      if (e->pdl) TRY(fork_big());
       return AB_OK;
     };
     if (e->want_virial)
@@ -1422,6 +1439,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   e->timeline = std::getenv("AB_TIMELINE") && std::getenv("AB_TIMELINE")[0] == '1';
   if (const char* fa = std::getenv("AB_FAR_AT")) e->far_at = std::max(0, std::min(2, std::atoi(fa)));
   if (const char* sk = std::getenv("AB_SKIP")) e->skip = std::atoi(sk);
+  e->pdl = std::getenv("AB_PDL") && std::getenv("AB_PDL")[0] == '1';
   // AB_PRIO=<rebo>,<far>: stream priorities of the REBO and far-LJ branches (scheduling
   // experiments; lower = higher priority, clamped to the device range; default 0 = the engine
   // stream's)

@@ -644,6 +644,9 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
                                                const int* owner, const int* gid, const char4* shift, double* F,
                                                StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
+  // programmatic dependent launch (AB_PDL): wait for the previous kernel's results (a no-op when
+  // the kernel was launched normally)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int q0 = min(Qu.count[0], Qu.cap[0]), q1 = min(Qu.count[1], Qu.cap[1]), q2 = min(Qu.count[2], Qu.cap[2]);
   const int nq = FULL ? *novf : q0 + q1 + q2;
   if (red_idle_block(nq, RR)) return;
