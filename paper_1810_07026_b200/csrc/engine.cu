@@ -1045,7 +1045,7 @@ ab_status enqueue_forces(ab_engine* e) {
   // grids and the per-block partial rows of the energy / virial / counter reduction
   const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
   const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4, g_slow = e->nsm * 2;
-  const int nrows = g_short + g_rebo + g_near + g_far + 2 * g_bstar + 2 * g_slow;
+  const int nrows = g_short + g_rebo + g_near + g_far + g_bstar + 3 * g_slow;  // b* full and NBMAX: g_slow
   CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
   CK(e->ovf_q.ensure(e->capQ));
   CK(e->ovf_q2.ensure(e->capQ));
@@ -1147,6 +1147,8 @@ ab_status enqueue_forces(ab_engine* e) {
       pdl[0].val.programmaticStreamSerializationAllowed = 1;
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3(g_bstar), lc.blockDim = dim3(128), lc.dynamicSmemBytes = 0, lc.stream = st;
+      cudaLaunchConfig_t lf = lc;  // the reverse-pass batch (usually empty): one wave of 2 CTAs / SM
+      lf.gridDim = dim3(g_slow);
       lc.attrs = pdl, lc.numAttrs = e->pdl ? 1 : 0;
       CK(cudaLaunchKernelEx(&lc, fast, Qu, (const int*)nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p,
                             e->small_i.p + 1, (const double4*)e->pos.p, S, (const signed char*)e->typ.p,
@@ -1154,7 +1156,7 @@ ab_status enqueue_forces(ab_engine* e) {
       // the two deferred batches are independent: the NBMAX one (few pairs, long threads) runs
       // on aux stream 0 (REBO is done or finishing there) beside the NB_FAST reverse-pass batch
       RedRows Rb = RR;
-      Rb.row0 += 2 * g_bstar;
+      Rb.row0 += g_bstar + g_slow;
       auto fork_big = [&]() -> ab_status {
         if (!serial) {
           CK(cudaEventRecord(e->ev_fork[0], st));
@@ -1166,7 +1168,7 @@ ab_status enqueue_forces(ab_engine* e) {
       };
       if (!e->pdl) TRY(fork_big());
       RR.row0 += g_bstar;
-      CK(cudaLaunchKernelEx(&lc, full, Qu, (const int*)e->ovf_q.p, (int*)nullptr, e->small_i.p + 9, (int*)nullptr,
+      CK(cudaLaunchKernelEx(&lf, full, Qu, (const int*)e->ovf_q.p, (int*)nullptr, e->small_i.p + 9, (int*)nullptr,
                             (int*)nullptr, (const double4*)e->pos.p, S, (const signed char*)e->typ.p,
                             (const int*)e->owner.p, (const int*)e->gid.p, (const char4*)e->shift.p, Fk, sb1, RR));
       if (e->pdl) TRY(fork_big());
