@@ -154,7 +154,10 @@ ab_status ab_compute(ab_engine* e, double* f, double* energy, double virial[6], 
  * thermo_every > 0 it receives rows (step, PE, KE, Etot) for steps 0, every, 2 every, ... <= nsteps
  * (nsteps/thermo_every + 1 rows, 4 doubles each).  The call returns once the last step is
  * enqueued on the engine's stream (it synchronises once per step on the rebuild decision only);
- * every call that returns data orders after it. */
+ * every call that returns data orders after it.  Internally the last step's second half-kick
+ * and its energy / counter reduction may be left pending (applied by the next step's drift
+ * kernel, or by the next call that reads or replaces velocities, positions, forces, energies or
+ * counters); no call can observe the difference. */
 ab_status ab_run_nve(ab_engine* e, int64_t nsteps, double dt_fs, int64_t thermo_every, double* thermo);
 
 ab_status ab_get_positions(ab_engine* e, double* xyz);  /* caller order; not re-wrapped between rebuilds */
