@@ -71,7 +71,10 @@ struct DBuf {
 inline int nblk(long long n, int t) { return (int)std::max<long long>(1, (n + t - 1) / t); }
 
 constexpr size_t SCRATCH_BYTES = 1024, SCRATCH_CT = 128, SCRATCH_SMALL = 512, SCRATCH_ZERO_BYTES = 512 + 64;
-constexpr size_t SCRATCH_TICKET = 1016;  // k_integrate1_img's last-block ticket (never memset after init)
+constexpr size_t SCRATCH_TICKET = 1016;
+#ifndef AB_INT_BLOCK
+#define AB_INT_BLOCK 128  // k_integrate1_img block (measured cfg2: 128 beats 256; 64 / 32 equal)
+#endif  // k_integrate1_img's last-block ticket (never memset after init)
 
 // ---- NCCL, resolved at run time (only the distributed mode needs it)
 struct NcclApi {
@@ -2135,7 +2138,7 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
         FlagOut fo{d->h_ct_dev, reinterpret_cast<unsigned int*>(d->scratch.p + SCRATCH_TICKET),
                    reinterpret_cast<unsigned long long*>(d->scratch.p), (int)(SCRATCH_ZERO_BYTES / 8), CT_OVF_SHORT,
                    d->ct.p};
-        k_integrate1_img<<<nblk(d->N, 128), 128, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, pre, pd0, pd1, dtf0, dtf1, dt,
+        k_integrate1_img<<<nblk(d->N, AB_INT_BLOCK), AB_INT_BLOCK, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, pre, pd0, pd1, dtf0, dtf1, dt,
                                                           d->xref.p, d->ct.p + CT_N, d->NX, d->goff.p, d->gcnt.p,
                                                           d->rshift.p, fo);
         d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = true;
