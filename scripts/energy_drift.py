@@ -1,7 +1,7 @@
 """Precision study (the paper's section 5.2 experiment): total-energy
 drift of long NVE runs in fp64, mixed and single precision (AB_SINGLE: fp32 accumulation) on the
 all-carbon nanotube (the paper's CNT workload) and on polyethylene.  argv: steps, dt_fs,
-systems (all | cnt | pe), precisions (comma list).  Prints one JSON line per (system, precision): the maximal
+systems (all | cnt | pe | cfg2), precisions (comma list).  Prints one JSON line per (system, precision): the maximal
 |E_tot(t) - E_tot(0)| per atom and the slope of a linear fit (eV/atom/ps)."""
 import json
 import os
@@ -20,7 +20,9 @@ systems = [I.nanotube(10, 10, 12, jitter=0.01, seed_x=41, seed_v=42, T=300.0, na
            I.polyethylene((2, 2, 6), 0.02, 43, 44, name="pe-2x2x6")]
 which = sys.argv[3] if len(sys.argv) > 3 else "all"
 precs = sys.argv[4].split(",") if len(sys.argv) > 4 else ["fp64", "mixed", "single"]
-systems = [s for s in systems if which == "all" or s.name.startswith(which)]
+if which == "cfg2":  # the headline workload (BASELINE configs[1], 32,256 atoms)
+    systems = [I.config(2)]
+systems = [s for s in systems if which in ("all", "cfg2") or s.name.startswith(which)]
 for s in systems:
     for prec in precs:
         e = E.make(s, prec)
