@@ -2132,8 +2132,10 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
       const bool pre = fused && d->kick_pending;  // the previous step's second half-kick, fused
       const double pd0 = pre ? d->kick_dtf[0] : 0.0, pd1 = pre ? d->kick_dtf[1] : 0.0;
       d->kick_pending = false;
-      // the fused kernel's last block leaves the displacement slot zero for the next step
-      if (!fused || s == 1) CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), st));
+      // the fused kernel's last block leaves the displacement slot zero for the next step, and every
+      // other writer of the slot (k_maxdisp, k_integrate1) is followed by an evaluation that zeroes
+      // the scratch block; a stale value could only be larger (a max), i.e. cause an early rebuild
+      if (!fused) CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), st));
       if (fused) {
         FlagOut fo{d->h_ct_dev, reinterpret_cast<unsigned int*>(d->scratch.p + SCRATCH_TICKET),
                    reinterpret_cast<unsigned long long*>(d->scratch.p), (int)(SCRATCH_ZERO_BYTES / 8), CT_OVF_SHORT,
