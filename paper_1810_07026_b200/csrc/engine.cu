@@ -1675,6 +1675,19 @@ ab_status to_caller(ab_engine* e, int which, double* host) {
   return AB_OK;
 }
 
+// A host-to-device copy straight from caller memory: from pageable memory cudaMemcpyAsync returns
+// once the data is staged, but from page-locked memory the DMA reads the caller's buffer later;
+// then wait for the copy, so the caller may reuse the buffer when the call returns (header: the
+// library copies every input array and never retains a caller pointer).
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 ab_status from_caller_vel(ab_engine* e, const double* host) {
   auto D = doms(e);
   double* buf = e->io.p;
@@ -1688,6 +1701,7 @@ ab_status from_caller_vel(ab_engine* e, const double* host) {
     ++d->launches;
   }
   CK(cudaGetLastError());
+  if (host_pinned(host)) CK(cudaStreamSynchronize(e->st));
   return AB_OK;
 }
 
@@ -1920,6 +1934,7 @@ ab_status ab_set_positions(ab_engine* e, const double* xyz) {
     k_from_caller_pos<<<nblk(e->N, 256), 256, 0, e->st>>>(e->N, e->gid.p, e->io.p, e->pos.p);
     CKL();
     e->forces_valid = false;
+    if (host_pinned(xyz)) CK(cudaStreamSynchronize(e->st));
     return AB_OK;
   }
   // slab domains: atoms may change owner arbitrarily -> redistribute (velocities kept)

@@ -277,3 +277,26 @@ def test_nve_deferred_half_kick_paths_agree(eng_mod, precision):
     else:
         assert np.linalg.norm(g["F"] - o["F"]) <= 1e-4 * np.linalg.norm(o["F"])
     assert np.array_equal(e.get_velocities(), v)
+
+
+def test_inputs_copied_from_pinned_caller_buffers(eng_mod):
+    """The library copies every input array (header): a page-locked caller buffer may be reused as
+    soon as ab_set_velocities / ab_set_positions return."""
+    import ctypes as C
+    import torch
+    s = I.config(2)
+    e = eng_mod.make(s)
+    e.run_nve(2, s.dt)  # work queued on the stream ahead of the copies
+    v0 = np.ascontiguousarray(s.v * 0.5)
+    vh = torch.from_numpy(v0.copy()).pin_memory()
+    dp = C.POINTER(C.c_double)
+    e.run_nve(3, s.dt)
+    e._ck(e.L.ab_set_velocities(e.h, C.cast(vh.data_ptr(), dp)))
+    vh.fill_(123.0)  # the caller reuses its buffer at once
+    assert np.array_equal(e.get_velocities(), v0)
+    x0 = e.get_positions()
+    xh = torch.from_numpy(np.ascontiguousarray(x0)).pin_memory()
+    e.run_nve(3, s.dt)
+    e._ck(e.L.ab_set_positions(e.h, C.cast(xh.data_ptr(), dp)))
+    xh.fill_(-7.0)
+    assert np.array_equal(e.get_positions(), x0)
