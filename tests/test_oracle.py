@@ -66,7 +66,7 @@ def test_g_spline_matches_scipy_hermite():
                 assert o[1] == 0.0  # clamped: zero derivative
 
 
-def test_grid_splines_knots_quadratic_and_c1():
+def test_grid_splines_knots_bilinear_and_c1():
     kv = CF.KV
     # exact at knots
     for x in range(5):
