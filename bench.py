@@ -1,23 +1,26 @@
 #!/usr/bin/env python
-"""bench.py -- AIREBO NVE throughput (atom-steps/s) of the B200 engine on BASELINE.json's config.
+"""bench.py -- AIREBO NVE throughput (atom-steps/s) of the B200 engine on BASELINE.json's metric config.
 
 Contract (driver): python bench.py --gpus N --steps K --warmup W [--impl reference]
-  * one JSON line on rank 0; value = whole-job atom-steps/s (all ranks), device-timed with CUDA
-    events on the engine's stream, max over ranks; inputs resident in HBM before the timed region.
-  * workload (N=1): BASELINE configs[1] = polyethylene 12x16x14 cells (32,256 atoms), +-0.02 A
-    jitter, 300 K, dt = 0.5 fs, NVE (velocity Verlet, skin 1 A, lists rebuilt on demand).
-    Each "step" = one full MD step (integrate, rebuild check, short list, REBO + bond order +
-    torsion, C_ij + LJ, b* batch, integrate).  L2 is flushed (256 MiB write) between timed steps.
+  * one JSON line on rank 0; value = whole-job atom-steps/s (all ranks' atoms x K / max-over-ranks
+    device time), CUDA events on the engine's stream; inputs resident in HBM before the timed region.
+  * workload (N=1): BASELINE configs[3] = cfg4, the polyethylene crystal 40x50x42 cells
+    (1,008,000 atoms), +-0.02 A jitter, 300 K, dt = 0.5 fs, NVE (velocity Verlet, skin 1 A, lists
+    rebuilt on demand) -- the configuration BASELINE's metric ("atom-steps/s (fp64 and mixed) at
+    1/2/4/8 B200") is quoted on, which fits one B200.  fp64 headline + a mixed sub-line.
+  * timed region = ONE ab_run_nve(K, dt, thermo_every=10) call (the loop includes
+    forces, integration, skin-triggered rebuilds and thermo output every 10 steps).  The working
+    set (LJ lists ~1 GB, positions, short lists) is far larger than the 126 MB L2, so no flush.
   * e2e: the same metric through the C-ABI with HOST buffers, the host holding the state: per step
     ab_set_velocities (H2D from pinned memory) + ab_run_nve(1 step, thermo row D2H) +
     ab_get_positions + ab_get_velocities (D2H), wall clock.
-  * default K = 100 steps (BASELINE: 100 NVE steps), so skin-triggered list rebuilds fall inside
-    the timed region at their natural rate (counted in counters.timed_rebuilds).
-  * --impl reference: the fp64 CPU oracle (oracle/) on the host cores, same workload.
+  * cpu_baseline / --impl reference: the fp64 CPU oracle (oracle/) on the host cores (see
+    cpu_oracle_baseline / run_reference for the bounded samples).
 Multi-GPU (N > 1, torchrun, one process per GPU): slab decomposition along x with
   the engine's own NCCL communicator (ab_create_dist): halo positions and ghost forces travel by
-  ncclSend/ncclRecv between slab neighbours every step.  Default weak scaling: the cfg2 block per
-  GPU (PE (12 N) x 16 x 14 cells, N x 32,256 atoms); --scaling strong keeps cfg --config fixed.
+  ncclSend/ncclRecv between slab neighbours every step.  Default: cfg4 strong scaling (the
+  1,008,000-atom system split over N slabs, BASELINE configs[3]); --config 5a / 5b: weak scaling,
+  the 2 M-atom diamond / PE block per GPU replicated along x (BASELINE configs[4]).
 """
 from __future__ import annotations
 
@@ -36,7 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "AIREBO atom-steps/s (fp64 and mixed) at 1/2/4/8 B200; % of FP64/FP32 peak"
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
 
 
 # ------------------------------------------------------------------ helpers
@@ -52,12 +55,40 @@ def reduce_max(x, ws, device=None):
 
 
 def workload(config, ws, scaling):
-    """The bench system: BASELINE configs[1] (cfg2) at N = 1; weak scaling replicates the cfg2
-    block along x (same seeds), strong scaling keeps the configured system."""
+    """The bench system: BASELINE config `config` at N = 1; at N > 1 strong scaling keeps it,
+    weak scaling replicates the per-GPU block along x (cfg5a / 5b: n_rep = N, same seeds)."""
     from paper_1810_07026_b200 import inputs as I
-    if ws == 1 or scaling == "strong" or config != 2:
-        return I.config(config)
-    return I.polyethylene((12 * ws, 16, 14), 0.02, 102, 202, name=f"cfg2-pe-32k-x{ws}")
+    if ws > 1 and scaling == "weak":
+        if config in ("5a", "5b"):
+            return I.config(config, n_rep=ws)
+        if config == 2:
+            return I.polyethylene((12 * ws, 16, 14), 0.02, 102, 202, name=f"cfg2-pe-32k-x{ws}")
+    return I.config(config)
+
+
+def default_scaling(config):
+    return "weak" if config in ("5a", "5b", 2) else "strong"
+
+
+CFG_TEXT = {1: "BASELINE configs[0]: tiny PE 1x1x10 cells, 120 atoms, 300 K, dt 0.5 fs",
+            2: "BASELINE configs[1]: PE 12x16x14 cells, 32,256 atoms, 300 K, dt 0.5 fs",
+            3: "BASELINE configs[2]: relaxed amorphous CH2, 64,002 atoms, 1500 K, dt 0.25 fs",
+            4: "BASELINE configs[3]: PE 40x50x42 cells, 1,008,000 atoms, 300 K, dt 0.5 fs, NVE, LJ cutoff 3 sigma, "
+               "torsion on (the metric's 1/2/4/8-GPU configuration)",
+            "5a": "BASELINE configs[4]: diamond 63n x 63 x 63 cells, 2,000,376 atoms per GPU, 1000 K, dt 0.5 fs",
+            "5b": "BASELINE configs[4]: PE 40n x 50 x 84 cells, 2,016,000 atoms per GPU, 300 K, dt 0.5 fs"}
+
+
+def config_dict(s, args, ws):
+    """The `config` object of the JSON line (shared by both arms, so they carry the same dict)."""
+    return {"workload": f"{s.name} ({CFG_TEXT.get(args.config, args.config)})", "atoms": s.n, "dt_fs": s.dt,
+            "precision": args.precision, "potential": args.potential,
+            "parallelism": "single GPU" if ws == 1 else f"slab{ws} (x slabs, NCCL halo send/recv)",
+            "scaling": "weak" if ws == 1 else args.scaling,
+            "l2": "not flushed: inputs larger than L2 (LJ lists ~1 GB + positions / short lists vs 126 MB L2)"
+                  if s.n >= 500000 else "L2 flushed (256 MiB write) before the timed region",
+            "timed_step": f"ab_run_nve(K, dt, thermo_every={args.thermo}): integrate, rebuild check / list rebuild, "
+                          "forces, integrate, thermo row every 10 steps"}
 
 
 def dist_env():
@@ -183,7 +214,7 @@ def run_ours(args, ws, rank, local):
     # a dedicated stream: the engine's kernels, the L2 flush and the timing events are all ordered
     # on it (torch's legacy default stream would leave the engine on its own stream)
     stream = torch.cuda.Stream(dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev) if s.n < 500000 else None
 
     def barrier():
         if ws > 1:
@@ -206,21 +237,19 @@ def run_ours(args, ws, rank, local):
             e.set_velocities(s.v)
         return e
 
-    def timed_steps(eng, K):
-        """K NVE steps, each bracketed by CUDA events on the engine's stream, L2 flushed before
-        each (outside the events).  Returns the per-step device times (ms)."""
-        ev = []
+    def timed_steps(eng, K, L2flush=False):
+        """ONE ab_run_nve(K, dt, thermo_every) call bracketed by CUDA events on the engine's
+        stream (the flush, if any, before the start event).  Returns the device time (ms)."""
         with torch.cuda.stream(stream):
-            for _ in range(K):
+            if L2flush:
                 flush.zero_()
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                eng.run_nve(1, s.dt)
-                b.record(stream)
-                ev.append((a, b))
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            eng.run_nve(K, s.dt, every=args.thermo)
+            b.record(stream)
         stream.synchronize()
-        return [a.elapsed_time(b) for a, b in ev]
+        return a.elapsed_time(b)
 
     def leg(precision):
         import ctypes as C
@@ -233,28 +262,28 @@ def run_ours(args, ws, rank, local):
         barrier()
         torch.cuda.synchronize()
         with ClockSampler(local) as clk:
-            times = timed_steps(eng, args.steps)
+            t_ms = timed_steps(eng, args.steps, L2flush=s.n < 500000)
         torch.cuda.synchronize()
         barrier()
         launches = eng.device_info()["kernel_launches"] - l0
         st = eng.stats()
         st["timed_rebuilds"] = st["n_rebuilds"] - nb0
-        total_ms = max_over_ranks(sum(times))
+        total_ms = max_over_ranks(t_ms)
         # profiled replay: the next K steps with the kernels one at a time (each has the GPU to
         # itself) and per-phase CUDA events on the engine stream -> per-kernel launch durations
         # for the roofline (the events cost ~10 % of a step and the concurrent DAG overlaps the
         # kernels, so the headline above is taken without them)
         eng.set_concurrency(False)
         eng.L.ab_set_profiling(eng.h, 1)
-        ptimes = timed_steps(eng, args.steps)
+        ptime = timed_steps(eng, args.steps)
         ms = (C.c_double * 8)()
         n = (C.c_int64 * 8)()
         eng.L.ab_get_phase_ms(eng.h, ms, n)
         eng.L.ab_set_profiling(eng.h, 0)
         eng.set_concurrency(True)
-        out = dict(eng=eng, times=times, total_ms=total_ms, clocks=clk.summary(), launches=launches,
+        out = dict(eng=eng, total_ms=total_ms, clocks=clk.summary(), launches=launches,
                    phase={p: (ms[q], int(n[q])) for q, p in enumerate(PHASES)}, stats=st,
-                   prof_total_ms=sum(ptimes))
+                   prof_total_ms=ptime)
         return out
 
     res = {}
@@ -370,7 +399,7 @@ def run_ours(args, ws, rank, local):
     # ---- CPU baseline: the oracle as it stands, on this host's cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_baseline(s, budget_s=args.cpu_budget)
+        cpu = cpu_oracle_baseline(s, args)
 
     if rank == 0:
         line = {
@@ -380,13 +409,7 @@ def run_ours(args, ws, rank, local):
             "vs_baseline": None,
             "dtype": {"fp64": "f64", "mixed": "f32+f64acc", "single": "f32"}[args.precision],
             "data": "synthetic (seeded generator, paper_1810_07026_b200/inputs.py)",
-            "config": {"workload": s.name + (" (BASELINE configs[1]: PE 12x16x14 cells, 32,256 atoms, 300 K, "
-                                             "dt 0.5 fs, NVE, LJ cutoff 3 sigma, torsion on)" if ws == 1 else
-                                             f" (cfg2 block per GPU along x, {ws} slabs)"),
-                       "atoms": n_atoms, "dt_fs": s.dt, "precision": args.precision, "potential": args.potential,
-                       "parallelism": "single GPU" if ws == 1 else f"slab{ws} (x slabs, NCCL halo send/recv)",
-                       "l2": "flushed between timed steps (256 MiB write)",
-                       "timed_step": "ab_run_nve(1): integrate, rebuild check, forces, integrate"},
+            "config": config_dict(s, args, ws),
             "roofline": roofline(main, args.precision),
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -395,7 +418,7 @@ def run_ours(args, ws, rank, local):
             "peak_measured_fma_tflops": peak_meas,
             "counters": {k: st[k] for k in ("n_lj", "n_C0", "n_bstar", "n_sb_trans", "n_bonds", "n_quads",
                                             "n_rebuilds", "timed_rebuilds", "n_ghosts")},
-            "step_ms_all": [round(t, 4) for t in main["times"]],
+            "thermo_rows_per_call": args.steps // args.thermo + 1,
         }
         if "mixed" in res and args.precision == "fp64":
             r = res["mixed"]
@@ -407,40 +430,80 @@ def run_ours(args, ws, rank, local):
         dist.destroy_process_group()
 
 
-def cpu_oracle_baseline(s, budget_s=15.0, max_steps=20):
+def sample_block(config):
+    """A bounded CPU sample of the workload: the same crystal / chemistry in a periodic block the
+    oracle steps in well under a second per step on the host's cores (per-atom work of a periodic
+    crystal does not depend on the block size).  cfg 1-3: the config itself."""
+    from paper_1810_07026_b200 import inputs as I
+    if config in (4, "5b"):
+        return I.polyethylene((12, 16, 14), 0.02, 104, 204, name="pe-12x16x14-sample")  # 32,256 atoms
+    if config == "5a":
+        return I.diamond((16, 16, 16), 0.03, 105, 205, name="diamond-16^3-sample")  # 32,768 atoms
+    return I.config(config)
+
+
+def cpu_oracle_baseline(s, args):
+    """The oracle as it stands: (i) all host cores on the FULL workload, one force
+    evaluation timed and extrapolated to atom-steps/s (cfgs 4-5 rule: the oracle rebuilds its lists
+    and AD forces every evaluation, the integration is negligible); (ii) one thread, ONE
+    velocity-Verlet NVE call of a few steps on the bounded sample block (K steps = K + 1
+    evaluations, all counted against K steps)."""
     from oracle import oracle as O
     cores = os.cpu_count() or 1
-    x, v = s.x.copy(), s.v.copy()
-    steps = 0
     t0 = time.perf_counter()
-    while steps < max_steps and time.perf_counter() - t0 < budget_s:
-        x, v, _ = O.nve(s.types, x, v, s.box, 1, s.dt, every=0, threads=cores)
-        steps += 1
-    t = time.perf_counter() - t0
-    return {"value": s.n * steps / t, "unit": "atom-steps/s", "cores": cores, "kind": "oracle",
-            "sample": f"{steps} velocity-Verlet steps of the full {s.n}-atom {s.name} (oracle recomputes lists and "
-                      f"AD forces from scratch every step), {t:.1f} s wall"}
+    O.compute(s.types, s.x, s.box, threads=cores)
+    t_all = time.perf_counter() - t0
+    b = sample_block(args.config)
+    k1 = 2
+    t0 = time.perf_counter()
+    O.nve(b.types, b.x, b.v, b.box, k1, b.dt, every=0, threads=1)
+    t_one = time.perf_counter() - t0
+    return {"value": s.n / t_all, "unit": "atom-steps/s", "cores": cores, "kind": "oracle",
+            "sample": f"one full force evaluation (lists + energy + AD forces + virial) of the {s.n}-atom {s.name} "
+                      f"on {cores} threads, {t_all:.1f} s wall, extrapolated as 1 evaluation per step",
+            "single_thread": {"value": b.n * k1 / t_one, "unit": "atom-steps/s", "cores": 1,
+                              "sample": f"one oracle NVE call of {k1} steps ({k1 + 1} evaluations) of {b.name} "
+                                        f"({b.n} atoms), {t_one:.1f} s wall"},
+            "host": host_info()}
+
+
+def host_info():
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": model}
 
 
 # ------------------------------------------------------------------ reference arm (the oracle)
 def run_reference(args, ws, rank, local):
+    """The oracle as it stands on the host cores, rank 0 only.  Each step is a bounded sample of the
+    workload: one oracle NVE call of K steps (after W warm-up steps) on sample_block(config), the
+    same crystal in a ~32 k-atom periodic block, value = sample atoms x K / wall seconds."""
     if rank != 0:
         return
     from oracle import oracle as O
     s = workload(args.config, ws, args.scaling)
+    b = sample_block(args.config)
     cores = os.cpu_count() or 1
-    x, v = s.x.copy(), s.v.copy()
-    x, v, _ = O.nve(s.types, x, v, s.box, args.warmup, s.dt, every=0, threads=cores)
+    x, v = b.x.copy(), b.v.copy()
+    x, v, _ = O.nve(b.types, x, v, b.box, args.warmup, b.dt, every=0, threads=cores)
     t0 = time.perf_counter()
-    x, v, _ = O.nve(s.types, x, v, s.box, args.steps, s.dt, every=0, threads=cores)
+    x, v, _ = O.nve(b.types, x, v, b.box, args.steps, b.dt, every=0, threads=cores)
     t = time.perf_counter() - t0
-    val = s.n * args.steps / t
+    val = b.n * args.steps / t
+    sample = (f"one oracle NVE call of {args.steps} steps ({args.steps + 1} evaluations) of {b.name} ({b.n} atoms), "
+              f"a periodic block of the workload's crystal, after {args.warmup} warm-up steps; {t:.1f} s wall")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "atom-steps/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": s.name + " (BASELINE configs[1])", "atoms": s.n, "dt_fs": s.dt},
-            "cpu_baseline": {"value": val, "unit": "atom-steps/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{args.steps} NVE steps of the full {s.n}-atom workload"},
+            "scaling": "weak" if ws == 1 else args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(s, args, ws),
+            "cpu_baseline": {"value": val, "unit": "atom-steps/s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": val, "unit": "atom-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -452,14 +515,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed", "single"])
-    ap.add_argument("--config", default=2, type=lambda v: int(v) if v.isdigit() else v)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--config", default=4, type=lambda v: int(v) if v.isdigit() else v)
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"])
+    ap.add_argument("--thermo", type=int, default=10, help="thermo row every THERMO steps (SURVEY §8(d): 10)")
     ap.add_argument("--potential", default="airebo", choices=["airebo", "rebo", "airebo-m"])
     ap.add_argument("--no-mixed", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
+    if args.scaling is None:
+        args.scaling = default_scaling(args.config)
     args.warmup = max(3, args.warmup)
     ws, rank, local = dist_env()
     if args.impl == "reference":

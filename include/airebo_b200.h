@@ -138,7 +138,8 @@ ab_status ab_set_box(ab_engine* e, const double L[3]);
  * at the next compute. */
 ab_status ab_set_atoms(ab_engine* e, int64_t n, const int32_t* type, const double* xyz);
 /* New positions for the same n atoms (caller order).  Lists are rebuilt only if some atom moved
- * more than skin/2 since the last build. */
+ * more than skin/2 since the last build.  A non-finite coordinate fails with
+ * AB_E_NONFINITE before anything is copied (engine state unchanged). */
 ab_status ab_set_positions(ab_engine* e, const double* xyz);
 ab_status ab_set_velocities(ab_engine* e, const double* v /* n*3, Angstrom/fs */);
 
@@ -167,6 +168,16 @@ ab_status ab_get_forces(ab_engine* e, double* f);       /* forces of the last ev
 /* Lists of the current positions as rows (i, j, sx, sy, sz), i and j caller indices, s the image
  * of j (position x_j + s L), sorted lexicographically.  rows == NULL: *count = number of rows. */
 ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows);
+
+/* Order-independent digest of the same row set, for lists too large to return as rows (the LJ
+ * half list of a 2 M-atom system has ~7e8 rows; the bit-exact list comparison of BASELINE's
+ * north star at full size, SURVEY reading A26).  With mix(z) = splitmix64's finaliser
+ *   z += 0x9e3779b97f4a7c15; z = (z ^ z>>30) * 0xbf58476d1ce4e5b9; z = (z ^ z>>27) * 0x94d049bb133111eb;
+ *   mix = z ^ z>>31
+ * each row hashes to h = mix(((u64)(u32)i << 32 | (u32)j) ^ mix((sx+128) << 16 | (sy+128) << 8 | (sz+128))),
+ * and digest = {number of rows, sum of h mod 2^64, xor of h}.  Output: digest[3] (caller-owned).
+ * Errors as ab_get_list. */
+ab_status ab_get_list_digest(ab_engine* e, ab_list which, uint64_t digest[3]);
 
 ab_status ab_get_stats(ab_engine* e, ab_stats* s);
 

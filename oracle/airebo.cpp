@@ -982,6 +982,48 @@ int oracle_list(const char* params, int n, const int* type, const double* x, con
   return 0;
 }
 
+// compute + the order-independent digests {count, sum h, xor h} of the three lists (rows as in
+// oracle_list; h = mix(((u64)(u32)i << 32 | (u32)j) ^ mix((sx+128) << 16 | (sy+128) << 8 | (sz+128))),
+// mix = splitmix64's finaliser) from ONE list build: the full-size parity tests compare lists of
+// ~1e9 rows this way.  dig: 9 u64 (short, bonds, LJ).
+static inline unsigned long long dmix(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+int oracle_compute_digest(const char* params, int n, const int* type, const double* x, const double* box, double* F,
+                          double* E3, double* W6, long long* cnt, int nthreads, unsigned long long* dig) {
+  Params P;
+  if (!load(params, P)) return -2;
+  Sys S{n, type, x, {box[0], box[1], box[2]}};
+  Lists Lo;
+  Opts o;
+  o.forces = F != nullptr || W6 != nullptr;
+  o.nthreads = nthreads;
+  build_lists(P, S, false, true, Lo);
+  Acc acc;
+  compute(P, S, Lo, o, acc);
+  if (F) std::memcpy(F, acc.F.data(), sizeof(double) * 3 * (size_t)n);
+  if (E3) std::memcpy(E3, acc.E, sizeof(acc.E));
+  if (W6) std::memcpy(W6, acc.W, sizeof(acc.W));
+  if (cnt) std::memcpy(cnt, acc.cnt, sizeof(acc.cnt));
+  for (int which = 0; which < 3; ++which) {
+    unsigned long long c = 0, sum = 0, xr = 0;
+    for (int i = 0; i < n; ++i)
+      for (const Nb& e : which == 2 ? Lo.lj[i] : Lo.shortl[i]) {
+        if (which == 1 && !canonical(i, e.j, e.s)) continue;
+        unsigned long long a = ((unsigned long long)(unsigned)i << 32) | (unsigned)e.j;
+        unsigned long long b = ((unsigned long long)(e.s[0] + 128) << 16) | ((unsigned long long)(e.s[1] + 128) << 8) |
+                               (unsigned long long)(e.s[2] + 128);
+        unsigned long long h = dmix(a ^ dmix(b));
+        ++c, sum += h, xr ^= h;
+      }
+    dig[3 * which] = c, dig[3 * which + 1] = sum, dig[3 * which + 2] = xr;
+  }
+  return 0;
+}
+
 // Stage outputs for stage-wise parity: per REBO half bond (canonical order of
 // oracle_list(which=1)) the values b, p_ij, p_ji, pi^rc, pi^dh, N_ij, N_ji, N^conj (8 per bond);
 // per LJ half pair (order of which=2): C_ij, b* (0 if not evaluated), Q, E (4 per pair).

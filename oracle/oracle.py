@@ -40,6 +40,8 @@ def lib():
         L = C.CDLL(LIB)
         dp, ip, lp = C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_longlong)
         L.oracle_compute.argtypes = [C.c_char_p, C.c_int, ip, dp, dp, dp, dp, dp, lp, C.c_int, C.c_int]
+        L.oracle_compute_digest.argtypes = [C.c_char_p, C.c_int, ip, dp, dp, dp, dp, dp, lp, C.c_int,
+                                            C.POINTER(C.c_ulonglong)]
         L.oracle_forces_sampled.argtypes = [C.c_char_p, C.c_int, ip, dp, dp, C.c_int, ip, dp, C.c_int]
         L.oracle_list.argtypes = [C.c_char_p, C.c_int, ip, dp, dp, C.c_int, lp, lp, C.c_int]
         L.oracle_stages.argtypes = [C.c_char_p, C.c_int, ip, dp, dp, dp, dp]
@@ -88,6 +90,25 @@ def compute(types, x, box, params=None, forces=True, brute=False, lj=True, rebo=
                                 _p(cnt, C.c_longlong), nt, flags))
     return dict(E=float(E3.sum()), terms=E3, F=F, W=W if forces else None,
                 counters={k: int(v) for k, v in zip(COUNTERS, cnt)})
+
+
+def compute_digest(types, x, box, params=None, threads=None):
+    """compute() (forces, energy terms, virial, counters) plus the order-independent digests
+    {count, sum h, xor h} of the short list, the REBO half bonds and the LJ half pairs from one
+    list build (ab_get_list_digest's definition; full-size list parity)."""
+    t, xx, b = _prep(types, x, box)
+    n = t.shape[0]
+    F = np.zeros((n, 3))
+    W = np.zeros(6)
+    E3 = np.zeros(3)
+    cnt = np.zeros(len(COUNTERS), dtype=np.int64)
+    dig = np.zeros(9, dtype=np.uint64)
+    nt = threads or os.cpu_count() or 1
+    _check(lib().oracle_compute_digest(params or params_text(), n, _p(t, C.c_int), _p(xx, C.c_double),
+                                       _p(b, C.c_double), _p(F, C.c_double), _p(E3, C.c_double), _p(W, C.c_double),
+                                       _p(cnt, C.c_longlong), nt, _p(dig, C.c_ulonglong)))
+    return dict(E=float(E3.sum()), terms=E3, F=F, W=W, counters={k: int(v) for k, v in zip(COUNTERS, cnt)},
+                digest=[tuple(int(v) for v in dig[3 * w:3 * w + 3]) for w in range(3)])
 
 
 def forces_sampled(types, x, box, sample, params=None, threads=None):

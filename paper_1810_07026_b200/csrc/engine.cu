@@ -258,7 +258,7 @@ struct ab_engine {
   long long graph_epoch = -1;    // layout version the graph was captured at
   long long layout = 0;          // bumped whenever buffers / capacities / kernel choices change
   double disp1 = -1.0, disp2 = -1.0;  // max displacement since the last build at the last two steps
-  unsigned long long h_flag[2] = {0, 0};
+  unsigned long long* h_flag = nullptr;  // pinned: the D2H of the reduced flags must not block the host
   double* h_th = nullptr;  // pinned staging of thermo rows
   size_t h_th_cap = 0;
   // host-side time breakdown of the NVE loop (AB_HOST_TIMING=1: printed by ab_destroy)
@@ -467,6 +467,9 @@ ab_status bind_consts(ab_engine* e) {
   for (int c = 0; c < 3; ++c) g.L[c] = e->L[c];
   g.mass[0] = hp.mass[0], g.mass[1] = hp.mass[1], g.ftm2v = hp.ftm2v, g.mvv2e = hp.mvv2e;
   g.potential = hp.potential;
+  // the banks are process-wide: kernels of the previous owner (or of this engine, after a box
+  // change) may still be in flight on other streams -- rewrite them only when the device is idle
+  CK(cudaDeviceSynchronize());
   CK(cudaMemcpyToSymbolAsync(c_geo, &g, sizeof(Geo), 0, cudaMemcpyHostToDevice, e->st));
   CK(cudaMemcpyToSymbolAsync(c_tabd, &e->td, sizeof(e->td), 0, cudaMemcpyHostToDevice, e->st));
   CK(cudaMemcpyToSymbolAsync(c_tabf, &e->tf, sizeof(e->tf), 0, cudaMemcpyHostToDevice, e->st));
@@ -950,7 +953,8 @@ ab_status halo_finish(ab_engine* e) {
 ab_status rebuild_all(ab_engine* e) {
   prof_begin(e, 5);
   auto D = doms(e);
-  for (ab_engine* d : D) d->ghosts_fresh = d->scratch_zeroed = false;  // the rebuild regenerates the images
+  // the rebuild regenerates the images and may reallocate F (F.ensure keeps no contents)
+  for (ab_engine* d : D) d->ghosts_fresh = d->scratch_zeroed = d->f_zeroed = false;
   if (!slabbed(e)) {
     auto t0 = std::chrono::steady_clock::now();
     setup_grid(e);
@@ -1504,7 +1508,9 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
             cudaMemset(e->scratch.p, 0, SCRATCH_BYTES) == cudaSuccess &&
             cudaMallocHost(&e->h_ct, sizeof(unsigned long long) * (CT_N + 1)) == cudaSuccess &&
             cudaMallocHost(&e->h_acc, sizeof(double) * ACC_N) == cudaSuccess &&
-            cudaMallocHost(&e->h_small, sizeof(int) * 8) == cudaSuccess;
+            cudaMallocHost(&e->h_small, sizeof(int) * 8) == cudaSuccess &&
+            cudaMallocHost(&e->h_flag, sizeof(unsigned long long) * 2) == cudaSuccess;
+  if (ok) e->h_flag[0] = e->h_flag[1] = 0;
   static_assert(sizeof(double) * ACC_N <= SCRATCH_CT, "scratch layout");
   static_assert(SCRATCH_CT + sizeof(unsigned long long) * (CT_N + 1) <= SCRATCH_SMALL, "scratch layout");
   ok = ok && cudaHostGetDevicePointer((void**)&e->h_ct_dev, e->h_ct, 0) == cudaSuccess;
@@ -1582,6 +1588,7 @@ void free_engine(ab_engine* e) {
   if (e->h_ct) cudaFreeHost(e->h_ct);
   if (e->h_acc) cudaFreeHost(e->h_acc);
   if (e->h_small) cudaFreeHost(e->h_small);
+  if (e->h_flag) cudaFreeHost(e->h_flag);
   if (e->h_th) cudaFreeHost(e->h_th);
   if (e->ev_disp) cudaEventDestroy(e->ev_disp);
   for (auto& p : e->pending) cudaEventDestroy(p.a), cudaEventDestroy(p.b);
@@ -1685,7 +1692,8 @@ static bool host_pinned(const void* p) {
     cudaGetLastError();
     return false;
   }
-  return a.type == cudaMemoryTypeHost;
+  // page-locked and managed memory are both read by the DMA after cudaMemcpyAsync returns
+  return a.type != cudaMemoryTypeUnregistered;
 }
 
 ab_status from_caller_vel(ab_engine* e, const double* host) {
@@ -1883,7 +1891,7 @@ ab_status ab_set_box(ab_engine* e, const double L[3]) {
   e->lists_valid = e->forces_valid = false;
   TRY(check_slab_box(e));
   if (g_const_owner == e) g_const_owner = nullptr;
-  if (e->gexec) cudaGraphExecDestroy(e->gexec);  // box changed: reload the constants
+  graph_drop(e);  // box changed: the captured graph is stale; reload the constants
   return bind_consts(e);
 }
 
@@ -1928,6 +1936,14 @@ static ab_status need_atoms(ab_engine* e) {
 ab_status ab_set_positions(ab_engine* e, const double* xyz) {
   TRY(need_atoms(e));
   if (bad_ptr(e, xyz, "xyz")) return AB_E_ARG;
+  {
+    const int64_t n = slabbed(e) ? e->Nglob : e->N;
+    for (int64_t i = 0; i < 3 * n; ++i)
+      if (!std::isfinite(xyz[i])) {
+        e->err = "non-finite coordinate of atom " + std::to_string(i / 3);
+        return AB_E_NONFINITE;
+      }
+  }
   TRY(flush_kick(e));
   if (!slabbed(e)) {
     CK(cudaMemcpyAsync(e->io.p, xyz, sizeof(double) * 3 * e->N, cudaMemcpyHostToDevice, e->st));
@@ -2269,8 +2285,10 @@ ab_status ab_get_forces(ab_engine* e, double* f) {
   return to_caller(e, 2, f);
 }
 
-// rows of one domain's list (canonical rows only for bonds / LJ)
-static ab_status list_rows(ab_engine* e, ab_engine* d, ab_list which, std::vector<std::array<int64_t, 5>>& out) {
+extern "C++" {
+// rows of one domain's list (canonical rows only for bonds / LJ), handed to visit(i, j, sx, sy, sz)
+template <class Visit>
+static ab_status list_visit(ab_engine* e, ab_engine* d, ab_list which, Visit&& visit) {
   const int N = d->N, NT = d->NT;
   std::vector<int> gid(NT);
   std::vector<char4> sh(NT);
@@ -2317,10 +2335,22 @@ static ab_status list_rows(ab_engine* e, ab_engine* d, ab_list which, std::vecto
           double rc = d->hp.pr[type_h(i) + type_h(J)].rc;
           if (!(r2 <= rc * rc)) continue;
         }
-        out.push_back({gid[i], gid[J], s.x, s.y, s.z});
+        visit(gid[i], gid[J], s.x, s.y, s.z);
       }
   return AB_OK;
 }
+static ab_status list_rows(ab_engine* e, ab_engine* d, ab_list which, std::vector<std::array<int64_t, 5>>& out) {
+  return list_visit(e, d, which, [&](int i, int j, int sx, int sy, int sz) { out.push_back({i, j, sx, sy, sz}); });
+}
+
+// order-independent row digest (header: ab_get_list_digest)
+static inline uint64_t dig_mix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+}  // extern "C++"
 
 ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows) {
   TRY(need_atoms(e));
@@ -2340,6 +2370,29 @@ ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows
   if (rows)
     for (size_t r = 0; r < out.size(); ++r)
       for (int c = 0; c < 5; ++c) rows[5 * r + c] = out[r][c];
+  return AB_OK;
+}
+
+ab_status ab_get_list_digest(ab_engine* e, ab_list which, uint64_t digest[3]) {
+  TRY(need_atoms(e));
+  if (bad_ptr(e, digest, "digest")) return AB_E_ARG;
+  if (which != AB_LIST_SHORT && which != AB_LIST_BONDS && which != AB_LIST_LJ) {
+    e->err = "unknown list";
+    return AB_E_ARG;
+  }
+  if (!e->forces_valid) {
+    TRY(prepare_all(e, true));
+    TRY(forces_all(e));
+  }
+  uint64_t c = 0, sum = 0, x = 0;
+  for (ab_engine* d : doms(e))
+    TRY(list_visit(e, d, which, [&](int i, int j, int sx, int sy, int sz) {
+      uint64_t a = ((uint64_t)(uint32_t)i << 32) | (uint32_t)j;
+      uint64_t b = ((uint64_t)(sx + 128) << 16) | ((uint64_t)(sy + 128) << 8) | (uint64_t)(sz + 128);
+      uint64_t h = dig_mix(a ^ dig_mix(b));
+      ++c, sum += h, x ^= h;
+    }));
+  digest[0] = c, digest[1] = sum, digest[2] = x;
   return AB_OK;
 }
 

@@ -41,7 +41,8 @@ EXPORTS = ["ab_create", "ab_destroy", "ab_last_error", "ab_set_stream", "ab_set_
            "ab_set_positions", "ab_set_velocities", "ab_compute", "ab_run_nve", "ab_get_positions",
            "ab_get_velocities", "ab_get_forces", "ab_get_list", "ab_get_stats", "ab_record_stages", "ab_get_stage",
            "ab_set_profiling", "ab_get_phase_ms", "ab_peak_flops", "ab_device_info", "ab_nccl_unique_id",
-           "ab_create_dist", "ab_create_virtual", "ab_slab_info", "ab_slab_of", "ab_set_concurrency"]
+           "ab_create_dist", "ab_create_virtual", "ab_slab_info", "ab_slab_of", "ab_set_concurrency",
+           "ab_get_list_digest"]
 
 _lib = None
 
@@ -71,6 +72,7 @@ def load(path: str = LIB_PATH):
     L.ab_get_velocities.argtypes = [vp, dp]
     L.ab_get_forces.argtypes = [vp, dp]
     L.ab_get_list.argtypes = [vp, C.c_int, i64p, i64p]
+    L.ab_get_list_digest.argtypes = [vp, C.c_int, C.POINTER(C.c_uint64)]
     L.ab_get_stats.argtypes = [vp, C.POINTER(ABStats)]
     L.ab_record_stages.argtypes = [vp, C.c_int]
     L.ab_get_stage.argtypes = [vp, C.c_int, i64p, dp]
@@ -223,6 +225,12 @@ class Engine:
         rows = np.zeros((cnt.value, 5), dtype=np.int64)
         self._ck(self.L.ab_get_list(self.h, which, C.byref(cnt), rows.ctypes.data_as(C.POINTER(C.c_int64))))
         return rows
+
+    def list_digest(self, which):
+        """(count, sum h, xor h) of the list's rows (ab_get_list_digest)."""
+        d = (C.c_uint64 * 3)()
+        self._ck(self.L.ab_get_list_digest(self.h, which, d))
+        return tuple(int(v) for v in d)
 
     def stats(self):
         s = ABStats()

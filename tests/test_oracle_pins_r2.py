@@ -265,3 +265,23 @@ def test_nconj_resummation_periodic_multi_image():
     """cfg1-type PE cell 1x1x2 with jitter: a chain meets its own periodic image along c."""
     s = I.polyethylene((1, 1, 2), 0.05, 7, None)
     check_resum(s.types, s.x, s.box)
+
+
+# ------------------------------------------------------------------ list digests (full-size list parity)
+def test_oracle_list_digest_matches_rows():
+    """oracle.compute_digest's three digests equal the numpy digest of oracle.get_list's rows, and
+    its forces / energies / counters are those of oracle.compute (same list build)."""
+    from tests.digest import digest
+    for s in (I.config(1), I.random_cluster(30, 1, spread=5.0, dmin=1.0), I.diamond((1, 1, 1), 0.05, 9)):
+        d = O.compute_digest(s.types, s.x, s.box)
+        for which in range(3):
+            assert d["digest"][which] == digest(O.get_list(s.types, s.x, s.box, which)), (s.name, which)
+        o = O.compute(s.types, s.x, s.box)
+        assert d["E"] == o["E"] and np.array_equal(d["F"], o["F"]) and d["counters"] == o["counters"]
+    # the digest separates sets that differ in one image shift or one index
+    r = O.get_list(I.config(1).types, I.config(1).x, I.config(1).box, 2)
+    r2 = r.copy()
+    r2[5, 4] += 1
+    r3 = r.copy()
+    r3[7, 1] += 1
+    assert digest(r) != digest(r2) and digest(r) != digest(r3)
