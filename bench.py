@@ -163,18 +163,19 @@ class ClockSampler:
 
 
 def algorithmic_flops(stats):
-    """Per-phase algorithmic flop counts per launch (SURVEY §8(d) op weights; DESIGN.md §Roofline).
-    LJ: 31 flops per half pair inside r_c, 9 per half list entry outside (skin); REBO: 700 per
-    bond (pair terms, P, pi^rc, T) + 65 per angle term + 260 per dihedral quad (pi^dh + torsion,
-    forward and reverse); b*: 1500 per evaluated pair; short list: 15 per entry."""
-    far_in, far_ent = stats["n_lj_far"], stats["n_lj_entries_far"] // 2
-    near_in, near_ent = stats["n_lj"] - far_in, (stats["n_lj_entries"] - stats["n_lj_entries_far"]) // 2
+    """Per-phase algorithmic flop counts per launch (SURVEY §8(d) op weights; DESIGN.md §5).
+    LJ: 31 flops per half pair inside r_c + 25 more per half pair in the taper band, split between
+    the near-pair kernel (k_lj_near: pairs that may need C_ij / b*) and the far-pair kernel
+    (k_lj_far, n_lj_far pairs, every taper pair); REBO: 700 per bond (pair terms, P, pi^rc, T) + 65
+    per angle term + 260 per dihedral quad (pi^dh + torsion, forward and reverse); b*: 1500 per
+    evaluated pair; short list: 15 per entry.  Skin entries are overhead, not algorithmic work."""
     rebo = 700 * stats["n_bonds"] + 65 * stats["n_angles"] + 260 * stats["n_quads"]
-    return {"short": 15 * stats["n_short"], "rebo": rebo, "lj_near": 31 * near_in + 9 * max(0, near_ent - near_in),
-            "bstar": 1500 * stats["n_bstar"], "lj_far": 31 * far_in + 9 * max(0, far_ent - far_in)}
+    far = stats["n_lj_far"]
+    return {"short": 15 * stats["n_short"], "rebo": rebo, "lj_near": 31 * (stats["n_lj"] - far),
+            "bstar": 1500 * stats["n_bstar"], "lj_far": 31 * far + 25 * stats["n_lj_taper"]}
 
 
-PHASES = ["short", "rebo", "lj_near", "bstar", "integrate", "rebuild", "lj_far", "comm"]
+PHASES = ["short", "rebo", "lj_near", "bstar", "integrate", "rebuild", "lj_far", "comm"]  # ab_get_phase_ms slots
 KERNEL_OF = {"short": "k_short", "rebo": "k_rebo", "lj_near": "k_lj_near", "bstar": "k_bstar", "lj_far": "k_lj_far"}
 
 

@@ -73,10 +73,12 @@ typedef struct ab_stats {
   int64_t n_badarg;    /* p^{sigma pi} arguments <= 0 (must be 0) */
   int64_t n_atoms, n_ghosts, n_rebuilds, n_steps, n_overflow_retries;
   int64_t lj_capacity, inter_capacity;
-  int64_t n_lj_entries; /* skinned full LJ-list entries streamed (both directions) */
+  int64_t n_lj_entries; /* LJ atom slots streamed (both directions): cluster slots (4 per listed
+                           cluster) with AB_LJ_CLUSTER=1, else skinned list entries */
   int64_t n_angles;     /* bond-order angle terms (k in N(i)\j plus l in N(j)\i, per half bond) */
-  int64_t n_lj_far;     /* ... of n_lj, pairs evaluated by the far-pair kernel (C = Q = 1 by construction) */
+  int64_t n_lj_far;     /* ... of n_lj, pairs of the far-pair kernel (AB_LJ_CLUSTER=1: pairs with r > 3 r_max) */
   int64_t n_lj_entries_far;
+  int64_t n_lj_taper;   /* ... of n_lj, pairs in the taper band r_lo < r <= r_c (reading A10) */
 } ab_stats;
 
 /* Create an engine on CUDA device `cuda_device` from parameter-file text (params/toy_ch.param
@@ -191,8 +193,9 @@ ab_status ab_record_stages(ab_engine* e, int on);
 ab_status ab_get_stage(ab_engine* e, int stage, int64_t* count, double* out);
 
 /* Per-phase device timing with CUDA events on the engine's stream (the paper's profile labels,
- * P:359-360): phase 0 short list + N_i, 1 REBO + bond order + torsion, 2 LJ near
- * pairs + C_ij reach sets, 3 b* batch, 4 integrator, 5 list rebuild, 6 LJ far pairs, 7 slab transfers
+ * P:359-360): phase 0 short list + N_i, 1 REBO + bond order + torsion, 2 LJ pairs +
+ * C_ij reach sets (the near pairs; every pair with AB_LJ_CLUSTER=1), 3 b* batch,
+ * 4 integrator, 5 list rebuild, 6 LJ far pairs (none with AB_LJ_CLUSTER=1), 7 slab transfers
  * (halo positions, ghost forces, migration; multi-domain engines only).
  * ab_get_phase_ms returns accumulated milliseconds ms[AB_NPHASE] and launch counts n[AB_NPHASE]
  * since profiling was switched on (on != 0 resets them). */

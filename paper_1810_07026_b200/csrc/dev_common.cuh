@@ -439,6 +439,7 @@ enum {
   CT_ANGLES,      // bond-order angle terms
   CT_LJFAR,       // canonical LJ pairs within r_c handled by the far kernel
   CT_LJENTFAR,    // far-list entries streamed
+  CT_LJTAPER,     // canonical LJ pairs in the taper band r_lo < r <= r_c
   CT_N
 };
 

@@ -34,6 +34,7 @@
 #include "k_dist.cuh"
 #include "k_lists.cuh"
 #include "k_lj.cuh"
+#include "k_ljc.cuh"
 #include "k_misc.cuh"
 #include "params.h"
 
@@ -183,6 +184,12 @@ struct ab_engine {
   DBuf<signed char> typ;
   DBuf<int> ljc[3], ljn[3], in_cnt, in_nbr;  // LJ near / pure / band lists, intermediate list
   int capL[3] = {0, 0, 0};
+  // j-cluster LJ path (k_cluster.cuh, k_ljc.cuh), AB_LJ_CLUSTER=1; default: per-atom near / far lists
+  bool cl_path = false;
+  ClGrid clg{};
+  int nrun = 0, NCL = 0, capC = 0;
+  DBuf<int> cl_k, cl_v, cl_k2, cl_v2, run_start, run_cl, cl_atom, clc, cln;
+  DBuf<double4> cpos, cbb;
   bool want_virial = true;
   DBuf<int> s_cnt, s_nbr;
   DBuf<unsigned char> s_dr, s_w, s_N;  // typed by precision at use
@@ -642,6 +649,59 @@ ab_status sort_locals(ab_engine* e) {
   return AB_OK;
 }
 
+// j-clusters of all atoms (locals + ghosts) for the LJ pair loop (k_cluster.cuh): columns of
+// ~2.5 A over the padded region, runs by (column, species), z-sorted, chopped into groups of 4
+ab_status build_clusters(ab_engine* e) {
+  const int NT = e->NT;
+  cudaStream_t st = e->st;
+  ClGrid& g = e->clg;
+  double span[3];
+  for (int c = 0; c < 3; ++c) g.lo[c] = e->grid.lo[c], span[c] = e->grid.nc[c] * e->grid.cs[c];
+  double cw = 2.5;
+  if (const char* v = std::getenv("AB_CL_COL")) cw = std::max(1.0, std::atof(v));
+  const double Rm = e->rcmax + e->hp.skin;
+  auto nside = [&](double w) { return 2 * ((int)std::ceil(Rm / w) + 1) + 1; };
+  while (std::floor(span[0] / cw) * std::floor(span[1] / cw) * 2 > CL_RUNS_MAX ||
+         2 * nside(cw) * nside(cw) > CL_MAXRUN)
+    cw *= 1.05;
+  g.ncx = std::max(1, (int)std::floor(span[0] / cw));
+  g.ncy = std::max(1, (int)std::floor(span[1] / cw));
+  g.cw[0] = span[0] / g.ncx, g.cw[1] = span[1] / g.ncy;
+  g.zspan = span[2];
+  e->nrun = g.ncx * g.ncy * 2;
+  CK(e->cl_k.ensure(NT));
+  CK(e->cl_v.ensure(NT));
+  CK(e->cl_k2.ensure(NT));
+  CK(e->cl_v2.ensure(NT));
+  CK(e->run_start.ensure(e->nrun + 1));
+  CK(e->run_cl.ensure(e->nrun + 1));
+  k_cl_keys<<<nblk(NT, 256), 256, 0, st>>>(NT, e->pos.p, g, e->cl_k.p, e->cl_v.p);
+  CKL();
+  size_t need = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, need, e->cl_k.p, e->cl_k2.p, e->cl_v.p, e->cl_v2.p, NT, 0, 31, st);
+  CK(e->cub_tmp.ensure(need));
+  size_t have = e->cub_tmp.n;
+  CK(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, have, e->cl_k.p, e->cl_k2.p, e->cl_v.p, e->cl_v2.p, NT, 0, 31, st));
+  ++e->launches;
+  k_cl_run_bounds<<<nblk(NT + 1, 256), 256, 0, st>>>(NT, e->nrun, e->cl_k2.p, e->run_start.p);
+  CKL();
+  k_cl_run_scan<<<1, 1024, 0, st>>>(e->nrun, e->run_start.p, e->run_cl.p);
+  CKL();
+  int ncl = 0;
+  CK(cudaMemcpyAsync(&ncl, e->run_cl.p + e->nrun, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  e->NCL = ncl;
+  CK(e->cl_atom.ensure((size_t)CL_SIZE * ncl + 1));
+  CK(e->cpos.ensure((size_t)CL_SIZE * ncl + 1));
+  CK(e->cbb.ensure(2 * (size_t)ncl + 1));
+  CK(cudaMemsetAsync(e->cl_atom.p, 0xff, sizeof(int) * CL_SIZE * (size_t)ncl, st));
+  k_cl_fill<<<nblk(NT, 256), 256, 0, st>>>(NT, e->cl_k2.p, e->cl_v2.p, e->run_start.p, e->run_cl.p, e->cl_atom.p);
+  CKL();
+  k_cl_bbox<<<nblk(ncl, 128), 128, 0, st>>>(ncl, e->cl_atom.p, e->pos.p, e->cbb.p, e->cpos.p);
+  CKL();
+  return AB_OK;
+}
+
 // images of the base atoms [0, NX) + binning of all atoms + skinned lists.  On entry: locals
 // sorted at [0, N), x-ghosts (slab domains) at [N, NX) with their bookkeeping set.
 ab_status images_and_lists(ab_engine* e) {
@@ -706,6 +766,8 @@ ab_status images_and_lists(ab_engine* e) {
   ++e->launches;
   k_cell_bounds<<<nblk(NT + 1, 256), 256, 0, st>>>(NT, e->ncell, e->key2.p, e->cell_start.p);
   CKL();
+  const bool clp = e->cl_path && e->hp.potential != kREBO;
+  if (clp) TRY(build_clusters(e));
   e->rb_ms[2] += tms(tq);
   tq = std::chrono::steady_clock::now();
   // 4. skinned lists: LJ (local atoms, full) and intermediate REBO (all atoms)
@@ -730,6 +792,12 @@ ab_status images_and_lists(ab_engine* e) {
     e->capL[2] = 32 + (int)(1.3 * rho * fpi * (r2 * r2 * r2 - std::min(r1, rnear) * std::min(r1, rnear) * std::min(r1, rnear)));
   }
   if (e->capI == 0) e->capI = 16;
+  if (clp && e->capC == 0) {  // clusters within r_c,max + skin + a cluster extent, 4 slots each
+    double vol = e->L[0] * e->L[1] * e->L[2];
+    if (slabbed(e)) vol = (e->xhi - e->xlo) * e->L[1] * e->L[2];
+    const double rho = std::max(N, 1) / vol, R = e->rcmax + skin + 2.5;
+    e->capC = 32 + (int)(1.4 * rho * 4.18879020478639 * R * R * R / CL_SIZE / 0.8);
+  }
   LJLists Lg;
   Lg.near2 = rnear * rnear;
   for (int p = 0; p < 3; ++p) {
@@ -744,7 +812,7 @@ ab_status images_and_lists(ab_engine* e) {
   Lg.reach = (e->rcmax + skin) * (1.0 + 1e-9) + 1e-9;
   for (int attempt = 0; attempt < 4; ++attempt) {
     for (int c = 0; c < 3; ++c) {
-      CK(e->ljn[c].ensure((size_t)N * e->capL[c]));
+      if (!clp) CK(e->ljn[c].ensure((size_t)N * e->capL[c]));
       Lg.cap[c] = e->capL[c];
       Lg.cnt[c] = e->ljc[c].p;
       Lg.nbr[c] = e->ljn[c].p;
@@ -756,7 +824,16 @@ ab_status images_and_lists(ab_engine* e) {
     if (dbg)
       for (auto& x : dbg_ev) cudaEventCreate(&x), cudaEventRecord(x, st);
     double t_pre = tms(tq);
-    if (e->hp.potential != kREBO) {  // REBO has no inter-molecular term: no LJ lists
+    if (clp) {
+      CK(e->clc.ensure(N));
+      CK(e->cln.ensure((size_t)N * e->capC));
+      ClLists CLs;
+      CLs.cap = e->capC, CLs.cnt = e->clc.p, CLs.nbr = e->cln.p, CLs.bqcnt = Lg.bqcnt;
+      for (int p = 0; p < 3; ++p) CLs.rcs[p] = (e->hp.pr[p].rc + skin) * (1.0 + 1e-9) + 1e-9, CLs.bq2[p] = Lg.bq2[p];
+      k_build_cl<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->clg, e->run_cl.p, e->cbb.p,
+                                                                e->cl_atom.p, CLs, e->small_i.p + 2);
+      CKL();
+    } else if (e->hp.potential != kREBO) {  // REBO has no inter-molecular term: no LJ lists
       k_build_lj<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
                                                                 e->nrLJ, Lg, e->small_i.p + 2);
       CKL();
@@ -782,8 +859,12 @@ ab_status images_and_lists(ab_engine* e) {
       for (auto& x : dbg_ev) cudaEventDestroy(x);
     }
     bool ok = true;
-    for (int c = 0; c < 3; ++c)
-      if (mx[c] > e->capL[c]) e->capL[c] = mx[c] + mx[c] / 8 + 32, ok = false;
+    if (clp) {
+      if (mx[0] > e->capC) e->capC = mx[0] + mx[0] / 8 + 32, ok = false;
+    } else {
+      for (int c = 0; c < 3; ++c)
+        if (mx[c] > e->capL[c]) e->capL[c] = mx[c] + mx[c] / 8 + 32, ok = false;
+    }
     if (mx[3] > e->capI) e->capI = mx[3] + 4, ok = false;
     if (ok) {
       int off = 0;
@@ -1025,8 +1106,10 @@ ab_status enqueue_forces(ab_engine* e) {
     st = e->chain;
   }
   StageBuf sb0{nullptr, nullptr, 0}, sb1{nullptr, nullptr, 0};
+  const bool clp = e->cl_path && e->hp.potential != kREBO;
   if (e->record) {
-    size_t n0 = (size_t)N * e->capS + 16, n1 = (size_t)N * (e->capL[0] + e->capL[1] + e->capL[2]) + 16;
+    size_t n0 = (size_t)N * e->capS + 16;
+    size_t n1 = (clp ? (size_t)N * e->capC * CL_SIZE : (size_t)N * (e->capL[0] + e->capL[1] + e->capL[2])) + 16;
     CK(e->stage0.ensure(n0 * 13));
     CK(e->stage1.ensure(n1 * 7));
     sb0 = StageBuf{e->stage0.p, e->small_i.p + 6, (int)n0};
@@ -1050,8 +1133,10 @@ ab_status enqueue_forces(ab_engine* e) {
   else CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
   ShortList<R> S = short_view<R>(e);
   // grids and the per-block partial rows of the energy / virial / counter reduction
-  const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4, g_near = nblk(N, NEAR_ATOMS);
-  const int g_far = std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4, g_slow = e->nsm * 2;
+  const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4;
+  const int g_near = clp ? std::min(nblk((long long)N * 32, 128), e->nsm * AB_LJC_MINBLOCKS) : nblk(N, NEAR_ATOMS);
+  const int g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4;
+  const int g_slow = e->nsm * 2;
   const int nrows = g_short + g_rebo + g_near + g_far + g_bstar + 3 * g_slow;  // b* full and NBMAX: g_slow
   CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
   CK(e->ovf_q.ensure(e->capQ));
@@ -1080,7 +1165,7 @@ ab_status enqueue_forces(ab_engine* e) {
   // the far kernel forks from the engine stream at e->far_at: 0 = at once, 1 = after the short
   // list, 2 = after the near kernel (it then fills the GPU beside the b* batch)
   auto launch_far = [&]() -> ab_status {
-    if (!lj) return AB_OK;
+    if (!lj || clp) return AB_OK;
     CK(cudaEventRecord(e->ev_fork[1], st));
     CK(cudaStreamWaitEvent(s_far, e->ev_fork[1], 0));
     cudaEvent_t t = prof_start(e, s_far);
@@ -1097,6 +1182,11 @@ ab_status enqueue_forces(ab_engine* e) {
     return AB_OK;
   };
   if (e->far_at == 0) TRY(launch_far());
+  if (clp) {  // current positions of the cluster slots (locals and ghost images)
+    k_cpos<<<nblk((long long)CL_SIZE * e->NCL, 256), 256, 0, st>>>(CL_SIZE * e->NCL, e->cl_atom.p, e->pos.p,
+                                                                   e->cpos.p);
+    CKL();
+  }
   {
     cudaEvent_t t = prof_start(e, st);
     k_short<R><<<g_short, 128, 0, st>>>(N, NT, e->pos.p, e->in_cnt.p, e->in_nbr.p, e->capI, S, e->gid.p,
@@ -1133,8 +1223,21 @@ ab_status enqueue_forces(ab_engine* e) {
       if (!(e->skip & 4)) kern<<<g_near, NEAR_GROUP * NEAR_ATOMS, 0, st>>>(A, S, e->owner.p, e->gid.p, e->shift.p, Fk, e->acc.p,
                                                        e->ct.p, Qu, sb1, RR);
     };
-    if (e->want_virial) morse ? near(k_lj_near<R, true, true, SG>) : near(k_lj_near<R, true, false, SG>);
-    else morse ? near(k_lj_near<R, false, true, SG>) : near(k_lj_near<R, false, false, SG>);
+    auto ljc = [&](auto kern) {
+      LjcArgs CA;
+      CA.N = N, CA.pos = e->pos.p, CA.cpos = e->cpos.p, CA.cl_atom = e->cl_atom.p;
+      CA.cap = e->capC, CA.cnt = e->clc.p, CA.nbr = e->cln.p;
+      if (!(e->skip & 4))
+        kern<<<g_near, 128, 0, st>>>(CA, S, e->owner.p, e->gid.p, e->shift.p, Fk, e->ct.p, Qu, sb1, RR);
+    };
+    if (clp) {
+      if (e->want_virial) morse ? ljc(k_ljc<R, true, true, SG>) : ljc(k_ljc<R, true, false, SG>);
+      else morse ? ljc(k_ljc<R, false, true, SG>) : ljc(k_ljc<R, false, false, SG>);
+    } else if (e->want_virial) {
+      morse ? near(k_lj_near<R, true, true, SG>) : near(k_lj_near<R, true, false, SG>);
+    } else {
+      morse ? near(k_lj_near<R, false, true, SG>) : near(k_lj_near<R, false, false, SG>);
+    }
     CKL();
     prof_stop(e, 2, st, t);
   }
@@ -1193,7 +1296,7 @@ ab_status enqueue_forces(ab_engine* e) {
     prof_stop(e, 3, st, t);
   }
   CK(cudaStreamWaitEvent(st, e->ev_join[0], 0));
-  if (lj) CK(cudaStreamWaitEvent(st, e->ev_join[1], 0));
+  if (lj && !clp) CK(cudaStreamWaitEvent(st, e->ev_join[1], 0));
   RR.row0 = 0;
   if (e->defer_reduce) {  // NVE step: reduced by k_post together with the second half-kick
     e->post_rr = RR, e->post_rows = nrows_used, e->post_pending = true;
@@ -1446,6 +1549,9 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   e->st = e->own;
   e->serial = std::getenv("AB_SERIAL_KERNELS") && std::getenv("AB_SERIAL_KERNELS")[0] == '1';
   e->timeline = std::getenv("AB_TIMELINE") && std::getenv("AB_TIMELINE")[0] == '1';
+  // AB_LJ_CLUSTER=1: the j-cluster LJ kernel (k_ljc.cuh; parity-green, measured 2.3x slower than
+  // the per-atom near / far kernels on cfg4) instead of k_lj_near + k_lj_far
+  e->cl_path = std::getenv("AB_LJ_CLUSTER") && std::getenv("AB_LJ_CLUSTER")[0] == '1';
   if (const char* fa = std::getenv("AB_FAR_AT")) e->far_at = std::max(0, std::min(2, std::atoi(fa)));
   if (const char* sk = std::getenv("AB_SKIP")) e->skip = std::atoi(sk);
   e->pdl = std::getenv("AB_PDL") && std::getenv("AB_PDL")[0] == '1';
@@ -1562,7 +1668,7 @@ void free_engine(ab_engine* e) {
     if (NC.ok) NC.commDestroy(e->comm);
     e->comm = nullptr;
   }
-  DBuf<double4>* b4[] = {&e->pos, &e->pos_tmp, &e->xref};
+  DBuf<double4>* b4[] = {&e->pos, &e->pos_tmp, &e->xref, &e->cpos, &e->cbb};
   for (auto* b : b4) b->release();
   e->acc.p = nullptr, e->ct.p = nullptr, e->small_i.p = nullptr;  // views into scratch
   e->scratch.release();
@@ -1572,7 +1678,8 @@ void free_engine(ab_engine* e) {
                      &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
                      &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_q, &e->ovf_q2,
                      &e->sendl[0], &e->sendl[1], &e->fl[0], &e->fl[1], &e->fl[2], &e->idx[0], &e->idx[1],
-                     &e->idx[2], &e->cnt_d};
+                     &e->idx[2], &e->cnt_d, &e->cl_k, &e->cl_v, &e->cl_k2, &e->cl_v2, &e->run_start, &e->run_cl,
+                     &e->cl_atom, &e->clc, &e->cln};
   for (auto* b : bi) b->release();
   DBuf<unsigned char>* bu[] = {&e->s_dr, &e->s_w, &e->s_N, &e->gtab, &e->cub_tmp, &e->sb[0], &e->sb[1], &e->rb[0], &e->rb[1],
                                &e->redx};
@@ -2298,6 +2405,43 @@ static ab_status list_visit(ab_engine* e, ab_engine* d, ab_list which, Visit&& v
     CK(cudaMemcpyAsync(sh.data(), d->shift.p, sizeof(char4) * NT, cudaMemcpyDeviceToHost, e->st));
     CK(cudaMemcpyAsync(pos.data(), d->pos.p, sizeof(double4) * NT, cudaMemcpyDeviceToHost, e->st));
   }
+  auto type_h = [&](int a) {
+    long long k;
+    std::memcpy(&k, &pos[a].w, sizeof(k));
+    return (int)(k & 3);
+  };
+  auto canon_of = [&](int i, int J) {
+    char4 s = sh[J];
+    return gid[i] != gid[J] ? gid[i] < gid[J] : (s.x > 0 || (s.x == 0 && (s.y > 0 || (s.y == 0 && s.z > 0))));
+  };
+  auto in_rc = [&](int i, int J) {  // exact (un-fused) r^2 <= r_c^2 as on the device
+    volatile double dx = pos[J].x - pos[i].x, dy = pos[J].y - pos[i].y, dz = pos[J].z - pos[i].z;
+    volatile double a = dx * dx, b = dy * dy, cc = dz * dz;
+    volatile double ab = a + b;
+    double r2 = ab + cc;
+    double rc = d->hp.pr[type_h(i) + type_h(J)].rc;
+    return r2 <= rc * rc;
+  };
+  if (which == AB_LIST_LJ && d->cl_path) {  // cluster lists: expand the slots of every listed cluster
+    if (d->hp.potential == kREBO) return AB_OK;
+    std::vector<int> cnt(N), nbr((size_t)N * d->capC), cla((size_t)CL_SIZE * d->NCL);
+    if (N) {
+      CK(cudaMemcpyAsync(cnt.data(), d->clc.p, sizeof(int) * N, cudaMemcpyDeviceToHost, e->st));
+      CK(cudaMemcpyAsync(nbr.data(), d->cln.p, sizeof(int) * N * (size_t)d->capC, cudaMemcpyDeviceToHost, e->st));
+      CK(cudaMemcpyAsync(cla.data(), d->cl_atom.p, sizeof(int) * cla.size(), cudaMemcpyDeviceToHost, e->st));
+    }
+    CK(cudaStreamSynchronize(e->st));
+    for (int i = 0; i < N; ++i)
+      for (int q = 0; q < cnt[i]; ++q) {
+        const int c = nbr[(size_t)i * d->capC + q];
+        for (int s = 0; s < CL_SIZE; ++s) {
+          const int J = cla[(size_t)CL_SIZE * c + s];
+          if (J < 0 || J == i || !canon_of(i, J) || !in_rc(i, J)) continue;
+          visit(gid[i], gid[J], sh[J].x, sh[J].y, sh[J].z);
+        }
+      }
+    return AB_OK;
+  }
   // (count, neighbour) tables of the requested list(s)
   int nl = which == AB_LIST_LJ ? 3 : 1;
   std::vector<int> cnt[3], nbr[3];
@@ -2314,11 +2458,6 @@ static ab_status list_visit(ab_engine* e, ab_engine* d, ab_list which, Visit&& v
     }
   }
   CK(cudaStreamSynchronize(e->st));
-  auto type_h = [&](int a) {
-    long long k;
-    std::memcpy(&k, &pos[a].w, sizeof(k));
-    return (int)(k & 3);
-  };
   for (int c = 0; c < nl; ++c)
     for (int i = 0; i < N; ++i)
       for (int q = 0; q < cnt[c][i]; ++q) {
@@ -2411,12 +2550,14 @@ ab_status ab_get_stats(ab_engine* e, ab_stats* s) {
   for (ab_engine* d : doms(e)) {
     s->n_ghosts += d->G;
     s->n_overflow_retries += d->retries;
-    s->lj_capacity = std::max<int64_t>(s->lj_capacity, d->capL[0] + d->capL[1] + d->capL[2]);
+    s->lj_capacity = std::max<int64_t>(s->lj_capacity, d->cl_path ? (int64_t)d->capC * CL_SIZE
+                                                                  : d->capL[0] + d->capL[1] + d->capL[2]);
     s->inter_capacity = std::max<int64_t>(s->inter_capacity, d->capI);
   }
   if (!e->subs.empty()) s->n_rebuilds = e->rebuilds;
   s->n_lj_entries = c[CT_LJENT], s->n_angles = c[CT_ANGLES];
   s->n_lj_far = c[CT_LJFAR], s->n_lj_entries_far = c[CT_LJENTFAR];
+  s->n_lj_taper = c[CT_LJTAPER];
   return AB_OK;
 }
 

@@ -446,7 +446,7 @@ constexpr int FAR_UNROLL = AB_FAR_UNROLL;
 template <typename R, bool VIRIAL, bool BAND, bool MORSE, bool SG = false>
 __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, double4 pi, int ti, long long ki,
                                          const int* gid, const char4* shift, StageBuf stage, double& fx, double& fy,
-                                         double& fz, double& en, double (&W)[6], unsigned& nlj) {
+                                         double& fz, double& en, double (&W)[6], unsigned& nlj, unsigned& ntp) {
   const Tab<R>& T = tab<R>();
   const int lane = threadIdx.x & 31;
   const int cnt = A.cnt[list][i];
@@ -459,6 +459,7 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
   const R rloa = T.rlo[ti], rlob = T.rlo[ti + 1];
   const R iva = T.inv_taper[ti], ivb = T.inv_taper[ti + 1];
   const double rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
+  const double rla = c_geo.rlo2[ti], rlb = c_geo.rlo2[ti + 1];
   // the next chunk's list indices are loaded one iteration ahead: the position gathers of a
   // chunk then wait on one memory latency, not on two dependent ones
   int Jn[FAR_UNROLL];
@@ -490,6 +491,7 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
       double r2 = BAND ? r2_exact(dx, dy, dz) : fma(dz, dz, fma(dy, dy, dx * dx));
       bool in = valid && (!BAND || r2 <= (hj ? rcb : rca));
       nlj += (in && ki < key_of(pj[u]));
+      if (BAND) ntp += (in && ki < key_of(pj[u]) && r2 > (hj ? rlb : rla));  // taper band (counter)
       R rr2 = in ? (R)r2 : R(1);
       R y = (BAND || MORSE) ? rsqrt_fast(rr2) : R(0);  // 1/r (taper / Morse only)
       R dVr;
@@ -535,7 +537,7 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   double en = 0;
   double W[6] = {0, 0, 0, 0, 0, 0};
-  unsigned nlj = 0;
+  unsigned nlj = 0, ntp = 0;
   unsigned long long ne = 0;
   // grid-stride over atoms: a resident grid, one warp per atom at a time
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < A.N; i += nwarps) {
@@ -543,8 +545,8 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     const int ti = type_of(pi);
     const long long ki = key_of(pi);
     double fx = 0, fy = 0, fz = 0;
-    far_list<R, VIRIAL, false, MORSE, SG>(A, 1, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
-    far_list<R, VIRIAL, true, MORSE, SG>(A, 2, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj);
+    far_list<R, VIRIAL, false, MORSE, SG>(A, 1, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
+    far_list<R, VIRIAL, true, MORSE, SG>(A, 2, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
     fx = warp_sum<SG>(fx);
     fy = warp_sum<SG>(fy);
     fz = warp_sum<SG>(fz);
@@ -556,6 +558,7 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, W[c]);
   red_add_u(rs, CT_LJ, (unsigned long long)nlj);
   red_add_u(rs, CT_LJFAR, (unsigned long long)nlj);
+  red_add_u(rs, CT_LJTAPER, (unsigned long long)ntp);
   red_add_u(rs, CT_LJENT, ne);
   red_add_u(rs, CT_LJENTFAR, ne);
   red_flush(rs, RR);

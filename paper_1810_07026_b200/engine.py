@@ -31,7 +31,7 @@ class ABStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "n_short", "n_bonds", "n_quads", "n_lj", "n_C0", "n_bstar", "n_sb_trans", "max_short", "max_reach",
         "n_badarg", "n_atoms", "n_ghosts", "n_rebuilds", "n_steps", "n_overflow_retries", "lj_capacity",
-        "inter_capacity", "n_lj_entries", "n_angles", "n_lj_far", "n_lj_entries_far")]
+        "inter_capacity", "n_lj_entries", "n_angles", "n_lj_far", "n_lj_entries_far", "n_lj_taper")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

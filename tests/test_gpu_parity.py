@@ -345,3 +345,21 @@ def test_inputs_copied_from_pinned_caller_buffers(eng_mod):
     e._ck(e.L.ab_set_positions(e.h, C.cast(xh.data_ptr(), dp)))
     xh.fill_(-7.0)
     assert np.array_equal(e.get_positions(), x0)
+
+
+@pytest.mark.parametrize("which", ["small", 2, 3])
+def test_cluster_lj_path_parity(eng_mod, which, monkeypatch):
+    """The opt-in j-cluster LJ kernel (AB_LJ_CLUSTER=1, k_ljc.cuh): same fp64 tolerances, counters
+    and LJ half list as the default near / far kernels and the oracle."""
+    monkeypatch.setenv("AB_LJ_CLUSTER", "1")
+    systems = systems_small()[:6] if which == "small" else [I.config(which)]
+    for s in systems:
+        o = O.compute(s.types, s.x, s.box)
+        g = run_gpu(eng_mod, s)
+        check_fp64(s, g, o)
+        for k in COUNTERS:
+            assert g["stats"][k] == o["counters"][k], (s.name, k, g["stats"][k], o["counters"][k])
+        assert np.array_equal(g["eng"].get_list(2), O.get_list(s.types, s.x, s.box, 2)), s.name
+        gm = run_gpu(eng_mod, s, "mixed")
+        rel = np.sqrt(((gm["F"] - o["F"]) ** 2).sum()) / max(np.sqrt((o["F"] ** 2).sum()), 1e-300)
+        assert rel <= 1e-4, (s.name, rel)
