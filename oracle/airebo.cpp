@@ -481,22 +481,44 @@ T clamp1(const T& c) {
   return c;
 }
 
+// g_i(cos theta) of centre species tc with coordination N (reading A34):
+// g_C(c, N) = g_C2(c) + S(N; nlo, nhi) (g_C(c) - g_C2(c)) if angle.C2 is given, else g_tc(c)
+template <class T>
+T gfun(const Params& P, int tc, const T& c, const T& N) {
+  if (tc != CARBON || !P.has_gC2) return hermite1(P.g[tc], c);
+  T g1 = hermite1(P.g[CARBON], c), g2 = hermite1(P.gC2, c);
+  return g2 + Sw(N, P.gC_nlo, P.gC_nhi) * (g1 - g2);
+}
+
+// lambda_jik (reading A33): constant table + kappa delta(t_i, H)
+// [(rho_{t_k H} - r_ik) - (rho_{t_j H} - r_ij)]; r_ij = |d| is the fictitious rho in b*
+template <class T>
+T lambda_jik(const Params& P, int tj, int ti, int tk, const T& rij, const T& rik) {
+  T lam(P.lam[tj][ti][tk]);
+  if (ti == CARBON || P.kappa == 0.0) return lam;
+  return lam + P.kappa * ((P.pair[tk][1].rho - rik) - (P.pair[tj][1].rho - rij));
+}
+
 // p^{sigma pi} of one side: [1 + sum_k w_ck g_c(cos th) e^{lam} + P]^{-1/2}
 template <class T>
 T p_sigma_pi(const Params& P, int tpartner, const V3<T>& d, const Side<T>& sd, std::vector<T>& cosv, T& NC, T& NH,
              bool& ok) {
+  using std::exp;
   using std::sqrt;
   T r = norm(d);
   T sum(0.0);
   NC = T(0.0);
   NH = T(0.0);
   cosv.clear();
+  for (size_t k = 0; k < sd.tk.size(); ++k) {  // N^C_ij, N^H_ij (O4): the side excludes the partner
+    if (sd.tk[k] == CARBON) NC = NC + sd.wk[k];
+    else NH = NH + sd.wk[k];
+  }
+  T Nside = NC + NH;
   for (size_t k = 0; k < sd.tk.size(); ++k) {
     T c = clamp1(dot(d, sd.dk[k]) / (r * sd.rk[k]));
     cosv.push_back(c);
-    sum = sum + sd.wk[k] * hermite1(P.g[sd.tc], c) * std::exp(P.lam[tpartner][sd.tc][sd.tk[k]]);
-    if (sd.tk[k] == CARBON) NC = NC + sd.wk[k];
-    else NH = NH + sd.wk[k];
+    sum = sum + sd.wk[k] * gfun(P, sd.tc, c, Nside) * exp(lambda_jik(P, tpartner, sd.tc, sd.tk[k], r, sd.rk[k]));
   }
   T arg = (1.0 + sum) + Pspline(P, sd.tc, tpartner, NC, NH);
   ok = val(arg) > 0.0;

@@ -35,7 +35,14 @@ struct Params {
   double mass[2], kB, mvv2e, ftm2v, skin;
   PairParams pair[2][2];  // symmetric [t_i][t_j]
   Spline1 g[2];           // g_C, g_H (centre species)
-  double lam[2][2][2];    // lambda_{j i k} indexed [t_j][t_i][t_k]
+  double lam[2][2][2];    // lambda_{j i k} indexed [t_j][t_i][t_k] (constant part)
+  // SURVEY §8(f) F3 (readings A33 / A34 of DESIGN.md), both optional and off by default:
+  //   lambda_jik = lam[t_j][t_i][t_k] + kappa delta(t_i, H) [(rho_{t_k H} - r_ik) - (rho_{t_j H} - r_ij)]
+  //   g_C(cos, N) = g_C2(cos) + S(N; nlo, nhi) (g_C(cos) - g_C2(cos)), N = N_i - w_ij
+  double kappa = 0.0;     // lambda.kappa (1/A)
+  bool has_gC2 = false;   // angle.C2.knots / values present
+  Spline1 gC2;
+  double gC_nlo = 3.2, gC_nhi = 3.7;  // angle.C.nlo / nhi
   double Plo[2];
   int Pn[2];
   std::vector<double> P[2];  // P_CC, P_CH (C-centred), index a*Pn[1]+b
@@ -159,6 +166,17 @@ inline std::string parse_params(const std::string& text, Params& p) {
   for (int j = 0; j < 2; ++j)
     for (int i = 0; i < 2; ++i)
       for (int k = 0; k < 2; ++k) p.lam[j][i][k] = one(std::string("lambda.") + S[j] + S[i] + S[k]);
+  if (kv.count("lambda.kappa")) p.kappa = one("lambda.kappa");
+  if (kv.count("angle.C2.knots") || kv.count("angle.C2.values")) {
+    p.has_gC2 = true;
+    p.gC2.x = nums("angle.C2.knots", 0);
+    p.gC2.y = nums("angle.C2.values", 0);
+    if (err.empty() && (p.gC2.x.size() != p.gC2.y.size() || p.gC2.x.size() < 2))
+      err = "angle.C2.knots/values length mismatch";
+  }
+  if (kv.count("angle.C.nlo")) p.gC_nlo = one("angle.C.nlo");
+  if (kv.count("angle.C.nhi")) p.gC_nhi = one("angle.C.nhi");
+  if (err.empty() && !(p.gC_nlo < p.gC_nhi)) err = "angle.C.nlo >= angle.C.nhi";
   auto plo = nums("grid.P.lo", 2), pn = nums("grid.P.n", 2);
   auto rlo = nums("grid.RT.lo", 3), rn = nums("grid.RT.n", 3);
   for (int a = 0; a < 2; ++a) p.Plo[a] = plo[a], p.Pn[a] = (int)pn[a];

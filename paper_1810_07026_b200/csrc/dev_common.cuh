@@ -24,8 +24,13 @@ struct Tab {
   R inv_taper[3];  // 1 / (r_c - r_lo)
   R meps[3], malpha[3], mre[3];  // AIREBO-M Morse radial form
   R explam[2][2][2];  // e^{lambda_{jik}} [t_j][t_i][t_k]
-  int gn[2];
-  R gx[2][16], gy[2][16], gm[2][16];
+  int gn[3];  // g_C, g_H, g_C2 (slot 2: F3 coordination-dependent g_C, reading A34)
+  R gx[3][16], gy[3][16], gm[3][16];
+  // F3 (readings A33 / A34): kappa != 0 -> lambda_jik depends on r_ij, r_ik for
+  // H centres; g2on -> g_C(cos, N) = g_C2 + S(N; gnlo, gnhi) (g_C - g_C2)
+  R kappa, rhoH[2];  // rho_{C H}, rho_{H H}
+  int g2on;
+  R gnlo, gnhi;
   R P[2][25], Rt[3][225], Tt[3][225];
   R conj_lo, conj_hi, s2lo, s2hi;
   R tors[2][2][2][2];
@@ -34,7 +39,7 @@ struct Tab {
   // __constant__ load serialises per distinct address (set by the engine)
   const R* gRT;  // [2][3][225]: pi^rc (which 0) and T (which 1) per species pair
   const R* gP;   // [2][25]
-  const R* gG;   // [3][2][16]: g knots, values, knot slopes per centre species
+  const R* gG;   // [3][3][16]: g knots, values, knot slopes per spline (g_C, g_H, g_C2)
 };
 
 struct Geo {  // double-only quantities: exact list / gate decisions, box, integrator
@@ -211,8 +216,8 @@ __device__ __forceinline__ R gspline(int sp, R c, R& dg) {
   const Tab<R>& T = tab<R>();
   const int n = T.gn[sp];
   const R* gx = T.gG + sp * 16;
-  const R* gy = T.gG + 32 + sp * 16;
-  const R* gm = T.gG + 64 + sp * 16;
+  const R* gy = T.gG + 48 + sp * 16;
+  const R* gm = T.gG + 96 + sp * 16;
   if (c <= __ldg(gx)) {
     dg = R(0);
     return __ldg(gy);

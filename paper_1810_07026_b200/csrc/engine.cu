@@ -415,19 +415,23 @@ void fill_tab(const HostParams& hp, Tab<R>& t) {
   for (int j = 0; j < 2; ++j)
     for (int i = 0; i < 2; ++i)
       for (int k = 0; k < 2; ++k) t.explam[j][i][k] = (R)std::exp(hp.lam[j][i][k]);
-  for (int c = 0; c < 2; ++c) {
-    int n = (int)hp.gknot[c].size();
+  for (int c = 0; c < 3; ++c) {  // g_C, g_H, g_C2 (slot 2 = g_C when angle.C2 is absent)
+    const std::vector<double>& kn = c < 2 ? hp.gknot[c] : (hp.gknot2.empty() ? hp.gknot[0] : hp.gknot2);
+    const std::vector<double>& va = c < 2 ? hp.gval[c] : (hp.gknot2.empty() ? hp.gval[0] : hp.gval2);
+    int n = (int)kn.size();
     t.gn[c] = n;
     for (int q = 0; q < 16; ++q) t.gx[c][q] = t.gy[c][q] = t.gm[c][q] = 0;
     for (int q = 0; q < n; ++q) {
-      t.gx[c][q] = (R)hp.gknot[c][q];
-      t.gy[c][q] = (R)hp.gval[c][q];
-      double m = (q == 0 || q == n - 1)
-                     ? 0.0
-                     : (hp.gval[c][q + 1] - hp.gval[c][q - 1]) / (hp.gknot[c][q + 1] - hp.gknot[c][q - 1]);
+      t.gx[c][q] = (R)kn[q];
+      t.gy[c][q] = (R)va[q];
+      double m = (q == 0 || q == n - 1) ? 0.0 : (va[q + 1] - va[q - 1]) / (kn[q + 1] - kn[q - 1]);
       t.gm[c][q] = (R)m;
     }
   }
+  t.kappa = (R)hp.kappa;
+  t.rhoH[0] = (R)hp.pr[1].rho, t.rhoH[1] = (R)hp.pr[2].rho;  // rho_{CH}, rho_{HH}
+  t.g2on = hp.gknot2.empty() ? 0 : 1;
+  t.gnlo = (R)hp.gnlo, t.gnhi = (R)hp.gnhi;
   for (int a = 0; a < 2; ++a)
     for (int q = 0; q < 25; ++q) t.P[a][q] = (R)hp.Ptab[a][q];
   for (int p = 0; p < 3; ++p)
@@ -1583,7 +1587,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   fill_tab(e->hp, e->tf);
   geo_fields(e);
   {  // global-memory spline tables (read through L1 with divergent knot indices)
-    const size_t nrt = 2 * 3 * 225, np = 2 * 25, ng = 3 * 2 * 16, nall = nrt + np + ng;
+    const size_t nrt = 2 * 3 * 225, np = 2 * 25, ng = 3 * 3 * 16, nall = nrt + np + ng;
     std::vector<double> hd(nall);
     std::vector<float> hf(nall);
     for (int w = 0; w < 2; ++w)
@@ -1591,11 +1595,11 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
         for (int q = 0; q < 225; ++q) hd[(w * 3 + p) * 225 + q] = w == 0 ? e->td.Rt[p][q] : e->td.Tt[p][q];
     for (int a = 0; a < 2; ++a)
       for (int q = 0; q < 25; ++q) hd[nrt + a * 25 + q] = e->td.P[a][q];
-    for (int c = 0; c < 2; ++c)
+    for (int c = 0; c < 3; ++c)
       for (int q = 0; q < 16; ++q) {
         hd[nrt + np + c * 16 + q] = e->td.gx[c][q];
-        hd[nrt + np + 32 + c * 16 + q] = e->td.gy[c][q];
-        hd[nrt + np + 64 + c * 16 + q] = e->td.gm[c][q];
+        hd[nrt + np + 48 + c * 16 + q] = e->td.gy[c][q];
+        hd[nrt + np + 96 + c * 16 + q] = e->td.gm[c][q];
       }
     for (size_t q = 0; q < nall; ++q) hf[q] = (float)hd[q];
     if (e->gtab.ensure(nall * (sizeof(double) + sizeof(float))) != cudaSuccess ||

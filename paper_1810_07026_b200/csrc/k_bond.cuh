@@ -44,6 +44,7 @@ struct BoState {
   R cl[NB], Gl[NB], dGl[NB];
   R Si, Sj, PxI, PyI, PxJ, PyJ;
   R pij, pji, Nij, Nji, Nconj;
+  R QI, dQI, QJ, dQJ;  // F3 g_C(cos, N) blend weight S(N) per side and dS/dN (sum_1 - sum_2)
   R Rv, Rx, Ry, Rz, Tv, Tx, Ty, Tz;  // derivatives w.r.t. (N_ij, N_ji, N^conj)
   R D, Tsum;
   int nquads;
@@ -85,6 +86,30 @@ __device__ __forceinline__ R F_conj(R x, R& dF) {
   return sw<R>(x, T.conj_lo, T.conj_hi, dF);
 }
 
+// F3 (reading A33): e^{lambda_jik} for centre t_c with partner t_p at distance r
+// (the fictitious rho in b*) and neighbour t_k at r_k; lambda depends on the distances for H
+// centres only: lambda.JIK + kappa [(rho_{t_k H} - r_k) - (rho_{t_p H} - r)]
+template <typename R>
+__device__ __forceinline__ R explam_r(int tp, int tc, int tk, R r, R rk) {
+  const Tab<R>& T = tab<R>();
+  R e = T.explam[tp][tc][tk];
+  if (tc == 1 && T.kappa != R(0)) e *= ex(T.kappa * ((T.rhoH[tk] - rk) - (T.rhoH[tp] - r)));
+  return e;
+}
+
+// F3 (reading A34): g of centre species tc, blended with g_C2 by the side's coordination weight Q
+template <typename R>
+__device__ __forceinline__ R gblend(int tc, R c, R Q, R& dg) {
+  R g = gspline<R>(tc, c, dg);
+  if (tc == 0 && tab<R>().g2on) {
+    R dg2;
+    R g2 = gspline<R>(2, c, dg2);
+    g = g2 + Q * (g - g2);
+    dg = dg2 + Q * (dg - dg2);
+  }
+  return g;
+}
+
 // ---------------------------------------------------------------- forward pass
 template <typename R, bool TORS, int NB, bool UNROLL = false>
 __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i, int J, V3<R> d, R r,
@@ -107,7 +132,8 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
   R ir = R(1) / r;
   st.u = ir * d;
   // ---- i side: k in N(i) \ {J}
-  R sumI = 0, NCi = 0, NHi = 0, Si = 0;
+  const bool blendI = ti == 0 && T.g2on;  // F3: sum with g_C and with g_C2, blended by S(N_ij)
+  R sumI = 0, sumI2 = 0, NCi = 0, NHi = 0, Si = 0;
 #pragma unroll(Unr<NB, UNROLL>::v)
   for (int a = 0; a < NB; ++a) {
     if (a >= nI) continue;
@@ -120,7 +146,9 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
     R c = clamp_cos(dot3(d, dk) * ir / rk);
     R dg;
     R g = gspline<R>(ti, c, dg);
-    sumI += wk * g * T.explam[tj][ti][tk];
+    const R ek = explam_r<R>(tj, ti, tk, r, rk);
+    sumI += wk * g * ek;
+    if (blendI) sumI2 += wk * gspline<R>(2, c, dg) * ek;
     if (tk == 0) {
       NCi += wk;
       R dF;
@@ -130,7 +158,8 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
     }
   }
   // ---- J side: l in N(J) \ {i}
-  R sumJ = 0, NCj = 0, NHj = 0, Sj = 0;
+  const bool blendJ = tj == 0 && T.g2on;
+  R sumJ = 0, sumJ2 = 0, NCj = 0, NHj = 0, Sj = 0;
   const V3<R> md = mk3(-d.x, -d.y, -d.z);
 #pragma unroll(Unr<NB, UNROLL>::v)
   for (int c = 0; c < NB; ++c) {
@@ -144,7 +173,9 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
     R cc = clamp_cos(dot3(md, dl) * ir / rl);
     R dg;
     R g = gspline<R>(tj, cc, dg);
-    sumJ += wl * g * T.explam[ti][tj][tl];
+    const R el = explam_r<R>(ti, tj, tl, r, rl);
+    sumJ += wl * g * el;
+    if (blendJ) sumJ2 += wl * gspline<R>(2, cc, dg) * el;
     if (tl == 0) {
       NCj += wl;
       R dF;
@@ -156,6 +187,19 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
     R dG;
     st.Gl[c] = guardG<R>(cc, dG);
     st.dGl[c] = dG;
+  }
+  st.QI = st.QJ = R(1), st.dQI = st.dQJ = R(0);
+  if (blendI) {  // g_C(cos, N_ij) = g_C2 + S(N_ij) (g_C - g_C2): sum = sum_2 + S (sum_1 - sum_2)
+    R dQ;
+    const R Q = sw<R>(NCi + NHi, T.gnlo, T.gnhi, dQ);
+    st.QI = Q, st.dQI = dQ * (sumI - sumI2);
+    sumI = sumI2 + Q * (sumI - sumI2);
+  }
+  if (blendJ) {
+    R dQ;
+    const R Q = sw<R>(NCj + NHj, T.gnlo, T.gnhi, dQ);
+    st.QJ = Q, st.dQJ = dQ * (sumJ - sumJ2);
+    sumJ = sumJ2 + Q * (sumJ - sumJ2);
   }
   R PI = 0, PJ = 0;
   st.PxI = st.PyI = st.PxJ = st.PyJ = 0;
@@ -272,8 +316,9 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
   gd = mk3<R>(0, 0, 0);
   fi = mk3<R>(0, 0, 0);
   fj = mk3<R>(0, 0, 0);
-  R Wl[NB], Cl[NB];
+  R Wl[NB], Cl[NB], Ll[NB];
   V3<R> gl[NB];
+  const bool lamI = ti == 1 && T.kappa != R(0), lamJ = tj == 1 && T.kappa != R(0);  // F3 lambda(r)
 #pragma unroll(Unr<NB, UNROLL>::v)
   for (int c = 0; c < NB; ++c) {
     if (c >= nJ) continue;
@@ -282,10 +327,12 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     int tl = typ[l];
     R wl = S.w[bj + q].x;
     R dg;
-    R g = gspline<R>(tj, st.cl[c], dg);
+    R g = gblend<R>(tj, st.cl[c], st.QJ, dg);
     R el = T.explam[ti][tj][tl];
+    if (lamJ) el = explam_r<R>(ti, tj, tl, r, S.dr[bj + q].w);
     R Pd = tl == 0 ? st.PxJ : st.PyJ;
-    Wl[c] = cJ * (g * el + Pd) + dNji;
+    Wl[c] = cJ * (g * el + Pd + st.dQJ) + dNji;
+    Ll[c] = lamJ ? cJ * wl * g * el * T.kappa : R(0);  // dE/dlambda_ijl (x kappa)
     if (tl == 0) {
       R dF;
       R Fl = F_conj<R>(S.Ntot[l] - wl, dF);
@@ -307,10 +354,13 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     V3<R> uk = irk * dk;
     R ck = clamp_cos(dot3(u, uk));
     R dg;
-    R g = gspline<R>(ti, ck, dg);
-    R ek = T.explam[tj][ti][tk];
-    R Wk = cI * (g * ek + (tk == 0 ? st.PxI : st.PyI)) + dNij;
+    R g = gblend<R>(ti, ck, st.QI, dg);
+    R ek = lamI ? explam_r<R>(tj, ti, tk, r, rk) : T.explam[tj][ti][tk];
+    R Wk = cI * (g * ek + (tk == 0 ? st.PxI : st.PyI) + st.dQI) + dNij;
     R Ck = cI * wk * dg * ek;
+    // lambda_jik(r_ij, r_ik) of an H centre (F3): d lambda/d r_ik = -kappa, d lambda/d r_ij = +kappa
+    const R Lk = lamI ? cI * wk * g * ek * T.kappa : R(0);
+    if (lamI) addto(gd, Lk * u);
     R chain = 0;
     if (tk == 0) {
       R dF;
@@ -362,7 +412,7 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
       }
     }
     // w_ik(r_ik) and cos(theta_jik) derivatives
-    addto(gk, (Wk * dwk) * uk);
+    addto(gk, (Wk * dwk - Lk) * uk);
     addto(gk, (Ck * irk) * (u - ck * uk));
     addto(gd, (Ck * ir) * (uk - ck * u));
     // force on k now; the +gk on i is accumulated in fi (one atomic per bond for i)
@@ -384,7 +434,8 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     V3<R> ul = irl * dl;
     R cl = st.cl[c];
     V3<R> g = gl[c];
-    addto(g, (Wl[c] * dwl) * ul);
+    addto(g, (Wl[c] * dwl - Ll[c]) * ul);
+    if (lamJ) addto(gd, Ll[c] * u);
     addto(g, (Cl[c] * irl) * (mk3(-u.x, -u.y, -u.z) - cl * ul));
     addto(gd, (-Cl[c] * ir) * (ul + cl * u));
     atomic_add3<SG>(F, owner[l], -(double)g.x, -(double)g.y, -(double)g.z);

@@ -180,6 +180,21 @@ std::string parse_host_params(const char* text, size_t len, HostParams& hp) {
   for (int j = 0; j < 2; ++j)
     for (int i = 0; i < 2; ++i)
       for (int k = 0; k < 2; ++k) hp.lam[j][i][k] = t.val(std::string("lambda.") + SP[j] + SP[i] + SP[k]);
+  // optional F3 keys: distance-dependent lambda, coordination-dependent g_C
+  if (t.recs.count("lambda.kappa")) hp.kappa = t.val("lambda.kappa");
+  if (t.recs.count("angle.C2.knots") || t.recs.count("angle.C2.values")) {
+    hp.gknot2 = t.vals("angle.C2.knots", 0);
+    hp.gval2 = t.vals("angle.C2.values", 0);
+    if (t.error.empty()) {
+      if (hp.gknot2.size() != hp.gval2.size() || hp.gknot2.size() < 2 || hp.gknot2.size() > 16)
+        t.error = "angle.C2.knots and angle.C2.values must have equal length in [2, 16]";
+      for (size_t q = 1; t.error.empty() && q < hp.gknot2.size(); ++q)
+        if (!(hp.gknot2[q] > hp.gknot2[q - 1])) t.error = "angle.C2.knots must increase";
+    }
+  }
+  if (t.recs.count("angle.C.nlo")) hp.gnlo = t.val("angle.C.nlo");
+  if (t.recs.count("angle.C.nhi")) hp.gnhi = t.val("angle.C.nhi");
+  if (t.error.empty() && !(hp.gnlo < hp.gnhi)) t.error = "angle.C.nlo >= angle.C.nhi";
   std::vector<double> plo = t.vals("grid.P.lo", 2), pn = t.vals("grid.P.n", 2);
   std::vector<double> rlo = t.vals("grid.RT.lo", 3), rn = t.vals("grid.RT.n", 3);
   for (int q = 0; q < 2; ++q) {

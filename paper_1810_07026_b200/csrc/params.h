@@ -24,7 +24,13 @@ struct HostParams {
   double mass[2] = {0, 0}, kB = 0, mvv2e = 0, ftm2v = 0, skin = 0;
   PairSet pr[3];
   std::vector<double> gknot[2], gval[2];  // g_C, g_H knots (cos theta) and values
-  double lam[2][2][2];                    // lambda_{jik} as [t_j][t_i][t_k]
+  double lam[2][2][2];                    // lambda_{jik} as [t_j][t_i][t_k] (constant part)
+  // SURVEY §8(f) F3, optional (readings A33 / A34 of DESIGN.md):
+  //   lambda_jik += kappa delta(t_i, H) [(rho_{t_k H} - r_ik) - (rho_{t_j H} - r_ij)]
+  //   g_C(cos, N) = g_C2(cos) + S(N; nlo, nhi) (g_C(cos) - g_C2(cos)), N = N_i - w_ij
+  double kappa = 0.0;
+  std::vector<double> gknot2, gval2;      // angle.C2 (empty: g_C independent of N)
+  double gnlo = 3.2, gnhi = 3.7;
   double grid_p_lo[2];
   int grid_p_n[2];
   double grid_rt_lo[3];
