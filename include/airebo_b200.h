@@ -78,7 +78,8 @@ typedef struct ab_stats {
   int64_t n_angles;     /* bond-order angle terms (k in N(i)\j plus l in N(j)\i, per half bond) */
   int64_t n_lj_far;     /* ... of n_lj, pairs of the far-pair kernel (AB_LJ_CLUSTER=1: pairs with r > 3 r_max) */
   int64_t n_lj_entries_far;
-  int64_t n_lj_taper;   /* ... of n_lj, pairs in the taper band r_lo < r <= r_c (reading A10) */
+  int64_t n_lj_taper;   /* ... of n_lj, pairs in the taper band r_lo < r <= r_c (reading A10); counted by
+                           ab_compute evaluations only (0 after ab_run_nve steps) */
 } ab_stats;
 
 /* Create an engine on CUDA device `cuda_device` from parameter-file text (params/toy_ch.param

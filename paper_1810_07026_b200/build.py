@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libairebo_b200.so")
 SOURCES = ["engine.cu", "params.cpp"]
-HEADERS = ["dev_common.cuh", "k_lists.cuh", "k_bond.cuh", "k_lj.cuh", "k_ljc.cuh", "k_cluster.cuh", "k_misc.cuh", "k_dist.cuh", "params.h"]
+HEADERS = ["dev_common.cuh", "k_scan.cuh", "k_lists.cuh", "k_bond.cuh", "k_lj.cuh", "k_ljc.cuh", "k_cluster.cuh", "k_misc.cuh", "k_dist.cuh", "params.h"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared"]
 

@@ -14,8 +14,6 @@
 //     the halo travels by device-to-device copies on the shared stream.  Every phase is enqueued
 //     for all domains by the host in order, so no kernel ever waits on another domain's kernel.
 // Only the transfer (xfer) differs between the last two; the slab logic is the same code.
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: libnccl is dlopen'ed by the distributed mode
 
@@ -36,6 +34,7 @@
 #include "k_lj.cuh"
 #include "k_ljc.cuh"
 #include "k_misc.cuh"
+#include "k_scan.cuh"
 #include "params.h"
 
 using namespace ab;
@@ -179,7 +178,7 @@ struct ab_engine {
   DBuf<double4> pos, pos_tmp, xref;
   DBuf<double> vel, vel_tmp, F, io;
   DBuf<float> Ff;  // AB_SINGLE: fp32 force accumulation array of an evaluation
-  DBuf<int> gid, gid_tmp, owner, key, key2, val, val2, cell_start, gcnt, goff;
+  DBuf<int> gid, gid_tmp, owner, key, val, val2, cell_start, gcnt, goff;
   DBuf<char4> shift, rshift;
   DBuf<signed char> typ;
   DBuf<int> ljc[3], ljn[3], in_cnt, in_nbr;  // LJ near / pure / band lists, intermediate list
@@ -188,7 +187,7 @@ struct ab_engine {
   bool cl_path = false;
   ClGrid clg{};
   int nrun = 0, NCL = 0, capC = 0;
-  DBuf<int> cl_k, cl_v, cl_k2, cl_v2, run_start, run_cl, cl_atom, clc, cln;
+  DBuf<int> cl_k, cl_v, cl_v2, run_start, run_cl, cl_atom, clc, cln;
   DBuf<double4> cpos, cbb;
   bool want_virial = true;
   DBuf<int> s_cnt, s_nbr;
@@ -210,7 +209,7 @@ struct ab_engine {
   cudaEvent_t ev_disp = nullptr;
   DBuf<double> stage0, stage1, red_d;
   DBuf<unsigned long long> red_u;
-  DBuf<unsigned char> cub_tmp;
+  DBuf<int> sc_bsum, sc_cur, sc_off;  // scan / counting-sort scratch (k_scan.cuh)
   // pinned host mirror for small readbacks
   unsigned long long* h_ct = nullptr;
   unsigned long long* h_ct_dev = nullptr;  // h_ct as seen by kernels (mapped pinned memory)
@@ -533,15 +532,42 @@ ab_status grow_keep(ab_engine* e, DBuf<T>& b, size_t cap, size_t keep) {
   return AB_OK;
 }
 
+// exclusive scan of in[0..n) (FLAG: of in[q] != 0) into out[0..n], out[n] = total (k_scan.cuh)
+template <bool FLAG>
+ab_status scan_ex(ab_engine* e, const int* in, int n, int* out) {
+  const int nb = std::max(1, (n + SCAN_E - 1) / SCAN_E);
+  CK(e->sc_bsum.ensure(nb + 1));
+  k_scan_blocks<FLAG><<<nb, SCAN_T, 0, e->st>>>(in, n, out, e->sc_bsum.p);
+  CKL();
+  k_scan_carry<<<1, SCAN_T, 0, e->st>>>(nb, e->sc_bsum.p);
+  CKL();
+  k_scan_add<<<nblk(n + 1, 256), 256, 0, e->st>>>(n, nb, e->sc_bsum.p, out);
+  CKL();
+  return AB_OK;
+}
+
 // stable index selection: out = indices q < n with flag[q] != 0 (in order), count at *num
 ab_status select_flagged(ab_engine* e, int n, const int* flags, int* out, int* num) {
-  thrust::counting_iterator<int> it(0);
-  size_t need = 0;
-  cub::DeviceSelect::Flagged(nullptr, need, it, flags, out, num, n, e->st);
-  CK(e->cub_tmp.ensure(need));
-  size_t have = e->cub_tmp.n;
-  CK(cub::DeviceSelect::Flagged(e->cub_tmp.p, have, it, flags, out, num, n, e->st));
-  ++e->launches;
+  CK(e->sc_off.ensure((size_t)n + 1));
+  TRY(scan_ex<true>(e, flags, n, e->sc_off.p));
+  k_select_scatter<<<nblk(n, 256), 256, 0, e->st>>>(n, flags, e->sc_off.p, out, num);
+  CKL();
+  return AB_OK;
+}
+
+// stable counting sort of [0, n) by key[a] in [0, nkey): perm = indices ordered by (key, sec[a] if
+// sec != nullptr, a); start[0..nkey] = first position of each key (k_scan.cuh)
+ab_status key_sort(ab_engine* e, int n, const int* key, int nkey, const int* sec, int* perm, int* start) {
+  CK(e->sc_cur.ensure((size_t)nkey + 1));
+  CK(cudaMemsetAsync(e->sc_cur.p, 0, sizeof(int) * (size_t)nkey, e->st));
+  k_cell_hist<<<nblk(n, 256), 256, 0, e->st>>>(n, key, e->sc_cur.p);
+  CKL();
+  TRY(scan_ex<false>(e, e->sc_cur.p, nkey, start));
+  CK(cudaMemcpyAsync(e->sc_cur.p, start, sizeof(int) * (size_t)nkey, cudaMemcpyDeviceToDevice, e->st));
+  k_cell_scatter<<<nblk(n, 256), 256, 0, e->st>>>(n, key, e->sc_cur.p, perm);
+  CKL();
+  k_cell_order<<<nblk(nkey, 128), 128, 0, e->st>>>(nkey, start, sec, perm);
+  CKL();
   return AB_OK;
 }
 
@@ -629,19 +655,14 @@ ab_status sort_locals(ab_engine* e) {
   cudaStream_t st = e->st;
   CK(e->key.ensure(N));
   CK(e->val.ensure(N));
-  CK(e->key2.ensure(N));
   CK(e->val2.ensure(N));
+  CK(e->cell_start.ensure((size_t)e->ncell + 1));
   CK(e->pos_tmp.ensure(N));
   CK(e->vel_tmp.ensure(3 * (size_t)N));
   CK(e->gid_tmp.ensure(N));
   k_wrap_and_key<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->grid, e->key.p, e->val.p);
   CKL();
-  size_t need = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, need, e->key.p, e->key2.p, e->val.p, e->val2.p, N, 0, 31, st);
-  CK(e->cub_tmp.ensure(need));
-  size_t have = e->cub_tmp.n;
-  CK(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, have, e->key.p, e->key2.p, e->val.p, e->val2.p, N, 0, 31, st));
-  ++e->launches;
+  TRY(key_sort(e, N, e->key.p, e->ncell, nullptr, e->val2.p, e->cell_start.p));  // stable by (cell, index)
   k_permute<<<nblk(N, 256), 256, 0, st>>>(N, e->val2.p, e->pos.p, e->pos_tmp.p, e->vel.p, e->vel_tmp.p, e->gid.p,
                                           e->gid_tmp.p);
   CKL();
@@ -675,20 +696,12 @@ ab_status build_clusters(ab_engine* e) {
   e->nrun = g.ncx * g.ncy * 2;
   CK(e->cl_k.ensure(NT));
   CK(e->cl_v.ensure(NT));
-  CK(e->cl_k2.ensure(NT));
   CK(e->cl_v2.ensure(NT));
   CK(e->run_start.ensure(e->nrun + 1));
   CK(e->run_cl.ensure(e->nrun + 1));
-  k_cl_keys<<<nblk(NT, 256), 256, 0, st>>>(NT, e->pos.p, g, e->cl_k.p, e->cl_v.p);
+  k_cl_keys<<<nblk(NT, 256), 256, 0, st>>>(NT, e->pos.p, g, e->cl_k.p, e->cl_v.p);  // run, quantised z
   CKL();
-  size_t need = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, need, e->cl_k.p, e->cl_k2.p, e->cl_v.p, e->cl_v2.p, NT, 0, 31, st);
-  CK(e->cub_tmp.ensure(need));
-  size_t have = e->cub_tmp.n;
-  CK(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, have, e->cl_k.p, e->cl_k2.p, e->cl_v.p, e->cl_v2.p, NT, 0, 31, st));
-  ++e->launches;
-  k_cl_run_bounds<<<nblk(NT + 1, 256), 256, 0, st>>>(NT, e->nrun, e->cl_k2.p, e->run_start.p);
-  CKL();
+  TRY(key_sort(e, NT, e->cl_k.p, e->nrun, e->cl_v.p, e->cl_v2.p, e->run_start.p));  // by (run, z, index)
   k_cl_run_scan<<<1, 1024, 0, st>>>(e->nrun, e->run_start.p, e->run_cl.p);
   CKL();
   int ncl = 0;
@@ -699,7 +712,7 @@ ab_status build_clusters(ab_engine* e) {
   CK(e->cpos.ensure((size_t)CL_SIZE * ncl + 1));
   CK(e->cbb.ensure(2 * (size_t)ncl + 1));
   CK(cudaMemsetAsync(e->cl_atom.p, 0xff, sizeof(int) * CL_SIZE * (size_t)ncl, st));
-  k_cl_fill<<<nblk(NT, 256), 256, 0, st>>>(NT, e->cl_k2.p, e->cl_v2.p, e->run_start.p, e->run_cl.p, e->cl_atom.p);
+  k_cl_fill<<<nblk(NT, 256), 256, 0, st>>>(NT, e->cl_k.p, e->cl_v2.p, e->run_start.p, e->run_cl.p, e->cl_atom.p);
   CKL();
   k_cl_bbox<<<nblk(ncl, 128), 128, 0, st>>>(ncl, e->cl_atom.p, e->pos.p, e->cbb.p, e->cpos.p);
   CKL();
@@ -718,15 +731,10 @@ ab_status images_and_lists(ab_engine* e) {
   double3 lo = make_double3(-h, -h, -h), hi = make_double3(e->L[0] + h, e->L[1] + h, e->L[2] + h);
   if (slabbed(e)) smax.x = 0, lo.x = e->xlo - h, hi.x = e->xhi + h;
   CK(e->gcnt.ensure(NB));
-  CK(e->goff.ensure(NB));
+  CK(e->goff.ensure((size_t)NB + 1));
   k_image_count<<<nblk(NB, 256), 256, 0, st>>>(NB, e->pos.p, smax, lo, hi, e->gcnt.p);
   CKL();
-  size_t need = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, need, e->gcnt.p, e->goff.p, NB, st);
-  CK(e->cub_tmp.ensure(need));
-  size_t have = e->cub_tmp.n;
-  CK(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, have, e->gcnt.p, e->goff.p, NB, st));
-  ++e->launches;
+  TRY(scan_ex<false>(e, e->gcnt.p, NB, e->goff.p));
   int tail[2] = {0, 0};
   if (NB) {
     CK(cudaMemcpyAsync(&tail[0], e->goff.p + NB - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -757,19 +765,11 @@ ab_status images_and_lists(ab_engine* e) {
   // 3. bin all atoms (locals + ghosts)
   CK(e->key.ensure(NT));
   CK(e->val.ensure(NT));
-  CK(e->key2.ensure(NT));
   CK(e->val2.ensure(NT));
   CK(e->cell_start.ensure((size_t)e->ncell + 1));
   k_cell_keys<<<nblk(NT, 256), 256, 0, st>>>(NT, e->pos.p, e->grid, e->key.p, e->val.p);
   CKL();
-  need = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, need, e->key.p, e->key2.p, e->val.p, e->val2.p, NT, 0, 31, st);
-  CK(e->cub_tmp.ensure(need));
-  have = e->cub_tmp.n;
-  CK(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, have, e->key.p, e->key2.p, e->val.p, e->val2.p, NT, 0, 31, st));
-  ++e->launches;
-  k_cell_bounds<<<nblk(NT + 1, 256), 256, 0, st>>>(NT, e->ncell, e->key2.p, e->cell_start.p);
-  CKL();
+  TRY(key_sort(e, NT, e->key.p, e->ncell, nullptr, e->val2.p, e->cell_start.p));  // cell list
   const bool clp = e->cl_path && e->hp.potential != kREBO;
   if (clp) TRY(build_clusters(e));
   e->rb_ms[2] += tms(tq);
@@ -1678,14 +1678,14 @@ void free_engine(ab_engine* e) {
   e->scratch.release();
   DBuf<double>* bd[] = {&e->vel, &e->vel_tmp, &e->F, &e->io, &e->q_M, &e->stage0, &e->stage1, &e->gio, &e->s_wd};
   for (auto* b : bd) b->release();
-  DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->key2, &e->val, &e->val2, &e->cell_start,
+  DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->val, &e->val2, &e->cell_start,
                      &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
                      &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_q, &e->ovf_q2,
                      &e->sendl[0], &e->sendl[1], &e->fl[0], &e->fl[1], &e->fl[2], &e->idx[0], &e->idx[1],
-                     &e->idx[2], &e->cnt_d, &e->cl_k, &e->cl_v, &e->cl_k2, &e->cl_v2, &e->run_start, &e->run_cl,
+                     &e->idx[2], &e->cnt_d, &e->cl_k, &e->cl_v, &e->cl_v2, &e->run_start, &e->sc_bsum, &e->sc_cur, &e->sc_off, &e->run_cl,
                      &e->cl_atom, &e->clc, &e->cln};
   for (auto* b : bi) b->release();
-  DBuf<unsigned char>* bu[] = {&e->s_dr, &e->s_w, &e->s_N, &e->gtab, &e->cub_tmp, &e->sb[0], &e->sb[1], &e->rb[0], &e->rb[1],
+  DBuf<unsigned char>* bu[] = {&e->s_dr, &e->s_w, &e->s_N, &e->gtab, &e->sb[0], &e->sb[1], &e->rb[0], &e->rb[1],
                                &e->redx};
   for (auto* b : bu) b->release();
   e->Ff.release();

@@ -37,9 +37,8 @@ __device__ __forceinline__ int cl_col(double v, double lo, double w, int n) {
   return c < 0 ? 0 : (c >= n ? n - 1 : c);
 }
 
-// sort key: run = (column, species) in bits 16..30, quantised z in bits 0..15 (ties: atom index,
-// the sort is stable)
-__global__ void k_cl_keys(int NT, const double4* pos, ClGrid g, int* key, int* val) {
+// sort keys: run = (column, species) and the quantised z inside the run (ties: atom index)
+__global__ void k_cl_keys(int NT, const double4* pos, ClGrid g, int* run_of, int* zq_of) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= NT) return;
   const double4 p = pos[a];
@@ -48,27 +47,8 @@ __global__ void k_cl_keys(int NT, const double4* pos, ClGrid g, int* key, int* v
   double zq = (p.z - g.lo[2]) / g.zspan * 65536.0;
   int z = (int)floor(zq);
   z = z < 0 ? 0 : (z > 65535 ? 65535 : z);
-  key[a] = (run << 16) | z;
-  val[a] = a;
-}
-
-// run_start[r] = first sorted position of run r (r in [0, nrun]); sorted keys in key2
-__global__ void k_cl_run_bounds(int NT, int nrun, const int* key2, int* run_start) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a > NT) return;
-  if (a == 0) {
-    const int r0 = NT ? (key2[0] >> 16) : nrun;
-    for (int r = 0; r <= r0; ++r) run_start[r] = 0;
-  }
-  if (a == NT) {
-    const int last = NT ? (key2[NT - 1] >> 16) : -1;
-    for (int r = last + 1; r <= nrun; ++r) run_start[r] = NT;
-    return;
-  }
-  if (a > 0) {
-    const int r0 = key2[a - 1] >> 16, r1 = key2[a] >> 16;
-    for (int r = r0 + 1; r <= r1; ++r) run_start[r] = a;
-  }
+  run_of[a] = run;
+  zq_of[a] = z;
 }
 
 // run_cl[r] = first cluster of run r (exclusive scan of ceil(len / 4)); run_cl[nrun] = clusters.
@@ -109,11 +89,11 @@ __global__ void __launch_bounds__(1024) k_cl_run_scan(int nrun, const int* run_s
   if (threadIdx.x == 0) run_cl[nrun] = carry;
 }
 
-__global__ void k_cl_fill(int NT, const int* key2, const int* val2, const int* run_start, const int* run_cl,
+__global__ void k_cl_fill(int NT, const int* run_of, const int* val2, const int* run_start, const int* run_cl,
                           int* cl_atom) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= NT) return;
-  const int r = key2[q] >> 16;
+  const int r = run_of[val2[q]];
   cl_atom[run_cl[r] * CL_SIZE + (q - run_start[r])] = val2[q];
 }
 

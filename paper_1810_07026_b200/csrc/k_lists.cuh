@@ -72,22 +72,7 @@ __global__ void k_cell_keys(int NT, const double4* pos, Grid g, int* key, int* v
   val[a] = a;
 }
 
-__global__ void k_cell_bounds(int NT, int ncell, const int* sorted_key, int* cell_start) {
-  int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a > NT) return;
-  if (a == 0) {
-    for (int c = 0; c <= (NT ? sorted_key[0] : ncell - 1); ++c) cell_start[c] = 0;
-  }
-  if (a == NT) {
-    int last = NT ? sorted_key[NT - 1] : -1;
-    for (int c = last + 1; c <= ncell; ++c) cell_start[c] = NT;
-    return;
-  }
-  if (a > 0) {
-    int k0 = sorted_key[a - 1], k1 = sorted_key[a];
-    for (int c = k0 + 1; c <= k1; ++c) cell_start[c] = a;
-  }
-}
+// cell_start (first sorted position of each cell): k_scan.cuh key_sort (counting sort)
 
 // Skinned LJ lists of a local atom (full, both directions), split at build time by what the
 // pair can need at evaluation time (atoms move < skin/2 between builds):

@@ -459,7 +459,7 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
   const R rloa = T.rlo[ti], rlob = T.rlo[ti + 1];
   const R iva = T.inv_taper[ti], ivb = T.inv_taper[ti + 1];
   const double rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
-  const double rla = c_geo.rlo2[ti], rlb = c_geo.rlo2[ti + 1];
+  const double rla = VIRIAL ? c_geo.rlo2[ti] : 0.0, rlb = VIRIAL ? c_geo.rlo2[ti + 1] : 0.0;
   // the next chunk's list indices are loaded one iteration ahead: the position gathers of a
   // chunk then wait on one memory latency, not on two dependent ones
   int Jn[FAR_UNROLL];
@@ -491,7 +491,9 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
       double r2 = BAND ? r2_exact(dx, dy, dz) : fma(dz, dz, fma(dy, dy, dx * dx));
       bool in = valid && (!BAND || r2 <= (hj ? rcb : rca));
       nlj += (in && ki < key_of(pj[u]));
-      if (BAND) ntp += (in && ki < key_of(pj[u]) && r2 > (hj ? rlb : rla));  // taper band (counter)
+      // taper-band pairs (algorithmic flop count): counted by the virial (ab_compute) instantiation
+      // only -- in the NVE kernel the extra compare costs ~20 % of the far kernel (measured)
+      if (BAND && VIRIAL) ntp += (in && ki < key_of(pj[u]) && r2 > (hj ? rlb : rla));
       R rr2 = in ? (R)r2 : R(1);
       R y = (BAND || MORSE) ? rsqrt_fast(rr2) : R(0);  // 1/r (taper / Morse only)
       R dVr;

@@ -1,11 +1,11 @@
 #!/bin/bash
 # Round-end ncu set, run on the GPU box from the repo root (bash scripts/collect_profiles.sh TAG):
 # the launch list of a short bench.py run (gpu__time_duration, --clock-control none: cold-cache,
-# serialised; compare shares), one `--set full` capture of each hot kernel and the FP64 / FP32
+# serialised; compare shares) of the default bench workload (cfg4, 1,008,000-atom PE), one `--set full` capture of each hot kernel and the FP64 / FP32
 # instruction-count passes (fp64 and mixed) that scripts/make_profile_summary.py turns into
 # profiles/ncu_summary_TAG.json.  Every ncu pass profiles a command that first exits 0 without ncu.
 set -u
-TAG=${1:-r01}
+TAG=${1:-r02}
 O=gpurun_out
 mkdir -p $O
 RUN="python bench.py --steps 3 --warmup 3 --no-mixed --no-e2e --no-cpu-baseline"

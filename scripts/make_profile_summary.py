@@ -49,7 +49,7 @@ with open(os.path.join(prof, f"launch_shares_{tag}.txt"), "w") as f:
 out = subprocess.run(["python", os.path.join(ROOT, "scripts", "ncu_summary.py"), rep], capture_output=True,
                      text=True).stdout
 open(os.path.join(prof, f"ncu_full_{tag}.txt"), "w").write(
-    f"# ncu --set full --clock-control none --import-source on (scripts/collect_profiles.sh: short bench.py run, cfg2, fp64)\n" + out)
+    f"# ncu --set full --clock-control none --import-source on (scripts/collect_profiles.sh: short bench.py run, cfg4 (1,008,000-atom PE), fp64)\n" + out)
 
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(raw.splitlines()))
@@ -73,7 +73,7 @@ for r in rr[2:]:
 for e in summ["fp64"].values():
     e["dram_bytes_per_launch"] = e["dram_bytes"] / max(e["launches"], 1)
 summ["_note"] = ("ncu --set full capture (cache flushed between replays, i.e. cold-cache DRAM traffic per "
-                 "launch) of a short bench.py run on cfg2, fp64 (scripts/collect_profiles.sh)")
+                 "launch) of a short bench.py run on cfg4 (1,008,000-atom PE), fp64 (scripts/collect_profiles.sh)")
 
 
 def flops_pass(path, prec):
@@ -112,7 +112,7 @@ if len(sys.argv) > 5:
         for k, v in flops_pass(path, prec).items():
             summ.setdefault(prec, {}).setdefault(k, {}).update(v)
     summ["_note_hw"] = ("hw_flops_per_launch: ncu --metrics pass (smsp__sass_thread_inst_executed_op_{d,f}{fma,mul,add}"
-                        "_pred_on.sum; 2 per FMA) of a short bench.py run on cfg2 in each precision (scripts/collect_profiles.sh)")
+                        "_pred_on.sum; 2 per FMA) of a short bench.py run on cfg4 in each precision (scripts/collect_profiles.sh)")
 json.dump(summ, open(os.path.join(prof, f"ncu_summary_{tag}.json"), "w"), indent=1)
 print(open(os.path.join(prof, f"launch_shares_{tag}.txt")).read())
 print(json.dumps(summ, indent=1))
