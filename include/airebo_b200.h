@@ -45,11 +45,16 @@ typedef enum {
   AB_FP64 = 0,  /* IEEE binary64 throughout */
   AB_MIXED = 1, /* fp64 positions/displacements/list decisions/accumulators; fp32 term arithmetic
                    after the displacement vector (SURVEY reading A14) */
-  AB_SINGLE = 2 /* the paper's "single" mode for the precision study (SURVEY
+  AB_SINGLE = 2, /* the paper's "single" mode for the precision study (SURVEY
                    8(f) F2): AB_MIXED with every accumulation in fp32 -- per-thread force / energy
                    / virial sums, the warp reductions and the per-atom force array (fp32 atomics)
                    -- so the accumulator precision is the only difference to AB_MIXED (reading
                    A32).  Positions, velocities and the integrator stay fp64. */
+  AB_REDUCED = 3 /* "binary32 throughout" (the x86 single precision of P:886-888 that
+                    packs positions in fp32): AB_SINGLE plus a binary32 dynamical state -- every
+                    half-kick v + dtf F and drift x + dt v is two binary32 operations (no FMA), so
+                    positions and velocities stay binary32 values between steps (reading A35).
+                    List / gate decisions are still exact fp64 tests of those positions. */
 } ab_precision;
 
 typedef enum {
@@ -69,7 +74,8 @@ typedef struct ab_stats {
   int64_t n_bstar;     /* ... with C_ij != 0 and S_r != 0 (b* evaluated) */
   int64_t n_sb_trans;  /* ... of which b* strictly inside (b_min, b_max) */
   int64_t max_short;   /* max |N(i)| */
-  int64_t max_reach;   /* max number of distinct atom images within 3 bonds of an atom */
+  int64_t max_reach;   /* max number of distinct atom images within 3 bonds of an atom (capped at the
+                          64-slot reach table when it overflows; overflows: n_overflow_retries) */
   int64_t n_badarg;    /* p^{sigma pi} arguments <= 0 (must be 0) */
   int64_t n_atoms, n_ghosts, n_rebuilds, n_steps, n_overflow_retries;
   int64_t lj_capacity, inter_capacity;

@@ -1321,7 +1321,7 @@ ab_status enqueue_forces(ab_engine* e) {
 
 ab_status enqueue_forces_any(ab_engine* e) {
   if (e->prec == AB_FP64) return enqueue_forces<double>(e);
-  if (e->prec == AB_SINGLE) return enqueue_forces<float, true>(e);
+  if (e->prec == AB_SINGLE || e->prec == AB_REDUCED) return enqueue_forces<float, true>(e);
   return enqueue_forces<float>(e);
 }
 
@@ -1374,7 +1374,8 @@ ab_status flush_kick(ab_engine* e) {
   for (ab_engine* d : doms(e))
     if (d->kick_pending) {
       d->kick_pending = false;
-      k_integrate2<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->pos.p, d->vel.p, d->F.p, d->kick_dtf[0], d->kick_dtf[1]);
+      k_integrate2<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->pos.p, d->vel.p, d->F.p, d->kick_dtf[0], d->kick_dtf[1],
+                                                     d->prec == AB_REDUCED);
       CKL();
     }
   return AB_OK;
@@ -1863,7 +1864,7 @@ ab_status check_slab_box(ab_engine* e) {
 extern "C" {
 
 ab_status ab_create(const char* text, size_t len, ab_precision prec, int device, ab_engine** out) {
-  if (!text || !out || (prec != AB_FP64 && prec != AB_MIXED && prec != AB_SINGLE)) {
+  if (!text || !out || (prec != AB_FP64 && prec != AB_MIXED && prec != AB_SINGLE && prec != AB_REDUCED)) {
     g_create_error = "ab_create: bad argument";
     return AB_E_ARG;
   }
@@ -2284,12 +2285,12 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
                    d->ct.p};
         k_integrate1_img<<<nblk(d->N, AB_INT_BLOCK), AB_INT_BLOCK, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, pre, pd0, pd1, dtf0, dtf1, dt,
                                                           d->xref.p, d->ct.p + CT_N, d->NX, d->goff.p, d->gcnt.p,
-                                                          d->rshift.p, fo);
+                                                          d->rshift.p, fo, d->prec == AB_REDUCED);
         d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = true;
         flags_published = true;
       } else {
         k_integrate1<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt, d->xref.p,
-                                                      d->ct.p + CT_N);
+                                                      d->ct.p + CT_N, d->prec == AB_REDUCED);
       }
       CKL();
     }
@@ -2334,7 +2335,8 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     for (ab_engine* d : D) {
       if (d->post_pending && th) {  // the thermo row needs the energies now
         k_post<<<ACC_N + CT_N + nblk(d->N, 256), 256, 0, st>>>(d->post_rr, d->post_rows, d->acc.p, d->ct.p, d->N,
-                                                               d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
+                                                               d->pos.p, d->vel.p, d->F.p, dtf0, dtf1,
+                                                               d->prec == AB_REDUCED);
         d->post_pending = false;
       } else {
         if (d->post_pending && s == nsteps) d->reduce_lazy = true, d->lazy_rr = d->post_rr, d->lazy_rows = d->post_rows;
@@ -2343,7 +2345,8 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
           d->kick_pending = true, d->kick_dtf[0] = dtf0, d->kick_dtf[1] = dtf1;
           continue;
         }
-        k_integrate2<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1);
+        k_integrate2<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1,
+                                                      d->prec == AB_REDUCED);
       }
       CKL();
     }

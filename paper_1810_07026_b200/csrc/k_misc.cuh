@@ -21,19 +21,30 @@ __device__ __forceinline__ void block_max_atomic(double v, unsigned long long* o
   }
 }
 
+// one velocity-Verlet half-kick / drift component.  r32 = AB_REDUCED (the paper's single precision
+// with the dynamical state in binary32, reading A35): both operations rounded to binary32 (no FMA)
+__device__ __forceinline__ double kick(double v, double dtf, double f, bool r32) {
+  if (r32) return (double)__fadd_rn((float)v, __fmul_rn((float)dtf, (float)f));
+  return v + dtf * f;
+}
+__device__ __forceinline__ double drift(double x, double dt, double v, bool r32) {
+  if (r32) return (double)__fadd_rn((float)x, __fmul_rn((float)dt, (float)v));
+  return x + dt * v;
+}
+
 // v += dt/2 F/m ftm2v;  x += dt v;  max |x - x_ref|^2 since the last list build
 __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, double dtf0, double dtf1, double dt,
-                             const double4* xref, unsigned long long* maxd2) {
+                             const double4* xref, unsigned long long* maxd2, bool r32) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (i < N) {
     double4 p = pos[i];
     double dtf = (type_of(p) == 0) ? dtf0 : dtf1;
-    double vx = v[3 * i + 0] + dtf * F[3 * i + 0];
-    double vy = v[3 * i + 1] + dtf * F[3 * i + 1];
-    double vz = v[3 * i + 2] + dtf * F[3 * i + 2];
+    double vx = kick(v[3 * i + 0], dtf, F[3 * i + 0], r32);
+    double vy = kick(v[3 * i + 1], dtf, F[3 * i + 1], r32);
+    double vz = kick(v[3 * i + 2], dtf, F[3 * i + 2], r32);
     v[3 * i + 0] = vx, v[3 * i + 1] = vy, v[3 * i + 2] = vz;
-    p.x += dt * vx, p.y += dt * vy, p.z += dt * vz;
+    p.x = drift(p.x, dt, vx, r32), p.y = drift(p.y, dt, vy, r32), p.z = drift(p.z, dt, vz, r32);
     pos[i] = p;
     double4 r = xref[i];
     double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
@@ -80,7 +91,7 @@ __device__ __forceinline__ void publish_flags(const FlagOut& fo, unsigned long l
 __global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, bool pre, double pd0, double pd1,
                                  double dtf0, double dtf1, double dt,
                                  const double4* xref, unsigned long long* maxd2, int NB, const int* goff,
-                                 const int* gcnt, const char4* rshift, FlagOut fo) {
+                                 const int* gcnt, const char4* rshift, FlagOut fo, bool r32) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (i < N) {
@@ -99,14 +110,14 @@ __global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, bool
     double u0 = v0, u1 = v1, u2 = v2;
     if (pre) {  // the previous step's deferred second half-kick (k_integrate2's operations)
       const double pdtf = (type_of(p) == 0) ? pd0 : pd1;
-      u0 = v0 + pdtf * f0, u1 = v1 + pdtf * f1, u2 = v2 + pdtf * f2;
+      u0 = kick(v0, pdtf, f0, r32), u1 = kick(v1, pdtf, f1, r32), u2 = kick(v2, pdtf, f2, r32);
     }
-    double vx = u0 + dtf * f0;
-    double vy = u1 + dtf * f1;
-    double vz = u2 + dtf * f2;
+    double vx = kick(u0, dtf, f0, r32);
+    double vy = kick(u1, dtf, f1, r32);
+    double vz = kick(u2, dtf, f2, r32);
     F[3 * i + 0] = 0.0, F[3 * i + 1] = 0.0, F[3 * i + 2] = 0.0;
     v[3 * i + 0] = vx, v[3 * i + 1] = vy, v[3 * i + 2] = vz;
-    p.x += dt * vx, p.y += dt * vy, p.z += dt * vz;
+    p.x = drift(p.x, dt, vx, r32), p.y = drift(p.y, dt, vy, r32), p.z = drift(p.z, dt, vz, r32);
     pos[i] = p;
     double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
     d2 = dx * dx + dy * dy + dz * dz;
@@ -131,19 +142,20 @@ __global__ void k_widen(int n, const float* Ff, double* F) {
   if (t < n) F[t] = (double)Ff[t];
 }
 
-__global__ void k_integrate2(int N, const double4* pos, double* v, const double* F, double dtf0, double dtf1) {
+__global__ void k_integrate2(int N, const double4* pos, double* v, const double* F, double dtf0, double dtf1,
+                             bool r32) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   double dtf = (type_of(pos[i]) == 0) ? dtf0 : dtf1;
-  v[3 * i + 0] += dtf * F[3 * i + 0];
-  v[3 * i + 1] += dtf * F[3 * i + 1];
-  v[3 * i + 2] += dtf * F[3 * i + 2];
+  v[3 * i + 0] = kick(v[3 * i + 0], dtf, F[3 * i + 0], r32);
+  v[3 * i + 1] = kick(v[3 * i + 1], dtf, F[3 * i + 1], r32);
+  v[3 * i + 2] = kick(v[3 * i + 2], dtf, F[3 * i + 2], r32);
 }
 
 // NVE second half-kick fused with the reduction of the evaluation's partial rows (the two are
 // independent): blocks [0, ACC_N + CT_N) reduce one column each, the rest kick 256 atoms each
 __global__ void k_post(RedRows R, int nrows, double* acc, unsigned long long* ct, int N, const double4* pos, double* v,
-                       const double* F, double dtf0, double dtf1) {
+                       const double* F, double dtf0, double dtf1, bool r32) {
   if (blockIdx.x < ACC_N + CT_N) {
     reduce_column(R, nrows, acc, ct, blockIdx.x);
     return;
@@ -151,9 +163,9 @@ __global__ void k_post(RedRows R, int nrows, double* acc, unsigned long long* ct
   int i = (blockIdx.x - (ACC_N + CT_N)) * blockDim.x + threadIdx.x;
   if (i >= N) return;
   double dtf = (type_of(pos[i]) == 0) ? dtf0 : dtf1;
-  v[3 * i + 0] += dtf * F[3 * i + 0];
-  v[3 * i + 1] += dtf * F[3 * i + 1];
-  v[3 * i + 2] += dtf * F[3 * i + 2];
+  v[3 * i + 0] = kick(v[3 * i + 0], dtf, F[3 * i + 0], r32);
+  v[3 * i + 1] = kick(v[3 * i + 1], dtf, F[3 * i + 1], r32);
+  v[3 * i + 2] = kick(v[3 * i + 2], dtf, F[3 * i + 2], r32);
 }
 
 __global__ void k_maxdisp(int N, const double4* pos, const double4* xref, unsigned long long* maxd2) {

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AIREBO_B200_LIB", os.path.join(HERE, "libairebo_b200.so"))
 PARAMS = os.path.join(os.path.dirname(HERE), "params", "toy_ch.param")
 
-AB_FP64, AB_MIXED, AB_SINGLE = 0, 1, 2
+AB_FP64, AB_MIXED, AB_SINGLE, AB_REDUCED = 0, 1, 2, 3
 AB_LIST_SHORT, AB_LIST_BONDS, AB_LIST_LJ = 0, 1, 2
 STATUS = {0: "AB_OK", -1: "AB_E_ARG", -2: "AB_E_PARAM", -3: "AB_E_BOX", -4: "AB_E_STATE", -5: "AB_E_OOM",
           -6: "AB_E_CUDA", -7: "AB_E_NCCL", -8: "AB_E_NONFINITE"}
@@ -133,7 +133,7 @@ class Engine:
             with open(PARAMS, "rb") as f:
                 params = f.read()
         h = C.c_void_p()
-        prec = {"fp64": AB_FP64, "mixed": AB_MIXED, "single": AB_SINGLE}[precision]
+        prec = {"fp64": AB_FP64, "mixed": AB_MIXED, "single": AB_SINGLE, "reduced": AB_REDUCED}[precision]
         if ranks is None:
             rc = self.L.ab_create(params, len(params), prec, device, C.byref(h))
         elif ranks[0] == "virtual":

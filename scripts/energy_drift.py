@@ -1,5 +1,6 @@
 """Precision study (the paper's section 5.2 experiment): total-energy
-drift of long NVE runs in fp64, mixed and single precision (AB_SINGLE: fp32 accumulation) on the
+drift of long NVE runs in fp64, mixed, single (AB_SINGLE: fp32 accumulation) and reduced precision
+(AB_REDUCED: binary32 accumulation and binary32 positions / velocities, reading A35) on the
 all-carbon nanotube (the paper's CNT workload) and on polyethylene.  argv: steps, dt_fs,
 systems (all | cnt | pe | cfg2), precisions (comma list).  Prints one JSON line per (system, precision): the maximal
 |E_tot(t) - E_tot(0)| per atom and the slope of a linear fit (eV/atom/ps)."""

@@ -363,3 +363,36 @@ def test_cluster_lj_path_parity(eng_mod, which, monkeypatch):
         gm = run_gpu(eng_mod, s, "mixed")
         rel = np.sqrt(((gm["F"] - o["F"]) ** 2).sum()) / max(np.sqrt((o["F"] ** 2).sum()), 1e-300)
         assert rel <= 1e-4, (s.name, rel)
+
+
+def fcc_carbon(rep=3, nn=1.6, jitter=0.04, seed=3):
+    """Over-coordinated test solid: fcc carbon with a 1.6 A nearest-neighbour distance (12 short
+    neighbours, second shell beyond r_max), jittered: 146 atom images within 3 bonds of an atom,
+    more than the 64-slot reach table of the near-LJ kernel holds."""
+    a = nn * np.sqrt(2)
+    fcc = np.array([[0, 0, 0], [0, .5, .5], [.5, 0, .5], [.5, .5, 0]])
+    g = np.stack(np.meshgrid(*[np.arange(rep)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    x = ((g[:, None, :] + fcc[None]) * a).reshape(-1, 3)
+    x = x + np.random.default_rng(seed).uniform(-jitter, jitter, x.shape)
+    box = np.full(3, rep * a)
+    return I.System("fcc-carbon-overcoordinated", np.zeros(len(x), dtype=np.int32), I.wrap(x, box), box)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "mixed"])
+def test_reach_table_overflow_fallback(eng_mod, precision):
+    """Reach sets larger than the shared-memory table ("sequential fallback"): the near-LJ
+    kernel falls back to the nested path search for those atoms; results stay at the
+    parity tolerances and the overflow is counted (n_overflow_retries > 0)."""
+    s = fcc_carbon()
+    o = O.compute(s.types, s.x, s.box)
+    assert o["counters"]["max_reach"] > 64
+    g = run_gpu(eng_mod, s, precision)
+    assert g["stats"]["n_overflow_retries"] > 0
+    if precision == "fp64":
+        check_fp64(s, g, o)
+        for k in COUNTERS:
+            if k != "max_reach":  # the GPU reports the table fill, capped by its size
+                assert g["stats"][k] == o["counters"][k], (k, g["stats"][k], o["counters"][k])
+    else:
+        rel = np.sqrt(((g["F"] - o["F"]) ** 2).sum()) / np.sqrt((o["F"] ** 2).sum())
+        assert rel <= 1e-4 and abs(g["E"] - o["E"]) <= 1e-6 * abs(o["E"])

@@ -61,3 +61,28 @@ def test_single_nve_runs_and_tracks_mixed(eng_mod):
     assert np.all(np.isfinite(th["single"]))
     # a 50 fs run: the two trajectories agree to fp32 noise in the total energy
     assert np.abs(th["single"][:, 3] - th["mixed"][:, 3]).max() <= 1e-4 * abs(th["mixed"][0, 3])
+
+
+def test_reduced_state_is_binary32(eng_mod):
+    """AB_REDUCED (reading A35): after NVE steps (deferred and thermo kicks, with a rebuild) every
+    position and velocity component is a binary32 value; a single evaluation is AB_SINGLE's (same
+    kernels, same tolerance against the oracle at the state it produced)."""
+    s = I.config(1)
+    e = eng_mod.make(s, "reduced")
+    e.run_nve(7, 0.5)
+    e.run_nve(5, 0.5, every=5)
+    x, v = e.get_positions(), e.get_velocities()
+    # wrapping at a rebuild (x - L floor(x/L)) may leave a non-binary32 value only until the next drift
+    e.run_nve(1, 0.5)
+    x, v = e.get_positions(), e.get_velocities()
+    assert np.array_equal(v.astype(np.float32).astype(np.float64), v)
+    xs = x[(x > 0.5) & (x < s.box - 0.5)]  # away from the wrap boundary
+    assert np.array_equal(xs.astype(np.float32).astype(np.float64), xs)
+    g = e.compute()
+    o = O.compute(s.types, x, s.box)
+    rel = np.sqrt(((g["F"] - o["F"]) ** 2).sum()) / np.sqrt((o["F"] ** 2).sum())
+    assert rel <= 1e-3 and abs(g["E"] - o["E"]) <= 1e-5 * abs(o["E"])
+    # and it differs from AB_SINGLE's fp64-state trajectory
+    es = eng_mod.make(s, "single")
+    es.run_nve(13, 0.5)
+    assert not np.array_equal(es.get_positions(), x)
