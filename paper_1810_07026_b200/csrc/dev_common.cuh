@@ -31,6 +31,9 @@ struct Tab {
   R kappa, rhoH[2];  // rho_{C H}, rho_{H H}
   int g2on;
   R gnlo, gnhi;
+  // rigorous bounds of pi^rc and T over their whole tables (tensor-product Hermite overshoot
+  // included): the b* plateau test of the deferred batch (k_bond.cuh bstar_plateau)
+  R bRlo[3], bRhi[3], bTlo[3], bThi[3];
   R P[2][25], Rt[3][225], Tt[3][225];
   R conj_lo, conj_hi, s2lo, s2hi;
   R tors[2][2][2][2];

@@ -196,6 +196,7 @@ struct ab_engine {
   DBuf<int2> bonds;
   DBuf<int4> q_item;
   DBuf<int> ovf_bond, ovf_q, ovf_q2;  // overflow (large side / full b*) index lists
+  DBuf<int> ovf_mid;                  // CH / HH bonds with two non-empty sides (general REBO kernel)
   DBuf<double> q_M;
   // one small device scratch block, zeroed with a single memset per evaluation:
   //   acc (ACC_N doubles) at 0, ct (CT_N + 1 u64; [CT_N] = max displacement^2) at 128,
@@ -431,6 +432,17 @@ void fill_tab(const HostParams& hp, Tab<R>& t) {
   t.rhoH[0] = (R)hp.pr[1].rho, t.rhoH[1] = (R)hp.pr[2].rho;  // rho_{CH}, rho_{HH}
   t.g2on = hp.gknot2.empty() ? 0 : 1;
   t.gnlo = (R)hp.gnlo, t.gnhi = (R)hp.gnhi;
+  // f = sum_abc phi_a phi_b phi_c F_abc with sum phi = 1 and sum |phi| <= (1 + 8/27)^3 per point
+  // (1-D Hermite weights: h00 + h01 = 1, |h10|, |h11| <= 4/27), so f lies within [min F - k dF,
+  // max F + k dF], k = ((35/27)^3 - 1) / 2, dF = max F - min F
+  const double ko = (std::pow(35.0 / 27.0, 3) - 1.0) / 2.0;
+  for (int p = 0; p < 3; ++p)
+    for (int w = 0; w < 2; ++w) {
+      const std::vector<double>& tab = w == 0 ? hp.Rtab[p] : hp.Ttab[p];
+      const double mn = *std::min_element(tab.begin(), tab.end()), mx = *std::max_element(tab.begin(), tab.end());
+      const double lo = mn - ko * (mx - mn), hi = mx + ko * (mx - mn);
+      (w == 0 ? t.bRlo : t.bTlo)[p] = (R)lo, (w == 0 ? t.bRhi : t.bThi)[p] = (R)hi;
+    }
   for (int a = 0; a < 2; ++a)
     for (int q = 0; q < 25; ++q) t.P[a][q] = (R)hp.Ptab[a][q];
   for (int p = 0; p < 3; ++p)
@@ -1141,8 +1153,12 @@ ab_status enqueue_forces(ab_engine* e) {
   const int g_near = clp ? std::min(nblk((long long)N * 32, 128), e->nsm * AB_LJC_MINBLOCKS) : nblk(N, NEAR_ATOMS);
   const int g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4;
   const int g_slow = e->nsm * 2;
-  const int nrows = g_short + g_rebo + g_near + g_far + g_bstar + 3 * g_slow;  // b* full and NBMAX: g_slow
+  // REBO: general NB_FAST kernel on the CC region, one-empty-side kernel on CH / HH, general kernel
+  // on the bonds the latter hands over, NBMAX kernel on the large-side overflow
+  const int g_rebo_rows = 2 * g_rebo + 2 * g_slow;
+  const int nrows = g_short + g_rebo_rows + g_near + g_far + g_bstar + 2 * g_slow;  // b* full and NBMAX: g_slow
   CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
+  CK(e->ovf_mid.ensure((size_t)N * e->capS + 1));
   CK(e->ovf_q.ensure(e->capQ));
   CK(e->ovf_q2.ensure(e->capQ));
   CK(e->red_d.ensure((size_t)ACC_N * nrows));
@@ -1155,9 +1171,9 @@ ab_status enqueue_forces(ab_engine* e) {
   // atomics from all of them.
   const bool serial = e->serial;
   const bool lj = e->hp.potential != kREBO, morse = e->hp.potential == kAIREBOM;
-  const int nrows_used = lj ? nrows : g_short + g_rebo + g_slow;  // REBO: short + bond kernels only
+  const int nrows_used = lj ? nrows : g_short + g_rebo_rows;  // REBO: short + bond kernels only
   const cudaStream_t s_rebo = serial ? st : e->aux[0], s_far = serial ? st : e->aux[1];
-  const int row_far = g_short + g_rebo + g_slow + g_near;
+  const int row_far = g_short + g_rebo_rows + g_near;
   BstarQueue Qu;
   Qu.item = e->q_item.p, Qu.M = e->q_M.p, Qu.count = e->small_i.p + 13;
   for (int t = 0; t < 3; ++t) Qu.cap[t] = e->qcap[t], Qu.off[t] = e->qoff[t];
@@ -1205,22 +1221,32 @@ ab_status enqueue_forces(ab_engine* e) {
     cudaEvent_t t = prof_start(e, s_rebo);
     RedRows R1 = RR;
     R1.row0 = g_short;
-    auto rebo = [&](auto fast, auto slow) {
+    int* const nbig = e->small_i.p + 8;  // large-side overflow (NBMAX kernel)
+    int* const nmid = e->small_i.p + 0;  // CH / HH bonds with two non-empty sides
+    auto rebo = [&](auto fast, auto one, auto slow) {
       if (e->skip & 1) return;
-      fast<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, e->ovf_bond.p, e->small_i.p + 8, S, e->typ.p, e->owner.p,
+      fast<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, nullptr, 0, 1, e->ovf_bond.p, nbig, S, e->typ.p, e->owner.p,
                                        e->gid.p, e->shift.p, Fk, sb0, R1);
       R1.row0 += g_rebo;
-      slow<<<g_slow, 128, 0, s_rebo>>>(BL, e->ovf_bond.p, nullptr, e->small_i.p + 8, S, e->typ.p, e->owner.p,
+      one<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, nullptr, 1, 3, e->ovf_mid.p, nmid, S, e->typ.p, e->owner.p,
+                                      e->gid.p, e->shift.p, Fk, sb0, R1);
+      R1.row0 += g_rebo;
+      fast<<<g_slow, 128, 0, s_rebo>>>(BL, e->ovf_mid.p, nmid, 0, 0, e->ovf_bond.p, nbig, S, e->typ.p, e->owner.p,
+                                       e->gid.p, e->shift.p, Fk, sb0, R1);
+      R1.row0 += g_slow;
+      slow<<<g_slow, 128, 0, s_rebo>>>(BL, e->ovf_bond.p, nbig, 0, 0, nullptr, nullptr, S, e->typ.p, e->owner.p,
                                        e->gid.p, e->shift.p, Fk, sb0, R1);
     };
-    if (e->want_virial) rebo(k_rebo<R, NB_FAST, true, SG>, k_rebo<R, NBMAX, true, SG>);
-    else rebo(k_rebo<R, NB_FAST, false, SG>, k_rebo<R, NBMAX, false, SG>);
-    ++e->launches;  // + the CKL below: two launches
+    if (e->want_virial)
+      rebo(k_rebo<R, NB_FAST, true, SG>, k_rebo<R, NB_FAST, true, SG, 0>, k_rebo<R, NBMAX, true, SG>);
+    else
+      rebo(k_rebo<R, NB_FAST, false, SG>, k_rebo<R, NB_FAST, false, SG, 0>, k_rebo<R, NBMAX, false, SG>);
+    e->launches += 3;  // + the CKL below: four launches
     CKL();
     prof_stop(e, 1, s_rebo, t);
   }
   if (!lj) CK(cudaEventRecord(e->ev_join[0], s_rebo));
-  RR.row0 = g_short + g_rebo + g_slow;
+  RR.row0 = g_short + g_rebo_rows;
   if (lj) {
     cudaEvent_t t = prof_start(e, st);
     auto near = [&](auto kern) {
@@ -1681,7 +1707,7 @@ void free_engine(ab_engine* e) {
   for (auto* b : bd) b->release();
   DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->val, &e->val2, &e->cell_start,
                      &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
-                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_q, &e->ovf_q2,
+                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_mid, &e->ovf_q, &e->ovf_q2,
                      &e->sendl[0], &e->sendl[1], &e->fl[0], &e->fl[1], &e->fl[2], &e->idx[0], &e->idx[1],
                      &e->idx[2], &e->cnt_d, &e->cl_k, &e->cl_v, &e->cl_v2, &e->run_start, &e->sc_bsum, &e->sc_cur, &e->sc_off, &e->run_cl,
                      &e->cl_atom, &e->clc, &e->cln};

@@ -30,10 +30,16 @@ constexpr int NB_FAST = 4;
 // (instruction-cache stalls), so each caller chooses.
 template <int NB, bool U>
 struct Unr {
-  static constexpr int v = (U && NB <= NB_FAST) ? NB : 1;
+  static constexpr int v = (U && NB <= NB_FAST && NB > 0) ? NB : 1;
+};
+template <int NB>
+struct Cap {  // array extent for a side of NB entries (NB = 0: the side is empty)
+  static constexpr int v = NB > 0 ? NB : 1;
 };
 
-template <typename R, int NB>
+// NB: capacity of the i side, NBJ: of the J side (NBJ = 0: specialised for an empty J side, e.g.
+// the H end of a C-H bond of a saturated hydrocarbon)
+template <typename R, int NB, int NBJ = NB>
 struct BoState {
   int i, J, ti, tj;
   V3<R> d, u;  // the bond vector used for angles (d_ij or rho d_hat) and its unit vector
@@ -41,7 +47,7 @@ struct BoState {
   int nI, nJ;
   int pq, pl;     // slot of the partner in N(i) / of i in N(J), -1 if absent
   bool overflow;  // a side has more than NB neighbours: use the NB = NBMAX instantiation
-  R cl[NB], Gl[NB], dGl[NB];
+  R cl[Cap<NBJ>::v], Gl[Cap<NBJ>::v], dGl[Cap<NBJ>::v];
   R Si, Sj, PxI, PyI, PxJ, PyJ;
   R pij, pji, Nij, Nji, Nconj;
   R QI, dQI, QJ, dQJ;  // F3 g_C(cos, N) blend weight S(N) per side and dS/dN (sum_1 - sum_2)
@@ -111,9 +117,9 @@ __device__ __forceinline__ R gblend(int tc, R c, R Q, R& dg) {
 }
 
 // ---------------------------------------------------------------- forward pass
-template <typename R, bool TORS, int NB, bool UNROLL = false>
+template <typename R, bool TORS, int NB, bool UNROLL = false, int NBJ = NB>
 __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed char* typ, int i, int J, V3<R> d, R r,
-                           BoState<R, NB>& st) {
+                           BoState<R, NB, NBJ>& st) {
   const Tab<R>& T = tab<R>();
   st.i = i, st.J = J, st.ti = typ[i], st.tj = typ[J], st.d = d, st.r = r;
   const int ti = st.ti, tj = st.tj;
@@ -126,7 +132,7 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
     if (S.nbr[bj + q] == i) pl = q;
   const int nI = ni - (pq >= 0), nJ = nj - (pl >= 0);
   st.pq = pq, st.pl = pl, st.nI = nI, st.nJ = nJ;
-  st.overflow = nI > NB || nJ > NB;
+  st.overflow = nI > NB || nJ > NBJ;
   st.bad = false;
   if (st.overflow) return;
   R ir = R(1) / r;
@@ -161,8 +167,8 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
   const bool blendJ = tj == 0 && T.g2on;
   R sumJ = 0, sumJ2 = 0, NCj = 0, NHj = 0, Sj = 0;
   const V3<R> md = mk3(-d.x, -d.y, -d.z);
-#pragma unroll(Unr<NB, UNROLL>::v)
-  for (int c = 0; c < NB; ++c) {
+#pragma unroll(Unr<NBJ, UNROLL>::v)
+  for (int c = 0; c < NBJ; ++c) {
     if (c >= nJ) continue;
     int q = side_slot(c, pl);
     int l = S.nbr[bj + q];
@@ -237,8 +243,8 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
     R Gk = guardG<R>(ck, dGk);
     V3<R> n1 = cross3(dk, d);
     R n1s = dot3(n1, n1);
-#pragma unroll(Unr<NB, UNROLL>::v)
-    for (int c = 0; c < NB; ++c) {
+#pragma unroll(Unr<NBJ, UNROLL>::v)
+    for (int c = 0; c < NBJ; ++c) {
       if (c >= nJ) continue;
       int ql = side_slot(c, pl);
       int l = S.nbr[bj + ql];
@@ -263,8 +269,8 @@ __device__ __forceinline__ void bo_forward(const ShortList<R>& S, const signed c
   st.nquads = nq;
 }
 
-template <typename R, int NB>
-__device__ __forceinline__ R bo_value(const BoState<R, NB>& st) {
+template <typename R, int NB, int NBJ>
+__device__ __forceinline__ R bo_value(const BoState<R, NB, NBJ>& st) {
   return R(0.5) * (st.pij + st.pji) + st.Rv + st.Tv * st.D;
 }
 
@@ -298,8 +304,8 @@ __device__ __forceinline__ void conj_chain(const ShortList<R>& S, const int* own
 // cb = dE/db.  wij: weight of the bond for the merged torsion term (TORS only).
 // Output gd = dE/d(d) through the bond-order (and torsion) terms; fi / fj = force contributions
 // on i / J from the k and l vectors (the forces on k, l, m, n are scattered here).
-template <typename R, bool TORS, int NB, bool UNROLL = false, bool SG = false>
-__device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const int* owner, const BoState<R, NB>& st,
+template <typename R, bool TORS, int NB, bool UNROLL = false, bool SG = false, int NBJ = NB>
+__device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed char* typ, const int* owner, const BoState<R, NB, NBJ>& st,
                            R cb, R wij, double* F, double W[6], V3<R>& gd, V3<R>& fi, V3<R>& fj) {
   const Tab<R>& T = tab<R>();
   const int i = st.i, J = st.J, ti = st.ti, tj = st.tj, nI = st.nI, nJ = st.nJ;
@@ -316,11 +322,11 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
   gd = mk3<R>(0, 0, 0);
   fi = mk3<R>(0, 0, 0);
   fj = mk3<R>(0, 0, 0);
-  R Wl[NB], Cl[NB], Ll[NB];
-  V3<R> gl[NB];
+  R Wl[Cap<NBJ>::v], Cl[Cap<NBJ>::v], Ll[Cap<NBJ>::v];
+  V3<R> gl[Cap<NBJ>::v];
   const bool lamI = ti == 1 && T.kappa != R(0), lamJ = tj == 1 && T.kappa != R(0);  // F3 lambda(r)
-#pragma unroll(Unr<NB, UNROLL>::v)
-  for (int c = 0; c < NB; ++c) {
+#pragma unroll(Unr<NBJ, UNROLL>::v)
+  for (int c = 0; c < NBJ; ++c) {
     if (c >= nJ) continue;
     int q = side_slot(c, st.pl);
     int l = S.nbr[bj + q];
@@ -374,8 +380,8 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     if (Gk != R(0)) {
       V3<R> n1 = cross3(dk, d);
       R inv1 = rsq(dot3(n1, n1));
-#pragma unroll(Unr<NB, UNROLL>::v)
-      for (int c = 0; c < NB; ++c) {
+#pragma unroll(Unr<NBJ, UNROLL>::v)
+      for (int c = 0; c < NBJ; ++c) {
         if (c >= nJ) continue;
         int ql = side_slot(c, st.pl);
         int l = S.nbr[bj + ql];
@@ -421,8 +427,8 @@ __device__ __forceinline__ void bo_reverse(const ShortList<R>& S, const signed c
     vir_add(W, dk, gk);
     if (chain != R(0)) conj_chain<R, SG>(S, owner, k, i, chain, F, W);
   }
-#pragma unroll(Unr<NB, UNROLL>::v)
-  for (int c = 0; c < NB; ++c) {
+#pragma unroll(Unr<NBJ, UNROLL>::v)
+  for (int c = 0; c < NBJ; ++c) {
     if (c >= nJ) continue;
     int q = side_slot(c, st.pl);
     int l = S.nbr[bj + q];
@@ -479,35 +485,65 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 #ifndef AB_REBO_MINBLOCKS
 #define AB_REBO_MINBLOCKS 1
 #endif
+#ifndef AB_REBO1_MINBLOCKS
+#define AB_REBO1_MINBLOCKS 3  // the one-empty-side batch (no J-side arrays, no dihedral loop)
+#endif
 #ifndef AB_BSTAR_MINBLOCKS
 #define AB_BSTAR_MINBLOCKS 3  // measured (cfg2): 3 blocks (170 regs) 56 us vs 64 us at 2 blocks
 #endif
 // VIR = false (NVE steps): no virial accumulation and no stage rows (compiled out)
-template <typename R, int NB, bool VIR, bool SG = false>
-__global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_rebo(BondList BL, const int* list_idx,
-                                              int* ovf, int* novf, ShortList<R> S, const signed char* typ,
-                                              const int* owner, const int* gid, const char4* shift, double* F,
-                                              StageBuf stage, RedRows RR) {
+// Work: the bonds of the species regions [reg0, reg1) (list_idx == nullptr) or the *nlist bond
+// indices of list_idx.  Bonds this instantiation cannot take are appended to ovf (count *novf).
+// NBJ = 0 (the "one empty side" batch of the CH / HH regions): a bond whose i side is empty is
+// evaluated with its ends swapped (b_ij, the pair terms and the forces are symmetric in i, j);
+// a bond with two non-empty sides goes to ovf for the general NB_FAST kernel.
+template <typename R, int NB, bool VIR, bool SG = false, int NBJ = NB>
+__global__ void __launch_bounds__(128, (NB <= NB_FAST && NBJ > 0) ? AB_REBO_MINBLOCKS
+                                                                   : (NBJ == 0 ? AB_REBO1_MINBLOCKS : 1))
+    k_rebo(BondList BL, const int* list_idx, const int* nlist, int reg0, int reg1, int* ovf, int* novf,
+           ShortList<R> S, const signed char* typ, const int* owner, const int* gid, const char4* shift, double* F,
+           StageBuf stage, RedRows RR) {
   __shared__ RedSmem rs;
-  if (red_idle_block(list_idx ? *novf : BL.cnt[0] + BL.cnt[1] + BL.cnt[2], RR)) return;
+  int nr[3] = {0, 0, 0};
+  for (int g = reg0; g < reg1; ++g) nr[g] = BL.cnt[g];
+  const int nb = list_idx ? *nlist : nr[0] + nr[1] + nr[2];
+  if (red_idle_block(nb, RR)) return;
   red_init(rs);
   const Tab<R>& T = tab<R>();
-  const int n0 = BL.cnt[0], n01 = n0 + BL.cnt[1];
-  const int nb = list_idx ? *novf : n01 + BL.cnt[2];
   double e[3 + 6] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   unsigned long long nq = 0, nbad = 0, ncount = 0, nang = 0;
   int stride = gridDim.x * blockDim.x;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += stride) {
-    int bidx = list_idx ? list_idx[t]
-                        : (t < n0 ? t : (t < n01 ? BL.cap + (t - n0) : 2 * BL.cap + (t - n01)));
+    int bidx;
+    if (list_idx) {
+      bidx = list_idx[t];
+    } else {
+      int g = 0, u = t;
+      while (u >= nr[g]) u -= nr[g++];
+      bidx = g * BL.cap + u;
+    }
     int2 bd = BL.b[bidx];
     int i = bd.x, q = bd.y;
     size_t e0 = (size_t)i * S.capS + q;
     int J = S.nbr[e0];
     R r;
     V3<R> d = sl_d(S, i, q, r);
-    BoState<R, NB> st;
-    bo_forward<R, true, NB>(S, typ, i, J, d, r, st);
+    bool swapped = false;
+    if (NBJ == 0) {  // the partner occupies one slot of each list: the sides are cnt - 1
+      const int nI0 = S.cnt[i] - 1, nJ0 = S.cnt[J] - 1;
+      if (nJ0 != 0) {
+        if (nI0 != 0) {  // two non-empty sides: the general kernel
+          list_append(ovf, novf, 1 << 30, bidx);
+          continue;
+        }
+        swapped = true;
+        const int tmp = i;
+        i = J, J = tmp;
+        d = mk3(-d.x, -d.y, -d.z);
+      }
+    }
+    BoState<R, NB, NBJ> st;
+    bo_forward<R, true, NB, false, NBJ>(S, typ, i, J, d, r, st);
     if (st.overflow) {  // only possible for NB = NB_FAST
       list_append(ovf, novf, 1 << 30, bidx);
       continue;
@@ -531,7 +567,7 @@ __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_
     R dVA = -dw * sb + w * sbb;
     R b = bo_value(st);
     V3<R> gd, fi, fj;
-    bo_reverse<R, true, NB, false, SG>(S, typ, owner, st, VA, w, F, VIR ? e + 3 : nullptr, gd, fi, fj);
+    bo_reverse<R, true, NB, false, SG, NBJ>(S, typ, owner, st, VA, w, F, VIR ? e + 3 : nullptr, gd, fi, fj);
     R dEdr = dVR + b * dVA + dw * st.Tsum;
     addto(gd, (dEdr * ir) * d);
     atomic_add3<SG>(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
@@ -545,11 +581,13 @@ __global__ void __launch_bounds__(128, NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1) k_
     nang += st.nI + st.nJ;
     if (VIR && stage.rows) {
       double* row = stage_row(stage, 13);
-      if (row) {
-        char4 s = shift[J];
-        row[0] = gid[i], row[1] = gid[J], row[2] = s.x, row[3] = s.y, row[4] = s.z;
-        row[5] = b, row[6] = st.pij, row[7] = st.pji, row[8] = st.Rv, row[9] = st.Tv * st.D;
-        row[10] = st.Nij, row[11] = st.Nji, row[12] = st.Nconj;
+      if (row) {  // in the canonical orientation of the bond list
+        const int a = swapped ? J : i, c = swapped ? i : J;
+        char4 s = shift[c];
+        row[0] = gid[a], row[1] = gid[c], row[2] = s.x, row[3] = s.y, row[4] = s.z;
+        row[5] = b, row[6] = swapped ? st.pji : st.pij, row[7] = swapped ? st.pij : st.pji, row[8] = st.Rv;
+        row[9] = st.Tv * st.D;
+        row[10] = swapped ? st.Nji : st.Nij, row[11] = swapped ? st.Nij : st.Nji, row[12] = st.Nconj;
       }
     }
   }
@@ -673,6 +711,73 @@ __device__ __forceinline__ R lj_v(int p, R r2, double r2d, R& dVr_over_r) {
   return V;
 }
 
+// b* plateau test of the deferred batch (exact shortcut, forward only): p_ij and p_ji are formed
+// as in bo_forward, pi^rc and T are bounded by their tables (Tab::bR*, bT*) and the dihedral sum
+// by D <= (sum_k w_ik)(sum_l w_jl) (every term is (1 - cos^2 w) w_ik w_jl G G, G <= 1).  If the
+// whole interval lies below b_min (S_b = 1) or above b_max (S_b = 0) by a rounding margin, S_b is
+// on a plateau exactly as the full evaluation would find it, and dS_b/db* = 0 (P:488-494:
+// "the derivatives of the overall term are zero").  Returns 1 (S_b = 1), 2 (S_b = 0) or 0
+// (undecided / bad argument / side larger than NB: *ovf).
+template <typename R, int NB>
+__device__ __forceinline__ int bstar_plateau(const ShortList<R>& S, const signed char* typ, int i, int J, V3<R> d,
+                                             R r, bool& ovf) {
+  const Tab<R>& T = tab<R>();
+  const int ti = typ[i], tj = typ[J];
+  const size_t bi = (size_t)i * S.capS, bj = (size_t)J * S.capS;
+  const int ni = S.cnt[i], nj = S.cnt[J];
+  int pq = -1, pl = -1;
+  for (int q = 0; q < ni; ++q)
+    if (S.nbr[bi + q] == J) pq = q;
+  for (int q = 0; q < nj; ++q)
+    if (S.nbr[bj + q] == i) pl = q;
+  const int nI = ni - (pq >= 0), nJ = nj - (pl >= 0);
+  ovf = nI > NB || nJ > NB;
+  if (ovf) return 0;
+  const R ir = R(1) / r;
+  R arg[2], wsum[2];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const int c = side ? tj : ti, o = side ? ti : tj, a0 = side ? J : i, n = side ? nJ : nI, ps = side ? pl : pq;
+    const size_t b0 = side ? bj : bi;
+    const V3<R> dd = side ? mk3(-d.x, -d.y, -d.z) : d;
+    const bool blend = c == 0 && T.g2on;
+    R s1 = 0, s2 = 0, NC = 0, NH = 0;
+    for (int a = 0; a < n; ++a) {
+      const int q = side_slot(a, ps);
+      const int k = S.nbr[b0 + q];
+      R rk;
+      const V3<R> dk = sl_d(S, a0, q, rk);
+      const R wk = S.w[b0 + q].x;
+      const int tk = typ[k];
+      const R cs = clamp_cos(dot3(dd, dk) * ir / rk);
+      R dg;
+      const R ek = explam_r<R>(o, c, tk, r, rk);
+      s1 += wk * gspline<R>(c, cs, dg) * ek;
+      if (blend) s2 += wk * gspline<R>(2, cs, dg) * ek;
+      if (tk == 0) NC += wk;
+      else NH += wk;
+    }
+    if (blend) {
+      R dQ;
+      const R Q = sw<R>(NC + NH, T.gnlo, T.gnhi, dQ);
+      s1 = s2 + Q * (s1 - s2);
+    }
+    R px, py;
+    arg[side] = R(1) + s1 + (c == 0 ? pspline<R>(o, NC, NH, px, py) : R(0));
+    wsum[side] = NC + NH;
+  }
+  if (!(arg[0] > R(0)) || !(arg[1] > R(0))) return 0;  // the full path counts the bad argument
+  const int p = ti + tj;
+  const R base = R(0.5) * (rsq(arg[0]) + rsq(arg[1]));
+  const R Dm = wsum[0] * wsum[1];
+  const R hi = base + T.bRhi[p] + (T.bThi[p] > R(0) ? T.bThi[p] : R(0)) * Dm;
+  const R lo = base + T.bRlo[p] + (T.bTlo[p] < R(0) ? T.bTlo[p] : R(0)) * Dm;
+  const R margin = sizeof(R) == 8 ? R(1e-12) : R(1e-5);
+  if (hi < T.bmin[p] - margin) return 1;
+  if (lo > T.bmax[p] + margin) return 2;
+  return 0;
+}
+
 // window-candidate queue in three regions by species pair (region t: item[off[t] .. off[t] +
 // cap[t]), count[t] entries), sized from the build-time bound so it cannot overflow
 struct BstarQueue {
@@ -727,13 +832,29 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
     R bs = 0, B = 1, dB = 0;
     if (win) {
       V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
-      bo_forward<R, false, NB, !FULL || NB <= NB_FAST>(S, typ, i, J, ds, rho, st);
-      if (!FULL && st.overflow) {  // a side larger than NB_FAST: the NBMAX kernel
-        list_append(ovf2, novf2, 1 << 30, qi);
-        continue;
+      // forward-only batch: an exact plateau test first (stage recording needs the b* value)
+      int plat = 0;
+      if (!FULL && !(VIR && stage.rows)) {
+        bool ov = false;
+        plat = bstar_plateau<R, NB>(S, typ, i, J, ds, rho, ov);
+        if (ov) {  // a side larger than NB_FAST: the NBMAX kernel
+          list_append(ovf2, novf2, 1 << 30, qi);
+          continue;
+        }
       }
-      bs = bo_value(st);
-      B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
+      if (plat) {
+        B = plat == 1 ? R(1) : R(0);
+        bs = plat == 1 ? T.bmin[p] - R(1) : T.bmax[p] + R(1);  // outside (b_min, b_max): not counted
+        st.bad = false;
+      } else {
+        bo_forward<R, false, NB, !FULL || NB <= NB_FAST>(S, typ, i, J, ds, rho, st);
+        if (!FULL && st.overflow) {  // a side larger than NB_FAST: the NBMAX kernel
+          list_append(ovf2, novf2, 1 << 30, qi);
+          continue;
+        }
+        bs = bo_value(st);
+        B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
+      }
     } else {
       st.bad = false;
     }
