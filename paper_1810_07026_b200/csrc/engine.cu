@@ -70,7 +70,7 @@ struct DBuf {
 // at least one block: every kernel bounds-checks, and an empty domain must still launch cleanly
 inline int nblk(long long n, int t) { return (int)std::max<long long>(1, (n + t - 1) / t); }
 
-constexpr size_t SCRATCH_BYTES = 1024, SCRATCH_CT = 128, SCRATCH_SMALL = 512, SCRATCH_ZERO_BYTES = 512 + 64;
+constexpr size_t SCRATCH_BYTES = 1024, SCRATCH_CT = 128, SCRATCH_SMALL = 512, SCRATCH_ZERO_BYTES = 512 + 96;
 constexpr size_t SCRATCH_TICKET = 1016;
 #ifndef AB_INT_BLOCK
 #define AB_INT_BLOCK 128  // k_integrate1_img block (measured cfg2: 128 beats 256; 64 / 32 equal)
@@ -197,6 +197,7 @@ struct ab_engine {
   DBuf<int4> q_item;
   DBuf<int> ovf_bond, ovf_q, ovf_q2;  // overflow (large side / full b*) index lists
   DBuf<int> ovf_mid;                  // CH / HH bonds with two non-empty sides (general REBO kernel)
+  DBuf<int> ovf_und;                  // b* candidates the plateau batch hands to the forward-pass kernel
   DBuf<double> q_M;
   // one small device scratch block, zeroed with a single memset per evaluation:
   //   acc (ACC_N doubles) at 0, ct (CT_N + 1 u64; [CT_N] = max displacement^2) at 128,
@@ -1156,9 +1157,10 @@ ab_status enqueue_forces(ab_engine* e) {
   // REBO: general NB_FAST kernel on the CC region, one-empty-side kernel on CH / HH, general kernel
   // on the bonds the latter hands over, NBMAX kernel on the large-side overflow
   const int g_rebo_rows = 2 * g_rebo + 2 * g_slow;
-  const int nrows = g_short + g_rebo_rows + g_near + g_far + g_bstar + 2 * g_slow;  // b* full and NBMAX: g_slow
+  const int nrows = g_short + g_rebo_rows + g_near + g_far + 2 * g_bstar + 2 * g_slow;  // b*: lite, fast, full, NBMAX
   CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
   CK(e->ovf_mid.ensure((size_t)N * e->capS + 1));
+  CK(e->ovf_und.ensure(e->capQ));
   CK(e->ovf_q.ensure(e->capQ));
   CK(e->ovf_q2.ensure(e->capQ));
   CK(e->red_d.ensure((size_t)ACC_N * nrows));
@@ -1277,8 +1279,12 @@ ab_status enqueue_forces(ab_engine* e) {
     cudaEvent_t t = prof_start(e, st);
     // forward-only fast path; pairs needing the reverse pass / path forces -> ovf_q (NB_FAST
     // sides, count small_i[9]), pairs with a large side -> ovf_q2 (NBMAX, count small_i[1])
-    auto bstar = [&](auto fast, auto full, auto big) -> ab_status {
+    int* const nund = e->small_i.p + 16;  // plateau batch -> forward-pass kernel
+    auto bstar = [&](auto lite, auto fast, auto full, auto big) -> ab_status {
       if (e->skip & 8) return AB_OK;
+      lite<<<g_bstar, 128, 0, st>>>(Qu, e->ovf_und.p, nund, e->pos.p, S, e->typ.p, e->owner.p, Fk,
+                                    sb1.rows != nullptr, RR);
+      RR.row0 += g_bstar;
       // AB_PDL=1: the fast and full b* kernels are launched as programmatic dependents of the
       // kernel before them on the stream (their CTAs launch while it drains and wait in
       // griddepcontrol.wait); the NBMAX batch then forks after the full kernel
@@ -1290,7 +1296,7 @@ ab_status enqueue_forces(ab_engine* e) {
       cudaLaunchConfig_t lf = lc;  // the reverse-pass batch (usually empty): one wave of 2 CTAs / SM
       lf.gridDim = dim3(g_slow);
       lc.attrs = pdl, lc.numAttrs = e->pdl ? 1 : 0;
-      CK(cudaLaunchKernelEx(&lc, fast, Qu, (const int*)nullptr, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p,
+      CK(cudaLaunchKernelEx(&lc, fast, Qu, (const int*)e->ovf_und.p, (const int*)nund, e->ovf_q.p, e->small_i.p + 9, e->ovf_q2.p,
                             e->small_i.p + 1, (const double4*)e->pos.p, S, (const signed char*)e->typ.p,
                             (const int*)e->owner.p, (const int*)e->gid.p, (const char4*)e->shift.p, Fk, sb1, RR));
       // the two deferred batches are independent: the NBMAX one (few pairs, long threads) runs
@@ -1302,25 +1308,26 @@ ab_status enqueue_forces(ab_engine* e) {
           CK(cudaEventRecord(e->ev_fork[0], st));
           CK(cudaStreamWaitEvent(s_rebo, e->ev_fork[0], 0));
         }
-        big<<<g_slow, 128, 0, s_rebo>>>(Qu, e->ovf_q2.p, nullptr, e->small_i.p + 1, nullptr, nullptr, e->pos.p, S,
+        big<<<g_slow, 128, 0, s_rebo>>>(Qu, e->ovf_q2.p, e->small_i.p + 1, nullptr, nullptr, nullptr, nullptr, e->pos.p, S,
                                         e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk, sb1, Rb);
         return AB_OK;
       };
       if (!e->pdl) TRY(fork_big());
       RR.row0 += g_bstar;
-      CK(cudaLaunchKernelEx(&lf, full, Qu, (const int*)e->ovf_q.p, (int*)nullptr, e->small_i.p + 9, (int*)nullptr,
+      CK(cudaLaunchKernelEx(&lf, full, Qu, (const int*)e->ovf_q.p, (const int*)(e->small_i.p + 9), (int*)nullptr,
+                            (int*)nullptr, (int*)nullptr,
                             (int*)nullptr, (const double4*)e->pos.p, S, (const signed char*)e->typ.p,
                             (const int*)e->owner.p, (const int*)e->gid.p, (const char4*)e->shift.p, Fk, sb1, RR));
       if (e->pdl) TRY(fork_big());
       return AB_OK;
     };
     if (e->want_virial)
-      TRY(bstar(k_bstar<R, NB_FAST, false, true, SG>, k_bstar<R, NB_FAST, true, true, SG>,
+      TRY(bstar(k_bstar_lite<R, true, SG>, k_bstar<R, NB_FAST, false, true, SG>, k_bstar<R, NB_FAST, true, true, SG>,
                 k_bstar<R, NBMAX, true, true, SG>));
     else
-      TRY(bstar(k_bstar<R, NB_FAST, false, false, SG>, k_bstar<R, NB_FAST, true, false, SG>,
-                k_bstar<R, NBMAX, true, false, SG>));
-    e->launches += 2;  // + the CKL below: three launches
+      TRY(bstar(k_bstar_lite<R, false, SG>, k_bstar<R, NB_FAST, false, false, SG>,
+                k_bstar<R, NB_FAST, true, false, SG>, k_bstar<R, NBMAX, true, false, SG>));
+    e->launches += 3;  // + the CKL below: four launches
     CKL();
     CK(cudaEventRecord(e->ev_join[0], s_rebo));
     prof_stop(e, 3, st, t);
@@ -1654,7 +1661,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   if (ok) {  // views into the scratch block (not separately allocated)
     e->acc.p = reinterpret_cast<double*>(e->scratch.p), e->acc.n = ACC_N;
     e->ct.p = reinterpret_cast<unsigned long long*>(e->scratch.p + SCRATCH_CT), e->ct.n = CT_N + 1;
-    e->small_i.p = reinterpret_cast<int*>(e->scratch.p + SCRATCH_SMALL), e->small_i.n = 16;
+    e->small_i.p = reinterpret_cast<int*>(e->scratch.p + SCRATCH_SMALL), e->small_i.n = 24;
   }
   if (!ok) {
     e->err = std::string("CUDA init failed: ") + cudaGetErrorString(cudaGetLastError());
@@ -1707,7 +1714,7 @@ void free_engine(ab_engine* e) {
   for (auto* b : bd) b->release();
   DBuf<int>* bi[] = {&e->gid, &e->gid_tmp, &e->owner, &e->key, &e->val, &e->val2, &e->cell_start,
                      &e->gcnt, &e->goff, &e->ljc[0], &e->ljc[1], &e->ljc[2], &e->ljn[0], &e->ljn[1],
-                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_mid, &e->ovf_q, &e->ovf_q2,
+                     &e->ljn[2], &e->in_cnt, &e->in_nbr, &e->s_cnt, &e->s_nbr, &e->ovf_bond, &e->ovf_mid, &e->ovf_und, &e->ovf_q, &e->ovf_q2,
                      &e->sendl[0], &e->sendl[1], &e->fl[0], &e->fl[1], &e->fl[2], &e->idx[0], &e->idx[1],
                      &e->idx[2], &e->cnt_d, &e->cl_k, &e->cl_v, &e->cl_v2, &e->run_start, &e->sc_bsum, &e->sc_cur, &e->sc_off, &e->run_cl,
                      &e->cl_atom, &e->clc, &e->cln};

@@ -795,7 +795,7 @@ struct BstarQueue {
 // FULL = true with NB_FAST register sides, a pair with a side larger than NB_FAST to ovf2 for
 // FULL = true with NB = NBMAX.
 template <typename R, int NB, bool FULL, bool VIR, bool SG = false>
-__global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBLOCKS : 1) k_bstar(BstarQueue Qu, const int* list_idx, int* ovf, int* novf, int* ovf2,
+__global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBLOCKS : 1) k_bstar(BstarQueue Qu, const int* list_idx, const int* nlist, int* ovf, int* novf, int* ovf2,
                                                int* novf2, const double4* pos, ShortList<R> S, const signed char* typ,
                                                const int* owner, const int* gid, const char4* shift, double* F,
                                                StageBuf stage, RedRows RR) {
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
   // the kernel was launched normally)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int q0 = min(Qu.count[0], Qu.cap[0]), q1 = min(Qu.count[1], Qu.cap[1]), q2 = min(Qu.count[2], Qu.cap[2]);
-  const int nq = FULL ? *novf : q0 + q1 + q2;
+  const int nq = list_idx ? *nlist : q0 + q1 + q2;
   if (red_idle_block(nq, RR)) return;
   red_init(rs);
   const Tab<R>& T = tab<R>();
@@ -812,8 +812,8 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
   unsigned long long ntr = 0, nb = 0, nbad = 0;
   int stride = gridDim.x * blockDim.x;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += stride) {
-    int qi = FULL ? list_idx[t]
-                  : (t < q0 ? Qu.off[0] + t : (t < q0 + q1 ? Qu.off[1] + (t - q0) : Qu.off[2] + (t - q0 - q1)));
+    int qi = list_idx ? list_idx[t]
+                      : (t < q0 ? Qu.off[0] + t : (t < q0 + q1 ? Qu.off[1] + (t - q0) : Qu.off[2] + (t - q0 - q1)));
     int4 it = Qu.item[qi];
     int i = it.x, J = it.y;
     double Md = Qu.M[qi];
@@ -832,29 +832,13 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
     R bs = 0, B = 1, dB = 0;
     if (win) {
       V3<R> ds = (rho * ir) * d;  // fictitious d* = rho d_hat (reading A8)
-      // forward-only batch: an exact plateau test first (stage recording needs the b* value)
-      int plat = 0;
-      if (!FULL && !(VIR && stage.rows)) {
-        bool ov = false;
-        plat = bstar_plateau<R, NB>(S, typ, i, J, ds, rho, ov);
-        if (ov) {  // a side larger than NB_FAST: the NBMAX kernel
-          list_append(ovf2, novf2, 1 << 30, qi);
-          continue;
-        }
+      bo_forward<R, false, NB, !FULL || NB <= NB_FAST>(S, typ, i, J, ds, rho, st);
+      if (!FULL && st.overflow) {  // a side larger than NB_FAST: the NBMAX kernel
+        list_append(ovf2, novf2, 1 << 30, qi);
+        continue;
       }
-      if (plat) {
-        B = plat == 1 ? R(1) : R(0);
-        bs = plat == 1 ? T.bmin[p] - R(1) : T.bmax[p] + R(1);  // outside (b_min, b_max): not counted
-        st.bad = false;
-      } else {
-        bo_forward<R, false, NB, !FULL || NB <= NB_FAST>(S, typ, i, J, ds, rho, st);
-        if (!FULL && st.overflow) {  // a side larger than NB_FAST: the NBMAX kernel
-          list_append(ovf2, novf2, 1 << 30, qi);
-          continue;
-        }
-        bs = bo_value(st);
-        B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
-      }
+      bs = bo_value(st);
+      B = sw<R>(bs, T.bmin[p], T.bmax[p], dB);
     } else {
       st.bad = false;
     }
@@ -906,6 +890,75 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && !FULL) ? AB_BSTAR_MINBL
   red_add_u(rs, CT_SBTRANS, ntr);
   red_add_u(rs, CT_BSTAR, nb);
   red_add_u(rs, CT_BADARG, nbad);
+  red_flush(rs, RR);
+}
+
+// ---------------------------------------------------------------- b* plateau batch (first pass)
+// Every queued window candidate with C = 1 (M = 0) whose S_b is decided exactly by
+// bstar_plateau (or that lies outside the S_r window): E = (S_r S_b + 1 - S_r) V with S_b in
+// {0, 1} and dS_b = 0, forces from S_r and V only.  Everything else -- fractional C, an
+// undecided b*, a bad p argument, a side larger than NB_FAST, and every pair while stage rows are
+// recorded -- is appended to und for the forward-pass kernel (k_bstar list mode).  Light on
+// registers: the full bond-order code is not in this kernel.
+#ifndef AB_BSTAR_LITE_MINBLOCKS
+#define AB_BSTAR_LITE_MINBLOCKS 6
+#endif
+template <typename R, bool VIR, bool SG = false>
+__global__ void __launch_bounds__(128, AB_BSTAR_LITE_MINBLOCKS) k_bstar_lite(BstarQueue Qu, int* und, int* nund,
+                                                                             const double4* pos, ShortList<R> S,
+                                                                             const signed char* typ, const int* owner,
+                                                                             double* F, bool record, RedRows RR) {
+  __shared__ RedSmem rs;
+  const int q0 = min(Qu.count[0], Qu.cap[0]), q1 = min(Qu.count[1], Qu.cap[1]), q2 = min(Qu.count[2], Qu.cap[2]);
+  const int nq = q0 + q1 + q2;
+  if (red_idle_block(nq, RR)) return;
+  red_init(rs);
+  const Tab<R>& T = tab<R>();
+  double e[1 + 6] = {0, 0, 0, 0, 0, 0, 0};
+  unsigned long long nb = 0;
+  const int stride = gridDim.x * blockDim.x;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nq; t += stride) {
+    const int qi = t < q0 ? Qu.off[0] + t : (t < q0 + q1 ? Qu.off[1] + (t - q0) : Qu.off[2] + (t - q0 - q1));
+    const int4 it = Qu.item[qi];
+    const int i = it.x, J = it.y;
+    if (record || Qu.M[qi] > 0.0) {
+      list_append(und, nund, 1 << 30, qi);
+      continue;
+    }
+    const double4 pi = pos[i], pj = pos[J];
+    const double dxd = __dsub_rn(pj.x, pi.x), dyd = __dsub_rn(pj.y, pi.y), dzd = __dsub_rn(pj.z, pi.z);
+    const double r2d = r2_exact(dxd, dyd, dzd);
+    const double rd = sqrt(r2d);
+    const int p = typ[i] + typ[J];
+    const bool win = (rd - c_tabd.sigma[p]) / (c_tabd.srhi[p] - c_tabd.sigma[p]) < 1.0;  // as k_bstar
+    const V3<R> d = mk3<R>((R)dxd, (R)dyd, (R)dzd);
+    const R r = (R)rd, ir = R(1) / r;
+    R B = 1;
+    if (win) {
+      const R rho = T.rho[p];
+      bool ov = false;
+      const int plat = bstar_plateau<R, NB_FAST>(S, typ, i, J, (rho * ir) * d, rho, ov);
+      if (ov || plat == 0) {
+        list_append(und, nund, 1 << 30, qi);
+        continue;
+      }
+      B = plat == 1 ? R(1) : R(0);
+    }
+    R dP = 0;
+    const R P = win ? sw<R>(r, T.sigma[p], T.srhi[p], dP) : R(0);
+    R dVr;
+    const R V = lj_v<R>(p, (R)r2d, r2d, dVr);
+    const R Q = P * B + R(1) - P;  // C = 1
+    const V3<R> gd = (Q * dVr + V * (B - R(1)) * dP * ir) * d;
+    atomic_add3<SG>(F, owner[i], (double)gd.x, (double)gd.y, (double)gd.z);
+    atomic_add3<SG>(F, owner[J], -(double)gd.x, -(double)gd.y, -(double)gd.z);
+    vir_add(VIR ? e + 1 : nullptr, d, gd);
+    e[0] = acc_round<SG>(e[0] + (double)(Q * V));
+    nb += win;
+  }
+  red_add_d(rs, ACC_ELJ, e[0]);
+  for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, e[1 + c]);
+  red_add_u(rs, CT_BSTAR, nb);
   red_flush(rs, RR);
 }
 
