@@ -1225,10 +1225,12 @@ ab_status enqueue_forces(ab_engine* e) {
     R1.row0 = g_short;
     int* const nbig = e->small_i.p + 8;  // large-side overflow (NBMAX kernel)
     int* const nmid = e->small_i.p + 0;  // CH / HH bonds with two non-empty sides
-    auto rebo = [&](auto fast, auto one, auto slow) {
+    auto rebo = [&](auto three, auto fast, auto one, auto slow) {
       if (e->skip & 1) return;
-      fast<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, nullptr, 0, 1, e->ovf_bond.p, nbig, S, e->typ.p, e->owner.p,
-                                       e->gid.p, e->shift.p, Fk, sb0, R1);
+      // CC region: sides of <= 3 neighbours (sp3 carbon) in the NB = 3 kernel, larger ones go on
+      // to the general NB_FAST kernel through the same hand-over list as the CH / HH bonds
+      three<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, nullptr, 0, 1, e->ovf_mid.p, nmid, S, e->typ.p, e->owner.p,
+                                        e->gid.p, e->shift.p, Fk, sb0, R1);
       R1.row0 += g_rebo;
       one<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, nullptr, 1, 3, e->ovf_mid.p, nmid, S, e->typ.p, e->owner.p,
                                       e->gid.p, e->shift.p, Fk, sb0, R1);
@@ -1240,9 +1242,11 @@ ab_status enqueue_forces(ab_engine* e) {
                                        e->gid.p, e->shift.p, Fk, sb0, R1);
     };
     if (e->want_virial)
-      rebo(k_rebo<R, NB_FAST, true, SG>, k_rebo<R, NB_FAST, true, SG, 0>, k_rebo<R, NBMAX, true, SG>);
+      rebo(k_rebo<R, 3, true, SG>, k_rebo<R, NB_FAST, true, SG>, k_rebo<R, NB_FAST, true, SG, 0>,
+           k_rebo<R, NBMAX, true, SG>);
     else
-      rebo(k_rebo<R, NB_FAST, false, SG>, k_rebo<R, NB_FAST, false, SG, 0>, k_rebo<R, NBMAX, false, SG>);
+      rebo(k_rebo<R, 3, false, SG>, k_rebo<R, NB_FAST, false, SG>, k_rebo<R, NB_FAST, false, SG, 0>,
+           k_rebo<R, NBMAX, false, SG>);
     e->launches += 3;  // + the CKL below: four launches
     CKL();
     prof_stop(e, 1, s_rebo, t);

@@ -485,6 +485,12 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 #ifndef AB_REBO_MINBLOCKS
 #define AB_REBO_MINBLOCKS 1
 #endif
+#ifndef AB_REBO_UNROLL  // which REBO instantiations unroll their side loops (registers vs i-cache)
+#define AB_REBO_UNROLL(nb) ((nb) <= 3)
+#endif
+#ifndef AB_REBO3_MINBLOCKS
+#define AB_REBO3_MINBLOCKS 2  // the sp3 C-C batch (sides of <= 3)
+#endif
 #ifndef AB_REBO1_MINBLOCKS
 #define AB_REBO1_MINBLOCKS 3  // the one-empty-side batch (no J-side arrays, no dihedral loop)
 #endif
@@ -498,8 +504,8 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 // evaluated with its ends swapped (b_ij, the pair terms and the forces are symmetric in i, j);
 // a bond with two non-empty sides goes to ovf for the general NB_FAST kernel.
 template <typename R, int NB, bool VIR, bool SG = false, int NBJ = NB>
-__global__ void __launch_bounds__(128, (NB <= NB_FAST && NBJ > 0) ? AB_REBO_MINBLOCKS
-                                                                   : (NBJ == 0 ? AB_REBO1_MINBLOCKS : 1))
+__global__ void __launch_bounds__(128, NBJ == 0 ? AB_REBO1_MINBLOCKS
+                                                  : (NB == 3 ? AB_REBO3_MINBLOCKS : (NB <= NB_FAST ? AB_REBO_MINBLOCKS : 1)))
     k_rebo(BondList BL, const int* list_idx, const int* nlist, int reg0, int reg1, int* ovf, int* novf,
            ShortList<R> S, const signed char* typ, const int* owner, const int* gid, const char4* shift, double* F,
            StageBuf stage, RedRows RR) {
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && NBJ > 0) ? AB_REBO_MINB
       }
     }
     BoState<R, NB, NBJ> st;
-    bo_forward<R, true, NB, false, NBJ>(S, typ, i, J, d, r, st);
+    bo_forward<R, true, NB, AB_REBO_UNROLL(NB), NBJ>(S, typ, i, J, d, r, st);
     if (st.overflow) {  // only possible for NB = NB_FAST
       list_append(ovf, novf, 1 << 30, bidx);
       continue;
@@ -567,7 +573,8 @@ __global__ void __launch_bounds__(128, (NB <= NB_FAST && NBJ > 0) ? AB_REBO_MINB
     R dVA = -dw * sb + w * sbb;
     R b = bo_value(st);
     V3<R> gd, fi, fj;
-    bo_reverse<R, true, NB, false, SG, NBJ>(S, typ, owner, st, VA, w, F, VIR ? e + 3 : nullptr, gd, fi, fj);
+    bo_reverse<R, true, NB, AB_REBO_UNROLL(NB), SG, NBJ>(S, typ, owner, st, VA, w, F, VIR ? e + 3 : nullptr, gd, fi,
+                                                          fj);
     R dEdr = dVR + b * dVA + dw * st.Tsum;
     addto(gd, (dEdr * ir) * d);
     atomic_add3<SG>(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
