@@ -173,6 +173,12 @@ struct ab_engine {
   RedRows post_rr{};
   int post_rows = 0;
   int qcap[3] = {0, 0, 0}, qoff[3] = {0, 0, 0};  // b* candidate queue regions (build-time bounds)
+  // slab domains, halo / interior overlap: the cell-sorted locals [far_i0, far_i1)
+  // whose LJ stencil lies inside the slab (no x-ghost partner until the next rebuild), the
+  // images of locals [NX, NX + G_loc) (the rest are images of x-ghosts); far_early: this step's
+  // far-LJ kernel for the interior atoms was launched beside the halo exchange
+  int far_i0 = 0, far_i1 = 0, G_loc = 0;
+  bool far_early = false;
   long long launches = 0, rebuilds = 0, steps = 0, retries = 0;
   // device state
   DBuf<double4> pos, pos_tmp, xref;
@@ -676,6 +682,22 @@ ab_status sort_locals(ab_engine* e) {
   k_wrap_and_key<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->grid, e->key.p, e->val.p);
   CKL();
   TRY(key_sort(e, N, e->key.p, e->ncell, nullptr, e->val2.p, e->cell_start.p));  // stable by (cell, index)
+  e->far_i0 = e->far_i1 = 0;
+  if (slabbed(e) && N) {  // interior x-columns: cells whose +-nrLJ x-stencil lies inside [xlo, xhi)
+    const Grid& g = e->grid;
+    int c0 = 0, c1 = g.nc[0] - 1;
+    while (c0 < g.nc[0] && g.lo[0] + c0 * g.cs[0] < e->xlo) ++c0;
+    while (c1 >= 0 && g.lo[0] + (c1 + 1) * g.cs[0] > e->xhi) --c1;
+    const int a = c0 + e->nrLJ, b = c1 - e->nrLJ;  // cell x-range of the interior atoms
+    if (a <= b) {
+      const int plane = g.nc[1] * g.nc[2];  // keys are x-major: an x-range is a contiguous range
+      int ab[2];
+      CK(cudaMemcpyAsync(&ab[0], e->cell_start.p + (size_t)a * plane, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&ab[1], e->cell_start.p + (size_t)(b + 1) * plane, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      e->far_i0 = ab[0], e->far_i1 = ab[1];
+    }
+  }
   k_permute<<<nblk(N, 256), 256, 0, st>>>(N, e->val2.p, e->pos.p, e->pos_tmp.p, e->vel.p, e->vel_tmp.p, e->gid.p,
                                           e->gid_tmp.p);
   CKL();
@@ -748,6 +770,11 @@ ab_status images_and_lists(ab_engine* e) {
   k_image_count<<<nblk(NB, 256), 256, 0, st>>>(NB, e->pos.p, smax, lo, hi, e->gcnt.p);
   CKL();
   TRY(scan_ex<false>(e, e->gcnt.p, NB, e->goff.p));
+  e->G_loc = 0;
+  if (slabbed(e) && N < NB) {  // images of the locals come first (k_image_fill order)
+    CK(cudaMemcpyAsync(&e->G_loc, e->goff.p + N, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
   int tail[2] = {0, 0};
   if (NB) {
     CK(cudaMemcpyAsync(&tail[0], e->goff.p + NB - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -762,6 +789,7 @@ ab_status images_and_lists(ab_engine* e) {
   tq = std::chrono::steady_clock::now();
   e->NT = NB + tail[0] + tail[1];
   e->G = e->NT - N;
+  if (!(N < NB)) e->G_loc = e->NT - NB;
   const int NT = e->NT;
   TRY(grow_keep(e, e->pos, NT, NB));
   TRY(grow_keep(e, e->gid, NT, NB));
@@ -1088,9 +1116,81 @@ void graph_drop(ab_engine* e) {
   e->graph_epoch = -1;
 }
 
-// ghosts follow the owned atoms (every step without a rebuild)
-ab_status refresh_ghosts_all(ab_engine* e) {
+// grid sizes of one force evaluation and the partial-row layout of its reduction:
+// short | REBO (CC sp3, one-empty-side, hand-over, NBMAX) | near LJ | far LJ | b* (lite, fast,
+// NBMAX, full) | [far LJ of the slab interior, launched beside the halo exchange]
+struct Grids {
+  int g_short, g_rebo, g_near, g_far, g_bstar, g_slow, base;
+};
+Grids grids_of(const ab_engine* e) {
+  Grids G;
+  const int N = e->N;
+  const bool clp = e->cl_path && e->hp.potential != kREBO;
+  G.g_short = nblk(e->NT, 128), G.g_rebo = e->nsm * 4;
+  G.g_near = clp ? std::min(nblk((long long)N * 32, 128), e->nsm * AB_LJC_MINBLOCKS) : nblk(N, NEAR_ATOMS);
+  G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * 8);
+  G.g_bstar = e->nsm * 4, G.g_slow = e->nsm * 2;
+  G.base = G.g_short + 2 * G.g_rebo + 2 * G.g_slow + G.g_near + G.g_far + 2 * G.g_bstar + 2 * G.g_slow;
+  return G;
+}
+
+// Slab domain, NVE step: the far-LJ pairs of the interior atoms [far_i0, far_i1) need no x-ghost
+// (their stencil lies inside the slab) -- launched on aux stream 1 as soon as the images of the
+// locals are current, so they run while the halo positions travel (SURVEY §8(e) "overlap
+// interior compute with the exchange").  F is zeroed here; enqueue_forces takes the remaining
+// atoms.  Off for stage recording, the fp32-accumulation modes, the cluster path and serial runs.
+template <typename R>
+ab_status launch_far_early_t(ab_engine* e) {
+  ab_engine* const d = e;  // (CK reports into e->err)
+  const Grids G = grids_of(d);
+  const int nrows = G.base + G.g_far;
+  CK(d->red_d.ensure((size_t)ACC_N * nrows));
+  CK(d->red_u.ensure((size_t)CT_N * nrows));
+  if (!d->f_zeroed) CK(cudaMemsetAsync(d->F.p, 0, sizeof(double) * 3 * d->NX, d->st));
+  d->f_zeroed = true;  // enqueue_forces must not zero F again
+  CK(cudaEventRecord(d->ev_fork[1], d->st));
+  CK(cudaStreamWaitEvent(d->aux[1], d->ev_fork[1], 0));
+  LJArgs A;
+  A.N = d->N, A.pos = d->pos.p;
+  A.r0b = d->far_i0, A.r0e = d->far_i1, A.r1b = A.r1e = 0;
+  for (int c = 0; c < 3; ++c) A.cap[c] = d->capL[c], A.cnt[c] = d->ljc[c].p, A.nbr[c] = d->ljn[c].p;
+  RedRows RR{d->red_d.p, d->red_u.p, nrows, G.base};
+  StageBuf sb{nullptr, nullptr, 0};
+  auto far = [&](auto kern) {
+    kern<<<G.g_far, 128, 0, d->aux[1]>>>(A, d->gid.p, d->shift.p, d->F.p, d->acc.p, d->ct.p, sb, RR);
+  };
+  const bool morse = d->hp.potential == kAIREBOM;
+  if (d->want_virial) morse ? far(k_lj_far<R, true, true>) : far(k_lj_far<R, true, false>);
+  else morse ? far(k_lj_far<R, false, true>) : far(k_lj_far<R, false, false>);
+  ++d->launches;
+  CK(cudaGetLastError());
+  d->far_early = true;
+  return AB_OK;
+}
+ab_status launch_far_early(ab_engine* d) {
+  d->far_early = false;
+  const bool ok = d->hp.potential != kREBO && !d->cl_path && !d->record && !d->serial && !(d->skip & 2) &&
+                  (d->prec == AB_FP64 || d->prec == AB_MIXED) && d->far_i1 > d->far_i0;
+  if (!ok) return AB_OK;
+  return d->prec == AB_FP64 ? launch_far_early_t<double>(d) : launch_far_early_t<float>(d);
+}
+
+// ghosts follow the owned atoms (every step without a rebuild); early: NVE step of slab domains,
+// the interior far-LJ pairs start beside the halo exchange (launch_far_early)
+ab_status refresh_ghosts_all(ab_engine* e, bool early = false) {
   auto D = doms(e);
+  early = early && slabbed(e) && std::getenv("AB_NO_OVERLAP") == nullptr;
+  if (early) {
+    for (ab_engine* d : D) {
+      if (d->G_loc > 0 && !d->ghosts_fresh) {  // images of the locals first: they need no halo
+        k_image_update<<<nblk(d->G_loc, 256), 256, 0, d->st>>>(d->NX, d->NX + d->G_loc, d->pos.p, d->owner.p,
+                                                                d->rshift.p);
+        ++d->launches;
+        CK(cudaGetLastError());
+      }
+      TRYD(d, launch_far_early(d));
+    }
+  }
   if (slabbed(e)) {
     for (ab_engine* d : D) TRYD(d, halo_pack(d));
     TRY(xfer(e));
@@ -1100,7 +1200,9 @@ ab_status refresh_ghosts_all(ab_engine* e) {
     if (d->ghosts_fresh) {
       d->ghosts_fresh = false;
     } else if (d->NT > d->NX) {
-      k_image_update<<<nblk(d->NT - d->NX, 256), 256, 0, d->st>>>(d->NX, d->NT, d->pos.p, d->owner.p, d->rshift.p);
+      const int first = d->NX + (early ? d->G_loc : 0);  // (early: the locals' images are done)
+      if (d->NT > first)
+        k_image_update<<<nblk(d->NT - first, 256), 256, 0, d->st>>>(first, d->NT, d->pos.p, d->owner.p, d->rshift.p);
       ++d->launches;
       cudaError_t ce = cudaGetLastError();
       if (ce != cudaSuccess) {
@@ -1150,14 +1252,13 @@ ab_status enqueue_forces(ab_engine* e) {
   else CK(cudaMemsetAsync(e->scratch.p, 0, SCRATCH_ZERO_BYTES, st));  // acc, counters, small ints
   ShortList<R> S = short_view<R>(e);
   // grids and the per-block partial rows of the energy / virial / counter reduction
-  const int g_short = nblk(NT, 128), g_rebo = e->nsm * 4;
-  const int g_near = clp ? std::min(nblk((long long)N * 32, 128), e->nsm * AB_LJC_MINBLOCKS) : nblk(N, NEAR_ATOMS);
-  const int g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * 8), g_bstar = e->nsm * 4;
-  const int g_slow = e->nsm * 2;
+  const Grids GR = grids_of(e);
+  const int g_short = GR.g_short, g_rebo = GR.g_rebo, g_near = GR.g_near, g_far = GR.g_far, g_bstar = GR.g_bstar;
+  const int g_slow = GR.g_slow;
   // REBO: general NB_FAST kernel on the CC region, one-empty-side kernel on CH / HH, general kernel
   // on the bonds the latter hands over, NBMAX kernel on the large-side overflow
   const int g_rebo_rows = 2 * g_rebo + 2 * g_slow;
-  const int nrows = g_short + g_rebo_rows + g_near + g_far + 2 * g_bstar + 2 * g_slow;  // b*: lite, fast, full, NBMAX
+  const int nrows = GR.base + (e->far_early ? g_far : 0);  // (+ the early interior far-LJ rows)
   CK(e->ovf_bond.ensure((size_t)N * e->capS + 1));
   CK(e->ovf_mid.ensure((size_t)N * e->capS + 1));
   CK(e->ovf_und.ensure(e->capQ));
@@ -1183,6 +1284,9 @@ ab_status enqueue_forces(ab_engine* e) {
   LJArgs A;
   A.N = N;
   A.pos = e->pos.p;
+  if (e->far_early) A.r0b = 0, A.r0e = e->far_i0, A.r1b = e->far_i1, A.r1e = N;  // the rest of the atoms
+  else A.r0b = 0, A.r0e = N, A.r1b = A.r1e = 0;
+  e->far_early = false;
   for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
   // the far kernel forks from the engine stream at e->far_at: 0 = at once, 1 = after the short
   // list, 2 = after the near kernel (it then fills the GPU beside the b* batch)
@@ -2185,7 +2289,7 @@ static ab_status step_forces(ab_engine* e) {
                          std::getenv("AB_GRAPH")[0] == '1';
   if (!graphable) {
     graph_drop(e);
-    TRY(refresh_ghosts_all(e));
+    TRY(refresh_ghosts_all(e, true));
     return forces_all(e, false);
   }
   if (!e->gexec || e->graph_epoch != e->layout) {

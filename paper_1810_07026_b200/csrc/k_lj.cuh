@@ -121,6 +121,7 @@ __device__ __forceinline__ R morse_plain(R em, R a, R re, R r, R ir, R& dVr) {
 
 struct LJArgs {
   int N;
+  int r0b, r0e, r1b, r1e;  // k_lj_far: the atoms [r0b, r0e) and [r1b, r1e) (slab interior / boundary split)
   const double4* pos;
   int cap[3];
   const int* cnt[3];
@@ -542,7 +543,9 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
   unsigned nlj = 0, ntp = 0;
   unsigned long long ne = 0;
   // grid-stride over atoms: a resident grid, one warp per atom at a time
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < A.N; i += nwarps) {
+  const int n0 = A.r0e - A.r0b, nall = n0 + (A.r1e - A.r1b);
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nall; t += nwarps) {
+    const int i = t < n0 ? A.r0b + t : A.r1b + (t - n0);
     const double4 pi = A.pos[i];
     const int ti = type_of(pi);
     const long long ki = key_of(pi);

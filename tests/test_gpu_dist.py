@@ -160,3 +160,32 @@ def test_empty_slab_domain(eng_mod):
     e.run_nve(5, 0.25)
     x = e.get_positions()
     assert np.abs(e.compute()["F"] - O.compute(s.types, x, s.box)["F"]).max() <= 1e-9
+
+
+@pytest.mark.parametrize("precision", ["fp64", "mixed"])
+def test_virtual_nve_halo_overlap(eng_mod, monkeypatch, precision):
+    """Slab NVE steps launch the far-LJ pairs of the interior atoms (LJ stencil inside the slab)
+    beside the halo exchange; the boundary atoms follow the exchange.  The
+    trajectory equals the non-overlapped one (AB_NO_OVERLAP=1) and the whole-box one to summation
+    roundoff, and the overlapped schedule really ran (two more launches per step: the locals'
+    image refresh and the interior far-LJ kernel)."""
+    s = I.config(2)  # L_x = 89 A: 2 slabs of 44.5 A with an interior
+    runs = {}
+    for tag in ("overlap", "plain", "whole"):
+        if tag == "plain":
+            monkeypatch.setenv("AB_NO_OVERLAP", "1")
+        else:
+            monkeypatch.delenv("AB_NO_OVERLAP", raising=False)
+        e = eng_mod.make(s, precision, ranks=None if tag == "whole" else ("virtual", 2))
+        l0 = e.device_info()["kernel_launches"]
+        th = e.run_nve(12, s.dt, every=6)
+        runs[tag] = (e.get_positions(), e.get_velocities(), th, e.device_info()["kernel_launches"] - l0)
+    xo, vo, tho, lo = runs["overlap"]
+    xp, vp, thp, lp = runs["plain"]
+    xw, vw, thw, lw = runs["whole"]
+    assert lo >= lp + 2 * 12 - 4, (lo, lp)  # (a rebuild step takes the plain path)
+    tol = 1e-10 if precision == "fp64" else 1e-8
+    assert np.abs(xo - xp).max() <= tol and np.abs(vo - vp).max() <= tol
+    # whole box vs slabs: fp32 terms in mixed mode make the evaluations differ beyond fp64 roundoff
+    assert np.abs(xo - xw).max() <= (tol if precision == "fp64" else 1e-6)
+    assert np.allclose(tho[:, 1:], thw[:, 1:], rtol=1e-10 if precision == "fp64" else 1e-6)
