@@ -60,7 +60,9 @@ typedef enum {
 typedef enum {
   AB_LIST_SHORT = 0, /* full REBO short list: r <= r_max(t_i,t_j), both directions */
   AB_LIST_BONDS = 1, /* REBO half bonds: short-list entries with i < j (image tie-break s >_lex 0) */
-  AB_LIST_LJ = 2     /* LJ half pairs with r <= r_c(t_i,t_j) (half convention P:275-278) */
+  AB_LIST_LJ = 2,    /* LJ half pairs with r <= r_c(t_i,t_j) (half convention P:275-278) */
+  AB_LIST_LJ_SKIN = 3 /* the skinned LJ half list of the last rebuild: half pairs with
+                         r <= r_c + skin at the build positions (rows of the current instances) */
 } ab_list;
 
 /* Integer counters of the last force evaluation (must equal the oracle's exactly in fp64) and

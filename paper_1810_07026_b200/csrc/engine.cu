@@ -2570,6 +2570,8 @@ static ab_status list_visit(ab_engine* e, ab_engine* d, ab_list which, Visit&& v
     double rc = d->hp.pr[type_h(i) + type_h(J)].rc;
     return r2 <= rc * rc;
   };
+  const bool skinned = which == AB_LIST_LJ_SKIN;
+  if (skinned) which = AB_LIST_LJ;  // the same rows without the r <= r_c filter
   if (which == AB_LIST_LJ && d->cl_path) {  // cluster lists: expand the slots of every listed cluster
     if (d->hp.potential == kREBO) return AB_OK;
     std::vector<int> cnt(N), nbr((size_t)N * d->capC), cla((size_t)CL_SIZE * d->NCL);
@@ -2584,7 +2586,7 @@ static ab_status list_visit(ab_engine* e, ab_engine* d, ab_list which, Visit&& v
         const int c = nbr[(size_t)i * d->capC + q];
         for (int s = 0; s < CL_SIZE; ++s) {
           const int J = cla[(size_t)CL_SIZE * c + s];
-          if (J < 0 || J == i || !canon_of(i, J) || !in_rc(i, J)) continue;
+          if (J < 0 || J == i || !canon_of(i, J) || (!skinned && !in_rc(i, J))) continue;
           visit(gid[i], gid[J], sh[J].x, sh[J].y, sh[J].z);
         }
       }
@@ -2614,7 +2616,7 @@ static ab_status list_visit(ab_engine* e, ab_engine* d, ab_list which, Visit&& v
         bool canon = gid[i] != gid[J] ? gid[i] < gid[J]
                                       : (s.x > 0 || (s.x == 0 && (s.y > 0 || (s.y == 0 && s.z > 0))));
         if (which != AB_LIST_SHORT && !canon) continue;
-        if (which == AB_LIST_LJ) {  // exact (un-fused) r^2 <= r_c^2 as on the device
+        if (which == AB_LIST_LJ && !skinned) {  // exact (un-fused) r^2 <= r_c^2 as on the device
           volatile double dx = pos[J].x - pos[i].x, dy = pos[J].y - pos[i].y, dz = pos[J].z - pos[i].z;
           volatile double a = dx * dx, b = dy * dy, cc = dz * dz;
           volatile double ab = a + b;
@@ -2642,7 +2644,7 @@ static inline uint64_t dig_mix(uint64_t z) {
 ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows) {
   TRY(need_atoms(e));
   if (bad_ptr(e, count, "count")) return AB_E_ARG;
-  if (which != AB_LIST_SHORT && which != AB_LIST_BONDS && which != AB_LIST_LJ) {
+  if (which != AB_LIST_SHORT && which != AB_LIST_BONDS && which != AB_LIST_LJ && which != AB_LIST_LJ_SKIN) {
     e->err = "unknown list";
     return AB_E_ARG;
   }
@@ -2663,7 +2665,7 @@ ab_status ab_get_list(ab_engine* e, ab_list which, int64_t* count, int64_t* rows
 ab_status ab_get_list_digest(ab_engine* e, ab_list which, uint64_t digest[3]) {
   TRY(need_atoms(e));
   if (bad_ptr(e, digest, "digest")) return AB_E_ARG;
-  if (which != AB_LIST_SHORT && which != AB_LIST_BONDS && which != AB_LIST_LJ) {
+  if (which != AB_LIST_SHORT && which != AB_LIST_BONDS && which != AB_LIST_LJ && which != AB_LIST_LJ_SKIN) {
     e->err = "unknown list";
     return AB_E_ARG;
   }

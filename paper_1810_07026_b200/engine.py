@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get("AIREBO_B200_LIB", os.path.join(HERE, "libairebo_b200.
 PARAMS = os.path.join(os.path.dirname(HERE), "params", "toy_ch.param")
 
 AB_FP64, AB_MIXED, AB_SINGLE, AB_REDUCED = 0, 1, 2, 3
-AB_LIST_SHORT, AB_LIST_BONDS, AB_LIST_LJ = 0, 1, 2
+AB_LIST_SHORT, AB_LIST_BONDS, AB_LIST_LJ, AB_LIST_LJ_SKIN = 0, 1, 2, 3
 STATUS = {0: "AB_OK", -1: "AB_E_ARG", -2: "AB_E_PARAM", -3: "AB_E_BOX", -4: "AB_E_STATE", -5: "AB_E_OOM",
           -6: "AB_E_CUDA", -7: "AB_E_NCCL", -8: "AB_E_NONFINITE"}
 

@@ -396,3 +396,22 @@ def test_reach_table_overflow_fallback(eng_mod, precision):
     else:
         rel = np.sqrt(((g["F"] - o["F"]) ** 2).sum()) / np.sqrt((o["F"] ** 2).sum())
         assert rel <= 1e-4 and abs(g["E"] - o["E"]) <= 1e-6 * abs(o["E"])
+
+
+def test_skinned_lj_list_at_build_positions(eng_mod, params_text):
+    """AB_LIST_LJ_SKIN: right after the build, the skinned LJ half list is the set of
+    half pairs with r <= r_c + skin -- the oracle's LJ list for a parameter text whose r_c are
+    r_c + skin (the same doubles), bit-exact; it contains AB_LIST_LJ."""
+    import re
+    skin = float(re.search(rb"neigh.skin ([0-9.eE+-]+)", params_text).group(1))
+    txt = params_text
+    for pair in (b"CC", b"CH", b"HH"):
+        m = re.search(rb"lj\." + pair + rb"\.rc ([0-9.eE+-]+)", txt)
+        txt = txt.replace(m.group(0), b"lj." + pair + b".rc " + repr(float(m.group(1)) + skin).encode())
+    for s in (I.config(1), I.random_cluster(40, 3, spread=6.0, dmin=1.0), I.diamond((2, 2, 2), 0.04, 21)):
+        e = eng_mod.make(s)
+        sk = e.get_list(3)
+        ref = O.get_list(s.types, s.x, s.box, 2, params=txt)
+        assert sk.shape == ref.shape and np.array_equal(sk, ref), s.name
+        lj = {tuple(r) for r in e.get_list(2)}
+        assert lj <= {tuple(r) for r in sk}
