@@ -1119,8 +1119,11 @@ void graph_drop(ab_engine* e) {
 // grid sizes of one force evaluation and the partial-row layout of its reduction:
 // short | REBO (CC sp3, one-empty-side, hand-over, NBMAX) | near LJ | far LJ | b* (lite, fast,
 // NBMAX, full) | [far LJ of the slab interior, launched beside the halo exchange]
+#ifndef AB_LITE_GRID
+#define AB_LITE_GRID 6  // blocks per SM of the b* plateau batch (grid-stride; measured 6: 0.33 ms vs 4: 0.43 on cfg4)
+#endif
 struct Grids {
-  int g_short, g_rebo, g_near, g_far, g_bstar, g_slow, base;
+  int g_short, g_rebo, g_near, g_far, g_bstar, g_lite, g_slow, base;
 };
 Grids grids_of(const ab_engine* e) {
   Grids G;
@@ -1129,8 +1132,8 @@ Grids grids_of(const ab_engine* e) {
   G.g_short = nblk(e->NT, 128), G.g_rebo = e->nsm * 4;
   G.g_near = clp ? std::min(nblk((long long)N * 32, 128), e->nsm * AB_LJC_MINBLOCKS) : nblk(N, NEAR_ATOMS);
   G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * 8);
-  G.g_bstar = e->nsm * 4, G.g_slow = e->nsm * 2;
-  G.base = G.g_short + 2 * G.g_rebo + 2 * G.g_slow + G.g_near + G.g_far + 2 * G.g_bstar + 2 * G.g_slow;
+  G.g_bstar = e->nsm * 4, G.g_lite = e->nsm * AB_LITE_GRID, G.g_slow = e->nsm * 2;
+  G.base = G.g_short + 2 * G.g_rebo + 2 * G.g_slow + G.g_near + G.g_far + G.g_lite + G.g_bstar + 2 * G.g_slow;
   return G;
 }
 
@@ -1160,8 +1163,8 @@ ab_status launch_far_early_t(ab_engine* e) {
     kern<<<G.g_far, 128, 0, d->aux[1]>>>(A, d->gid.p, d->shift.p, d->F.p, d->acc.p, d->ct.p, sb, RR);
   };
   const bool morse = d->hp.potential == kAIREBOM;
-  if (d->want_virial) morse ? far(k_lj_far<R, true, true>) : far(k_lj_far<R, true, false>);
-  else morse ? far(k_lj_far<R, false, true>) : far(k_lj_far<R, false, false>);
+  if (d->want_virial) morse ? far(k_lj_far<R, true, true, false, true>) : far(k_lj_far<R, true, false, false, true>);
+  else morse ? far(k_lj_far<R, false, true, false, true>) : far(k_lj_far<R, false, false, false, true>);
   ++d->launches;
   CK(cudaGetLastError());
   d->far_early = true;
@@ -1284,7 +1287,8 @@ ab_status enqueue_forces(ab_engine* e) {
   LJArgs A;
   A.N = N;
   A.pos = e->pos.p;
-  if (e->far_early) A.r0b = 0, A.r0e = e->far_i0, A.r1b = e->far_i1, A.r1e = N;  // the rest of the atoms
+  const bool far_split = e->far_early;  // the interior atoms' far pairs are already running
+  if (far_split) A.r0b = 0, A.r0e = e->far_i0, A.r1b = e->far_i1, A.r1e = N;  // the rest of the atoms
   else A.r0b = 0, A.r0e = N, A.r1b = A.r1e = 0;
   e->far_early = false;
   for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
@@ -1300,8 +1304,14 @@ ab_status enqueue_forces(ab_engine* e) {
     auto far = [&](auto kern) {
       if (!(e->skip & 2)) kern<<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, Fk, e->acc.p, e->ct.p, sb1, R6);
     };
-    if (e->want_virial) morse ? far(k_lj_far<R, true, true, SG>) : far(k_lj_far<R, true, false, SG>);
-    else morse ? far(k_lj_far<R, false, true, SG>) : far(k_lj_far<R, false, false, SG>);
+    if (far_split) {
+      if (e->want_virial) morse ? far(k_lj_far<R, true, true, SG, true>) : far(k_lj_far<R, true, false, SG, true>);
+      else morse ? far(k_lj_far<R, false, true, SG, true>) : far(k_lj_far<R, false, false, SG, true>);
+    } else if (e->want_virial) {
+      morse ? far(k_lj_far<R, true, true, SG>) : far(k_lj_far<R, true, false, SG>);
+    } else {
+      morse ? far(k_lj_far<R, false, true, SG>) : far(k_lj_far<R, false, false, SG>);
+    }
     CKL();
     prof_stop(e, 6, s_far, t);
     CK(cudaEventRecord(e->ev_join[1], s_far));
@@ -1390,9 +1400,9 @@ ab_status enqueue_forces(ab_engine* e) {
     int* const nund = e->small_i.p + 16;  // plateau batch -> forward-pass kernel
     auto bstar = [&](auto lite, auto fast, auto full, auto big) -> ab_status {
       if (e->skip & 8) return AB_OK;
-      lite<<<g_bstar, 128, 0, st>>>(Qu, e->ovf_und.p, nund, e->pos.p, S, e->typ.p, e->owner.p, Fk,
-                                    sb1.rows != nullptr, RR);
-      RR.row0 += g_bstar;
+      lite<<<GR.g_lite, 128, 0, st>>>(Qu, e->ovf_und.p, nund, e->pos.p, S, e->typ.p, e->owner.p, Fk,
+                                      sb1.rows != nullptr, RR);
+      RR.row0 += GR.g_lite;
       // AB_PDL=1: the fast and full b* kernels are launched as programmatic dependents of the
       // kernel before them on the stream (their CTAs launch while it drains and wait in
       // griddepcontrol.wait); the NBMAX batch then forks after the full kernel

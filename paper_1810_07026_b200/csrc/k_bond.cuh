@@ -492,7 +492,7 @@ __device__ __forceinline__ void list_append(int* list, int* cnt, int cap, int v)
 #define AB_REBO3_MINBLOCKS 2  // the sp3 C-C batch (sides of <= 3)
 #endif
 #ifndef AB_REBO1_MINBLOCKS
-#define AB_REBO1_MINBLOCKS 3  // the one-empty-side batch (no J-side arrays, no dihedral loop)
+#define AB_REBO1_MINBLOCKS 4  // the one-empty-side batch (no J-side arrays, no dihedral loop; measured 4 beats 3)
 #endif
 #ifndef AB_BSTAR_MINBLOCKS
 #define AB_BSTAR_MINBLOCKS 3  // measured (cfg2): 3 blocks (170 regs) 56 us vs 64 us at 2 blocks

@@ -528,7 +528,7 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
   }
 }
 
-template <typename R, bool VIRIAL, bool MORSE, bool SG = false>
+template <typename R, bool VIRIAL, bool MORSE, bool SG = false, bool RANGED = false>
 #ifndef AB_FAR_MINBLOCKS
 #define AB_FAR_MINBLOCKS 4
 #endif
@@ -543,9 +543,11 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
   unsigned nlj = 0, ntp = 0;
   unsigned long long ne = 0;
   // grid-stride over atoms: a resident grid, one warp per atom at a time
-  const int n0 = A.r0e - A.r0b, nall = n0 + (A.r1e - A.r1b);
-  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nall; t += nwarps) {
-    const int i = t < n0 ? A.r0b + t : A.r1b + (t - n0);
+  // RANGED (slab interior / boundary split): the two atom ranges one after the other; otherwise
+  // every atom (a separate instantiation: the range bookkeeping cost 6 % of the kernel on cfg4)
+  for (int range = 0; range < (RANGED ? 2 : 1); ++range) {
+  const int rb = RANGED ? (range ? A.r1b : A.r0b) : 0, re = RANGED ? (range ? A.r1e : A.r0e) : A.N;
+  for (int i = rb + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < re; i += nwarps) {
     const double4 pi = A.pos[i];
     const int ti = type_of(pi);
     const long long ki = key_of(pi);
@@ -557,6 +559,7 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     fz = warp_sum<SG>(fz);
     if (lane == 0) atomic_add3<SG>(F, i, fx, fy, fz);
     if (lane == 0) ne += (unsigned long long)(A.cnt[1][i] + A.cnt[2][i]);
+  }
   }
   red_add_d(rs, ACC_ELJ, 0.5 * en);
   if (VIRIAL)
