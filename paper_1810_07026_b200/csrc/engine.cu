@@ -181,7 +181,7 @@ struct ab_engine {
   bool far_early = false;
   long long launches = 0, rebuilds = 0, steps = 0, retries = 0;
   // device state
-  DBuf<double4> pos, pos_tmp, xref;
+  DBuf<double4> pos, pos_tmp, xref, spos;  // spos: positions in the cell-sorted order (list builds)
   DBuf<double> vel, vel_tmp, F, io;
   DBuf<float> Ff;  // AB_SINGLE: fp32 force accumulation array of an evaluation
   DBuf<int> gid, gid_tmp, owner, key, val, val2, cell_start, gcnt, goff;
@@ -811,6 +811,9 @@ ab_status images_and_lists(ab_engine* e) {
   k_cell_keys<<<nblk(NT, 256), 256, 0, st>>>(NT, e->pos.p, e->grid, e->key.p, e->val.p);
   CKL();
   TRY(key_sort(e, NT, e->key.p, e->ncell, nullptr, e->val2.p, e->cell_start.p));  // cell list
+  CK(e->spos.ensure(NT));
+  k_sorted_pos<<<nblk(NT, 256), 256, 0, st>>>(NT, e->val2.p, e->pos.p, e->spos.p);
+  CKL();
   const bool clp = e->cl_path && e->hp.potential != kREBO;
   if (clp) TRY(build_clusters(e));
   e->rb_ms[2] += tms(tq);
@@ -879,14 +882,14 @@ ab_status images_and_lists(ab_engine* e) {
                                                                 e->cl_atom.p, CLs, e->small_i.p + 2);
       CKL();
     } else if (e->hp.potential != kREBO) {  // REBO has no inter-molecular term: no LJ lists
-      k_build_lj<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
+      k_build_lj<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->spos.p, e->grid, e->cell_start.p, e->val2.p,
                                                                 e->nrLJ, Lg, e->small_i.p + 2);
       CKL();
     } else {
       for (int c = 0; c < 3; ++c)
         if (N) CK(cudaMemsetAsync(e->ljc[c].p, 0, sizeof(int) * N, st));
     }
-    k_build_inter<<<nblk((long long)NT * 32, 128), 128, 0, st>>>(NT, e->pos.p, e->grid, e->cell_start.p, e->val2.p,
+    k_build_inter<<<nblk((long long)NT * 32, 128), 128, 0, st>>>(NT, e->pos.p, e->spos.p, e->grid, e->cell_start.p, e->val2.p,
                                                                   e->nrI, (e->rmaxmax + skin) * (1.0 + 1e-9) + 1e-9,
                                                                   e->capI, e->in_cnt.p, e->in_nbr.p,
                                                                   e->small_i.p + 5);
@@ -1824,7 +1827,7 @@ void free_engine(ab_engine* e) {
     if (NC.ok) NC.commDestroy(e->comm);
     e->comm = nullptr;
   }
-  DBuf<double4>* b4[] = {&e->pos, &e->pos_tmp, &e->xref, &e->cpos, &e->cbb};
+  DBuf<double4>* b4[] = {&e->pos, &e->pos_tmp, &e->xref, &e->spos, &e->cpos, &e->cbb};
   for (auto* b : b4) b->release();
   e->acc.p = nullptr, e->ct.p = nullptr, e->small_i.p = nullptr;  // views into scratch
   e->scratch.release();

@@ -159,14 +159,23 @@ __device__ __forceinline__ int stencil_columns(const Grid& g, double4 p, int nr,
   return run;
 }
 
-// candidate f of the flattened stencil, scanning forward from column k (k <= f's column)
-__device__ __forceinline__ int stencil_at(const int* cb, const int* pre, const int* cell_atoms, int f, int& k) {
+// candidate f of the flattened stencil, scanning forward from column k (k <= f's column): its
+// position in the cell-sorted order (cell_atoms[s] = atom index, spos[s] = its position: a
+// column's z-run of candidates is contiguous there, so a warp's 32 candidates are ~8 lines)
+__device__ __forceinline__ int stencil_at(const int* cb, const int* pre, int f, int& k) {
   while (pre[k + 1] <= f) ++k;
-  return cell_atoms[cb[k] + f - pre[k]];
+  return cb[k] + f - pre[k];
 }
 
-__global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, Grid g, const int* cell_start,
-                                                  const int* cell_atoms, int nr, LJLists Lg, int* maxcnt) {
+// positions in the cell-sorted order of the last binning (list builds)
+__global__ void k_sorted_pos(int NT, const int* cell_atoms, const double4* pos, double4* spos) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < NT) spos[q] = pos[cell_atoms[q]];
+}
+
+__global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, const double4* spos, Grid g,
+                                                  const int* cell_start, const int* cell_atoms, int nr, LJLists Lg,
+                                                  int* maxcnt) {
   __shared__ int s_cb[4][STENCIL_MAXCOL], s_pre[4][STENCIL_MAXCOL + 1];
   int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= N) return;
@@ -184,13 +193,15 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, Gri
   int k = 0;  // column of the chunk's first candidate (warp-uniform)
   // software pipeline: the next chunk's index and position loads are in flight while this
   // chunk is classified and appended
-  int b = lane < total ? stencil_at(cb, pre, cell_atoms, lane, k) : -1;
-  double4 pb = b >= 0 ? pos[b] : make_double4(0, 0, 0, 0);
+  int sq = lane < total ? stencil_at(cb, pre, lane, k) : -1;
+  int b = sq >= 0 ? cell_atoms[sq] : -1;
+  double4 pb = sq >= 0 ? spos[sq] : make_double4(0, 0, 0, 0);
   for (int base = 0; base < total; base += 32) {
     int kn = __shfl_sync(0xffffffffu, k, 31);
     const int fn = base + 32 + lane;
-    const int bn = fn < total ? stencil_at(cb, pre, cell_atoms, fn, kn) : -1;
-    const double4 pbn = bn >= 0 ? pos[bn] : make_double4(0, 0, 0, 0);
+    const int sqn = fn < total ? stencil_at(cb, pre, fn, kn) : -1;
+    const int bn = sqn >= 0 ? cell_atoms[sqn] : -1;
+    const double4 pbn = sqn >= 0 ? spos[sqn] : make_double4(0, 0, 0, 0);
     const bool ok = b >= 0 && b != a;
     double r2 = 1e300;
     int pr = 0;
@@ -220,9 +231,9 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, Gri
 }
 
 // intermediate REBO list: all atoms (locals + ghosts), r_b <= r_max(p) + skin
-__global__ void __launch_bounds__(128) k_build_inter(int NT, const double4* pos, Grid g, const int* cell_start,
-                                                     const int* cell_atoms, int nr, double reach, int cap, int* cnt,
-                                                     int* nbr, int* maxcnt) {
+__global__ void __launch_bounds__(128) k_build_inter(int NT, const double4* pos, const double4* spos, Grid g,
+                                                     const int* cell_start, const int* cell_atoms, int nr, double reach,
+                                                     int cap, int* cnt, int* nbr, int* maxcnt) {
   __shared__ int s_cb[4][STENCIL_MAXCOL], s_pre[4][STENCIL_MAXCOL + 1];
   int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= NT) return;
@@ -237,10 +248,11 @@ __global__ void __launch_bounds__(128) k_build_inter(int NT, const double4* pos,
   int k = 0;
   for (int base = 0; base < total; base += 32) {
     const int f = base + lane;
-    const int b = f < total ? stencil_at(cb, pre, cell_atoms, f, k) : -1;
+    const int sq = f < total ? stencil_at(cb, pre, f, k) : -1;
+    const int b = sq >= 0 ? cell_atoms[sq] : -1;
     bool in = false;
     if (b >= 0 && b != a) {
-      const double4 pb = pos[b];
+      const double4 pb = spos[sq];
       const double r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
       in = r2 <= c_geo.rmax_s2[ta + type_of(pb)];
     }
