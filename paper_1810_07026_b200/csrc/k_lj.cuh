@@ -211,70 +211,61 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   const int ni = cntN > 0 ? S.cnt[i] : 0;
 #endif
   // Flattened walk: level 1 (k in N(i)) one lane per k; level 2 (l in N(k)) the (k, l) pairs are
-  // spread over the group's lanes; level 3 (m in N(l)) each lane walks its own (k, l) pairs.
-  // Products keep the association (w_ik w_kl) w_lm of the paper's nested enumeration, so M is
-  // bitwise that of the serial walk (the fallback for large neighbourhoods).
-  constexpr int L2MAX = 4;  // (k, l) pairs per lane
-  int k1 = -1, n1 = 0;
-  double w1 = 0;
-  if (gl < ni && gl < NEAR_GROUP) {
-    k1 = S.nbr[bi + gl];
-    w1 = S.wd[bi + gl];
-    n1 = S.cnt[k1];
-    reach_insert(s, k1, w1);
-  }
+  // spread over the group's lanes (the owner lane of pair e found by a binary search over the
+  // group's exclusive prefix counts, all through shuffles: no indexed arrays, no local memory);
+  // level 3 (m in N(l)) the lane walks right away.  Products keep the association
+  // (w_ik w_kl) w_lm of the paper's nested enumeration, so M is bitwise that of the serial walk
+  // (the fallback for large neighbourhoods).
   const unsigned gmask = (NEAR_GROUP == 32 ? 0xffffffffu : ((1u << NEAR_GROUP) - 1u)) << (threadIdx.x & 31 & ~(NEAR_GROUP - 1));
-  int kk[NEAR_GROUP], pp[NEAR_GROUP + 1];
-  double ww[NEAR_GROUP];
-  pp[0] = 0;
-#pragma unroll
-  for (int t = 0; t < NEAR_GROUP; ++t) {
-    kk[t] = __shfl_sync(gmask, k1, t, NEAR_GROUP);
-    ww[t] = __shfl_sync(gmask, w1, t, NEAR_GROUP);
-    pp[t + 1] = pp[t] + __shfl_sync(gmask, n1, t, NEAR_GROUP);
-  }
-  const int T2 = pp[NEAR_GROUP];
-  if (ni <= NEAR_GROUP && T2 <= NEAR_GROUP * L2MAX) {
-    int l2[L2MAX];
-    double w2[L2MAX];
-    int n2 = 0;
-    for (int e = gl; e < T2; e += NEAR_GROUP) {
-      int t = 0;
-#pragma unroll
-      for (int u = 1; u < NEAR_GROUP; ++u) t += (e >= pp[u]);
-      int k = 0, b = 0;
-      double wk = 0;
-#pragma unroll
-      for (int u = 0; u < NEAR_GROUP; ++u)
-        if (u == t) k = kk[u], wk = ww[u], b = e - pp[u];
-      const size_t ek = (size_t)k * S.capS + b;
-      const int l = S.nbr[ek];
-      if (l == i) continue;
-      const double w12 = wk * S.wd[ek];
-      reach_insert(s, l, w12);
-#pragma unroll
-      for (int u = 0; u < L2MAX; ++u)
-        if (u == n2) l2[u] = l, w2[u] = w12;
-      ++n2;
+  if (ni <= NEAR_GROUP) {
+    int k1 = -1, n1 = 0;
+    double w1 = 0;
+    if (gl < ni) {
+      k1 = S.nbr[bi + gl];
+      w1 = S.wd[bi + gl];
+      n1 = S.cnt[k1];
+      reach_insert(s, k1, w1);
     }
+    int incl = n1;
 #pragma unroll
-    for (int u = 0; u < L2MAX; ++u) {
-      if (u >= n2) break;
-      const int l = l2[u];
-      const double w12 = w2[u];
-      const size_t bl = (size_t)l * S.capS;
-      const int nl = S.cnt[l];
-      for (int c = 0; c < nl; ++c) {
-        const int m = S.nbr[bl + c];
-        if (m == i) continue;
-        reach_insert(s, m, w12 * S.wd[bl + c]);
+    for (int o = 1; o < NEAR_GROUP; o <<= 1) {
+      const int u = __shfl_up_sync(gmask, incl, o, NEAR_GROUP);
+      if (gl >= o) incl += u;
+    }
+    const int excl = incl - n1;
+    const int T2 = __shfl_sync(gmask, incl, NEAR_GROUP - 1, NEAR_GROUP);
+    for (int base = 0; base < T2; base += NEAR_GROUP) {
+      const int e = base + gl;
+      int t = 0;  // last lane with excl_t <= e (lanes without entries share the next one's excl)
+#pragma unroll
+      for (int bb = NEAR_GROUP / 2; bb > 0; bb >>= 1) {
+        const int ex = __shfl_sync(gmask, excl, t + bb, NEAR_GROUP);
+        if (ex <= e) t += bb;
+      }
+      const int k = __shfl_sync(gmask, k1, t, NEAR_GROUP);
+      const double wk = __shfl_sync(gmask, w1, t, NEAR_GROUP);
+      const int off = e - __shfl_sync(gmask, excl, t, NEAR_GROUP);
+      if (e < T2) {
+        const size_t ek = (size_t)k * S.capS + off;
+        const int l = S.nbr[ek];
+        if (l != i) {
+          const double w12 = wk * S.wd[ek];
+          reach_insert(s, l, w12);
+          const size_t bl = (size_t)l * S.capS;
+          const int nl = S.cnt[l];
+          for (int c = 0; c < nl; ++c) {
+            const int m = S.nbr[bl + c];
+            if (m == i) continue;
+            reach_insert(s, m, w12 * S.wd[bl + c]);
+          }
+        }
       }
     }
   } else {  // large neighbourhood: one lane per k walks its paths (the nested enumeration)
     for (int t = gl; t < ni; t += NEAR_GROUP) {
       int k = S.nbr[bi + t];
       double w1t = S.wd[bi + t];
-      if (t >= NEAR_GROUP) reach_insert(s, k, w1t);
+      reach_insert(s, k, w1t);
       size_t bk = (size_t)k * S.capS;
       int nk = S.cnt[k];
       for (int b = 0; b < nk; ++b) {
