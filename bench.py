@@ -176,7 +176,7 @@ def algorithmic_flops(stats):
 
 
 PHASES = ["short", "rebo", "lj_near", "bstar", "integrate", "rebuild", "lj_far", "comm"]  # ab_get_phase_ms slots
-KERNEL_OF = {"short": "k_short", "rebo": "k_rebo", "lj_near": "k_lj_near", "bstar": "k_bstar", "lj_far": "k_lj_far"}
+KERNEL_OF = {"short": "k_short", "rebo": "k_rebo", "lj_near": "k_lj_near", "bstar": "k_bstar_lite", "lj_far": "k_lj_far"}
 
 
 def fp64_peak_tflops(sm_mhz, nsm=148):
@@ -332,7 +332,7 @@ def run_ours(args, ws, rank, local):
         dram = None
         try:
             summ = json.load(open(PROFILE_SUMMARY)).get(precision, {})
-            per = {"k_short": 1, "k_rebo": 2, "k_lj_near": 1, "k_lj_far": 1, "k_bstar": 3}
+            per = {"k_short": 1, "k_rebo": 2, "k_lj_near": 1, "k_lj_far": 1, "k_bstar_lite": 1}
             if all(k in summ and summ[k].get("dram_bytes_per_launch") for k in per):
                 byts = sum(summ[k]["dram_bytes_per_launch"] * n for k, n in per.items())
                 hbm = None

@@ -46,30 +46,32 @@ with open(os.path.join(prof, f"launch_shares_{tag}.txt"), "w") as f:
     for k, (us, n) in sorted(tot.items(), key=lambda x: -x[1][0]):
         f.write(f"{k[:60]:60s} {us:12.1f} {n:9d} {us / n:9.2f} {100 * us / all_us:6.2f}%\n")
 
-out = subprocess.run(["python", os.path.join(ROOT, "scripts", "ncu_summary.py"), rep], capture_output=True,
-                     text=True).stdout
+reps = rep.split(",")  # several --set full captures (a gpurun call returns <= 64 MiB)
+out = "".join(subprocess.run(["python", os.path.join(ROOT, "scripts", "ncu_summary.py"), r], capture_output=True,
+                             text=True).stdout for r in reps)
 open(os.path.join(prof, f"ncu_full_{tag}.txt"), "w").write(
     f"# ncu --set full --clock-control none --import-source on (scripts/collect_profiles.sh: short bench.py run, cfg4 (1,008,000-atom PE), fp64)\n" + out)
 
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rr = list(csv.reader(raw.splitlines()))
-hdr = rr[0]
-col = {n: i for i, n in enumerate(hdr)}
 summ = {"fp64": {}}
-for r in rr[2:]:
-    kname = re.sub(r"<.*|\(.*", "", r[col["Kernel Name"]]).replace("void ", "").replace("ab::", "").strip()
-    d = {}
-    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
-        if key in col:
-            unit = rr[1][col[key]]
-            v = float(r[col[key]].replace(",", ""))
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3,
-                     "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
-            d[key] = v * scale
-    e = summ["fp64"].setdefault(kname, {"launches": 0, "dram_bytes": 0.0, "duration_us": 0.0})
-    e["launches"] += 1
-    e["dram_bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
-    e["duration_us"] += d.get("gpu__time_duration.sum", 0)
+for rep1 in reps:
+  raw = subprocess.run(["ncu", "-i", rep1, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+  rr = list(csv.reader(raw.splitlines()))
+  hdr = rr[0]
+  col = {n: i for i, n in enumerate(hdr)}
+  for r in rr[2:]:
+      kname = re.sub(r"<.*|\(.*", "", r[col["Kernel Name"]]).replace("void ", "").replace("ab::", "").strip()
+      d = {}
+      for key in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
+          if key in col:
+              unit = rr[1][col[key]]
+              v = float(r[col[key]].replace(",", ""))
+              scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3,
+                       "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
+              d[key] = v * scale
+      e = summ["fp64"].setdefault(kname, {"launches": 0, "dram_bytes": 0.0, "duration_us": 0.0})
+      e["launches"] += 1
+      e["dram_bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+      e["duration_us"] += d.get("gpu__time_duration.sum", 0)
 for e in summ["fp64"].values():
     e["dram_bytes_per_launch"] = e["dram_bytes"] / max(e["launches"], 1)
 summ["_note"] = ("ncu --set full capture (cache flushed between replays, i.e. cold-cache DRAM traffic per "
