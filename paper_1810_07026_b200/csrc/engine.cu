@@ -25,6 +25,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <map>
 
 #include "../../include/airebo_b200.h"
 #include "dev_common.cuh"
@@ -72,6 +73,9 @@ inline int nblk(long long n, int t) { return (int)std::max<long long>(1, (n + t 
 
 constexpr size_t SCRATCH_BYTES = 1024, SCRATCH_CT = 128, SCRATCH_SMALL = 512, SCRATCH_ZERO_BYTES = 512 + 96;
 constexpr size_t SCRATCH_TICKET = 1016;
+// bits of the max displacement^2 of any local atom since the last build (atomicMax by the drift /
+// displacement kernels, zeroed at every build; never in the zeroed region): the far-LJ kernel's bins
+constexpr size_t SCRATCH_DBOUND = 1000;
 #ifndef AB_INT_BLOCK
 #define AB_INT_BLOCK 128  // k_integrate1_img block (measured cfg2: 128 beats 256; 64 / 32 equal)
 #endif  // k_integrate1_img's last-block ticket (never memset after init)
@@ -187,7 +191,8 @@ struct ab_engine {
   DBuf<int> gid, gid_tmp, owner, key, val, val2, cell_start, gcnt, goff;
   DBuf<char4> shift, rshift;
   DBuf<signed char> typ;
-  DBuf<int> ljc[3], ljn[3], in_cnt, in_nbr;  // LJ near / pure / band lists, intermediate list
+  DBuf<int> ljc[3], ljn[3], in_cnt, in_nbr;  // LJ near / far / (unused) lists, intermediate list
+  DBuf<unsigned short> ljboff;               // far-row bin ends (k_lists.cuh FB_*)
   int capL[3] = {0, 0, 0};
   // j-cluster LJ path (k_cluster.cuh, k_ljc.cuh), AB_LJ_CLUSTER=1; default: per-atom near / far lists
   bool cl_path = false;
@@ -826,18 +831,22 @@ ab_status images_and_lists(ab_engine* e) {
   for (int c = 0; c < 3; ++c) CK(e->ljc[c].ensure(N));
   CK(e->in_cnt.ensure(NT));
   const double skin = e->hp.skin;
-  const double rnear = 3 * e->rmaxmax + skin;
+  // a_p: radius of the S_r window pre-filter (r^2 < a_p^2 = (2^(1/6) sigma)^2 (1 + 1e-9), c_geo.srhi2_hi)
+  double fa[3], amax = 0;
+  for (int p = 0; p < 3; ++p) {
+    const double srhi = e->hp.pr[p].sigma * 1.122462048309373;
+    fa[p] = std::sqrt(srhi * srhi * (1.0 + 1e-9));
+    amax = std::max(amax, fa[p]);
+  }
   if (e->capL[0] == 0 && e->hp.potential == kREBO) e->capL[0] = e->capL[1] = e->capL[2] = 1;
   if (e->capL[0] == 0) {  // first build: capacities from the mean density (grown on overflow)
     double vol = e->L[0] * e->L[1] * e->L[2];
     if (slabbed(e)) vol = (e->xhi - e->xlo) * e->L[1] * e->L[2];
     double rho = std::max(N, 1) / vol, fpi = 4.18879020478639;
-    double rlo_max = 0;
-    for (int p = 0; p < 3; ++p) rlo_max = std::max(rlo_max, e->hp.pr[p].rlo);
-    double r1 = std::max(rnear, rlo_max - skin), r2 = e->rcmax + skin;
-    e->capL[0] = 32 + (int)(1.3 * rho * fpi * rnear * rnear * rnear);
-    e->capL[1] = 32 + (int)(1.3 * rho * fpi * (r1 * r1 * r1 - rnear * rnear * rnear));
-    e->capL[2] = 32 + (int)(1.3 * rho * fpi * (r2 * r2 * r2 - std::min(r1, rnear) * std::min(r1, rnear) * std::min(r1, rnear)));
+    const double rn = amax + skin, r2 = e->rcmax + skin, r1 = std::max(amax - skin, 0.0);
+    e->capL[0] = 32 + (int)(1.3 * rho * fpi * rn * rn * rn);
+    e->capL[1] = 32 + (int)(1.3 * rho * fpi * (r2 * r2 * r2 - r1 * r1 * r1));
+    e->capL[2] = 1;
   }
   if (e->capI == 0) e->capI = 16;
   if (clp && e->capC == 0) {  // clusters within r_c,max + skin + a cluster extent, 4 slots each
@@ -847,15 +856,16 @@ ab_status images_and_lists(ab_engine* e) {
     e->capC = 32 + (int)(1.4 * rho * 4.18879020478639 * R * R * R / CL_SIZE / 0.8);
   }
   LJLists Lg;
-  Lg.near2 = rnear * rnear;
   for (int p = 0; p < 3; ++p) {
-    double b = e->hp.pr[p].rlo - skin;
-    Lg.pure2[p] = b > rnear ? b * b : -1.0;
-    // a canonical pair can be queued as a window candidate (r^2 < (2^(1/6) sigma)^2 (1 + 1e-9))
-    // until the next build only if r_b <= 2^(1/6) sigma (1 + 1e-9) + skin now (pairs move < skin)
-    double q = e->hp.pr[p].sigma * 1.122462048309373 * (1.0 + 1e-9) + skin;
-    Lg.bq2[p] = q * q;
+    // rounding margins (1e-7 A) on the safe side: every pair that can be inside / outside the
+    // window before the next build is in the near / far list
+    const double lo = fa[p] - skin - 1e-7, hi = fa[p] + skin + 1e-7;
+    Lg.flo2[p] = lo > 0 ? lo * lo : 0.0;
+    Lg.bq2[p] = hi * hi;
+    Lg.fa[p] = fa[p];
+    Lg.rlo[p] = e->hp.pr[p].rlo, Lg.rc[p] = e->hp.pr[p].rc, Lg.rc2[p] = Lg.rc[p] * Lg.rc[p];
   }
+  Lg.skin = skin;
   Lg.bqcnt = e->small_i.p + 6;
   Lg.reach = (e->rcmax + skin) * (1.0 + 1e-9) + 1e-9;
   for (int attempt = 0; attempt < 4; ++attempt) {
@@ -865,6 +875,9 @@ ab_status images_and_lists(ab_engine* e) {
       Lg.cnt[c] = e->ljc[c].p;
       Lg.nbr[c] = e->ljn[c].p;
     }
+    if (!clp) CK(e->ljboff.ensure((size_t)N * FB_STRIDE));
+    Lg.boff = e->ljboff.p;
+    Lg.fcap_smem = e->capL[1];
     CK(e->in_nbr.ensure((size_t)NT * e->capI));
     CK(cudaMemsetAsync(e->small_i.p + 2, 0, 7 * sizeof(int), st));
     const bool dbg = std::getenv("AB_HOST_TIMING") && std::getenv("AB_HOST_TIMING")[0] == '2';
@@ -882,8 +895,18 @@ ab_status images_and_lists(ab_engine* e) {
                                                                 e->cl_atom.p, CLs, e->small_i.p + 2);
       CKL();
     } else if (e->hp.potential != kREBO) {  // REBO has no inter-molecular term: no LJ lists
-      k_build_lj<<<nblk((long long)N * 32, 128), 128, 0, st>>>(N, e->pos.p, e->spos.p, e->grid, e->cell_start.p, e->val2.p,
-                                                                e->nrLJ, Lg, e->small_i.p + 2);
+      // far entries staged in shared memory: 4 warps per block, 1 if the rows are very long
+      const size_t per_warp = (size_t)((e->capL[1] + 3) / 4) * 5 * sizeof(int);
+      const int wpb = per_warp * 4 <= 200 * 1024 ? 4 : 1;
+      if (per_warp * wpb > 200 * 1024) {
+        e->err = "LJ far list longer than the shared-memory staging of the list build supports";
+        return AB_E_STATE;
+      }
+      const size_t dyn = per_warp * wpb;
+      if (dyn > 48 * 1024) CK(cudaFuncSetAttribute(k_build_lj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+      k_build_lj<<<nblk((long long)N * 32, 32 * wpb), 32 * wpb, dyn, st>>>(N, e->pos.p, e->spos.p, e->grid,
+                                                                            e->cell_start.p, e->val2.p, e->nrLJ, Lg,
+                                                                            e->small_i.p + 2);
       CKL();
     } else {
       for (int c = 0; c < 3; ++c)
@@ -933,6 +956,7 @@ ab_status images_and_lists(ab_engine* e) {
   CK(e->xref.ensure(N));
   k_copy_xref<<<nblk(N, 256), 256, 0, st>>>(N, e->pos.p, e->xref.p);
   CKL();
+  CK(cudaMemsetAsync(e->scratch.p + SCRATCH_DBOUND, 0, sizeof(unsigned long long), st));
   e->lists_valid = true;
   ++e->rebuilds;
   return AB_OK;
@@ -1128,6 +1152,29 @@ void graph_drop(ab_engine* e) {
 struct Grids {
   int g_short, g_rebo, g_near, g_far, g_bstar, g_lite, g_slow, base;
 };
+// far-LJ / near-LJ kernel arguments (lists of the last build, displacement bound of the far bins)
+LJArgs lj_args(ab_engine* e) {
+  LJArgs A;
+  A.N = e->N;
+  A.pos = e->pos.p;
+  A.r0b = 0, A.r0e = e->N, A.r1b = A.r1e = 0;
+  for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
+  A.boff = e->ljboff.p;
+  A.xref = e->xref.p;
+  // slab domains: halo atoms are displaced by other ranks' steps -- the rebuild invariant (every
+  // atom moved <= skin/2) bounds them; whole box: the device-side bound of this engine
+  A.dbound = slabbed(e) ? nullptr : reinterpret_cast<const unsigned long long*>(e->scratch.p + SCRATCH_DBOUND);
+  A.skin = e->hp.skin;
+  bool binned = e->hp.skin > 0.0;
+  for (int p = 0; p < 3; ++p) {
+    const PairSet& s = e->hp.pr[p];
+    const double a = std::sqrt(s.sigma * 1.122462048309373 * s.sigma * 1.122462048309373 * (1.0 + 1e-9));
+    binned = binned && a + 2.0 * e->hp.skin + 1e-6 <= s.rlo && s.rlo < s.rc;
+  }
+  A.binned = binned ? 1 : 0;
+  return A;
+}
+
 Grids grids_of(const ab_engine* e) {
   Grids G;
   const int N = e->N;
@@ -1156,10 +1203,8 @@ ab_status launch_far_early_t(ab_engine* e) {
   d->f_zeroed = true;  // enqueue_forces must not zero F again
   CK(cudaEventRecord(d->ev_fork[1], d->st));
   CK(cudaStreamWaitEvent(d->aux[1], d->ev_fork[1], 0));
-  LJArgs A;
-  A.N = d->N, A.pos = d->pos.p;
+  LJArgs A = lj_args(d);
   A.r0b = d->far_i0, A.r0e = d->far_i1, A.r1b = A.r1e = 0;
-  for (int c = 0; c < 3; ++c) A.cap[c] = d->capL[c], A.cnt[c] = d->ljc[c].p, A.nbr[c] = d->ljn[c].p;
   RedRows RR{d->red_d.p, d->red_u.p, nrows, G.base};
   StageBuf sb{nullptr, nullptr, 0};
   auto far = [&](auto kern) {
@@ -1234,7 +1279,7 @@ ab_status enqueue_forces(ab_engine* e) {
   const bool clp = e->cl_path && e->hp.potential != kREBO;
   if (e->record) {
     size_t n0 = (size_t)N * e->capS + 16;
-    size_t n1 = (clp ? (size_t)N * e->capC * CL_SIZE : (size_t)N * (e->capL[0] + e->capL[1] + e->capL[2])) + 16;
+    size_t n1 = (clp ? (size_t)N * e->capC * CL_SIZE : (size_t)N * (e->capL[0] + e->capL[1] + e->capL[2] + NEAR_SLOTS)) + 16;
     CK(e->stage0.ensure(n0 * 13));
     CK(e->stage1.ensure(n1 * 7));
     sb0 = StageBuf{e->stage0.p, e->small_i.p + 6, (int)n0};
@@ -1287,14 +1332,11 @@ ab_status enqueue_forces(ab_engine* e) {
   Qu.item = e->q_item.p, Qu.M = e->q_M.p, Qu.count = e->small_i.p + 13;
   for (int t = 0; t < 3; ++t) Qu.cap[t] = e->qcap[t], Qu.off[t] = e->qoff[t];
   const BondList BL{e->bonds.p, e->small_i.p + 10, e->N * e->capS + 1};
-  LJArgs A;
-  A.N = N;
-  A.pos = e->pos.p;
+  LJArgs A = lj_args(e);
   const bool far_split = e->far_early;  // the interior atoms' far pairs are already running
   if (far_split) A.r0b = 0, A.r0e = e->far_i0, A.r1b = e->far_i1, A.r1e = N;  // the rest of the atoms
   else A.r0b = 0, A.r0e = N, A.r1b = A.r1e = 0;
   e->far_early = false;
-  for (int c = 0; c < 3; ++c) A.cap[c] = e->capL[c], A.cnt[c] = e->ljc[c].p, A.nbr[c] = e->ljn[c].p;
   // the far kernel forks from the engine stream at e->far_at: 0 = at once, 1 = after the short
   // list, 2 = after the near kernel (it then fills the GPU beside the b* batch)
   auto launch_far = [&]() -> ab_status {
@@ -1662,7 +1704,8 @@ ab_status prepare_all(ab_engine* e, bool check_disp) {
   if (check_disp) {
     for (ab_engine* d : doms(e)) {
       CK(cudaMemsetAsync(d->ct.p + CT_N, 0, sizeof(unsigned long long), e->st));
-      k_maxdisp<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->pos.p, d->xref.p, d->ct.p + CT_N);
+      k_maxdisp<<<nblk(d->N, 256), 256, 0, e->st>>>(d->N, d->pos.p, d->xref.p, d->ct.p + CT_N,
+                                                     reinterpret_cast<unsigned long long*>(d->scratch.p + SCRATCH_DBOUND));
       CKL();
     }
     TRY(enqueue_flags(e));
@@ -1844,6 +1887,7 @@ void free_engine(ab_engine* e) {
                                &e->redx};
   for (auto* b : bu) b->release();
   e->Ff.release();
+  e->ljboff.release();
   e->shift.release();
   e->rshift.release();
   e->typ.release();
@@ -2438,13 +2482,17 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
                    reinterpret_cast<unsigned long long*>(d->scratch.p), (int)(SCRATCH_ZERO_BYTES / 8), CT_OVF_SHORT,
                    d->ct.p};
         k_integrate1_img<<<nblk(d->N, AB_INT_BLOCK), AB_INT_BLOCK, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, pre, pd0, pd1, dtf0, dtf1, dt,
-                                                          d->xref.p, d->ct.p + CT_N, d->NX, d->goff.p, d->gcnt.p,
+                                                          d->xref.p, d->ct.p + CT_N,
+                                                          reinterpret_cast<unsigned long long*>(d->scratch.p + SCRATCH_DBOUND),
+                                                          d->NX, d->goff.p, d->gcnt.p,
                                                           d->rshift.p, fo, d->prec == AB_REDUCED);
         d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = true;
         flags_published = true;
       } else {
         k_integrate1<<<nblk(d->N, 256), 256, 0, st>>>(d->N, d->pos.p, d->vel.p, d->F.p, dtf0, dtf1, dt, d->xref.p,
-                                                      d->ct.p + CT_N, d->prec == AB_REDUCED);
+                                                      d->ct.p + CT_N,
+                                                      reinterpret_cast<unsigned long long*>(d->scratch.p + SCRATCH_DBOUND),
+                                                      d->prec == AB_REDUCED);
       }
       CKL();
     }
@@ -2605,8 +2653,14 @@ static ab_status list_visit(ab_engine* e, ab_engine* d, ab_list which, Visit&& v
       }
     return AB_OK;
   }
-  // (count, neighbour) tables of the requested list(s)
-  int nl = which == AB_LIST_LJ ? 3 : 1;
+  // (count, neighbour) tables of the requested list(s).  LJ: the near list and the far list
+  // without its L bins (the overlap shell, k_lists.cuh: those pairs are near-list members too)
+  int nl = which == AB_LIST_LJ ? 2 : 1;
+  std::vector<unsigned short> boff;
+  if (which == AB_LIST_LJ && N && d->capL[1] > 1) {
+    boff.resize((size_t)N * FB_STRIDE);
+    CK(cudaMemcpyAsync(boff.data(), d->ljboff.p, sizeof(unsigned short) * boff.size(), cudaMemcpyDeviceToHost, e->st));
+  }
   std::vector<int> cnt[3], nbr[3];
   int cap[3];
   for (int c = 0; c < nl; ++c) {
@@ -2623,7 +2677,7 @@ static ab_status list_visit(ab_engine* e, ab_engine* d, ab_list which, Visit&& v
   CK(cudaStreamSynchronize(e->st));
   for (int c = 0; c < nl; ++c)
     for (int i = 0; i < N; ++i)
-      for (int q = 0; q < cnt[c][i]; ++q) {
+      for (int q = (c == 1 && !boff.empty()) ? (int)boff[(size_t)i * FB_STRIDE + FB_P - 1] : 0; q < cnt[c][i]; ++q) {
         int J = nbr[c][(size_t)i * cap[c] + q];
         char4 s = sh[J];
         bool canon = gid[i] != gid[J] ? gid[i] < gid[J]
@@ -2743,17 +2797,37 @@ ab_status ab_get_stage(ab_engine* e, int stage, int64_t* count, double* out) {
     return AB_E_STATE;
   }
   const int width = stage == 0 ? 13 : 7;
-  int64_t total = 0;
+  std::vector<double> all;
   for (ab_engine* d : doms(e)) {
     int n[2];
     CK(cudaMemcpyAsync(n, d->small_i.p + 6, 2 * sizeof(int), cudaMemcpyDeviceToHost, e->st));
     CK(cudaStreamSynchronize(e->st));
-    int rows = n[stage];
-    if (out && rows)
-      CK(cudaMemcpy(out + total * width, stage == 0 ? d->stage0.p : d->stage1.p, sizeof(double) * width * rows,
+    const int rows = n[stage];
+    const size_t at = all.size();
+    all.resize(at + (size_t)width * rows);
+    if (rows)
+      CK(cudaMemcpy(all.data() + at, stage == 0 ? d->stage0.p : d->stage1.p, sizeof(double) * width * rows,
                     cudaMemcpyDeviceToHost));
-    total += rows;
   }
+  int64_t total = (int64_t)(all.size() / width);
+  if (stage == 1) {
+    // a far-zone pair of the reach set has two rows: k_lj_far's (C = 1) and k_lj_near's correction
+    // (C = 1 - M < 1); the pair's C_ij is the smaller one
+    std::map<std::array<double, 5>, size_t> best;
+    for (int64_t r = 0; r < total; ++r) {
+      const double* row = all.data() + (size_t)r * width;
+      std::array<double, 5> k{row[0], row[1], row[2], row[3], row[4]};
+      auto it = best.find(k);
+      if (it == best.end()) best.emplace(k, (size_t)r);
+      else if (row[5] < all[it->second * width + 5]) it->second = (size_t)r;
+    }
+    std::vector<double> ded;
+    ded.reserve(best.size() * width);
+    for (auto& kv : best) ded.insert(ded.end(), all.begin() + kv.second * width, all.begin() + (kv.second + 1) * width);
+    all.swap(ded);
+    total = (int64_t)best.size();
+  }
+  if (out && total) std::memcpy(out, all.data(), sizeof(double) * width * total);
   *count = total;
   return AB_OK;
 }

@@ -75,23 +75,61 @@ __global__ void k_cell_keys(int NT, const double4* pos, Grid g, int* key, int* v
 // cell_start (first sorted position of each cell): k_scan.cuh key_sort (counting sort)
 
 // Skinned LJ lists of a local atom (full, both directions), split at build time by what the
-// pair can need at evaluation time (atoms move < skin/2 between builds):
-//   near : r_b <= 3 r_max,max + skin     -> may need C_ij (r <= 3 r_max) or b* (r < 2^(1/6) sigma)
-//   pure : near < r_b <= r_lo(p) - skin  -> C = 1, Q = 1, S_taper = 1 guaranteed: plain 12-6 LJ
-//   band : the rest, r_b <= r_c + skin   -> C = 1, Q = 1, taper and cutoff tested per pair
-// One warp per atom; candidates stream over contiguous z-runs of the cell stencil and are
-// appended with warp-ballot compaction in candidate order (the paper's "inserting at once
-// multiple elements into a single neighbor list"), so lists are deterministic.
+// pair can need at evaluation time (atoms move < skin/2 between builds).  With
+// a_p = 2^(1/6) sigma_p sqrt(1 + 1e-9) the radius of the S_r window pre-filter (r^2 < a_p^2: the
+// pair may need b*) the evaluation splits the pairs by their CURRENT r^2:
+//   r^2 <  a_p^2 : k_lj_near (C_ij from the reach set; C = 0 skipped, otherwise the b* batch)
+//   r^2 >= a_p^2 : k_lj_far with C = 1; k_lj_near subtracts M V for the few pairs of its reach
+//                  set that lie there (E = (1 - M) V = C V, P:467 / P:473-477).
+// So the lists overlap in a shell of width 2 skin around a_p:
+//   list 0 (near): r_b <= a_p + skin                  (all pairs that can be inside the window)
+//   list 1 (far) : a_p - skin <= r_b <= r_c + skin    (all pairs that can be outside it)
+//   list 2       : unused (count 0)
+// The far row is ordered by distance bins of the build distance r_b, so the far kernel can skip,
+// or evaluate without the taper / cutoff / window tests, the bins that the current displacement
+// bound settles for the whole bin (FB_* below; edges relative to a_p, r_lo(p), r_c(p)):
+//   L_k (k < 8) : the overlap shell, r_b in [a - skin + k skin/4, a - skin + (k+1) skin/4) (= list-0 members)
+//   P           : a + skin < r_b < r_lo - skin      (always C = 1 zone, untapered: pure)
+//   A_k (k < 8) : r_lo - skin + k skin/8 <= r_b < r_lo - skin + (k+1) skin/8
+//   B           : r_lo <= r_b <= r_c
+//   C_k (k < 8) : r_c + k skin/8 < r_b <= r_c + (k+1) skin/8
+// Bins are filled in candidate order (stable counting sort per row), so rows are deterministic.
+// boff[a * FB_STRIDE + b] = end offset of bin b in atom a's far row.
+constexpr int FB_L0 = 0, FB_P = 8, FB_A0 = 9, FB_B = 17, FB_C0 = 18, FB_N = 26, FB_STRIDE = 32;
+
+// One warp per atom; candidates stream over contiguous z-runs of the cell stencil.  Near entries
+// are appended with warp-ballot compaction in candidate order (the paper's "inserting at once
+// multiple elements into a single neighbor list"); far entries are staged in shared
+// memory with their bin and written bin by bin.
 struct LJLists {
   int cap[3];
   int* cnt[3];
   int* nbr[3];
-  double near2;    // (3 r_max,max + skin)^2
-  double pure2[3]; // (r_lo(p) - skin)^2, or -1 if that band is empty
-  double bq2[3];   // (2^(1/6) sigma_p (1 + 1e-9) + skin)^2: canonical pairs that can become b*
+  unsigned short* boff;  // far-row bin ends [N][FB_STRIDE]
+  double flo2[3];  // (a_p - skin)^2 with a rounding margin (0 if a_p <= skin): lower end of the far list
+  double fa[3];    // a_p
+  double rlo[3], rc[3], rc2[3];
+  double skin;
+  double bq2[3];   // (a_p + skin)^2 with a rounding margin: the near list (canonical members bound the b* queue)
   int* bqcnt;      // [3] per species pair: bound of the b* candidate queue until the next build
   double reach;    // (r_c,max + skin) with a rounding margin: stencil culling radius
+  int fcap_smem;   // far entries staged per warp (= cap[1])
 };
+
+__device__ __forceinline__ int far_bin(const LJLists& Lg, int p, double r2, bool nearp) {
+  const double r = sqrt(r2), s = Lg.skin;
+  const double h2 = s * 0.25, h8 = s * 0.125;
+  auto kb = [](double x, double h) {
+    if (!(h > 0.0)) return 0;
+    double k = floor(x / h);
+    return k < 0.0 ? 0 : (k > 7.0 ? 7 : (int)k);
+  };
+  if (nearp) return FB_L0 + kb(r - (Lg.fa[p] - s), h2);
+  if (r < Lg.rlo[p] - s) return FB_P;
+  if (r < Lg.rlo[p]) return FB_A0 + kb(r - (Lg.rlo[p] - s), h8);
+  if (r2 <= Lg.rc2[p]) return FB_B;
+  return FB_C0 + kb(r - Lg.rc[p], h8);
+}
 
 // Stencil culling: a column (ax, ay) of cells is scanned only over the z-range of cells that
 // intersect the sphere of radius R around p (the full (2 nr + 1)^3 cube scans ~3x the sphere).
@@ -177,18 +215,24 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
                                                   const int* cell_start, const int* cell_atoms, int nr, LJLists Lg,
                                                   int* maxcnt) {
   __shared__ int s_cb[4][STENCIL_MAXCOL], s_pre[4][STENCIL_MAXCOL + 1];
+  __shared__ int s_hist[4][FB_N + 1];
+  extern __shared__ int s_dyn[];  // per warp: fcap_smem indices, then fcap_smem bin bytes
   int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= N) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int fcap = Lg.fcap_smem;
+  int* fJ = s_dyn + (size_t)w * ((fcap + 3) / 4) * 5;
+  unsigned char* fB = reinterpret_cast<unsigned char*>(fJ + fcap);
   const double4 p = pos[a];
   const int ta = type_of(p);
-  int n[3] = {0, 0, 0};
+  int n0 = 0, nf = 0;
   int nq[3] = {0, 0, 0};
   const long long ka = key_of(p);
-  int* row[3];
-  for (int c = 0; c < 3; ++c) row[c] = Lg.nbr[c] + (size_t)a * Lg.cap[c];
+  int* row0 = Lg.nbr[0] + (size_t)a * Lg.cap[0];
   int* cb = s_cb[w];
   int* pre = s_pre[w];
+  int* hist = s_hist[w];
+  if (lane <= FB_N) hist[lane] = 0;
   const int total = stencil_columns(g, p, nr, Lg.reach, cell_start, cb, pre);
   int k = 0;  // column of the chunk's first candidate (warp-uniform)
   // software pipeline: the next chunk's index and position loads are in flight while this
@@ -210,23 +254,62 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
       pr = ta + type_of(pb);
     }
     const bool in = ok && r2 <= c_geo.rc_s2[pr];
-    const bool nearp = in && r2 <= Lg.near2;
-    const bool purep = in && !nearp && r2 <= Lg.pure2[pr];
-    const bool bandp = in && !nearp && !purep;
-    warp_append(nearp, row[0], Lg.cap[0], n[0], b);
-    warp_append(purep, row[1], Lg.cap[1], n[1], b);
-    warp_append(bandp, row[2], Lg.cap[2], n[2], b);
-    const bool bq = nearp && r2 <= Lg.bq2[pr] && ka < key_of(pb);
+    const bool nearp = in && r2 <= Lg.bq2[pr];
+    const bool farp = in && r2 >= Lg.flo2[pr];
+    warp_append(nearp, row0, Lg.cap[0], n0, b);
+    {  // stage far entries with their bin (candidate order); histogram: one add per distinct bin
+      const unsigned m = __ballot_sync(0xffffffffu, farp);
+      const int slot = nf + __popc(m & ((1u << lane) - 1u));
+      const bool st = farp && slot < fcap;
+      const int bin = st ? far_bin(Lg, pr, r2, nearp) : FB_N + lane;
+      const unsigned grp = __match_any_sync(0xffffffffu, bin);
+      if (st) {
+        fJ[slot] = b, fB[slot] = (unsigned char)bin;
+        if ((grp & ((1u << lane) - 1u)) == 0u) hist[bin] += __popc(grp);
+      }
+      __syncwarp();
+      nf += __popc(m);
+    }
+    const bool bq = nearp && ka < key_of(pb);
 #pragma unroll
     for (int t = 0; t < 3; ++t) nq[t] += __popc(__ballot_sync(0xffffffffu, bq && pr == t));
     b = bn, pb = pbn, k = kn;
   }
-  if (lane == 0) {
-    for (int c = 0; c < 3; ++c) {
-      Lg.cnt[c][a] = n[c];
-      atomicMax(maxcnt + c, n[c]);
-      if (nq[c]) atomicAdd(Lg.bqcnt + c, nq[c]);
+  __syncwarp();
+  // bin ends (inclusive scan of the histogram) and the stable scatter of the staged entries
+  const int nfs = min(nf, fcap);
+  if (nf <= Lg.cap[1]) {
+    int hv = lane < FB_N ? hist[lane] : 0;
+    int incl = hv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
     }
+    if (lane < FB_N) Lg.boff[(size_t)a * FB_STRIDE + lane] = (unsigned short)incl;
+    __syncwarp();
+    if (lane < FB_N) hist[lane] = incl - hv;  // running cursor per bin
+    __syncwarp();
+    int* row1 = Lg.nbr[1] + (size_t)a * Lg.cap[1];
+    for (int c0 = 0; c0 < nfs; c0 += 32) {
+      const int q = c0 + lane;
+      const int bin = q < nfs ? (int)fB[q] : FB_N + lane;  // out-of-range lanes in groups of their own
+      const unsigned grp = __match_any_sync(0xffffffffu, bin);
+      const int rank = __popc(grp & ((1u << lane) - 1u));
+      if (q < nfs) row1[hist[bin] + rank] = fJ[q];
+      __syncwarp();
+      if (q < nfs && rank == 0) hist[bin] += __popc(grp);
+      __syncwarp();
+    }
+  }
+  if (lane == 0) {
+    Lg.cnt[0][a] = n0;
+    Lg.cnt[1][a] = nf;
+    Lg.cnt[2][a] = 0;
+    atomicMax(maxcnt + 0, n0);
+    atomicMax(maxcnt + 1, nf);
+    for (int c = 0; c < 3; ++c)
+      if (nq[c]) atomicAdd(Lg.bqcnt + c, nq[c]);
   }
 }
 

@@ -3,21 +3,23 @@
 //
 // Both kernels stream FULL skinned lists (both directions): every pair is evaluated from both
 // ends, so F_i is a register gather with one atomic per atom and nothing is scattered onto j.
-// The lists are split at build time (k_build_lj) by what a pair can need at evaluation time:
+// The pairs are split by their current distance against a_p = 2^(1/6) sigma_p sqrt(1 + 1e-9), the
+// S_r window pre-filter (k_lists.cuh: near list r_b <= a_p + skin, far list r_b >= a_p - skin):
 //
-// k_lj_near -- 8 lanes per local atom i (4 atoms per warp), near list (r_b <= 3 r_max + skin).
+// k_lj_near -- 8 lanes per local atom i (4 atoms per warp).
 //   The lane group first maps out every atom image reachable from i in 1, 2 or 3 bonds with the
 //   maximum path-weight product M (the paper's "map out all the atoms j connected to atom i
 //   once") into a 64-slot open-addressing table in shared memory (keys = image
 //   index, value = M via atomicMax on its bit pattern, M >= 0).  Overflow (table or 2-hop list)
 //   -> the direct nested search of P:844-853 for that atom (the paper's "sequential fallback",
-//   P:866).  Per pair: cutoff, C = 1 - M (lookup within 3 r_max), skip if C == 0 (gate order of
-//   P:824-830), pairs inside the S_r window are deferred to the b* batch (canonical direction
-//   only), others give E/2 = C V/2 and the pair force on i.  Forces from dC
-//   (0 < C < 1, reactive systems only) are applied once, by the canonical direction.
-// k_lj_far -- one warp per local atom i, pure + band lists: C = Q = 1 guaranteed by the build.
-//   No shared memory, branch-free bodies (taper evaluated for every band lane and selected),
-//   4 independent gathers in flight per lane.
+//   P:866).  Window pairs (r^2 < a_p^2): C = 1 - M, skip if C == 0 (gate order of P:824-830),
+//   otherwise deferred to the b* batch (canonical direction only).  Then the reach set
+//   is walked once more: for its members J in the far zone (r^2 >= a_p^2, r <= r_c), which
+//   k_lj_far evaluated with C = 1, i subtracts M V (E = C V = V - M V) and the force of
+//   it; forces from dC (0 < M < 1, reactive systems only) once, by the canonical direction.
+// k_lj_far -- one warp per local atom i over the far row (C = 1; distance bins decide per bin
+//   whether a pair needs the window / cutoff tests and the taper, or can be skipped).
+//   No shared memory, branch-free bodies, 4 independent gathers in flight per lane.
 // Counters count canonical directions only (key_i < key_J), so they equal the oracle's half sums.
 #pragma once
 #include "dev_common.cuh"
@@ -126,6 +128,11 @@ struct LJArgs {
   int cap[3];
   const int* cnt[3];
   const int* nbr[3];
+  const unsigned short* boff;          // far-row bin ends (k_lists.cuh FB_*)
+  const double4* xref;                 // positions at the last build (per-atom displacement)
+  const unsigned long long* dbound;    // bits of max displacement^2 of any atom since the build (nullptr: skin/2)
+  double skin;
+  int binned;                          // 0: every far entry through the fully tested body
 };
 
 __device__ __forceinline__ void stage_lj_row(StageBuf stage, int gi, int gj, char4 sh, double C, double bs) {
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 #ifdef AB_ABL_NOREACH
   const int ni = 0;  // ablation (timing experiments only): no reach set
 #else
-  const int ni = cntN > 0 ? S.cnt[i] : 0;
+  const int ni = active ? S.cnt[i] : 0;
 #endif
   // Flattened walk: level 1 (k in N(i)) one lane per k; level 2 (l in N(k)) the (k, l) pairs are
   // spread over the group's lanes (the owner lane of pair e found by a binary search over the
@@ -286,18 +293,18 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   __syncwarp();
   const bool ovf = s.ovf != 0;
 
-  // 2. pairs.  The next entry's index and position are loaded before the current one is
-  // processed (two gathers in flight per lane).  Pairs that may lie in the S_r window
-  // (r^2 < (2^(1/6) sigma)^2 (1 + 1e-9), a superset of S_r != 0) are not evaluated here: the
-  // canonical side queues them and the b* batch takes the exact fp64 window decision and
-  // evaluates the whole pair (b* if S_r != 0, else the plain gated LJ) for both atoms.
+  // 2. window pairs (near list, r^2 < a_p^2 now).  The next entry's index and position are loaded
+  // before the current one is processed.  A pair with C_ij = 0 is skipped (Alg. 3); every other
+  // pair may have S_r != 0: the canonical side queues it and the b* batch takes the exact fp64
+  // window decision and evaluates the whole pair (b* if S_r != 0, else the plain gated LJ) for
+  // both atoms.  No LJ arithmetic here.
   double fx = 0, fy = 0, fz = 0, en = 0;
   double W[6] = {0, 0, 0, 0, 0, 0};
   unsigned nlj = 0, nc0 = 0;
+  const double4 pi = A.pos[active ? i : 0];
+  const int ti = type_of(pi);
+  const long long ki = key_of(pi);
   if (cntN > 0) {
-    const double4 pi = A.pos[i];
-    const int ti = type_of(pi);
-    const long long ki = key_of(pi);
     const int* row = A.nbr[0] + (size_t)i * A.cap[0];
     int Jn = gl < cntN ? row[gl] : i;
     double4 pjn = A.pos[Jn];
@@ -311,42 +318,16 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
       const double r2 = r2_exact(dx, dy, dz);
       const int p = ti + type_of(pj);
-      const bool inr = r2 <= pd[p];
+      const bool inw = r2 < pd[3 + p];  // window zone (a_p < r_c: inside the cutoff)
       const bool canon = ki < key_of(pj);
       double Md = 0.0;
 #ifndef AB_ABL_NOLOOKUP
-      if (inr && r2 <= c_geo.reach2) Md = ovf ? (double)path_search(S, i, J).M : reach_lookup_fast(s, J);
+      if (inw && r2 <= c_geo.reach2) Md = ovf ? (double)path_search(S, i, J).M : reach_lookup_fast(s, J);
 #endif
-      const bool c0 = Md == 1.0;  // C_ij == 0 (Alg. 3 "continue")
-      const bool cand = inr && !c0 && r2 < pd[3 + p];  // possible S_r != 0: b* batch
-      const bool norm = inr && !c0 && !cand;
-      nlj += inr && canon;
+      const bool c0 = inw && Md == 1.0;  // C_ij == 0 (Alg. 3 "continue")
+      const bool cand = inw && !c0;
+      nlj += inw && canon;
       nc0 += c0 && canon;
-      // LJ for every lane (weight 0 unless norm)
-      R rr2 = norm ? (R)r2 : R(1);
-      // 1/r^2 by a reciprocal for the 12-6 form (1/r only for Morse and the rare taper)
-      R y = MORSE ? rsqrt_fast(rr2) : R(0);
-      R dVr;
-      R V = MORSE ? morse_plain<R>(pr_[p], pr_[3 + p], pm_[p], rr2 * y, y, dVr)
-                  : lj_plain<R>(pr_[p], pr_[3 + p], rcp_fast(rr2), dVr);
-      if (norm && r2 > pd[6 + p]) {  // taper S(r; r_lo, r_c) (reading A10): rare in the near list
-        if (!MORSE) y = rsqrt_fast(rr2);
-        R r = rr2 * y, dsw;
-        R sv = sw<R>(r, pr_[6 + p], pr_[9 + p], dsw);
-        dVr = dVr * sv + V * dsw * y;
-        V = V * sv;
-      }
-      R C = norm ? (R)(1.0 - Md) : R(0);  // 1 - M in fp64 (gate, reading A14)
-      R fr = C * dVr;  // F_i += fr d  (E(d), d = x_j - x_i)
-      fx = acc_round<SG>(fx + (double)(fr * (R)dx));
-      fy = acc_round<SG>(fy + (double)(fr * (R)dy));
-      fz = acc_round<SG>(fz + (double)(fr * (R)dz));
-      en = acc_round<SG>(en + (double)(C * V));
-      if (VIRIAL) {
-        V3<R> dd = mk3<R>((R)dx, (R)dy, (R)dz);
-        vir_add(W, dd, (R(0.5) * fr) * dd);
-      }
-      // rare work last
       if (cand && canon) {  // deferred to the b* batch: the whole pair, once, by the canonical side
 #if AB_NEAR_BLOCKQ
         // staged in the block's shared-memory queue, flushed with one global atomic per species
@@ -379,15 +360,62 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
         }
 #endif
       }
-      if (norm && canon && Md > 0.0) {  // 0 < C < 1: dC/dx along the maximising path, once per pair
-        PathRes<R> pr = path_search(S, i, J);
+      if (VIRIAL && stage.rows && canon && c0) stage_lj_row(stage, gid[i], gid[J], shift[J], 0.0, 0.0);
+    }
+  }
+
+  // 3. reach-set correction of the far-zone pairs (r^2 >= a_p^2, r <= r_c): k_lj_far evaluated
+  // them with C = 1, the pair's share is C V = V - M V, so i subtracts M V (and its force) for
+  // every image J of its reach set there; forces from dC/dx along the maximising path (0 < M < 1)
+  // once, by the canonical side.  The table holds every reachable image unless it overflowed;
+  // then the far row is scanned with the nested path search (P:866's sequential fallback).
+  if (active) {
+    auto correct = [&](int J, double Md) {
+      const double4 pj = A.pos[J];
+      const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
+      const double r2 = r2_exact(dx, dy, dz);
+      const int p = ti + type_of(pj);
+      if (!(r2 >= pd[3 + p] && r2 <= pd[p])) return;
+      const bool canon = ki < key_of(pj);
+      R dVr;
+      const R V = lj_v<R>(p, (R)r2, r2, dVr);
+      const R fr = -(R)Md * dVr;
+      fx = acc_round<SG>(fx + (double)(fr * (R)dx));
+      fy = acc_round<SG>(fy + (double)(fr * (R)dy));
+      fz = acc_round<SG>(fz + (double)(fr * (R)dz));
+      en = acc_round<SG>(en - (double)((R)Md * V));
+      if (VIRIAL) {
+        V3<R> dd = mk3<R>((R)dx, (R)dy, (R)dz);
+        vir_add(W, dd, (R(0.5) * fr) * dd);
+      }
+      nc0 += Md == 1.0 && canon;
+      if (canon && Md < 1.0) {  // 0 < C < 1: dC/dx along the maximising path, once per pair
+        PathRes<R> prs = path_search(S, i, J);
         double Wp[6] = {0, 0, 0, 0, 0, 0};
-        path_forces<R, SG>(S, owner, pr, -V, F, Wp);
+        path_forces<R, SG>(S, owner, prs, -V, F, Wp);
         if (VIRIAL)
           for (int c = 0; c < 6; ++c) W[c] += Wp[c];
       }
-      if (VIRIAL && stage.rows && canon && inr && norm) stage_lj_row(stage, gid[i], gid[J], shift[J], (double)C, 0.0);
-      if (VIRIAL && stage.rows && canon && inr && c0) stage_lj_row(stage, gid[i], gid[J], shift[J], 0.0, 0.0);
+      if (VIRIAL && stage.rows && canon) stage_lj_row(stage, gid[i], gid[J], shift[J], 1.0 - Md, 0.0);
+    };
+    if (!ovf) {
+      for (int q = gl; q < NEAR_SLOTS; q += NEAR_GROUP) {
+        const int J = s.keys[q];
+        if (J == REACH_EMPTY) continue;
+        const double Md = __longlong_as_double((long long)s.mbits[q]);
+        if (Md > 0.0) correct(J, Md);
+      }
+    } else {
+      const int* row1 = A.nbr[1] + (size_t)i * A.cap[1];
+      const int c1 = A.cnt[1][i];
+      for (int q = gl; q < c1; q += NEAR_GROUP) {
+        const int J = row1[q];
+        const double4 pj = A.pos[J];
+        const double r2 = r2_exact(__dsub_rn(pj.x, pi.x), __dsub_rn(pj.y, pi.y), __dsub_rn(pj.z, pi.z));
+        if (r2 > c_geo.reach2) continue;
+        const double Md = (double)path_search(S, i, J).M;
+        if (Md > 0.0) correct(J, Md);
+      }
     }
   }
 
@@ -395,7 +423,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   fx = group_sum<NEAR_GROUP, SG>(fx);
   fy = group_sum<NEAR_GROUP, SG>(fy);
   fz = group_sum<NEAR_GROUP, SG>(fz);
-  if (gl == 0 && cntN > 0) atomic_add3<SG>(F, i, fx, fy, fz);
+  if (gl == 0 && active) atomic_add3<SG>(F, i, fx, fy, fz);
 #if AB_NEAR_BLOCKQ
   // flush the block's b* candidates: one global atomic per species pair
   __syncthreads();
@@ -430,37 +458,115 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 }
 
 // ---------------------------------------------------------------------------------- far pairs
+// One warp per local atom i over its far row (pairs with r^2 >= a_p^2 at evaluation time, C = 1;
+// k_lj_near corrects the reach-set pairs among them).  The row is ordered by build-distance bins
+// (k_lists.cuh); with m = |x_i - x_i,build| + max_k |x_k - x_k,build| (+1e-7) every pair distance
+// is within m of its build distance, which settles whole bins:
+//   L bins entirely below a_p             -> skipped (k_lj_near's pairs)
+//   L bins straddling a_p                 -> LOW body: exact r^2, window test, no taper / cutoff
+//   L bins above a_p, P, A bins below r_lo -> PURE body: no decisions (fused r^2, no taper)
+//   A bins reaching r_lo, B, C bins        -> HIGH body: exact r^2, window + cutoff tests, taper
+//   C bins entirely beyond r_c            -> skipped
+// Branch-free bodies (out-of-range lanes weighted by 0), 4 independent gathers in flight per lane;
+// the taper (half-cosine polynomial) only runs when some lane of the warp is in the taper band.
 #ifndef AB_FAR_UNROLL
 #define AB_FAR_UNROLL 4
 #endif
 constexpr int FAR_UNROLL = AB_FAR_UNROLL;
 
-template <typename R, bool VIRIAL, bool BAND, bool MORSE, bool SG = false>
-__device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, double4 pi, int ti, long long ki,
-                                         const int* gid, const char4* shift, StageBuf stage, double& fx, double& fy,
-                                         double& fz, double& en, double (&W)[6], unsigned& nlj, unsigned& ntp) {
-  const Tab<R>& T = tab<R>();
+// one far entry (a lane of a 32-entry chunk).  PURE: settled by the bins (no decision, r^2 may be
+// fused, no taper); GEN: exact (un-fused) window / cutoff decisions as the oracle's, and the taper
+// S(r; r_lo, r_c) (reading A10) evaluated only when some lane of the warp is in the taper band.
+template <typename R, bool VIRIAL, bool PURE, bool MORSE>
+struct FarPar {
+  R e4a, e4b, s2a, s2b, rea, reb, rloa, rlob, iva, ivb;
+  double rca, rcb, sha, shb, rla, rlb, tva, tvb;
+  __device__ __forceinline__ FarPar(int ti) {
+    const Tab<R>& T = tab<R>();
+    e4a = MORSE ? T.meps[ti] : R(4) * T.eps[ti], e4b = MORSE ? T.meps[ti + 1] : R(4) * T.eps[ti + 1];
+    s2a = MORSE ? T.malpha[ti] : T.sigma2[ti], s2b = MORSE ? T.malpha[ti + 1] : T.sigma2[ti + 1];
+    rea = MORSE ? T.mre[ti] : R(0), reb = MORSE ? T.mre[ti + 1] : R(0);
+    rloa = T.rlo[ti], rlob = T.rlo[ti + 1];
+    iva = T.inv_taper[ti], ivb = T.inv_taper[ti + 1];
+    rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
+    sha = c_geo.srhi2_hi[ti], shb = c_geo.srhi2_hi[ti + 1];
+    rla = c_geo.rlo2[ti], rlb = c_geo.rlo2[ti + 1];
+    // taper vote threshold: a little below r_lo^2 (the exact decision is t <= 0 below)
+    tva = rla * (1.0 - 1e-9), tvb = rlb * (1.0 - 1e-9);
+  }
+};
+
+template <typename R, bool VIRIAL, bool PURE, bool MORSE, bool SG>
+__device__ __forceinline__ void far_entry(const FarPar<R, VIRIAL, PURE, MORSE>& P, bool valid, double4 pj, int J, int i,
+                                          double4 pi, long long ki, const int* gid, const char4* shift,
+                                          StageBuf stage, double& fx, double& fy, double& fz, double& en,
+                                          double (&W)[6], unsigned& nlj, unsigned& ntp) {
+  const bool hj = type_of(pj) != 0;
+  const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
+  const double r2 = PURE ? fma(dz, dz, fma(dy, dy, dx * dx)) : r2_exact(dx, dy, dz);
+  bool in = valid;
+  if (!PURE) in = in && r2 >= (hj ? P.shb : P.sha) && r2 <= (hj ? P.rcb : P.rca);
+  const bool canon = ki < key_of(pj);
+  nlj += (in && canon);
+  // taper-band pairs (algorithmic flop count): counted by the virial (ab_compute) instantiation only
+  if (!PURE && VIRIAL) ntp += (in && canon && r2 > (hj ? P.rlb : P.rla));
+  const R rr2 = in ? (R)r2 : R(1);
+  R dVr, V;
+  if (MORSE) {
+    const R y = rsqrt_fast(rr2);
+    V = morse_plain<R>(hj ? P.e4b : P.e4a, hj ? P.s2b : P.s2a, hj ? P.reb : P.rea, rr2 * y, y, dVr);
+  } else {
+    V = lj_plain<R>(hj ? P.e4b : P.e4a, hj ? P.s2b : P.s2a, rcp_fast(rr2), dVr);
+  }
+  if (!PURE) {
+    const bool tap = in && r2 > (hj ? P.tvb : P.tva);
+    if (__any_sync(0xffffffffu, tap)) {
+      const R y = rsqrt_fast(rr2);
+      const R r = rr2 * y;
+      const R iv = hj ? P.ivb : P.iva;
+      const R tt = (r - (hj ? P.rlob : P.rloa)) * iv;
+      R sv, ds;
+      halfcos_poly(tt < R(0) ? R(0) : tt, sv, ds);
+      sv = tt <= R(0) ? R(1) : sv;
+      ds = tt <= R(0) ? R(0) : ds * iv;
+      dVr = dVr * sv + V * ds * y;
+      V = V * sv;
+    }
+  }
+  dVr = in ? dVr : R(0);
+  V = in ? V : R(0);
+  const R rx = (R)dx, ry = (R)dy, rz = (R)dz;
+  fx = acc_round<SG>(fx + (double)(dVr * rx));
+  fy = acc_round<SG>(fy + (double)(dVr * ry));
+  fz = acc_round<SG>(fz + (double)(dVr * rz));
+  en = acc_round<SG>(en + (double)V);
+  if (VIRIAL) {
+    V3<R> dd = mk3<R>(rx, ry, rz);
+    vir_add(W, dd, (R(0.5) * dVr) * dd);
+  }
+  if (VIRIAL && stage.rows && in && canon) stage_lj_row(stage, gid[i], gid[J], shift[J], 1.0, 0.0);
+}
+
+// the far row [s0, s3) as one stream of 32-entry chunks, FAR_UNROLL chunks per iteration (their
+// gathers in flight together, the next iteration's indices loaded one iteration ahead); a chunk
+// entirely inside the PURE range [s1, s2) takes the pure body (warp-uniform branch)
+template <typename R, bool VIRIAL, bool MORSE, bool SG>
+__device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, int s2, int s3, double4 pi, int ti,
+                                        long long ki, const int* gid, const char4* shift, StageBuf stage,
+                                        double& fx, double& fy, double& fz, double& en, double (&W)[6],
+                                        unsigned& nlj, unsigned& ntp) {
+  if (s0 >= s3) return;
   const int lane = threadIdx.x & 31;
-  const int cnt = A.cnt[list][i];
-  const int* row = A.nbr[list] + (size_t)i * A.cap[list];
-  // t_i is warp-uniform, so a pair is one of two species pairs: hold both parameter sets in
-  // registers and select (no divergent constant-cache loads in the loop)
-  const R e4a = MORSE ? T.meps[ti] : R(4) * T.eps[ti], e4b = MORSE ? T.meps[ti + 1] : R(4) * T.eps[ti + 1];
-  const R s2a = MORSE ? T.malpha[ti] : T.sigma2[ti], s2b = MORSE ? T.malpha[ti + 1] : T.sigma2[ti + 1];
-  const R rea = MORSE ? T.mre[ti] : R(0), reb = MORSE ? T.mre[ti + 1] : R(0);
-  const R rloa = T.rlo[ti], rlob = T.rlo[ti + 1];
-  const R iva = T.inv_taper[ti], ivb = T.inv_taper[ti + 1];
-  const double rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
-  const double rla = VIRIAL ? c_geo.rlo2[ti] : 0.0, rlb = VIRIAL ? c_geo.rlo2[ti + 1] : 0.0;
-  // the next chunk's list indices are loaded one iteration ahead: the position gathers of a
-  // chunk then wait on one memory latency, not on two dependent ones
+  const int* row = A.nbr[1] + (size_t)i * A.cap[1];
+  const FarPar<R, VIRIAL, true, MORSE> PP(ti);
+  const FarPar<R, VIRIAL, false, MORSE> PG(ti);
   int Jn[FAR_UNROLL];
 #pragma unroll
   for (int u = 0; u < FAR_UNROLL; ++u) {
-    int q = u * 32 + lane;
-    Jn[u] = q < cnt ? row[q] : -1;
+    const int q = s0 + u * 32 + lane;
+    Jn[u] = q < s3 ? row[q] : -1;
   }
-  for (int base = 0; base < cnt; base += 32 * FAR_UNROLL) {
+  for (int base = s0; base < s3; base += 32 * FAR_UNROLL) {
     int J[FAR_UNROLL];
     double4 pj[FAR_UNROLL];
 #pragma unroll
@@ -469,54 +575,51 @@ __device__ __forceinline__ void far_list(const LJArgs& A, int list, int i, doubl
     for (int u = 0; u < FAR_UNROLL; ++u) pj[u] = A.pos[J[u] >= 0 ? J[u] : i];
 #pragma unroll
     for (int u = 0; u < FAR_UNROLL; ++u) {
-      int q = base + 32 * FAR_UNROLL + u * 32 + lane;
-      Jn[u] = q < cnt ? row[q] : -1;
+      const int q = base + 32 * FAR_UNROLL + u * 32 + lane;
+      Jn[u] = q < s3 ? row[q] : -1;
     }
-    // branch-free bodies: every lane evaluates, invalid / out-of-cutoff lanes are weighted by 0
 #pragma unroll
     for (int u = 0; u < FAR_UNROLL; ++u) {
-      const bool valid = J[u] >= 0;
-      const bool hj = type_of(pj[u]) != 0;
-      double dx = __dsub_rn(pj[u].x, pi.x), dy = __dsub_rn(pj[u].y, pi.y), dz = __dsub_rn(pj[u].z, pi.z);
-      // pure entries are inside r_lo <= r_c by construction (no decision: r^2 may be fused);
-      // band entries: exact (un-fused) cutoff decision, as the oracle's
-      double r2 = BAND ? r2_exact(dx, dy, dz) : fma(dz, dz, fma(dy, dy, dx * dx));
-      bool in = valid && (!BAND || r2 <= (hj ? rcb : rca));
-      nlj += (in && ki < key_of(pj[u]));
-      // taper-band pairs (algorithmic flop count): counted by the virial (ab_compute) instantiation
-      // only -- in the NVE kernel the extra compare costs ~20 % of the far kernel (measured)
-      if (BAND && VIRIAL) ntp += (in && ki < key_of(pj[u]) && r2 > (hj ? rlb : rla));
-      R rr2 = in ? (R)r2 : R(1);
-      R y = (BAND || MORSE) ? rsqrt_fast(rr2) : R(0);  // 1/r (taper / Morse only)
-      R dVr;
-      R V = MORSE ? morse_plain<R>(hj ? e4b : e4a, hj ? s2b : s2a, hj ? reb : rea, rr2 * y, y, dVr)
-                  : lj_plain<R>(hj ? e4b : e4a, hj ? s2b : s2a, BAND ? y * y : rcp_fast(rr2), dVr);
-      if (BAND) {  // taper S(r; r_lo, r_c) (reading A10), branch-free
-        R r = rr2 * y;
-        R iv = hj ? ivb : iva;
-        R tt = (r - (hj ? rlob : rloa)) * iv;
-        R sv, ds;
-        halfcos_poly(tt < R(0) ? R(0) : tt, sv, ds);
-        sv = tt <= R(0) ? R(1) : sv;
-        ds = tt <= R(0) ? R(0) : ds * iv;
-        dVr = dVr * sv + V * ds * y;
-        V = V * sv;
-      }
-      R wgt = in ? R(1) : R(0);
-      dVr *= wgt;
-      V *= wgt;
-      R rx = (R)dx, ry = (R)dy, rz = (R)dz;
-      fx = acc_round<SG>(fx + (double)(dVr * rx));
-      fy = acc_round<SG>(fy + (double)(dVr * ry));
-      fz = acc_round<SG>(fz + (double)(dVr * rz));
-      en = acc_round<SG>(en + (double)V);
-      if (VIRIAL) {
-        V3<R> dd = mk3<R>(rx, ry, rz);
-        vir_add(W, dd, (R(0.5) * dVr) * dd);
-      }
-      if (VIRIAL && stage.rows && in && ki < key_of(pj[u])) stage_lj_row(stage, gid[i], gid[J[u]], shift[J[u]], 1.0, 0.0);
+      const int c0 = base + 32 * u;
+      if (c0 >= s3) break;
+      if (c0 >= s1 && c0 + 32 <= s2)
+        far_entry<R, VIRIAL, true, MORSE, SG>(PP, J[u] >= 0, pj[u], J[u], i, pi, ki, gid, shift, stage, fx, fy, fz,
+                                              en, W, nlj, ntp);
+      else
+        far_entry<R, VIRIAL, false, MORSE, SG>(PG, J[u] >= 0, pj[u], J[u], i, pi, ki, gid, shift, stage, fx, fy, fz,
+                                               en, W, nlj, ntp);
     }
   }
+}
+
+// warp-uniform segment bounds of atom i's far row: [s0, s1) LOW, [s1, s2) PURE, [s2, s3) HIGH
+__device__ __forceinline__ void far_segments(const LJArgs& A, int i, double4 pi, int& s0, int& s1, int& s2, int& s3) {
+  const int lane = threadIdx.x & 31;
+  const int cnt = A.cnt[1][i];
+  if (!A.binned) {
+    s0 = s1 = s2 = 0, s3 = cnt;
+    return;
+  }
+  const int endv = lane < FB_N ? (int)A.boff[(size_t)i * FB_STRIDE + lane] : cnt;
+  auto start = [&](int b) {
+    const int v = __shfl_sync(0xffffffffu, endv, b > 0 ? b - 1 : 0);
+    return b > 0 ? v : 0;
+  };
+  const double4 xr = A.xref[i];
+  const double ex = pi.x - xr.x, ey = pi.y - xr.y, ez = pi.z - xr.z;
+  const double di = sqrt(ex * ex + ey * ey + ez * ez);
+  const double D = A.dbound ? sqrt(__longlong_as_double((long long)*A.dbound)) : 0.5 * A.skin;
+  const double m = di + D + 1e-7, skin = A.skin, h2 = 0.25 * skin, h8 = 0.125 * skin;
+  int kL0 = 0, kL1, kA = 0, kC = 0;
+  while (kL0 < 8 && (kL0 + 1) * h2 + m <= skin) ++kL0;  // L bins entirely below a_p
+  kL1 = kL0;
+  while (kL1 < 8 && !(kL1 * h2 - m >= skin)) ++kL1;     // first L bin entirely above a_p
+  while (kA < 8 && (kA + 1) * h8 + m <= skin) ++kA;     // A bins entirely below r_lo
+  while (kC < 8 && !(kC * h8 - m >= 0.0)) ++kC;         // first C bin entirely beyond r_c
+  s0 = start(FB_L0 + kL0);
+  s1 = start(FB_L0 + kL1);
+  s2 = start(FB_A0 + kA);
+  s3 = kC < 8 ? start(FB_C0 + kC) : cnt;
 }
 
 template <typename R, bool VIRIAL, bool MORSE, bool SG = false, bool RANGED = false>
@@ -542,14 +645,15 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     const double4 pi = A.pos[i];
     const int ti = type_of(pi);
     const long long ki = key_of(pi);
+    int s0, s1, s2, s3;
+    far_segments(A, i, pi, s0, s1, s2, s3);
     double fx = 0, fy = 0, fz = 0;
-    far_list<R, VIRIAL, false, MORSE, SG>(A, 1, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
-    far_list<R, VIRIAL, true, MORSE, SG>(A, 2, i, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
+    far_row<R, VIRIAL, MORSE, SG>(A, i, s0, s1, s2, s3, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
     fx = warp_sum<SG>(fx);
     fy = warp_sum<SG>(fy);
     fz = warp_sum<SG>(fz);
     if (lane == 0) atomic_add3<SG>(F, i, fx, fy, fz);
-    if (lane == 0) ne += (unsigned long long)(A.cnt[1][i] + A.cnt[2][i]);
+    if (lane == 0) ne += (unsigned long long)(s3 - s0);
   }
   }
   red_add_d(rs, ACC_ELJ, 0.5 * en);

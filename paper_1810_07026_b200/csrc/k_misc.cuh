@@ -6,7 +6,7 @@
 namespace ab {
 
 // block-wide max of non-negative doubles, one atomic per block (bit-pattern order == value order)
-__device__ __forceinline__ void block_max_atomic(double v, unsigned long long* out) {
+__device__ __forceinline__ void block_max_atomic(double v, unsigned long long* out, unsigned long long* out2 = nullptr) {
   __shared__ double sm[32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -18,6 +18,7 @@ __device__ __forceinline__ void block_max_atomic(double v, unsigned long long* o
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (l == 0 && v > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(v));
+    if (out2 && l == 0 && v > 0.0) atomicMax(out2, (unsigned long long)__double_as_longlong(v));
   }
 }
 
@@ -34,7 +35,7 @@ __device__ __forceinline__ double drift(double x, double dt, double v, bool r32)
 
 // v += dt/2 F/m ftm2v;  x += dt v;  max |x - x_ref|^2 since the last list build
 __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, double dtf0, double dtf1, double dt,
-                             const double4* xref, unsigned long long* maxd2, bool r32) {
+                             const double4* xref, unsigned long long* maxd2, unsigned long long* dbound, bool r32) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (i < N) {
@@ -50,7 +51,7 @@ __global__ void k_integrate1(int N, double4* pos, double* v, const double* F, do
     double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
     d2 = dx * dx + dy * dy + dz * dz;
   }
-  block_max_atomic(d2, maxd2);
+  block_max_atomic(d2, maxd2, dbound);
 }
 
 // Rebuild flags straight to the host: the last block to finish (ticket) copies the maximal
@@ -90,8 +91,8 @@ __device__ __forceinline__ void publish_flags(const FlagOut& fo, unsigned long l
 // rebuild laid out contiguously at NB + goff[i] (k_image_fill), with k_image_update's operations.
 __global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, bool pre, double pd0, double pd1,
                                  double dtf0, double dtf1, double dt,
-                                 const double4* xref, unsigned long long* maxd2, int NB, const int* goff,
-                                 const int* gcnt, const char4* rshift, FlagOut fo, bool r32) {
+                                 const double4* xref, unsigned long long* maxd2, unsigned long long* dbound, int NB,
+                                 const int* goff, const int* gcnt, const char4* rshift, FlagOut fo, bool r32) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (i < N) {
@@ -132,7 +133,7 @@ __global__ void k_integrate1_img(int N, double4* pos, double* v, double* F, bool
       if (k < ng) image(g0 + k, sh[k]);
     for (int k = IMG_PRE; k < ng; ++k) image(g0 + k, rshift[g0 + k]);
   }
-  block_max_atomic(d2, maxd2);
+  block_max_atomic(d2, maxd2, dbound);
   if (fo.host) publish_flags(fo, maxd2);
 }
 
@@ -168,7 +169,8 @@ __global__ void k_post(RedRows R, int nrows, double* acc, unsigned long long* ct
   v[3 * i + 2] = kick(v[3 * i + 2], dtf, F[3 * i + 2], r32);
 }
 
-__global__ void k_maxdisp(int N, const double4* pos, const double4* xref, unsigned long long* maxd2) {
+__global__ void k_maxdisp(int N, const double4* pos, const double4* xref, unsigned long long* maxd2,
+                          unsigned long long* dbound) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double d2 = 0.0;
   if (i < N) {
@@ -176,7 +178,7 @@ __global__ void k_maxdisp(int N, const double4* pos, const double4* xref, unsign
     double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
     d2 = dx * dx + dy * dy + dz * dz;
   }
-  block_max_atomic(d2, maxd2);
+  block_max_atomic(d2, maxd2, dbound);
 }
 
 // sum m v^2 / 2 (mvv2e applied on the host)
