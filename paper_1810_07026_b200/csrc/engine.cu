@@ -379,12 +379,19 @@ __global__ void k_fma_peak(T* out, int iters, T a, T b) {
       return e_ == cudaErrorMemoryAllocation ? AB_E_OOM : AB_E_CUDA;                      \
     }                                                                                     \
   } while (0)
+// AB_DEBUG_SYNC=1 (diagnostics only): synchronise after every launch and name the source line
+static bool debug_sync() {
+  static int v = -1;
+  if (v < 0) v = std::getenv("AB_DEBUG_SYNC") && std::getenv("AB_DEBUG_SYNC")[0] == '1';
+  return v == 1;
+}
 #define CKL()                                                                             \
   do {                                                                                    \
     ++e->launches;                                                                        \
     cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ == cudaSuccess && debug_sync()) e_ = cudaDeviceSynchronize();                  \
     if (e_ != cudaSuccess) {                                                              \
-      e->err = std::string("CUDA launch error: ") + cudaGetErrorString(e_);               \
+      e->err = std::string("CUDA launch error: ") + cudaGetErrorString(e_) + " (engine.cu:" + std::to_string(__LINE__) + ")"; \
       return AB_E_CUDA;                                                                   \
     }                                                                                     \
   } while (0)
@@ -866,6 +873,7 @@ ab_status images_and_lists(ab_engine* e) {
     Lg.rlo[p] = e->hp.pr[p].rlo, Lg.rc[p] = e->hp.pr[p].rc, Lg.rc2[p] = Lg.rc[p] * Lg.rc[p];
   }
   Lg.skin = skin;
+  Lg.ih2 = skin > 0 ? 4.0 / skin : 0.0, Lg.ih8 = skin > 0 ? 8.0 / skin : 0.0;
   Lg.bqcnt = e->small_i.p + 6;
   Lg.reach = (e->rcmax + skin) * (1.0 + 1e-9) + 1e-9;
   for (int attempt = 0; attempt < 4; ++attempt) {

@@ -109,7 +109,7 @@ struct LJLists {
   double flo2[3];  // (a_p - skin)^2 with a rounding margin (0 if a_p <= skin): lower end of the far list
   double fa[3];    // a_p
   double rlo[3], rc[3], rc2[3];
-  double skin;
+  double skin, ih2, ih8;  // skin, 4 / skin, 8 / skin (0 if skin = 0)
   double bq2[3];   // (a_p + skin)^2 with a rounding margin: the near list (canonical members bound the b* queue)
   int* bqcnt;      // [3] per species pair: bound of the b* candidate queue until the next build
   double reach;    // (r_c,max + skin) with a rounding margin: stencil culling radius
@@ -118,17 +118,15 @@ struct LJLists {
 
 __device__ __forceinline__ int far_bin(const LJLists& Lg, int p, double r2, bool nearp) {
   const double r = sqrt(r2), s = Lg.skin;
-  const double h2 = s * 0.25, h8 = s * 0.125;
-  auto kb = [](double x, double h) {
-    if (!(h > 0.0)) return 0;
-    double k = floor(x / h);
-    return k < 0.0 ? 0 : (k > 7.0 ? 7 : (int)k);
+  auto kb = [](double x, double ih) {  // bin of x >= 0 in steps of 1/ih, clamped to [0, 7]
+    const double k = x * ih;
+    return k < 1.0 ? 0 : (k >= 7.0 ? 7 : (int)k);
   };
-  if (nearp) return FB_L0 + kb(r - (Lg.fa[p] - s), h2);
+  if (nearp) return FB_L0 + kb(r - (Lg.fa[p] - s), Lg.ih2);
   if (r < Lg.rlo[p] - s) return FB_P;
-  if (r < Lg.rlo[p]) return FB_A0 + kb(r - (Lg.rlo[p] - s), h8);
+  if (r < Lg.rlo[p]) return FB_A0 + kb(r - (Lg.rlo[p] - s), Lg.ih8);
   if (r2 <= Lg.rc2[p]) return FB_B;
-  return FB_C0 + kb(r - Lg.rc[p], h8);
+  return FB_C0 + kb(r - Lg.rc[p], Lg.ih8);
 }
 
 // Stencil culling: a column (ax, ay) of cells is scanned only over the z-range of cells that
@@ -257,17 +255,14 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
     const bool nearp = in && r2 <= Lg.bq2[pr];
     const bool farp = in && r2 >= Lg.flo2[pr];
     warp_append(nearp, row0, Lg.cap[0], n0, b);
-    {  // stage far entries with their bin (candidate order); histogram: one add per distinct bin
+    {  // stage far entries with their bin (candidate order) and count them per bin
       const unsigned m = __ballot_sync(0xffffffffu, farp);
       const int slot = nf + __popc(m & ((1u << lane) - 1u));
-      const bool st = farp && slot < fcap;
-      const int bin = st ? far_bin(Lg, pr, r2, nearp) : FB_N + lane;
-      const unsigned grp = __match_any_sync(0xffffffffu, bin);
-      if (st) {
+      if (farp && slot < fcap) {
+        const int bin = far_bin(Lg, pr, r2, nearp);
         fJ[slot] = b, fB[slot] = (unsigned char)bin;
-        if ((grp & ((1u << lane) - 1u)) == 0u) hist[bin] += __popc(grp);
+        atomicAdd(&hist[bin], 1);
       }
-      __syncwarp();
       nf += __popc(m);
     }
     const bool bq = nearp && ka < key_of(pb);
@@ -287,6 +282,18 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
       if (lane >= o) incl += u;
     }
     if (lane < FB_N) Lg.boff[(size_t)a * FB_STRIDE + lane] = (unsigned short)incl;
+#ifdef AB_DEBUG_BOUNDS
+    {
+      const int last = __shfl_sync(0xffffffffu, incl, FB_N - 1);
+      const int prev = __shfl_up_sync(0xffffffffu, incl, 1);
+      const bool bad = (lane > 0 && lane < FB_N && incl < prev) || last != nfs;
+      if (__any_sync(0xffffffffu, bad) && lane == 0) {
+        printf("k_build_lj a=%d nf=%d nfs=%d last=%d hist:", a, nf, nfs, last);
+        for (int t = 0; t < FB_N; ++t) printf(" %d", hist[t]);
+        printf("\n");
+      }
+    }
+#endif
     __syncwarp();
     if (lane < FB_N) hist[lane] = incl - hv;  // running cursor per bin
     __syncwarp();
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
       const int rank = __popc(grp & ((1u << lane) - 1u));
       if (q < nfs) row1[hist[bin] + rank] = fJ[q];
       __syncwarp();
-      if (q < nfs && rank == 0) hist[bin] += __popc(grp);
+      if (q < nfs && rank == 0) atomicAdd(&hist[bin], __popc(grp));
       __syncwarp();
     }
   }

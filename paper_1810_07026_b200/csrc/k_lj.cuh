@@ -377,8 +377,18 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       const int p = ti + type_of(pj);
       if (!(r2 >= pd[3 + p] && r2 <= pd[p])) return;
       const bool canon = ki < key_of(pj);
+      const R rr2 = (R)r2;
+      R y = MORSE ? rsqrt_fast(rr2) : R(0);
       R dVr;
-      const R V = lj_v<R>(p, (R)r2, r2, dVr);
+      R V = MORSE ? morse_plain<R>(pr_[p], pr_[3 + p], pm_[p], rr2 * y, y, dVr)
+                  : lj_plain<R>(pr_[p], pr_[3 + p], rcp_fast(rr2), dVr);
+      if (r2 > pd[6 + p]) {  // taper S(r; r_lo, r_c) (reading A10)
+        if (!MORSE) y = rsqrt_fast(rr2);
+        R r = rr2 * y, dsw;
+        R sv = sw<R>(r, pr_[6 + p], pr_[9 + p], dsw);
+        dVr = dVr * sv + V * dsw * y;
+        V = V * sv;
+      }
       const R fr = -(R)Md * dVr;
       fx = acc_round<SG>(fx + (double)(fr * (R)dx));
       fy = acc_round<SG>(fy + (double)(fr * (R)dy));
@@ -399,11 +409,24 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       if (VIRIAL && stage.rows && canon) stage_lj_row(stage, gid[i], gid[J], shift[J], 1.0 - Md, 0.0);
     };
     if (!ovf) {
-      for (int q = gl; q < NEAR_SLOTS; q += NEAR_GROUP) {
-        const int J = s.keys[q];
-        if (J == REACH_EMPTY) continue;
-        const double Md = __longlong_as_double((long long)s.mbits[q]);
-        if (Md > 0.0) correct(J, Md);
+      // occupied slots with M > 0 as one 64-bit mask (bit q = slot q), then dealt out to the lanes
+      // 8 at a time (the group stays converged through the arithmetic)
+      unsigned long long vm = 0ull;
+#pragma unroll
+      for (int k = 0; k < NEAR_SLOTS / NEAR_GROUP; ++k) {
+        const int q = gl + NEAR_GROUP * k;
+        const bool v = s.keys[q] != REACH_EMPTY && s.mbits[q] != 0ull;
+        const unsigned b = (__ballot_sync(gmask, v) >> (threadIdx.x & 31 & ~(NEAR_GROUP - 1))) & ((1u << NEAR_GROUP) - 1u);
+        vm |= (unsigned long long)b << (NEAR_GROUP * k);
+      }
+      while (vm) {
+        unsigned long long t = vm;
+        for (int u = 0; u < gl; ++u) t &= t - 1ull;
+        if (t) {
+          const int q = __ffsll((long long)t) - 1;
+          correct(s.keys[q], __longlong_as_double((long long)s.mbits[q]));
+        }
+        for (int u = 0; u < NEAR_GROUP && vm; ++u) vm &= vm - 1ull;
       }
     } else {
       const int* row1 = A.nbr[1] + (size_t)i * A.cap[1];
@@ -479,20 +502,20 @@ constexpr int FAR_UNROLL = AB_FAR_UNROLL;
 // S(r; r_lo, r_c) (reading A10) evaluated only when some lane of the warp is in the taper band.
 template <typename R, bool VIRIAL, bool PURE, bool MORSE>
 struct FarPar {
-  R e4a, e4b, s2a, s2b, rea, reb, rloa, rlob, iva, ivb;
-  double rca, rcb, sha, shb, rla, rlb, tva, tvb;
-  __device__ __forceinline__ FarPar(int ti) {
+  R e4a, e4b, s2a, s2b, rea, reb;
+  double rca, rcb, sha, shb, tva, tvb;
+  int ti;
+  __device__ __forceinline__ FarPar(int ti_) : ti(ti_) {
     const Tab<R>& T = tab<R>();
     e4a = MORSE ? T.meps[ti] : R(4) * T.eps[ti], e4b = MORSE ? T.meps[ti + 1] : R(4) * T.eps[ti + 1];
     s2a = MORSE ? T.malpha[ti] : T.sigma2[ti], s2b = MORSE ? T.malpha[ti + 1] : T.sigma2[ti + 1];
     rea = MORSE ? T.mre[ti] : R(0), reb = MORSE ? T.mre[ti + 1] : R(0);
-    rloa = T.rlo[ti], rlob = T.rlo[ti + 1];
-    iva = T.inv_taper[ti], ivb = T.inv_taper[ti + 1];
-    rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
-    sha = c_geo.srhi2_hi[ti], shb = c_geo.srhi2_hi[ti + 1];
-    rla = c_geo.rlo2[ti], rlb = c_geo.rlo2[ti + 1];
-    // taper vote threshold: a little below r_lo^2 (the exact decision is t <= 0 below)
-    tva = rla * (1.0 - 1e-9), tvb = rlb * (1.0 - 1e-9);
+    if (!PURE) {
+      rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
+      sha = c_geo.srhi2_hi[ti], shb = c_geo.srhi2_hi[ti + 1];
+      // taper vote threshold: a little below r_lo^2 (the exact decision is t <= 0 below)
+      tva = c_geo.rlo2[ti] * (1.0 - 1e-9), tvb = c_geo.rlo2[ti + 1] * (1.0 - 1e-9);
+    }
   }
 };
 
@@ -509,7 +532,7 @@ __device__ __forceinline__ void far_entry(const FarPar<R, VIRIAL, PURE, MORSE>& 
   const bool canon = ki < key_of(pj);
   nlj += (in && canon);
   // taper-band pairs (algorithmic flop count): counted by the virial (ab_compute) instantiation only
-  if (!PURE && VIRIAL) ntp += (in && canon && r2 > (hj ? P.rlb : P.rla));
+  if (!PURE && VIRIAL) ntp += (in && canon && r2 > c_geo.rlo2[P.ti + (hj ? 1 : 0)]);
   const R rr2 = in ? (R)r2 : R(1);
   R dVr, V;
   if (MORSE) {
@@ -520,11 +543,13 @@ __device__ __forceinline__ void far_entry(const FarPar<R, VIRIAL, PURE, MORSE>& 
   }
   if (!PURE) {
     const bool tap = in && r2 > (hj ? P.tvb : P.tva);
-    if (__any_sync(0xffffffffu, tap)) {
+    if (__any_sync(0xffffffffu, tap)) {  // (parameters from the constant bank: rare, off the register budget)
+      const Tab<R>& T = tab<R>();
+      const int pp = P.ti + (hj ? 1 : 0);
       const R y = rsqrt_fast(rr2);
       const R r = rr2 * y;
-      const R iv = hj ? P.ivb : P.iva;
-      const R tt = (r - (hj ? P.rlob : P.rloa)) * iv;
+      const R iv = T.inv_taper[pp];
+      const R tt = (r - T.rlo[pp]) * iv;
       R sv, ds;
       halfcos_poly(tt < R(0) ? R(0) : tt, sv, ds);
       sv = tt <= R(0) ? R(1) : sv;
@@ -592,8 +617,11 @@ __device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, 
   }
 }
 
-// warp-uniform segment bounds of atom i's far row: [s0, s1) LOW, [s1, s2) PURE, [s2, s3) HIGH
-__device__ __forceinline__ void far_segments(const LJArgs& A, int i, double4 pi, int& s0, int& s1, int& s2, int& s3) {
+// warp-uniform segment bounds of atom i's far row: [s0, s1) tested, [s1, s2) PURE, [s2, s3) tested.
+// D = displacement bound of every atom (kernel-uniform).  Bin counts in closed form: m carries a
+// 1e-7 A margin, far above the rounding of the divisions, so every bin decision stays conservative.
+__device__ __forceinline__ void far_segments(const LJArgs& A, int i, double4 pi, double D, int& s0, int& s1, int& s2,
+                                             int& s3) {
   const int lane = threadIdx.x & 31;
   const int cnt = A.cnt[1][i];
   if (!A.binned) {
@@ -607,19 +635,26 @@ __device__ __forceinline__ void far_segments(const LJArgs& A, int i, double4 pi,
   };
   const double4 xr = A.xref[i];
   const double ex = pi.x - xr.x, ey = pi.y - xr.y, ez = pi.z - xr.z;
-  const double di = sqrt(ex * ex + ey * ey + ez * ez);
-  const double D = A.dbound ? sqrt(__longlong_as_double((long long)*A.dbound)) : 0.5 * A.skin;
-  const double m = di + D + 1e-7, skin = A.skin, h2 = 0.25 * skin, h8 = 0.125 * skin;
-  int kL0 = 0, kL1, kA = 0, kC = 0;
-  while (kL0 < 8 && (kL0 + 1) * h2 + m <= skin) ++kL0;  // L bins entirely below a_p
-  kL1 = kL0;
-  while (kL1 < 8 && !(kL1 * h2 - m >= skin)) ++kL1;     // first L bin entirely above a_p
-  while (kA < 8 && (kA + 1) * h8 + m <= skin) ++kA;     // A bins entirely below r_lo
-  while (kC < 8 && !(kC * h8 - m >= 0.0)) ++kC;         // first C bin entirely beyond r_c
+  const double m = sqrt(ex * ex + ey * ey + ez * ez) + D + 1e-7, skin = A.skin;
+  const double i2 = 4.0 / skin, i8 = 8.0 / skin;
+  auto clamp8 = [](double x) { return x <= 0.0 ? 0 : (x >= 8.0 ? 8 : (int)x); };
+  const int kL0 = clamp8(floor((skin - m) * i2));  // L bins with (k+1) skin/4 + m <= skin: below a_p
+  const int kL1 = max(kL0, clamp8(ceil((skin + m) * i2)));  // first L bin with k skin/4 - m >= skin: above a_p
+  const int kA = clamp8(floor((skin - m) * i8));   // A bins with (k+1) skin/8 + m <= skin: below r_lo
+  const int kC = clamp8(ceil(m * i8));             // first C bin with k skin/8 - m >= 0: beyond r_c
   s0 = start(FB_L0 + kL0);
   s1 = start(FB_L0 + kL1);
   s2 = start(FB_A0 + kA);
   s3 = kC < 8 ? start(FB_C0 + kC) : cnt;
+#ifdef AB_DEBUG_BOUNDS
+  if (!(0 <= s0 && s0 <= s1 && s1 <= s2 && s2 <= s3 && s3 <= cnt && cnt <= A.cap[1]) && lane == 0) {
+    printf("far_segments i=%d cnt=%d cap=%d s=%d %d %d %d k=%d %d %d %d m=%g D=%g ends:", i, cnt, A.cap[1], s0, s1, s2, s3,
+           kL0, kL1, kA, kC, m, D);
+    for (int t = 0; t < FB_N; ++t) printf(" %d", (int)A.boff[(size_t)i * FB_STRIDE + t]);
+    printf("\n");
+    __trap();
+  }
+#endif
 }
 
 template <typename R, bool VIRIAL, bool MORSE, bool SG = false, bool RANGED = false>
@@ -636,6 +671,7 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
   double W[6] = {0, 0, 0, 0, 0, 0};
   unsigned nlj = 0, ntp = 0;
   unsigned long long ne = 0;
+  const double D = A.dbound ? sqrt(__longlong_as_double((long long)*A.dbound)) : 0.5 * A.skin;
   // grid-stride over atoms: a resident grid, one warp per atom at a time
   // RANGED (slab interior / boundary split): the two atom ranges one after the other; otherwise
   // every atom (a separate instantiation: the range bookkeeping cost 6 % of the kernel on cfg4)
@@ -646,7 +682,7 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     const int ti = type_of(pi);
     const long long ki = key_of(pi);
     int s0, s1, s2, s3;
-    far_segments(A, i, pi, s0, s1, s2, s3);
+    far_segments(A, i, pi, D, s0, s1, s2, s3);
     double fx = 0, fy = 0, fz = 0;
     far_row<R, VIRIAL, MORSE, SG>(A, i, s0, s1, s2, s3, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
     fx = warp_sum<SG>(fx);
