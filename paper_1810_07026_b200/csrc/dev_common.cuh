@@ -149,6 +149,9 @@ __device__ __forceinline__ double rsqrt_fast(double a) {
 }
 __device__ __forceinline__ float rsqrt_fast(float a) { return rsqrtf(a); }
 
+__device__ __forceinline__ double fma_r(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float fma_r(float a, float b, float c) { return fmaf(a, b, c); }
+
 // 1/a: hardware approximation + two Newton steps (y += y (1 - a y)), a > 0 and finite
 __device__ __forceinline__ double rcp_fast(double a) {
   double y;

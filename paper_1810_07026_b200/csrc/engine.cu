@@ -201,6 +201,7 @@ struct ab_engine {
   DBuf<int> cl_k, cl_v, cl_v2, run_start, run_cl, cl_atom, clc, cln;
   DBuf<double4> cpos, cbb;
   bool want_virial = true;
+  bool want_energy = true;  // false: an NVE step whose energies / counters nobody reads (far LJ forces only)
   DBuf<int> s_cnt, s_nbr;
   DBuf<unsigned char> s_dr, s_w, s_N;  // typed by precision at use
   DBuf<double> s_wd;                   // fp64 switch weights of the short list (C_ij gate)
@@ -1220,7 +1221,8 @@ ab_status launch_far_early_t(ab_engine* e) {
   };
   const bool morse = d->hp.potential == kAIREBOM;
   if (d->want_virial) morse ? far(k_lj_far<R, true, true, false, true>) : far(k_lj_far<R, true, false, false, true>);
-  else morse ? far(k_lj_far<R, false, true, false, true>) : far(k_lj_far<R, false, false, false, true>);
+  else if (d->want_energy) morse ? far(k_lj_far<R, false, true, false, true>) : far(k_lj_far<R, false, false, false, true>);
+  else morse ? far(k_lj_far<R, false, true, false, true, false>) : far(k_lj_far<R, false, false, false, true, false>);
   ++d->launches;
   CK(cudaGetLastError());
   d->far_early = true;
@@ -1359,11 +1361,13 @@ ab_status enqueue_forces(ab_engine* e) {
     };
     if (far_split) {
       if (e->want_virial) morse ? far(k_lj_far<R, true, true, SG, true>) : far(k_lj_far<R, true, false, SG, true>);
-      else morse ? far(k_lj_far<R, false, true, SG, true>) : far(k_lj_far<R, false, false, SG, true>);
+      else if (e->want_energy) morse ? far(k_lj_far<R, false, true, SG, true>) : far(k_lj_far<R, false, false, SG, true>);
+      else morse ? far(k_lj_far<R, false, true, SG, true, false>) : far(k_lj_far<R, false, false, SG, true, false>);
     } else if (e->want_virial) {
       morse ? far(k_lj_far<R, true, true, SG>) : far(k_lj_far<R, true, false, SG>);
     } else {
-      morse ? far(k_lj_far<R, false, true, SG>) : far(k_lj_far<R, false, false, SG>);
+      if (e->want_energy) morse ? far(k_lj_far<R, false, true, SG>) : far(k_lj_far<R, false, false, SG>);
+      else morse ? far(k_lj_far<R, false, true, SG, false, false>) : far(k_lj_far<R, false, false, SG, false, false>);
     }
     CKL();
     prof_stop(e, 6, s_far, t);
@@ -2357,6 +2361,7 @@ static ab_status step_forces(ab_engine* e) {
     TRY(refresh_ghosts_all(e, true));
     return forces_all(e, false);
   }
+  e->want_energy = true;  // one captured graph serves every step
   if (!e->gexec || e->graph_epoch != e->layout) {
     graph_drop(e);
     cudaGraph_t g = nullptr;
@@ -2459,7 +2464,8 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
     std::vector<ab_engine*> ds;
     ~DeferGuard() {
       for (ab_engine* d : ds)
-        d->defer_reduce = false, d->post_pending = false, d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = false;
+        d->defer_reduce = false, d->post_pending = false, d->ghosts_fresh = d->f_zeroed = d->scratch_zeroed = false,
+        d->want_energy = true;
     }
   } defer_guard{D};
   for (ab_engine* d : D) d->defer_reduce = true;
@@ -2470,6 +2476,8 @@ static ab_status run_nve_impl(ab_engine* e, int64_t nsteps, double dt, int64_t e
   auto ms_since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
   for (int64_t s = 1; s <= nsteps; ++s) {
     const bool th = thermo && every > 0 && s % every == 0;
+    // energies / counters of this step are read only on thermo steps and after the call's last step
+    for (ab_engine* d : D) d->want_energy = th || s == nsteps;
     auto t0 = clk::now();
     e->tl_sub = 8;
     prof_begin(e, 4);

@@ -497,74 +497,77 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 #endif
 constexpr int FAR_UNROLL = AB_FAR_UNROLL;
 
-// one far entry (a lane of a 32-entry chunk).  PURE: settled by the bins (no decision, r^2 may be
-// fused, no taper); GEN: exact (un-fused) window / cutoff decisions as the oracle's, and the taper
-// S(r; r_lo, r_c) (reading A10) evaluated only when some lane of the warp is in the taper band.
-template <typename R, bool VIRIAL, bool PURE, bool MORSE>
+// Far-pair parameters of the two species pairs (t_i, t_j = C / H) a warp can meet (t_i is warp-
+// uniform): 12-6 form V = e4 s6 (s6 - 1), (dV/dr)/r = inv_r2 s6 (6 e4 - 12 e4 s6), s6 = (sigma^2 inv_r2)^3.
+template <typename R, bool MORSE>
 struct FarPar {
-  R e4a, e4b, s2a, s2b, rea, reb;
+  R e4a, e4b, s2a, s2b, c12a, c12b, c6a, c6b;  // 4 eps, sigma^2, 12 * 4 eps, 6 * 4 eps (Morse: eps, alpha, r_e, -)
   double rca, rcb, sha, shb, tva, tvb;
   int ti;
   __device__ __forceinline__ FarPar(int ti_) : ti(ti_) {
     const Tab<R>& T = tab<R>();
     e4a = MORSE ? T.meps[ti] : R(4) * T.eps[ti], e4b = MORSE ? T.meps[ti + 1] : R(4) * T.eps[ti + 1];
     s2a = MORSE ? T.malpha[ti] : T.sigma2[ti], s2b = MORSE ? T.malpha[ti + 1] : T.sigma2[ti + 1];
-    rea = MORSE ? T.mre[ti] : R(0), reb = MORSE ? T.mre[ti + 1] : R(0);
-    if (!PURE) {
-      rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
-      sha = c_geo.srhi2_hi[ti], shb = c_geo.srhi2_hi[ti + 1];
-      // taper vote threshold: a little below r_lo^2 (the exact decision is t <= 0 below)
-      tva = c_geo.rlo2[ti] * (1.0 - 1e-9), tvb = c_geo.rlo2[ti + 1] * (1.0 - 1e-9);
-    }
+    c12a = MORSE ? T.mre[ti] : R(12) * e4a, c12b = MORSE ? T.mre[ti + 1] : R(12) * e4b;
+    c6a = R(6) * e4a, c6b = R(6) * e4b;
+    rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
+    sha = c_geo.srhi2_hi[ti], shb = c_geo.srhi2_hi[ti + 1];
+    // taper vote threshold: a little below r_lo^2 (the exact decision is t <= 0 below)
+    tva = c_geo.rlo2[ti] * (1.0 - 1e-9), tvb = c_geo.rlo2[ti + 1] * (1.0 - 1e-9);
   }
 };
 
-template <typename R, bool VIRIAL, bool PURE, bool MORSE, bool SG>
-__device__ __forceinline__ void far_entry(const FarPar<R, VIRIAL, PURE, MORSE>& P, bool valid, double4 pj, int J, int i,
+// One far entry (a lane of a 32-entry chunk), branch-free except the taper: PURE = the chunk lies
+// in the bins settled as "window-free, untapered, inside r_c" (warp-uniform; no decision taken);
+// otherwise the exact (un-fused) window / cutoff decisions of the oracle, and the taper
+// S(r; r_lo, r_c) (reading A10) when some lane of the warp is in the taper band.
+// ENERGY = false (NVE steps whose energies / counters nobody reads): forces only.
+template <typename R, bool VIRIAL, bool ENERGY, bool MORSE, bool SG>
+__device__ __forceinline__ void far_entry(const FarPar<R, MORSE>& P, bool pure, bool valid, double4 pj, int J, int i,
                                           double4 pi, long long ki, const int* gid, const char4* shift,
                                           StageBuf stage, double& fx, double& fy, double& fz, double& en,
                                           double (&W)[6], unsigned& nlj, unsigned& ntp) {
   const bool hj = type_of(pj) != 0;
   const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
-  const double r2 = PURE ? fma(dz, dz, fma(dy, dy, dx * dx)) : r2_exact(dx, dy, dz);
-  bool in = valid;
-  if (!PURE) in = in && r2 >= (hj ? P.shb : P.sha) && r2 <= (hj ? P.rcb : P.rca);
-  const bool canon = ki < key_of(pj);
-  nlj += (in && canon);
+  const double r2 = r2_exact(dx, dy, dz);
+  const bool in = valid && (pure || (r2 >= (hj ? P.shb : P.sha) && r2 <= (hj ? P.rcb : P.rca)));
+  const bool canon = ENERGY && ki < key_of(pj);
+  if (ENERGY) nlj += (in && canon);
   // taper-band pairs (algorithmic flop count): counted by the virial (ab_compute) instantiation only
-  if (!PURE && VIRIAL) ntp += (in && canon && r2 > c_geo.rlo2[P.ti + (hj ? 1 : 0)]);
+  if (VIRIAL) ntp += (in && canon && r2 > c_geo.rlo2[P.ti + (hj ? 1 : 0)]);
   const R rr2 = in ? (R)r2 : R(1);
   R dVr, V;
   if (MORSE) {
     const R y = rsqrt_fast(rr2);
-    V = morse_plain<R>(hj ? P.e4b : P.e4a, hj ? P.s2b : P.s2a, hj ? P.reb : P.rea, rr2 * y, y, dVr);
+    V = morse_plain<R>(hj ? P.e4b : P.e4a, hj ? P.s2b : P.s2a, hj ? P.c12b : P.c12a, rr2 * y, y, dVr);
   } else {
-    V = lj_plain<R>(hj ? P.e4b : P.e4a, hj ? P.s2b : P.s2a, rcp_fast(rr2), dVr);
+    const R inv = rcp_fast(rr2);
+    const R sr2 = (hj ? P.s2b : P.s2a) * inv;
+    const R s6 = sr2 * sr2 * sr2;
+    dVr = inv * (s6 * fma_r(-(hj ? P.c12b : P.c12a), s6, hj ? P.c6b : P.c6a));
+    V = (hj ? P.e4b : P.e4a) * fma_r(s6, s6, -s6);  // (also the taper's dS term)
   }
-  if (!PURE) {
-    const bool tap = in && r2 > (hj ? P.tvb : P.tva);
-    if (__any_sync(0xffffffffu, tap)) {  // (parameters from the constant bank: rare, off the register budget)
-      const Tab<R>& T = tab<R>();
-      const int pp = P.ti + (hj ? 1 : 0);
-      const R y = rsqrt_fast(rr2);
-      const R r = rr2 * y;
-      const R iv = T.inv_taper[pp];
-      const R tt = (r - T.rlo[pp]) * iv;
-      R sv, ds;
-      halfcos_poly(tt < R(0) ? R(0) : tt, sv, ds);
-      sv = tt <= R(0) ? R(1) : sv;
-      ds = tt <= R(0) ? R(0) : ds * iv;
-      dVr = dVr * sv + V * ds * y;
-      V = V * sv;
-    }
+  const bool tap = !pure && in && r2 > (hj ? P.tvb : P.tva);
+  if (__any_sync(0xffffffffu, tap)) {  // (parameters from the constant bank: rare, off the register budget)
+    const Tab<R>& T = tab<R>();
+    const int pp = P.ti + (hj ? 1 : 0);
+    const R y = rsqrt_fast(rr2);
+    const R r = rr2 * y;
+    const R iv = T.inv_taper[pp];
+    const R tt = (r - T.rlo[pp]) * iv;
+    R sv, ds;
+    halfcos_poly(tt < R(0) ? R(0) : tt, sv, ds);
+    sv = tt <= R(0) ? R(1) : sv;
+    ds = tt <= R(0) ? R(0) : ds * iv;
+    dVr = dVr * sv + V * ds * y;
+    V = V * sv;
   }
   dVr = in ? dVr : R(0);
-  V = in ? V : R(0);
   const R rx = (R)dx, ry = (R)dy, rz = (R)dz;
   fx = acc_round<SG>(fx + (double)(dVr * rx));
   fy = acc_round<SG>(fy + (double)(dVr * ry));
   fz = acc_round<SG>(fz + (double)(dVr * rz));
-  en = acc_round<SG>(en + (double)V);
+  if (ENERGY) en = acc_round<SG>(en + (double)(in ? V : R(0)));
   if (VIRIAL) {
     V3<R> dd = mk3<R>(rx, ry, rz);
     vir_add(W, dd, (R(0.5) * dVr) * dd);
@@ -573,9 +576,9 @@ __device__ __forceinline__ void far_entry(const FarPar<R, VIRIAL, PURE, MORSE>& 
 }
 
 // the far row [s0, s3) as one stream of 32-entry chunks, FAR_UNROLL chunks per iteration (their
-// gathers in flight together, the next iteration's indices loaded one iteration ahead); a chunk
-// entirely inside the PURE range [s1, s2) takes the pure body (warp-uniform branch)
-template <typename R, bool VIRIAL, bool MORSE, bool SG>
+// gathers in flight together and their bodies interleaved, the next iteration's indices loaded
+// one iteration ahead); a chunk entirely inside the PURE range [s1, s2) skips the decisions
+template <typename R, bool VIRIAL, bool ENERGY, bool MORSE, bool SG>
 __device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, int s2, int s3, double4 pi, int ti,
                                         long long ki, const int* gid, const char4* shift, StageBuf stage,
                                         double& fx, double& fy, double& fz, double& en, double (&W)[6],
@@ -583,8 +586,7 @@ __device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, 
   if (s0 >= s3) return;
   const int lane = threadIdx.x & 31;
   const int* row = A.nbr[1] + (size_t)i * A.cap[1];
-  const FarPar<R, VIRIAL, true, MORSE> PP(ti);
-  const FarPar<R, VIRIAL, false, MORSE> PG(ti);
+  const FarPar<R, MORSE> P(ti);
   int Jn[FAR_UNROLL];
 #pragma unroll
   for (int u = 0; u < FAR_UNROLL; ++u) {
@@ -606,13 +608,8 @@ __device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, 
 #pragma unroll
     for (int u = 0; u < FAR_UNROLL; ++u) {
       const int c0 = base + 32 * u;
-      if (c0 >= s3) break;
-      if (c0 >= s1 && c0 + 32 <= s2)
-        far_entry<R, VIRIAL, true, MORSE, SG>(PP, J[u] >= 0, pj[u], J[u], i, pi, ki, gid, shift, stage, fx, fy, fz,
-                                              en, W, nlj, ntp);
-      else
-        far_entry<R, VIRIAL, false, MORSE, SG>(PG, J[u] >= 0, pj[u], J[u], i, pi, ki, gid, shift, stage, fx, fy, fz,
-                                               en, W, nlj, ntp);
+      far_entry<R, VIRIAL, ENERGY, MORSE, SG>(P, c0 >= s1 && c0 + 32 <= s2, J[u] >= 0, pj[u], J[u], i, pi, ki, gid,
+                                              shift, stage, fx, fy, fz, en, W, nlj, ntp);
     }
   }
 }
@@ -657,7 +654,7 @@ __device__ __forceinline__ void far_segments(const LJArgs& A, int i, double4 pi,
 #endif
 }
 
-template <typename R, bool VIRIAL, bool MORSE, bool SG = false, bool RANGED = false>
+template <typename R, bool VIRIAL, bool MORSE, bool SG = false, bool RANGED = false, bool ENERGY = true>
 #ifndef AB_FAR_MINBLOCKS
 #define AB_FAR_MINBLOCKS 4
 #endif
@@ -684,7 +681,7 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     int s0, s1, s2, s3;
     far_segments(A, i, pi, D, s0, s1, s2, s3);
     double fx = 0, fy = 0, fz = 0;
-    far_row<R, VIRIAL, MORSE, SG>(A, i, s0, s1, s2, s3, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
+    far_row<R, VIRIAL, ENERGY || VIRIAL, MORSE, SG>(A, i, s0, s1, s2, s3, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
     fx = warp_sum<SG>(fx);
     fy = warp_sum<SG>(fy);
     fz = warp_sum<SG>(fz);
