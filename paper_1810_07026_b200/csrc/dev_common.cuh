@@ -22,6 +22,7 @@ struct Tab {
   R rmin[3], rmax[3], Q[3], alpha[3], A[3], B[3][3], beta[3][3];
   R eps[3], sigma[3], sigma2[3], rc[3], rlo[3], bmin[3], bmax[3], rho[3], srhi[3];
   R inv_taper[3];  // 1 / (r_c - r_lo)
+  R lj_e4[3], lj_c12[3], lj_c6[3];  // 4 eps, 12 * 4 eps, 6 * 4 eps (far-pair 12-6 form)
   R meps[3], malpha[3], mre[3];  // AIREBO-M Morse radial form
   R explam[2][2][2];  // e^{lambda_{jik}} [t_j][t_i][t_k]
   int gn[3];  // g_C, g_H, g_C2 (slot 2: F3 coordination-dependent g_C, reading A34)
@@ -48,6 +49,7 @@ struct Tab {
 struct Geo {  // double-only quantities: exact list / gate decisions, box, integrator
   double rmax2[3], rc2[3], rmax_s2[3], rc_s2[3], rlo2[3], reach2;
   double srhi2_hi[3];  // (2^(1/6) sigma)^2 (1 + 1e-9): pre-filter of the exact S_r window test
+  double tv2[3];       // r_lo^2 (1 - 1e-9): taper vote threshold of the far-pair kernel
   double L[3];
   double mass[2], ftm2v, mvv2e;
   int potential;  // 0 AIREBO, 1 REBO, 2 AIREBO-M
@@ -166,31 +168,27 @@ __device__ __forceinline__ float rcp_fast(float a) { return __frcp_rn(a); }
 // Branch-free half-cosine on t in [0, 1] (caller clamps): S = (1 + cos(pi t))/2 and dS/dt, from
 // x = pi (t - 1/2) in [-pi/2, pi/2]: cos(pi t) = -sin x, sin(pi t) = cos x, Taylor polynomials
 // truncated below the working precision (fp64: x^21 / x^20 terms, error < 3e-17; fp32: x^13 / x^12).
+// (coefficients in the constant bank: DFMA takes them as c[][] operands instead of a uniform-
+// register pair per literal)
+__constant__ double c_hc_s[10] = {-1.9572941063391263e-20, 8.2206352466243295e-18, -2.8114572543455206e-15,
+                                  7.6471637318198164e-13, -1.6059043836821613e-10, 2.5052108385441720e-08,
+                                  -2.7557319223985893e-06, 1.9841269841269841e-04, -8.3333333333333333e-03,
+                                  1.6666666666666667e-01};  // -1/21!, 1/19!, ..., -1/5!, -(-1/3!)
+__constant__ double c_hc_c[10] = {4.1103176233121648e-19, -1.5619206968586225e-16, 4.7794773323873853e-14,
+                                  -1.1470745597729725e-11, 2.0876756987868099e-09, -2.7557319223985891e-07,
+                                  2.4801587301587302e-05, -1.3888888888888889e-03, 4.1666666666666667e-02,
+                                  -0.5};  // 1/20!, -1/18!, ..., 1/4!, -1/2!
 __device__ __forceinline__ void halfcos_poly(double t, double& S, double& dSdt) {
   double x = (t - 0.5) * CUDART_PI;
   double x2 = x * x;
-  double s = -1.9572941063391263e-20;  // -1/21!
-  s = fma(s, x2, 8.2206352466243295e-18);   // 1/19!
-  s = fma(s, x2, -2.8114572543455206e-15);  // -1/17!
-  s = fma(s, x2, 7.6471637318198164e-13);   // 1/15!
-  s = fma(s, x2, -1.6059043836821613e-10);  // -1/13!
-  s = fma(s, x2, 2.5052108385441720e-08);   // 1/11!
-  s = fma(s, x2, -2.7557319223985893e-06);  // -1/9!
-  s = fma(s, x2, 1.9841269841269841e-04);   // 1/7!
-  s = fma(s, x2, -8.3333333333333333e-03);  // -1/5!
-  s = fma(s, x2, 1.6666666666666667e-01);   // -(-1/3!)
-  s = x - x * x2 * s;                       // sin x
-  double c = 4.1103176233121648e-19;        // 1/20!
-  c = fma(c, x2, -1.5619206968586225e-16);  // -1/18!
-  c = fma(c, x2, 4.7794773323873853e-14);   // 1/16!
-  c = fma(c, x2, -1.1470745597729725e-11);  // -1/14!
-  c = fma(c, x2, 2.0876756987868099e-09);   // 1/12!
-  c = fma(c, x2, -2.7557319223985891e-07);  // -1/10!
-  c = fma(c, x2, 2.4801587301587302e-05);   // 1/8!
-  c = fma(c, x2, -1.3888888888888889e-03);  // -1/6!
-  c = fma(c, x2, 4.1666666666666667e-02);   // 1/4!
-  c = fma(c, x2, -0.5);                     // -1/2!
-  c = fma(c, x2, 1.0);                      // cos x
+  double s = c_hc_s[0];
+#pragma unroll
+  for (int k = 1; k < 10; ++k) s = fma(s, x2, c_hc_s[k]);
+  s = x - x * x2 * s;  // sin x
+  double c = c_hc_c[0];
+#pragma unroll
+  for (int k = 1; k < 10; ++k) c = fma(c, x2, c_hc_c[k]);
+  c = fma(c, x2, 1.0);  // cos x
   S = 0.5 - 0.5 * s;
   dSdt = -0.5 * CUDART_PI * c;
 }

@@ -431,6 +431,7 @@ void fill_tab(const HostParams& hp, Tab<R>& t) {
     t.rlo[p] = (R)s.rlo, t.bmin[p] = (R)s.bmin, t.bmax[p] = (R)s.bmax, t.rho[p] = (R)s.rho;
     t.srhi[p] = (R)(s.sigma * 1.122462048309373);  // 2^(1/6) sigma (reading A11)
     t.inv_taper[p] = (R)(1.0 / (s.rc - s.rlo));
+    t.lj_e4[p] = (R)(4.0 * s.eps), t.lj_c12[p] = (R)(48.0 * s.eps), t.lj_c6[p] = (R)(24.0 * s.eps);
   }
   for (int j = 0; j < 2; ++j)
     for (int i = 0; i < 2; ++i)
@@ -501,6 +502,7 @@ ab_status bind_consts(ab_engine* e) {
     g.rmax_s2[p] = (s.rmax + hp.skin) * (s.rmax + hp.skin);
     g.rc_s2[p] = (s.rc + hp.skin) * (s.rc + hp.skin);
     g.rlo2[p] = s.rlo * s.rlo;
+    g.tv2[p] = g.rlo2[p] * (1.0 - 1e-9);
     double srhi = s.sigma * 1.122462048309373;
     g.srhi2_hi[p] = srhi * srhi * (1.0 + 1e-9);
     rmm = std::max(rmm, s.rmax);
@@ -1174,6 +1176,7 @@ LJArgs lj_args(ab_engine* e) {
   // atom moved <= skin/2) bounds them; whole box: the device-side bound of this engine
   A.dbound = slabbed(e) ? nullptr : reinterpret_cast<const unsigned long long*>(e->scratch.p + SCRATCH_DBOUND);
   A.skin = e->hp.skin;
+  A.i2 = e->hp.skin > 0 ? 4.0 / e->hp.skin : 0.0, A.i8 = e->hp.skin > 0 ? 8.0 / e->hp.skin : 0.0;
   bool binned = e->hp.skin > 0.0;
   for (int p = 0; p < 3; ++p) {
     const PairSet& s = e->hp.pr[p];

@@ -28,17 +28,18 @@
 namespace ab {
 
 #ifndef AB_NEAR_GROUP
-#define AB_NEAR_GROUP 8
+#define AB_NEAR_GROUP 4
 #endif
 #ifndef AB_NEAR_SLOTS
 #define AB_NEAR_SLOTS 64
 #endif
-constexpr int NEAR_GROUP = AB_NEAR_GROUP;        // lanes per atom (measured: 8 beats 16 and 32)
+constexpr int NEAR_GROUP = AB_NEAR_GROUP;        // lanes per atom (measured on cfg4: 4 beats 8 and 16)
 #ifndef AB_NEAR_BLOCK
 #define AB_NEAR_BLOCK 128
 #endif
 constexpr int NEAR_ATOMS = AB_NEAR_BLOCK / NEAR_GROUP;  // atoms per block
 constexpr int NEAR_SLOTS = AB_NEAR_SLOTS;        // reach table slots per atom (measured: 64 beats 128)
+static_assert(NEAR_SLOTS <= 64, "the correction pass keeps the occupied slots in a 64-bit mask");
 
 #ifndef AB_NEAR_BLOOM
 #define AB_NEAR_BLOOM 16 // 32-bit words of the per-atom Bloom filter in front of the table (0: none)
@@ -131,7 +132,7 @@ struct LJArgs {
   const unsigned short* boff;          // far-row bin ends (k_lists.cuh FB_*)
   const double4* xref;                 // positions at the last build (per-atom displacement)
   const unsigned long long* dbound;    // bits of max displacement^2 of any atom since the build (nullptr: skin/2)
-  double skin;
+  double skin, i2, i8;                 // skin, 4 / skin, 8 / skin
   int binned;                          // 0: every far entry through the fully tested body
 };
 
@@ -169,7 +170,7 @@ __device__ __forceinline__ double reach_lookup_fast(const ReachSmem& s, int key)
 
 template <typename R, bool VIRIAL, bool MORSE, bool SG = false>
 #ifndef AB_NEAR_MINBLOCKS
-#define AB_NEAR_MINBLOCKS 7  // measured: 7 blocks (73 regs) beat 6 (80 regs) and 8 (64 regs, spills)
+#define AB_NEAR_MINBLOCKS 6  // measured (cfg4, 4-lane groups): 6 blocks beat 7
 #endif
 __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_lj_near(LJArgs A, ShortList<R> S, const int* owner,
                                                                     const int* gid, const char4* shift, double* F,
@@ -409,24 +410,25 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       if (VIRIAL && stage.rows && canon) stage_lj_row(stage, gid[i], gid[J], shift[J], 1.0 - Md, 0.0);
     };
     if (!ovf) {
-      // occupied slots with M > 0 as one 64-bit mask (bit q = slot q), then dealt out to the lanes
-      // 8 at a time (the group stays converged through the arithmetic)
+      // occupied slots with M > 0 as one 64-bit mask (bit q = slot q; lane gl reads slots
+      // 8 gl .. 8 gl + 7, OR-reduced over the group), then dealt out to the lanes 8 at a time in
+      // slot order (the n-th set bit by __fns on the two halves): the group stays converged
+      constexpr int SPL = NEAR_SLOTS / NEAR_GROUP;
       unsigned long long vm = 0ull;
 #pragma unroll
-      for (int k = 0; k < NEAR_SLOTS / NEAR_GROUP; ++k) {
-        const int q = gl + NEAR_GROUP * k;
-        const bool v = s.keys[q] != REACH_EMPTY && s.mbits[q] != 0ull;
-        const unsigned b = (__ballot_sync(gmask, v) >> (threadIdx.x & 31 & ~(NEAR_GROUP - 1))) & ((1u << NEAR_GROUP) - 1u);
-        vm |= (unsigned long long)b << (NEAR_GROUP * k);
+      for (int k = 0; k < SPL; ++k) {
+        const int q = SPL * gl + k;
+        if (s.keys[q] != REACH_EMPTY && s.mbits[q] != 0ull) vm |= 1ull << q;
       }
-      while (vm) {
-        unsigned long long t = vm;
-        for (int u = 0; u < gl; ++u) t &= t - 1ull;
-        if (t) {
-          const int q = __ffsll((long long)t) - 1;
+#pragma unroll
+      for (int o = 1; o < NEAR_GROUP; o <<= 1) vm |= __shfl_xor_sync(gmask, vm, o, NEAR_GROUP);
+      const unsigned lo = (unsigned)vm, hi = (unsigned)(vm >> 32);
+      const int clo = __popc(lo), tot = clo + __popc(hi);
+      for (int n = gl; n - gl < tot; n += NEAR_GROUP) {
+        if (n < tot) {
+          const int q = n < clo ? (int)__fns(lo, 0, n + 1) : 32 + (int)__fns(hi, 0, n - clo + 1);
           correct(s.keys[q], __longlong_as_double((long long)s.mbits[q]));
         }
-        for (int u = 0; u < NEAR_GROUP && vm; ++u) vm &= vm - 1ull;
       }
     } else {
       const int* row1 = A.nbr[1] + (size_t)i * A.cap[1];
@@ -506,14 +508,13 @@ struct FarPar {
   int ti;
   __device__ __forceinline__ FarPar(int ti_) : ti(ti_) {
     const Tab<R>& T = tab<R>();
-    e4a = MORSE ? T.meps[ti] : R(4) * T.eps[ti], e4b = MORSE ? T.meps[ti + 1] : R(4) * T.eps[ti + 1];
+    e4a = MORSE ? T.meps[ti] : T.lj_e4[ti], e4b = MORSE ? T.meps[ti + 1] : T.lj_e4[ti + 1];
     s2a = MORSE ? T.malpha[ti] : T.sigma2[ti], s2b = MORSE ? T.malpha[ti + 1] : T.sigma2[ti + 1];
-    c12a = MORSE ? T.mre[ti] : R(12) * e4a, c12b = MORSE ? T.mre[ti + 1] : R(12) * e4b;
-    c6a = R(6) * e4a, c6b = R(6) * e4b;
+    c12a = MORSE ? T.mre[ti] : T.lj_c12[ti], c12b = MORSE ? T.mre[ti + 1] : T.lj_c12[ti + 1];
+    c6a = T.lj_c6[ti], c6b = T.lj_c6[ti + 1];
     rca = c_geo.rc2[ti], rcb = c_geo.rc2[ti + 1];
     sha = c_geo.srhi2_hi[ti], shb = c_geo.srhi2_hi[ti + 1];
-    // taper vote threshold: a little below r_lo^2 (the exact decision is t <= 0 below)
-    tva = c_geo.rlo2[ti] * (1.0 - 1e-9), tvb = c_geo.rlo2[ti + 1] * (1.0 - 1e-9);
+    tva = c_geo.tv2[ti], tvb = c_geo.tv2[ti + 1];  // taper vote: a little below r_lo^2
   }
 };
 
@@ -633,7 +634,7 @@ __device__ __forceinline__ void far_segments(const LJArgs& A, int i, double4 pi,
   const double4 xr = A.xref[i];
   const double ex = pi.x - xr.x, ey = pi.y - xr.y, ez = pi.z - xr.z;
   const double m = sqrt(ex * ex + ey * ey + ez * ez) + D + 1e-7, skin = A.skin;
-  const double i2 = 4.0 / skin, i8 = 8.0 / skin;
+  const double i2 = A.i2, i8 = A.i8;
   auto clamp8 = [](double x) { return x <= 0.0 ? 0 : (x >= 8.0 ? 8 : (int)x); };
   const int kL0 = clamp8(floor((skin - m) * i2));  // L bins with (k+1) skin/4 + m <= skin: below a_p
   const int kL1 = max(kL0, clamp8(ceil((skin + m) * i2)));  // first L bin with k skin/4 - m >= skin: above a_p
