@@ -600,6 +600,6 @@ __host__ __device__ __forceinline__ long long make_key(int gid, int sx, int sy, 
          ((long long)(sz + 128) << 2) | (long long)type;
 }
 __device__ __forceinline__ long long key_of(const double4& p) { return __double_as_longlong(p.w); }
-__device__ __forceinline__ int type_of(const double4& p) { return (int)(__double_as_longlong(p.w) & 3); }
+__device__ __forceinline__ int type_of(const double4& p) { return __double2loint(p.w) & 3; }
 
 }  // namespace ab

@@ -116,17 +116,23 @@ struct LJLists {
   int fcap_smem;   // far entries staged per warp (= cap[1])
 };
 
+// Branch-free (the categories differ between the lanes of a chunk): every candidate bin is
+// formed and the category selects one.  r = r2 rsqrt(r2) with two Newton steps (~1e-16 relative,
+// far below the 1e-7 A margins of the evaluation-time bin classification); P (taken as untapered
+// without a displacement test) keeps a 1e-9 A safety gap below r_lo - skin.
 __device__ __forceinline__ int far_bin(const LJLists& Lg, int p, double r2, bool nearp) {
-  const double r = sqrt(r2), s = Lg.skin;
+  const double r = r2 > 0.0 ? r2 * rsqrt_fast(r2) : 0.0, s = Lg.skin;
   auto kb = [](double x, double ih) {  // bin of x >= 0 in steps of 1/ih, clamped to [0, 7]
     const double k = x * ih;
     return k < 1.0 ? 0 : (k >= 7.0 ? 7 : (int)k);
   };
-  if (nearp) return FB_L0 + kb(r - (Lg.fa[p] - s), Lg.ih2);
-  if (r < Lg.rlo[p] - s) return FB_P;
-  if (r < Lg.rlo[p]) return FB_A0 + kb(r - (Lg.rlo[p] - s), Lg.ih8);
-  if (r2 <= Lg.rc2[p]) return FB_B;
-  return FB_C0 + kb(r - Lg.rc[p], Lg.ih8);
+  const double rlo = Lg.rlo[p];
+  const int bL = FB_L0 + kb(r - (Lg.fa[p] - s), Lg.ih2);
+  const int bA = FB_A0 + kb(r - (rlo - s), Lg.ih8);
+  const int bC = FB_C0 + kb(r - Lg.rc[p], Lg.ih8);
+  const int bHi = r2 <= Lg.rc2[p] ? FB_B : bC;
+  const int bFar = r < rlo - s - 1e-9 ? FB_P : (r < rlo ? bA : bHi);
+  return nearp ? bL : bFar;
 }
 
 // Stencil culling: a column (ax, ay) of cells is scanned only over the z-range of cells that
