@@ -76,6 +76,8 @@ constexpr size_t SCRATCH_TICKET = 1016;
 // bits of the max displacement^2 of any local atom since the last build (atomicMax by the drift /
 // displacement kernels, zeroed at every build; never in the zeroed region): the far-LJ kernel's bins
 constexpr size_t SCRATCH_DBOUND = 1000;
+// max reach-set size seen by k_lj_near since the last build (atomicMax; read + zeroed at each build)
+constexpr size_t SCRATCH_MAXREACH = 992;
 #ifndef AB_INT_BLOCK
 #define AB_INT_BLOCK 128  // k_integrate1_img block (measured cfg2: 128 beats 256; 64 / 32 equal)
 #endif  // k_integrate1_img's last-block ticket (never memset after init)
@@ -201,6 +203,7 @@ struct ab_engine {
   DBuf<int> cl_k, cl_v, cl_v2, run_start, run_cl, cl_atom, clc, cln;
   DBuf<double4> cpos, cbb;
   bool want_virial = true;
+  int near_slots = 64;      // k_lj_near reach-table size (32 while the reach sets stay <= 20 images)
   bool want_energy = true;  // false: an NVE step whose energies / counters nobody reads (far LJ forces only)
   DBuf<int> s_cnt, s_nbr;
   DBuf<unsigned char> s_dr, s_w, s_N;  // typed by precision at use
@@ -879,6 +882,8 @@ ab_status images_and_lists(ab_engine* e) {
   Lg.ih2 = skin > 0 ? 4.0 / skin : 0.0, Lg.ih8 = skin > 0 ? 8.0 / skin : 0.0;
   Lg.bqcnt = e->small_i.p + 6;
   Lg.reach = (e->rcmax + skin) * (1.0 + 1e-9) + 1e-9;
+  for (int t = 0; t < 2; ++t)  // per species of the atom: its largest LJ cutoff (C: CC / CH, H: CH / HH) + skin
+    Lg.reach_t[t] = (std::max(e->hp.pr[t].rc, e->hp.pr[t + 1].rc) + skin) * (1.0 + 1e-9) + 1e-9;
   for (int attempt = 0; attempt < 4; ++attempt) {
     for (int c = 0; c < 3; ++c) {
       if (!clp) CK(e->ljn[c].ensure((size_t)N * e->capL[c]));
@@ -931,8 +936,16 @@ ab_status images_and_lists(ab_engine* e) {
     if (dbg) cudaEventRecord(dbg_ev[2], st);
     int mx[7];
     CK(cudaMemcpyAsync(mx, e->small_i.p + 2, 7 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    unsigned long long mreach = 0;
+    if (attempt == 0) {
+      CK(cudaMemcpyAsync(&mreach, e->scratch.p + SCRATCH_MAXREACH, sizeof(mreach), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemsetAsync(e->scratch.p + SCRATCH_MAXREACH, 0, sizeof(mreach), st));
+    }
     auto tw = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st));
+    // the next interval's reach-table size (AB_NEAR_SLOTS_FIXED=64: always 64, diagnostics / tests)
+    const bool fixed64 = std::getenv("AB_NEAR_SLOTS_FIXED") && std::atoi(std::getenv("AB_NEAR_SLOTS_FIXED")) == 64;
+    if (mreach && !fixed64) e->near_slots = mreach <= 20 ? 32 : 64;
     if (dbg) {
       float k1 = 0;
       cudaEventElapsedTime(&k1, dbg_ev[1], dbg_ev[2]);
@@ -1184,6 +1197,7 @@ LJArgs lj_args(ab_engine* e) {
     binned = binned && a + 2.0 * e->hp.skin + 1e-6 <= s.rlo && s.rlo < s.rc;
   }
   A.binned = binned ? 1 : 0;
+  A.maxreach = reinterpret_cast<unsigned long long*>(e->scratch.p + SCRATCH_MAXREACH);
   return A;
 }
 
@@ -1446,7 +1460,8 @@ ab_status enqueue_forces(ab_engine* e) {
     } else if (e->want_virial) {
       morse ? near(k_lj_near<R, true, true, SG>) : near(k_lj_near<R, true, false, SG>);
     } else {
-      morse ? near(k_lj_near<R, false, true, SG>) : near(k_lj_near<R, false, false, SG>);
+      if (e->near_slots == 32) morse ? near(k_lj_near<R, false, true, SG, 32>) : near(k_lj_near<R, false, false, SG, 32>);
+      else morse ? near(k_lj_near<R, false, true, SG>) : near(k_lj_near<R, false, false, SG>);
     }
     CKL();
     prof_stop(e, 2, st, t);

@@ -113,6 +113,7 @@ struct LJLists {
   double bq2[3];   // (a_p + skin)^2 with a rounding margin: the near list (canonical members bound the b* queue)
   int* bqcnt;      // [3] per species pair: bound of the b* candidate queue until the next build
   double reach;    // (r_c,max + skin) with a rounding margin: stencil culling radius
+  double reach_t[2];  // the same per species of the listed atom (C: max r_c(CC, CH), H: max r_c(CH, HH))
   int fcap_smem;   // far entries staged per warp (= cap[1])
 };
 
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
   int* pre = s_pre[w];
   int* hist = s_hist[w];
   if (lane <= FB_N) hist[lane] = 0;
-  const int total = stencil_columns(g, p, nr, Lg.reach, cell_start, cb, pre);
+  const int total = stencil_columns(g, p, nr, Lg.reach_t[ta], cell_start, cb, pre);
   int k = 0;  // column of the chunk's first candidate (warp-uniform)
   // software pipeline: the next chunk's index and position loads are in flight while this
   // chunk is classified and appended

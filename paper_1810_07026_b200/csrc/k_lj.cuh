@@ -54,14 +54,16 @@ struct NearBlockQ {
   double m[3][NEAR_BQ];
 };
 
-struct ReachSmem {
-  int keys[NEAR_SLOTS];
-  unsigned long long mbits[NEAR_SLOTS];
-  int nins, ovf;
+template <int SL>
+struct alignas(16) ReachSmem {  // (16-byte aligned arrays: cleared with vector stores)
+  int keys[SL];
+  unsigned long long mbits[SL];
 #if AB_NEAR_BLOOM
   unsigned bloom[AB_NEAR_BLOOM];  // one bit per inserted key: a clear bit proves M = 0
 #endif
+  int nins, ovf;
 };
+static_assert(NEAR_SLOTS % 4 == 0 && AB_NEAR_BLOOM % 4 == 0, "vector clear of the reach table");
 #if AB_NEAR_BLOOM
 __device__ __forceinline__ unsigned bloom_bit(int key) {  // bits independent of the table slot
   return (((unsigned)key * 0x9E3779B1u) >> 7) & (32u * AB_NEAR_BLOOM - 1u);
@@ -69,13 +71,15 @@ __device__ __forceinline__ unsigned bloom_bit(int key) {  // bits independent of
 #endif
 
 __host__ __device__ constexpr int log2i(int v) { return v <= 1 ? 0 : 1 + log2i(v / 2); }
+template <int SL>
 __device__ __forceinline__ unsigned reach_hash(int key) {
-  return ((unsigned)key * 2654435761u) >> (32 - log2i(NEAR_SLOTS));
+  return ((unsigned)key * 2654435761u) >> (32 - log2i(SL));
 }
 
-__device__ __forceinline__ void reach_insert(ReachSmem& s, int key, double M) {
-  unsigned h = reach_hash(key);
-  for (int probe = 0; probe < NEAR_SLOTS; ++probe) {
+template <int SL>
+__device__ __forceinline__ void reach_insert(ReachSmem<SL>& s, int key, double M) {
+  unsigned h = reach_hash<SL>(key);
+  for (int probe = 0; probe < SL; ++probe) {
     int old = atomicCAS(&s.keys[h], REACH_EMPTY, key);
     if (old == REACH_EMPTY || old == key) {
       if (old == REACH_EMPTY) {
@@ -88,18 +92,19 @@ __device__ __forceinline__ void reach_insert(ReachSmem& s, int key, double M) {
       atomicMax(&s.mbits[h], (unsigned long long)__double_as_longlong(M));
       return;
     }
-    h = (h + 1) & (NEAR_SLOTS - 1);
+    h = (h + 1) & (SL - 1);
   }
   s.ovf = 1;
 }
 
-__device__ __forceinline__ double reach_lookup(const ReachSmem& s, int key) {
-  unsigned h = reach_hash(key);
-  for (int probe = 0; probe < NEAR_SLOTS; ++probe) {
+template <int SL>
+__device__ __forceinline__ double reach_lookup(const ReachSmem<SL>& s, int key) {
+  unsigned h = reach_hash<SL>(key);
+  for (int probe = 0; probe < SL; ++probe) {
     int k = s.keys[h];
     if (k == key) return __longlong_as_double((long long)s.mbits[h]);
     if (k == REACH_EMPTY) return 0.0;
-    h = (h + 1) & (NEAR_SLOTS - 1);
+    h = (h + 1) & (SL - 1);
   }
   return 0.0;
 }
@@ -134,6 +139,7 @@ struct LJArgs {
   const unsigned long long* dbound;    // bits of max displacement^2 of any atom since the build (nullptr: skin/2)
   double skin, i2, i8;                 // skin, 4 / skin, 8 / skin
   int binned;                          // 0: every far entry through the fully tested body
+  unsigned long long* maxreach;        // k_lj_near: persistent max reach-set size (nullptr: off)
 };
 
 __device__ __forceinline__ void stage_lj_row(StageBuf stage, int gi, int gj, char4 sh, double C, double bs) {
@@ -152,23 +158,24 @@ __device__ __forceinline__ double group_sum(double v) {
 // 8 lanes per atom.  The reach table holds the maximal path product per reachable image; the
 // pair loop is branch-light (the rare b* / fractional-C / stage work sits at the end of the
 // body) so the group stays converged through the LJ arithmetic.
-__device__ __forceinline__ double reach_lookup_fast(const ReachSmem& s, int key) {
+template <int SL>
+__device__ __forceinline__ double reach_lookup_fast(const ReachSmem<SL>& s, int key) {
 #if AB_NEAR_BLOOM
   const unsigned b = bloom_bit(key);
   if (!((s.bloom[b >> 5] >> (b & 31u)) & 1u)) return 0.0;  // not in the reach set: M = 0
 #endif
-  unsigned h = reach_hash(key);
+  unsigned h = reach_hash<SL>(key);
 #pragma unroll
   for (int probe = 0; probe < 4; ++probe) {
     int k = s.keys[h];
     if (k == key) return __longlong_as_double((long long)s.mbits[h]);
     if (k == REACH_EMPTY) return 0.0;
-    h = (h + 1) & (NEAR_SLOTS - 1);
+    h = (h + 1) & (SL - 1);
   }
-  return reach_lookup(s, key);  // long probe chain: rare
+  return reach_lookup<SL>(s, key);  // long probe chain: rare
 }
 
-template <typename R, bool VIRIAL, bool MORSE, bool SG = false>
+template <typename R, bool VIRIAL, bool MORSE, bool SG = false, int SL = NEAR_SLOTS>
 #ifndef AB_NEAR_MINBLOCKS
 #define AB_NEAR_MINBLOCKS 6  // measured (cfg4, 4-lane groups): 6 blocks beat 7
 #endif
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
                                                                     const int* gid, const char4* shift, double* F,
                                                                     double* acc, unsigned long long* ct,
                                                                     BstarQueue Qu, StageBuf stage, RedRows RR) {
-  __shared__ ReachSmem sm_all[NEAR_ATOMS];
+  __shared__ ReachSmem<SL> sm_all[NEAR_ATOMS];
   __shared__ RedSmem rs;
 #if AB_NEAR_BLOCKQ
   __shared__ NearBlockQ bq;
@@ -197,19 +204,18 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   if (MORSE && threadIdx.x < 3) pm_[threadIdx.x] = T.mre[threadIdx.x];
   red_init(rs);
   const int grp = threadIdx.x / NEAR_GROUP, gl = threadIdx.x % NEAR_GROUP;
-  ReachSmem& s = sm_all[grp];
+  ReachSmem<SL>& s = sm_all[grp];
   const int i = blockIdx.x * NEAR_ATOMS + grp;
   const bool active = i < A.N;
   const int cntN = active ? A.cnt[0][i] : 0;
 
   // 1. reach set of i: lane per neighbour k of i enumerates k, l in N(k), m in N(l)
-  for (int q = gl; q < NEAR_SLOTS; q += NEAR_GROUP) {
-    s.keys[q] = REACH_EMPTY;
-    s.mbits[q] = 0ull;
-  }
+  for (int q = gl; q < SL / 4; q += NEAR_GROUP)
+    reinterpret_cast<int4*>(s.keys)[q] = make_int4(REACH_EMPTY, REACH_EMPTY, REACH_EMPTY, REACH_EMPTY);
+  for (int q = gl; q < SL / 2; q += NEAR_GROUP) reinterpret_cast<ulonglong2*>(s.mbits)[q] = make_ulonglong2(0ull, 0ull);
   if (gl == 0) s.nins = 0, s.ovf = 0;
 #if AB_NEAR_BLOOM
-  for (int q = gl; q < AB_NEAR_BLOOM; q += NEAR_GROUP) s.bloom[q] = 0u;
+  for (int q = gl; q < AB_NEAR_BLOOM / 4; q += NEAR_GROUP) reinterpret_cast<uint4*>(s.bloom)[q] = make_uint4(0u, 0u, 0u, 0u);
 #endif
   __syncwarp();
   const size_t bi = (size_t)(active ? i : 0) * S.capS;
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       // occupied slots with M > 0 as one 64-bit mask (bit q = slot q; lane gl reads slots
       // 8 gl .. 8 gl + 7, OR-reduced over the group), then dealt out to the lanes 8 at a time in
       // slot order (the n-th set bit by __fns on the two halves): the group stays converged
-      constexpr int SPL = NEAR_SLOTS / NEAR_GROUP;
+      constexpr int SPL = SL / NEAR_GROUP;
       unsigned long long vm = 0ull;
 #pragma unroll
       for (int k = 0; k < SPL; ++k) {
@@ -480,6 +486,9 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   red_add_u(rs, CT_OVF_REACH, gl == 0 && ovf ? 1ull : 0ull);
   red_add_u(rs, CT_LJENT, gl == 0 ? (unsigned long long)cntN : 0ull);
   red_flush(rs, RR);
+  // max reach-set size since the last list build (persistent, read by the host at the next
+  // rebuild to size the table: 32 slots while every set stays small, else 64)
+  if (threadIdx.x == 0 && A.maxreach && rs.u[CT_MAXREACH]) atomicMax(A.maxreach, rs.u[CT_MAXREACH]);
 }
 
 // ---------------------------------------------------------------------------------- far pairs

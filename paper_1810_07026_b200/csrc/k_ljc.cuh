@@ -48,7 +48,7 @@ struct LjcPar {  // the two species pairs a warp-uniform centre species can form
 };
 template <typename R>
 struct LjcWarp {
-  ReachSmem s;
+  ReachSmem<NEAR_SLOTS> s;
   LjcQueue<R> q[3];
   LjcPar<R> P;  // per-warp copy (shared memory: keeps the registers for the pair arithmetic)
 };
@@ -65,7 +65,7 @@ struct LjcArgs {
 
 // reach set of atom i over the short list, one warp (see header)
 template <typename R>
-__device__ __forceinline__ void reach_build_warp(ReachSmem& s, const ShortList<R>& S, int i) {
+__device__ __forceinline__ void reach_build_warp(ReachSmem<NEAR_SLOTS>& s, const ShortList<R>& S, int i) {
   const int lane = threadIdx.x & 31;
   for (int q = lane; q < NEAR_SLOTS; q += 32) s.keys[q] = REACH_EMPTY, s.mbits[q] = 0ull;
 #if AB_NEAR_BLOOM

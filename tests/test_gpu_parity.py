@@ -415,3 +415,29 @@ def test_skinned_lj_list_at_build_positions(eng_mod, params_text):
         assert sk.shape == ref.shape and np.array_equal(sk, ref), s.name
         lj = {tuple(r) for r in e.get_list(2)}
         assert lj <= {tuple(r) for r in sk}
+
+
+def test_adaptive_reach_table_after_rebuild(eng_mod, monkeypatch):
+    """After a list build that saw only small reach sets (PE: <= 16 images) the NVE near-pair kernel
+    switches to the 32-slot reach table; its trajectory equals the 64-slot one and the forces at
+    the end frame equal the oracle's."""
+    s = I.config(1)
+    out = []
+    for fixed in (False, True):
+        if fixed:
+            monkeypatch.setenv("AB_NEAR_SLOTS_FIXED", "64")
+        e = eng_mod.make(s)
+        e.run_nve(2, 0.5)
+        e.set_box(s.box)  # forces a list build, which reads the max reach of the steps before
+        e.run_nve(40, 0.5, every=10)
+        out.append(e.get_positions())
+        if fixed:
+            monkeypatch.delenv("AB_NEAR_SLOTS_FIXED")
+        else:
+            x = out[0]
+            F = e.compute()["F"]
+            o = O.compute(s.types, x, s.box)
+            assert np.abs(F - o["F"]).max() <= 1e-9
+    d = out[0] - out[1]
+    d -= s.box * np.round(d / s.box)
+    assert np.abs(d).max() <= 1e-9
