@@ -506,6 +506,9 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 #ifndef AB_FAR_UNROLL
 #define AB_FAR_UNROLL 4
 #endif
+#ifndef AB_FAR_PIPE
+#define AB_FAR_PIPE 0
+#endif
 constexpr int FAR_UNROLL = AB_FAR_UNROLL;
 
 // Far-pair parameters of the two species pairs (t_i, t_j = C / H) a warp can meet (t_i is warp-
@@ -597,6 +600,46 @@ __device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, 
   const int lane = threadIdx.x & 31;
   const int* row = A.nbr[1] + (size_t)i * A.cap[1];
   const FarPar<R, MORSE> P(ti);
+#if AB_FAR_PIPE
+  // software pipeline one iteration deep: the next iteration's positions are in flight while this
+  // one computes (indices two iterations ahead)
+  constexpr int U = FAR_UNROLL;
+  int Jc[U], Jn[U];
+  double4 pn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int q = s0 + u * 32 + lane;
+    Jc[u] = q < s3 ? row[q] : -1;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) pn[u] = A.pos[Jc[u] >= 0 ? Jc[u] : i];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int q = s0 + 32 * U + u * 32 + lane;
+    Jn[u] = q < s3 ? row[q] : -1;
+  }
+  for (int base = s0; base < s3; base += 32 * U) {
+    int J[U];
+    double4 pj[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) J[u] = Jc[u], pj[u] = pn[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) Jc[u] = Jn[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) pn[u] = A.pos[Jc[u] >= 0 ? Jc[u] : i];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = base + 64 * U + u * 32 + lane;
+      Jn[u] = q < s3 ? row[q] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c0 = base + 32 * u;
+      far_entry<R, VIRIAL, ENERGY, MORSE, SG>(P, c0 >= s1 && c0 + 32 <= s2, J[u] >= 0, pj[u], J[u], i, pi, ki, gid,
+                                              shift, stage, fx, fy, fz, en, W, nlj, ntp);
+    }
+  }
+#else
   int Jn[FAR_UNROLL];
 #pragma unroll
   for (int u = 0; u < FAR_UNROLL; ++u) {
@@ -622,6 +665,7 @@ __device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, 
                                               shift, stage, fx, fy, fz, en, W, nlj, ntp);
     }
   }
+#endif
 }
 
 // warp-uniform segment bounds of atom i's far row: [s0, s1) tested, [s1, s2) PURE, [s2, s3) tested.

@@ -441,3 +441,44 @@ def test_adaptive_reach_table_after_rebuild(eng_mod, monkeypatch):
     d = out[0] - out[1]
     d -= s.box * np.round(d / s.box)
     assert np.abs(d).max() <= 1e-9
+
+
+def _engine_with_skin(eng_mod, s, skin):
+    import re
+    txt = open(eng_mod.PARAMS, "rb").read().decode()
+    txt = re.sub(r"^neigh\.skin .*$", f"neigh.skin {skin}", txt, flags=re.M).encode()
+    e = eng_mod.Engine("fp64", 0, params=txt)
+    e.set_box(s.box)
+    e.set_atoms(s.types, s.x)
+    return e
+
+
+@pytest.mark.parametrize("skin", [1.0, 2.5])
+def test_far_bins_under_displacement(eng_mod, skin):
+    """Far-row bins settled by the displacement bound (k_lists.cuh FB_*): after the list
+    build every atom is moved by up to 0.49 skin (no rebuild), so pairs cross the window radius,
+    r_lo and r_c relative to their build distances; forces, energy and counters must still equal
+    the oracle at the new positions.  skin 2.5 A breaks a_p + 2 skin <= r_lo (H-H): the unbinned
+    fallback, every far entry fully tested."""
+    s = I.config(2)
+    e = _engine_with_skin(eng_mod, s, skin)
+    e.compute()  # builds the lists at s.x
+    rng = np.random.default_rng(7)
+    d = rng.normal(size=s.x.shape)
+    d *= (0.49 * skin * rng.uniform(0.2, 1.0, size=(s.n, 1))) / np.linalg.norm(d, axis=1, keepdims=True)
+    out = np.any((s.x + d < 0.0) | (s.x + d >= s.box), axis=1)
+    d[out] = 0.0  # no atom crosses a face (a wrap would count as a box-length displacement)
+    x = s.x + d
+    nb0 = e.stats()["n_rebuilds"]
+    e.set_positions(x)
+    g = e.compute()
+    assert e.stats()["n_rebuilds"] == nb0  # evaluated on the lists of the first build
+    o = O.compute(s.types, x, s.box)
+    check_fp64(s, g, o)
+    st = e.stats()
+    for k in COUNTERS:
+        assert st[k] == o["counters"][k], (skin, k, st[k], o["counters"][k])
+    # the LJ half pairs within r_c at the displaced positions, from the build-time rows
+    a = e.get_list(2)
+    b = O.get_list(s.types, x, s.box, 2)
+    assert a.shape == b.shape and np.array_equal(a, b)
