@@ -1207,7 +1207,10 @@ Grids grids_of(const ab_engine* e) {
   const bool clp = e->cl_path && e->hp.potential != kREBO;
   G.g_short = nblk(e->NT, 128), G.g_rebo = e->nsm * 4;
   G.g_near = clp ? std::min(nblk((long long)N * 32, 128), e->nsm * AB_LJC_MINBLOCKS) : nblk(N, NEAR_ATOMS);
-  G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * 8);
+#ifndef AB_FAR_GRID
+#define AB_FAR_GRID 32  // blocks per SM of the far-LJ grid (contiguous ranges of ~N / (32 nsm) atoms)
+#endif
+  G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * AB_FAR_GRID);
   G.g_bstar = e->nsm * 4, G.g_lite = e->nsm * AB_LITE_GRID, G.g_slow = e->nsm * 2;
   G.base = G.g_short + 2 * G.g_rebo + 2 * G.g_slow + G.g_near + G.g_far + G.g_lite + G.g_bstar + 2 * G.g_slow;
   return G;
