@@ -164,6 +164,20 @@ __device__ __forceinline__ double rcp_fast(double a) {
   return fma(y, e, y);
 }
 __device__ __forceinline__ float rcp_fast(float a) { return __frcp_rn(a); }
+// one-Newton-step variants (relative error ~1e-14 from the ~2^-23 hardware seeds): the far-LJ
+// pair arithmetic, whose per-pair terms are far below the 1e-9 eV/A force gate
+__device__ __forceinline__ double rcp_nr1(double a) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  return fma(y, fma(-a, y, 1.0), y);
+}
+__device__ __forceinline__ float rcp_nr1(float a) { return __frcp_rn(a); }
+__device__ __forceinline__ double rsqrt_nr1(double a) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  return y * fma(-0.5 * a * y, y, 1.5);
+}
+__device__ __forceinline__ float rsqrt_nr1(float a) { return rsqrtf(a); }
 
 // Branch-free half-cosine on t in [0, 1] (caller clamps): S = (1 + cos(pi t))/2 and dS/dt, from
 // x = pi (t - 1/2) in [-pi/2, pi/2]: cos(pi t) = -sin x, sin(pi t) = cos x, Taylor polynomials

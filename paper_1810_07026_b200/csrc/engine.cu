@@ -161,6 +161,7 @@ struct ab_engine {
   int capI = 0, capS = 0, capQ = 0;
   int far_at = 0;
   bool pdl = false;  // AB_PDL=1: programmatic dependent launch of the b* kernels
+  bool rebo_g4 = false;  // AB_REBO_G4=1: the sp3 C-C batch 4 lanes per bond (k_rebo_g4; measured slower)
   int skip = 0;  // AB_SKIP bit mask (timing ablations only, results wrong): 1 REBO, 2 far, 4 near, 8 b*  // enqueue_forces: fork point of the far-LJ kernel (AB_FAR_AT)
   // NVE steps: the reduction of the partial rows is fused into the second half-kick (k_post)
   bool defer_reduce = false, post_pending = false;
@@ -1416,12 +1417,17 @@ ab_status enqueue_forces(ab_engine* e) {
     R1.row0 = g_short;
     int* const nbig = e->small_i.p + 8;  // large-side overflow (NBMAX kernel)
     int* const nmid = e->small_i.p + 0;  // CH / HH bonds with two non-empty sides
-    auto rebo = [&](auto three, auto fast, auto one, auto slow) {
+    auto rebo = [&](auto three, auto grp, auto fast, auto one, auto slow) {
       if (e->skip & 1) return;
-      // CC region: sides of <= 3 neighbours (sp3 carbon) in the NB = 3 kernel, larger ones go on
-      // to the general NB_FAST kernel through the same hand-over list as the CH / HH bonds
-      three<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, nullptr, 0, 1, e->ovf_mid.p, nmid, S, e->typ.p, e->owner.p,
-                                        e->gid.p, e->shift.p, Fk, sb0, R1);
+      // CC region: sides of <= 3 neighbours (sp3 carbon) in the 4-lanes-per-bond kernel (or the
+      // NB = 3 thread-per-bond kernel), larger ones go on to the general NB_FAST kernel through
+      // the same hand-over list as the CH / HH bonds
+      if (e->rebo_g4)
+        grp<<<g_rebo, 128, 0, s_rebo>>>(BL, 0, e->ovf_mid.p, nmid, S, e->typ.p, e->owner.p, e->gid.p, e->shift.p, Fk,
+                                        sb0, R1);
+      else
+        three<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, nullptr, 0, 1, e->ovf_mid.p, nmid, S, e->typ.p, e->owner.p,
+                                          e->gid.p, e->shift.p, Fk, sb0, R1);
       R1.row0 += g_rebo;
       one<<<g_rebo, 128, 0, s_rebo>>>(BL, nullptr, nullptr, 1, 3, e->ovf_mid.p, nmid, S, e->typ.p, e->owner.p,
                                       e->gid.p, e->shift.p, Fk, sb0, R1);
@@ -1433,11 +1439,11 @@ ab_status enqueue_forces(ab_engine* e) {
                                        e->gid.p, e->shift.p, Fk, sb0, R1);
     };
     if (e->want_virial)
-      rebo(k_rebo<R, 3, true, SG>, k_rebo<R, NB_FAST, true, SG>, k_rebo<R, NB_FAST, true, SG, 0>,
-           k_rebo<R, NBMAX, true, SG>);
+      rebo(k_rebo<R, 3, true, SG>, k_rebo_g4<R, true, SG>, k_rebo<R, NB_FAST, true, SG>,
+           k_rebo<R, NB_FAST, true, SG, 0>, k_rebo<R, NBMAX, true, SG>);
     else
-      rebo(k_rebo<R, 3, false, SG>, k_rebo<R, NB_FAST, false, SG>, k_rebo<R, NB_FAST, false, SG, 0>,
-           k_rebo<R, NBMAX, false, SG>);
+      rebo(k_rebo<R, 3, false, SG>, k_rebo_g4<R, false, SG>, k_rebo<R, NB_FAST, false, SG>,
+           k_rebo<R, NB_FAST, false, SG, 0>, k_rebo<R, NBMAX, false, SG>);
     e->launches += 3;  // + the CKL below: four launches
     CKL();
     prof_stop(e, 1, s_rebo, t);
@@ -1790,6 +1796,7 @@ ab_status init_engine(ab_engine* e, const char* text, size_t len, ab_precision p
   if (const char* fa = std::getenv("AB_FAR_AT")) e->far_at = std::max(0, std::min(2, std::atoi(fa)));
   if (const char* sk = std::getenv("AB_SKIP")) e->skip = std::atoi(sk);
   e->pdl = std::getenv("AB_PDL") && std::getenv("AB_PDL")[0] == '1';
+  if (const char* rg = std::getenv("AB_REBO_G4")) e->rebo_g4 = rg[0] != '0';
   // AB_PRIO=<rebo>,<far>: stream priorities of the REBO and far-LJ branches (scheduling
   // experiments; lower = higher priority, clamped to the device range; default 0 = the engine
   // stream's)

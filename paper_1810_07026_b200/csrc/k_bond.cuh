@@ -608,6 +608,326 @@ __global__ void __launch_bounds__(128, NBJ == 0 ? AB_REBO1_MINBLOCKS
   red_flush(rs, RR);
 }
 
+// ---------------------------------------------------------------- REBO + torsion, 4 lanes per bond
+// The sp3 C-C batch (both sides <= 3 neighbours; P:496-506 for b_ij, Alg. 2 P:390-407 for the
+// torsion) with a lane group per bond instead of one thread: lane s of the group takes side
+// neighbour s of i (k_s) and of J (l_s).  The side sums of the forward pass are reduced over the
+// group; the P splines (lanes 0 / 1) and the pi^rc / T splines (lanes 2 / 3) are evaluated once
+// per group and broadcast; the dihedral / torsion double sum runs as one fused loop over l (each
+// lane its own k): the forward sums D, T and the reverse-pass terms of the same (k, l) pair
+// together (their coefficients need only dE/db = V_A, p_ij / p_ji and T_ij, all known before the
+// loop; the D-dependent parts dN/dN_ij ... are added after it).  The l-side accumulators are
+// reduced to their owning lane; every lane scatters the forces of its own k and l (and their
+// N^conj chains), lane 0 those of i and J.  Per term the arithmetic is that of bo_forward /
+// bo_reverse; only the summation order differs.
+constexpr int RG = 4;
+#ifndef AB_REBOG_MINBLOCKS
+#define AB_REBOG_MINBLOCKS 3
+#endif
+
+template <typename R>
+__device__ __forceinline__ R gsum(unsigned gm, R v) {
+  v += __shfl_xor_sync(gm, v, 1, RG);
+  v += __shfl_xor_sync(gm, v, 2, RG);
+  return v;
+}
+template <typename R>
+__device__ __forceinline__ R gbc(unsigned gm, R v, int src) {
+  return __shfl_sync(gm, v, src, RG);
+}
+
+template <typename R, bool VIR, bool SG = false>
+__global__ void __launch_bounds__(128, AB_REBOG_MINBLOCKS)
+    k_rebo_g4(BondList BL, int reg, int* ovf, int* novf, ShortList<R> S, const signed char* typ, const int* owner,
+              const int* gid, const char4* shift, double* F, StageBuf stage, RedRows RR) {
+  __shared__ RedSmem rs;
+  const int nb = BL.cnt[reg];
+  if (red_idle_block(nb * RG, RR)) return;
+  red_init(rs);
+  const Tab<R>& T = tab<R>();
+  const int lane = threadIdx.x & 31, s = lane & (RG - 1), gsh = lane & ~(RG - 1);
+  const unsigned gm = 0xFu << gsh;
+  double e[3 + 6] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double* const Wv = VIR ? e + 3 : nullptr;
+  unsigned long long nq = 0, nbad = 0, ncount = 0, nang = 0;
+  const int gstride = (gridDim.x * blockDim.x) / RG;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) / RG; t < nb; t += gstride) {
+    const int bidx = reg * BL.cap + t;
+    const int2 bd = BL.b[bidx];
+    const int i = bd.x, q = bd.y;
+    const size_t bi = (size_t)i * S.capS;
+    const int J = S.nbr[bi + q];
+    const size_t bj = (size_t)J * S.capS;
+    const int ni = S.cnt[i], nj = S.cnt[J];
+    if (ni > RG || nj > RG) {  // a side of more than 3: the general kernel
+      if (s == 0) list_append(ovf, novf, 1 << 30, bidx);
+      continue;
+    }
+    const int nbI = s < ni ? S.nbr[bi + s] : -1, nbJ = s < nj ? S.nbr[bj + s] : -1;
+    const unsigned mI = (__ballot_sync(gm, nbI == J) >> gsh) & 0xFu;
+    const unsigned mJ = (__ballot_sync(gm, nbJ == i) >> gsh) & 0xFu;
+    const int pq = mI ? __ffs(mI) - 1 : -1, pl = mJ ? __ffs(mJ) - 1 : -1;
+    const int nI = ni - (pq >= 0), nJ = nj - (pl >= 0);
+    if (nI > 3 || nJ > 3) {
+      if (s == 0) list_append(ovf, novf, 1 << 30, bidx);
+      continue;
+    }
+    R r;
+    const V3<R> d = sl_d(S, i, q, r);
+    const R ir = R(1) / r;
+    const V3<R> u = ir * d, mu = mk3(-u.x, -u.y, -u.z), md = mk3(-d.x, -d.y, -d.z);
+    const int ti = typ[i], tj = typ[J];
+    const bool blendI = ti == 0 && T.g2on, blendJ = tj == 0 && T.g2on;
+    const bool lamI = ti == 1 && T.kappa != R(0), lamJ = tj == 1 && T.kappa != R(0);
+    // ---- this lane's side neighbours: k = k_s of i, l = l_s of J
+    const bool hasK = s < nI, hasL = s < nJ;
+    int k = -1, tk = 0, l = -1, tl = 0;
+    R rk = 1, wk = 0, dwk = 0, ck = 0, g1k = 0, dg1k = 0, g2k = 0, dg2k = 0, ek = 0, Fk = 0, dFk = 0;
+    R rl = 1, wl = 0, dwl = 0, cl = 0, g1l = 0, dg1l = 0, g2l = 0, dg2l = 0, el = 0, Fl = 0, dFl = 0, Gl = 0, dGl = 0;
+    V3<R> dk = mk3<R>(0, 0, 0), dl = mk3<R>(0, 0, 0), uk = dk, ul = dk;
+    R aSI = 0, aSI2 = 0, aNCI = 0, aNHI = 0, aCI = 0, aSJ = 0, aSJ2 = 0, aNCJ = 0, aNHJ = 0, aCJ = 0;
+    if (hasK) {
+      const int qk = side_slot(s, pq);
+      k = S.nbr[bi + qk];
+      dk = sl_d(S, i, qk, rk);
+      const auto wv = S.w[bi + qk];
+      wk = wv.x, dwk = wv.y;
+      tk = typ[k];
+      uk = (R(1) / rk) * dk;
+      ck = clamp_cos(dot3(u, uk));
+      g1k = gspline<R>(ti, ck, dg1k);
+      if (blendI) g2k = gspline<R>(2, ck, dg2k);
+      ek = explam_r<R>(tj, ti, tk, r, rk);
+      aSI = wk * g1k * ek, aSI2 = wk * g2k * ek;
+      if (tk == 0) {
+        aNCI = wk;
+        Fk = F_conj<R>(S.Ntot[k] - wk, dFk);
+        aCI = wk * Fk;
+      } else {
+        aNHI = wk;
+      }
+    }
+    if (hasL) {
+      const int ql = side_slot(s, pl);
+      l = S.nbr[bj + ql];
+      dl = sl_d(S, J, ql, rl);
+      const auto wv = S.w[bj + ql];
+      wl = wv.x, dwl = wv.y;
+      tl = typ[l];
+      ul = (R(1) / rl) * dl;
+      cl = clamp_cos(dot3(mu, ul));
+      g1l = gspline<R>(tj, cl, dg1l);
+      if (blendJ) g2l = gspline<R>(2, cl, dg2l);
+      el = explam_r<R>(ti, tj, tl, r, rl);
+      aSJ = wl * g1l * el, aSJ2 = wl * g2l * el;
+      if (tl == 0) {
+        aNCJ = wl;
+        Fl = F_conj<R>(S.Ntot[l] - wl, dFl);
+        aCJ = wl * Fl;
+      } else {
+        aNHJ = wl;
+      }
+      Gl = guardG<R>(cl, dGl);
+    }
+    // ---- group sums of the two sides
+    R sumI = gsum(gm, aSI), NCi = gsum(gm, aNCI), NHi = gsum(gm, aNHI), Si = gsum(gm, aCI);
+    R sumJ = gsum(gm, aSJ), NCj = gsum(gm, aNCJ), NHj = gsum(gm, aNHJ), Sj = gsum(gm, aCJ);
+    R QI = 1, dQI = 0, QJ = 1, dQJ = 0;
+    if (blendI) {  // g_C(cos, N_ij) = g_C2 + S(N_ij) (g_C - g_C2) (reading A34)
+      const R sumI2 = gsum(gm, aSI2);
+      R dQ;
+      QI = sw<R>(NCi + NHi, T.gnlo, T.gnhi, dQ);
+      dQI = dQ * (sumI - sumI2);
+      sumI = sumI2 + QI * (sumI - sumI2);
+    }
+    if (blendJ) {
+      const R sumJ2 = gsum(gm, aSJ2);
+      R dQ;
+      QJ = sw<R>(NCj + NHj, T.gnlo, T.gnhi, dQ);
+      dQJ = dQ * (sumJ - sumJ2);
+      sumJ = sumJ2 + QJ * (sumJ - sumJ2);
+    }
+    const R Nij = NCi + NHi, Nji = NCj + NHj, Nconj = R(1) + Si * Si + Sj * Sj;
+    // ---- splines, one per lane: P_ij (0), P_ji (1), pi^rc (2), T_ij (3)
+    R sv = 0, sx = 0, sy = 0, sz = 0;
+    if (s < 2) {
+      const int tc = s ? tj : ti, tp = s ? ti : tj;
+      if (tc == 0) sv = pspline<R>(tp, s ? NCj : NCi, s ? NHj : NHi, sx, sy);
+    } else {
+      const int p = ti + tj;
+      if (ti == 1 && tj == 0)  // CH tables take the carbon-side N first
+        sv = rtspline<R>(s - 2, p, Nji, Nij, Nconj, sy, sx, sz);
+      else
+        sv = rtspline<R>(s - 2, p, Nij, Nji, Nconj, sx, sy, sz);
+    }
+    const R PI = gbc(gm, sv, 0), PxI = gbc(gm, sx, 0), PyI = gbc(gm, sy, 0);
+    const R PJ = gbc(gm, sv, 1), PxJ = gbc(gm, sx, 1), PyJ = gbc(gm, sy, 1);
+    const R Rv = gbc(gm, sv, 2), Rx = gbc(gm, sx, 2), Ry = gbc(gm, sy, 2), Rz = gbc(gm, sz, 2);
+    const R Tv = gbc(gm, sv, 3), Tx = gbc(gm, sx, 3), Ty = gbc(gm, sy, 3), Tz = gbc(gm, sz, 3);
+    const R argI = R(1) + sumI + PI, argJ = R(1) + sumJ + PJ;
+    const bool bad = !(argI > R(0)) || !(argJ > R(0));
+    const R pij = rsq(argI), pji = rsq(argJ);
+    // ---- pair terms f_R, f_A; dE/db = V_A
+    const R w = S.w[bi + q].x, dw = S.w[bi + q].y;
+    const int p = ti + tj;
+    const R ea = ex(-T.alpha[p] * r);
+    const R qr = R(1) + T.Q[p] * ir;
+    const R VR = w * qr * T.A[p] * ea;
+    const R dVR = dw * qr * T.A[p] * ea + w * T.A[p] * ea * (-T.Q[p] * ir * ir - T.alpha[p] * qr);
+    R sb = 0, sbb = 0;
+#pragma unroll
+    for (int n = 0; n < 3; ++n) {
+      const R eb = T.B[p][n] * ex(-T.beta[p][n] * r);
+      sb += eb;
+      sbb += T.beta[p][n] * eb;
+    }
+    const R VA = -w * sb, dVA = -dw * sb + w * sbb;
+    const R cb = VA;
+    const R cI = R(-0.25) * cb * pij * pij * pij, cJ = R(-0.25) * cb * pji * pji * pji;
+    const R cD = cb * Tv;
+    // ---- reverse-pass side terms that do not depend on D
+    R gk_ = g1k, dgk_ = dg1k, gl_ = g1l, dgl_ = dg1l;
+    if (blendI) gk_ = g2k + QI * (g1k - g2k), dgk_ = dg2k + QI * (dg1k - dg2k);
+    if (blendJ) gl_ = g2l + QJ * (g1l - g2l), dgl_ = dg2l + QJ * (dg1l - dg2l);
+    R Wk = cI * (gk_ * ek + (tk == 0 ? PxI : PyI) + dQI);
+    R Ck = cI * wk * dgk_ * ek;
+    const R Lk = lamI ? cI * wk * gk_ * ek * T.kappa : R(0);
+    R Wl = cJ * (gl_ * el + (tl == 0 ? PxJ : PyJ) + dQJ);
+    R Cl = cJ * wl * dgl_ * el;
+    const R Ll = lamJ ? cJ * wl * gl_ * el * T.kappa : R(0);
+    V3<R> gk = mk3<R>(0, 0, 0), gd = mk3<R>(0, 0, 0);
+    // ---- fused dihedral / torsion loop: this lane's k against every l of the group
+    R Dp = 0, Tp = 0;
+    int nqp = 0;
+    R aW[3] = {0, 0, 0}, aC[3] = {0, 0, 0};
+    V3<R> ag[3] = {gk, gk, gk};
+    R dGk;
+    const R Gk = hasK ? guardG<R>(ck, dGk) : R(0);
+    const V3<R> n1 = cross3(dk, d);
+    const R inv1 = Gk != R(0) ? rsq(dot3(n1, n1)) : R(0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (c >= nJ) break;  // (group-uniform)
+      const int lc = __shfl_sync(gm, l * 4 + tl, c, RG);
+      const V3<R> dlc = mk3(gbc(gm, dl.x, c), gbc(gm, dl.y, c), gbc(gm, dl.z, c));
+      const R wlc = gbc(gm, wl, c), Glc = gbc(gm, Gl, c), dGlc = gbc(gm, dGl, c);
+      if (!hasK || (lc >> 2) == k) continue;
+      ++nqp;
+      if (Gk == R(0) || Glc == R(0)) continue;
+      const V3<R> n2 = cross3(md, dlc);
+      const R inv2 = rsq(dot3(n2, n2));
+      const R cw = dot3(n1, n2) * inv1 * inv2;
+      const R GG = Gk * Glc, wG = wk * wlc, base = wG * GG;
+      Dp += (R(1) - cw * cw) * base;
+      R coef = cD * (R(1) - cw * cw), dcoef = cD * (R(-2) * cw);
+      {
+        const R tors = T.tors[tk][ti][tj][lc & 3];
+        R dv;
+        const R v = vtors<R>(cw, dv);
+        Tp += tors * base * v;
+        coef += tors * w * v;
+        dcoef += tors * w * dv;
+      }
+      const R dEdcw = dcoef * base;
+      Wk += coef * wlc * GG;
+      aW[c] += coef * wk * GG;
+      Ck += coef * wG * Glc * dGk;
+      aC[c] += coef * wG * Gk * dGlc;
+      // d cos w / d a = b x g1, / d e = b x g2, / d b = g1 x a + g2 x e  (a = d_ik, b = d, e = d_jl)
+      const V3<R> g1 = inv1 * (inv2 * n2 - (cw * inv1) * n1);
+      const V3<R> g2 = inv2 * (inv1 * n1 - (cw * inv2) * n2);
+      addto(gk, dEdcw * cross3(d, g1));
+      addto(ag[c], dEdcw * cross3(d, g2));
+      addto(gd, dEdcw * (cross3(g1, dk) + cross3(g2, dlc)));
+    }
+    const R D = gsum(gm, Dp), Ts = gsum(gm, Tp);
+    nqp += __shfl_xor_sync(gm, nqp, 1, RG);
+    nqp += __shfl_xor_sync(gm, nqp, 2, RG);
+    // l-side accumulators to their owning lane
+    V3<R> gl = mk3<R>(0, 0, 0);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (c >= nJ) break;
+      const R sW = gsum(gm, aW[c]), sC = gsum(gm, aC[c]);
+      const V3<R> sg = mk3(gsum(gm, ag[c].x), gsum(gm, ag[c].y), gsum(gm, ag[c].z));
+      if (s == c) Wl += sW, Cl += sC, gl = sg;
+    }
+    // ---- D-dependent terms; forces on k (with its N^conj chain) and on l
+    const R dNij = cb * (Rx + Tx * D), dNji = cb * (Ry + Ty * D), dNc = cb * (Rz + Tz * D);
+    V3<R> fi = mk3<R>(0, 0, 0), fj = fi;
+    if (hasK) {
+      Wk += dNij;
+      R chain = 0;
+      if (tk == 0) {
+        Wk += dNc * R(2) * Si * Fk;
+        chain = dNc * R(2) * Si * wk * dFk;
+      }
+      if (lamI) addto(gd, Lk * u);
+      const R irk = R(1) / rk;
+      addto(gk, (Wk * dwk - Lk) * uk);
+      addto(gk, (Ck * irk) * (u - ck * uk));
+      addto(gd, (Ck * ir) * (uk - ck * u));
+      atomic_add3<SG>(F, owner[k], -(double)gk.x, -(double)gk.y, -(double)gk.z);
+      fi = gk;
+      vir_add(Wv, dk, gk);
+      if (chain != R(0)) conj_chain<R, SG>(S, owner, k, i, chain, F, Wv);
+    }
+    if (hasL) {
+      Wl += dNji;
+      R chain = 0;
+      if (tl == 0) {
+        Wl += dNc * R(2) * Sj * Fl;
+        chain = dNc * R(2) * Sj * wl * dFl;
+      }
+      const R irl = R(1) / rl;
+      addto(gl, (Wl * dwl - Ll) * ul);
+      if (lamJ) addto(gd, Ll * u);
+      addto(gl, (Cl * irl) * (mu - cl * ul));
+      addto(gd, (-Cl * ir) * (ul + cl * u));
+      atomic_add3<SG>(F, owner[l], -(double)gl.x, -(double)gl.y, -(double)gl.z);
+      fj = gl;
+      vir_add(Wv, dl, gl);
+      if (chain != R(0)) conj_chain<R, SG>(S, owner, l, J, chain, F, Wv);
+    }
+    // ---- i and J (lane 0)
+    gd = mk3(gsum(gm, gd.x), gsum(gm, gd.y), gsum(gm, gd.z));
+    fi = mk3(gsum(gm, fi.x), gsum(gm, fi.y), gsum(gm, fi.z));
+    fj = mk3(gsum(gm, fj.x), gsum(gm, fj.y), gsum(gm, fj.z));
+    if (s == 0) {
+      const R b = R(0.5) * (pij + pji) + Rv + Tv * D;
+      const R dEdr = dVR + b * dVA + dw * Ts;
+      addto(gd, (dEdr * ir) * d);
+      atomic_add3<SG>(F, owner[i], (double)(gd.x + fi.x), (double)(gd.y + fi.y), (double)(gd.z + fi.z));
+      atomic_add3<SG>(F, owner[J], (double)(fj.x - gd.x), (double)(fj.y - gd.y), (double)(fj.z - gd.z));
+      vir_add(Wv, d, gd);
+      e[0] = acc_round<SG>(e[0] + (double)(VR + b * VA));
+      e[1] = acc_round<SG>(e[1] + (double)(w * Ts));
+      nq += nqp;
+      nbad += bad;
+      ncount += 1;
+      nang += nI + nJ;
+      if (VIR && stage.rows) {
+        double* row = stage_row(stage, 13);
+        if (row) {
+          const char4 sj = shift[J];
+          row[0] = gid[i], row[1] = gid[J], row[2] = sj.x, row[3] = sj.y, row[4] = sj.z;
+          row[5] = b, row[6] = pij, row[7] = pji, row[8] = Rv;
+          row[9] = Tv * D;
+          row[10] = Nij, row[11] = Nji, row[12] = Nconj;
+        }
+      }
+    }
+  }
+  red_add_d(rs, ACC_EREBO, e[0]);
+  red_add_d(rs, ACC_ETORS, e[1]);
+  for (int c = 0; c < 6; ++c) red_add_d(rs, ACC_W + c, e[3 + c]);
+  red_add_u(rs, CT_ANGLES, nang);
+  red_add_u(rs, CT_QUADS, nq);
+  red_add_u(rs, CT_BADARG, nbad);
+  red_add_u(rs, CT_BONDS, ncount);
+  red_flush(rs, RR);
+}
+
 // ---------------------------------------------------------------- C_ij path search
 // Direct nested search for M = max{w_ij, w_ik w_kj, w_ik w_kl w_lj} and its maximising path,
 // used when 0 < C_ij < 1 (forces along the path) or when the per-atom reach table overflowed.

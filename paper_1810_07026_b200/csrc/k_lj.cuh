@@ -552,22 +552,26 @@ __device__ __forceinline__ void far_entry(const FarPar<R, MORSE>& P, bool pure, 
   // taper-band pairs (algorithmic flop count): counted by the virial (ab_compute) instantiation only
   if (VIRIAL) ntp += (in && canon && r2 > c_geo.rlo2[P.ti + (hj ? 1 : 0)]);
   const R rr2 = in ? (R)r2 : R(1);
-  R dVr, V;
+  R dVr, V = R(0), s6 = R(0), c6 = R(0);
   if (MORSE) {
     const R y = rsqrt_fast(rr2);
     V = morse_plain<R>(hj ? P.e4b : P.e4a, hj ? P.s2b : P.s2a, hj ? P.c12b : P.c12a, rr2 * y, y, dVr);
   } else {
-    const R inv = rcp_fast(rr2);
+    // 1/r^2 from one hardware reciprocal + one Newton step (relative error ~1e-14, far below the
+    // fp64 parity gate); c12 = 2 c6, so only sigma^2 and c6 = 24 eps are selected per species
+    const R inv = rcp_nr1(rr2);
     const R sr2 = (hj ? P.s2b : P.s2a) * inv;
-    const R s6 = sr2 * sr2 * sr2;
-    dVr = inv * (s6 * fma_r(-(hj ? P.c12b : P.c12a), s6, hj ? P.c6b : P.c6a));
-    V = (hj ? P.e4b : P.e4a) * fma_r(s6, s6, -s6);  // (also the taper's dS term)
+    s6 = sr2 * sr2 * sr2;
+    c6 = hj ? P.c6b : P.c6a;
+    dVr = c6 * (inv * (s6 * fma_r(R(-2), s6, R(1))));
+    if (ENERGY) V = (c6 * R(1.0 / 6.0)) * fma_r(s6, s6, -s6);  // 4 eps (s6^2 - s6)
   }
   const bool tap = !pure && in && r2 > (hj ? P.tvb : P.tva);
   if (__any_sync(0xffffffffu, tap)) {  // (parameters from the constant bank: rare, off the register budget)
     const Tab<R>& T = tab<R>();
     const int pp = P.ti + (hj ? 1 : 0);
-    const R y = rsqrt_fast(rr2);
+    if (!MORSE && !ENERGY) V = (c6 * R(1.0 / 6.0)) * fma_r(s6, s6, -s6);  // the taper's dS term
+    const R y = rsqrt_nr1(rr2);
     const R r = rr2 * y;
     const R iv = T.inv_taper[pp];
     const R tt = (r - T.rlo[pp]) * iv;
