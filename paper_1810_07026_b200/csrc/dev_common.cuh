@@ -616,4 +616,19 @@ __host__ __device__ __forceinline__ long long make_key(int gid, int sx, int sy, 
 __device__ __forceinline__ long long key_of(const double4& p) { return __double_as_longlong(p.w); }
 __device__ __forceinline__ int type_of(const double4& p) { return __double2loint(p.w) & 3; }
 
+// One position record (x, y, z, key: 32 bytes, 32-byte aligned) with ONE 256-bit load
+// (sm_100 ld.global.v4.f64 -> LDG.E.256) instead of the two 128-bit loads a double4 access
+// compiles to: a scattered gather then costs one L1 pass per partner, not two.  Only for arrays
+// the running kernel does not write (the asm carries no memory dependence).  W = false: plain load.
+#ifndef AB_NEAR_POS256
+#define AB_NEAR_POS256 0
+#endif
+template <bool W = true>
+__device__ __forceinline__ double4 ld_pos(const double4* p) {
+  if (!W) return *p;
+  double4 v;
+  asm("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
 }  // namespace ab

@@ -95,6 +95,12 @@ __global__ void k_cell_keys(int NT, const double4* pos, Grid g, int* key, int* v
 //   C_k (k < 8) : r_c + k skin/8 < r_b <= r_c + (k+1) skin/8
 // Bins are filled in candidate order (stable counting sort per row), so rows are deterministic.
 // boff[a * FB_STRIDE + b] = end offset of bin b in atom a's far row.
+#ifndef AB_SHORT_POS256
+#define AB_SHORT_POS256 1  // measured cfg4: k_short 0.2455 -> 0.2439 ms
+#endif
+#ifndef AB_BUILD_POS256
+#define AB_BUILD_POS256 1  // measured cfg4: rebuild 0.6764 -> 0.6731 ms per step
+#endif
 constexpr int FB_L0 = 0, FB_P = 8, FB_A0 = 9, FB_B = 17, FB_C0 = 18, FB_N = 26, FB_STRIDE = 32;
 
 // One warp per atom; candidates stream over contiguous z-runs of the cell stencil.  Near entries
@@ -244,13 +250,13 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
   // chunk is classified and appended
   int sq = lane < total ? stencil_at(cb, pre, lane, k) : -1;
   int b = sq >= 0 ? cell_atoms[sq] : -1;
-  double4 pb = sq >= 0 ? spos[sq] : make_double4(0, 0, 0, 0);
+  double4 pb = sq >= 0 ? ld_pos<AB_BUILD_POS256 != 0>(spos + sq) : make_double4(0, 0, 0, 0);
   for (int base = 0; base < total; base += 32) {
     int kn = __shfl_sync(0xffffffffu, k, 31);
     const int fn = base + 32 + lane;
     const int sqn = fn < total ? stencil_at(cb, pre, fn, kn) : -1;
     const int bn = sqn >= 0 ? cell_atoms[sqn] : -1;
-    const double4 pbn = sqn >= 0 ? spos[sqn] : make_double4(0, 0, 0, 0);
+    const double4 pbn = sqn >= 0 ? ld_pos<AB_BUILD_POS256 != 0>(spos + sqn) : make_double4(0, 0, 0, 0);
     const bool ok = b >= 0 && b != a;
     double r2 = 1e300;
     int pr = 0;
@@ -349,7 +355,7 @@ __global__ void __launch_bounds__(128) k_build_inter(int NT, const double4* pos,
     const int b = sq >= 0 ? cell_atoms[sq] : -1;
     bool in = false;
     if (b >= 0 && b != a) {
-      const double4 pb = spos[sq];
+      const double4 pb = ld_pos<AB_BUILD_POS256 != 0>(spos + sq);
       const double r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
       in = r2 <= c_geo.rmax_s2[ta + type_of(pb)];
     }
@@ -430,7 +436,7 @@ __global__ void k_short(int N, int NT, const double4* pos, const int* in_cnt, co
 #pragma unroll
     for (int u = 0; u < SHORT_BATCH; ++u) bq[u] = q0 + u < ci ? row[q0 + u] : a;
 #pragma unroll
-    for (int u = 0; u < SHORT_BATCH; ++u) pq[u] = pos[bq[u]];
+    for (int u = 0; u < SHORT_BATCH; ++u) pq[u] = ld_pos<AB_SHORT_POS256 != 0>(pos + bq[u]);
 #pragma unroll
     for (int u = 0; u < SHORT_BATCH; ++u) {
       if (q0 + u >= ci) break;

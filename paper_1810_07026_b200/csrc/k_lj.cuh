@@ -314,13 +314,13 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   if (cntN > 0) {
     const int* row = A.nbr[0] + (size_t)i * A.cap[0];
     int Jn = gl < cntN ? row[gl] : i;
-    double4 pjn = A.pos[Jn];
+    double4 pjn = ld_pos<AB_NEAR_POS256 != 0>(A.pos + Jn);
     for (int q = gl; q < cntN; q += NEAR_GROUP) {
       const int J = Jn;
       const double4 pj = pjn;
       if (q + NEAR_GROUP < cntN) {
         Jn = row[q + NEAR_GROUP];
-        pjn = A.pos[Jn];
+        pjn = ld_pos<AB_NEAR_POS256 != 0>(A.pos + Jn);
       }
       const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
       const double r2 = r2_exact(dx, dy, dz);
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   // then the far row is scanned with the nested path search (P:866's sequential fallback).
   if (active) {
     auto correct = [&](int J, double Md) {
-      const double4 pj = A.pos[J];
+      const double4 pj = ld_pos<AB_NEAR_POS256 != 0>(A.pos + J);
       const double dx = __dsub_rn(pj.x, pi.x), dy = __dsub_rn(pj.y, pi.y), dz = __dsub_rn(pj.z, pi.z);
       const double r2 = r2_exact(dx, dy, dz);
       const int p = ti + type_of(pj);
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
       const int c1 = A.cnt[1][i];
       for (int q = gl; q < c1; q += NEAR_GROUP) {
         const int J = row1[q];
-        const double4 pj = A.pos[J];
+        const double4 pj = ld_pos<AB_NEAR_POS256 != 0>(A.pos + J);
         const double r2 = r2_exact(__dsub_rn(pj.x, pi.x), __dsub_rn(pj.y, pi.y), __dsub_rn(pj.z, pi.z));
         if (r2 > c_geo.reach2) continue;
         const double Md = (double)path_search(S, i, J).M;
@@ -509,6 +509,21 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 #ifndef AB_FAR_PIPE
 #define AB_FAR_PIPE 0
 #endif
+#ifndef AB_FAR_TAIL
+#define AB_FAR_TAIL 0
+#endif
+#ifndef AB_FAR_PREF
+#define AB_FAR_PREF 1  // 1: next row of the warp prefetched into L2 (measured cfg4: far 2.557 -> 2.402 ms), 2: into L1 (same), 3: + its first positions
+#endif
+#ifndef AB_FAR_IDX
+#define AB_FAR_IDX 2  // (measured cfg4: 2.341 -> 2.332 ms) 1: far-row indices loaded with the streaming policy (ld.global.cs), 2: L1::no_allocate
+#endif
+#ifndef AB_FAR_POS256
+#define AB_FAR_POS256 1  // partner positions gathered with one 256-bit load (ld_pos; measured cfg4: far 2.41 -> 2.34 ms)
+#endif
+#ifndef AB_FAR_PJ
+#define AB_FAR_PJ 0
+#endif
 #ifndef AB_FAR_SWEEP
 #define AB_FAR_SWEEP 1  // measured (cfg4): contiguous per-block atom ranges 2.71 -> 2.66 ms
 #endif
@@ -516,6 +531,20 @@ constexpr int FAR_UNROLL = AB_FAR_UNROLL;
 
 // Far-pair parameters of the two species pairs (t_i, t_j = C / H) a warp can meet (t_i is warp-
 // uniform): 12-6 form V = e4 s6 (s6 - 1), (dV/dr)/r = inv_r2 s6 (6 e4 - 12 e4 s6), s6 = (sigma^2 inv_r2)^3.
+// far-row index / partner position loads (A/B knobs above)
+__device__ __forceinline__ int far_ld_idx(const int* p) {
+#if AB_FAR_IDX == 1
+  return __ldcs(p);
+#elif AB_FAR_IDX == 2
+  int v;
+  asm("ld.global.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ double4 far_ld_pos(const double4* p) { return ld_pos<AB_FAR_POS256 != 0>(p); }
+
 template <typename R, bool MORSE>
 struct FarPar {
   R e4a, e4b, s2a, s2b, c12a, c12b, c6a, c6b;  // 4 eps, sigma^2, 12 * 4 eps, 6 * 4 eps (Morse: eps, alpha, r_e, -)
@@ -651,20 +680,52 @@ __device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, 
 #pragma unroll
   for (int u = 0; u < FAR_UNROLL; ++u) {
     const int q = s0 + u * 32 + lane;
-    Jn[u] = q < s3 ? row[q] : -1;
+    Jn[u] = q < s3 ? far_ld_idx(row + q) : -1;
   }
+#if AB_FAR_PJ
+  // indices two iterations ahead, so the next iteration's partner positions can be prefetched
+  // into L1 while this iteration computes (no registers held for them)
+  int Jnn[FAR_UNROLL];
+#pragma unroll
+  for (int u = 0; u < FAR_UNROLL; ++u) {
+    const int q = s0 + 32 * FAR_UNROLL + u * 32 + lane;
+    Jnn[u] = q < s3 ? far_ld_idx(row + q) : -1;
+  }
+#endif
+#if AB_FAR_TAIL
+  // rows end anywhere inside an iteration of FAR_UNROLL chunks: the last <= FAR_TAIL chunks run as
+  // one shorter iteration (their indices are already in Jn), so the empty chunks of the last full
+  // iteration (1.5 of ~12 per row on cfg4) are not evaluated
+  constexpr int FAR_TAIL = FAR_UNROLL / 2;
+  int base = s0;
+  for (; s3 - base > 32 * FAR_TAIL; base += 32 * FAR_UNROLL) {
+#else
   for (int base = s0; base < s3; base += 32 * FAR_UNROLL) {
+#endif
     int J[FAR_UNROLL];
     double4 pj[FAR_UNROLL];
 #pragma unroll
     for (int u = 0; u < FAR_UNROLL; ++u) J[u] = Jn[u];
 #pragma unroll
-    for (int u = 0; u < FAR_UNROLL; ++u) pj[u] = A.pos[J[u] >= 0 ? J[u] : i];
+    for (int u = 0; u < FAR_UNROLL; ++u) pj[u] = far_ld_pos(A.pos + (J[u] >= 0 ? J[u] : i));
+#if AB_FAR_PJ
+#pragma unroll
+    for (int u = 0; u < FAR_UNROLL; ++u) {
+      Jn[u] = Jnn[u];
+      if (Jn[u] >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.pos + Jn[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < FAR_UNROLL; ++u) {
+      const int q = base + 64 * FAR_UNROLL + u * 32 + lane;
+      Jnn[u] = q < s3 ? far_ld_idx(row + q) : -1;
+    }
+#else
 #pragma unroll
     for (int u = 0; u < FAR_UNROLL; ++u) {
       const int q = base + 32 * FAR_UNROLL + u * 32 + lane;
-      Jn[u] = q < s3 ? row[q] : -1;
+      Jn[u] = q < s3 ? far_ld_idx(row + q) : -1;
     }
+#endif
 #pragma unroll
     for (int u = 0; u < FAR_UNROLL; ++u) {
       const int c0 = base + 32 * u;
@@ -672,6 +733,19 @@ __device__ __forceinline__ void far_row(const LJArgs& A, int i, int s0, int s1, 
                                               shift, stage, fx, fy, fz, en, W, nlj, ntp);
     }
   }
+#if AB_FAR_TAIL
+  if (base < s3) {
+    double4 pj[FAR_TAIL];
+#pragma unroll
+    for (int u = 0; u < FAR_TAIL; ++u) pj[u] = A.pos[Jn[u] >= 0 ? Jn[u] : i];
+#pragma unroll
+    for (int u = 0; u < FAR_TAIL; ++u) {
+      const int c0 = base + 32 * u;
+      far_entry<R, VIRIAL, ENERGY, MORSE, SG>(P, c0 >= s1 && c0 + 32 <= s2, Jn[u] >= 0, pj[u], Jn[u], i, pi, ki, gid,
+                                              shift, stage, fx, fy, fz, en, W, nlj, ntp);
+    }
+  }
+#endif
 #endif
 }
 
@@ -749,13 +823,49 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     const long long ki = key_of(pi);
     int s0, s1, s2, s3;
     far_segments(A, i, pi, D, s0, s1, s2, s3);
+#if AB_FAR_PREF && AB_FAR_SWEEP
+    {  // the warp's next row (a fresh DRAM stream whose first indices nothing else would have
+       // requested before the row starts): one 128-byte line per lane, as far as this row reaches
+      const int inx = i + wpb, off = lane * 32;
+      if (inx < b1 && off < s3 + 32 && off < A.cap[1]) {
+        const int* q = A.nbr[1] + (size_t)inx * A.cap[1] + off;
+#if AB_FAR_PREF == 2
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+#else
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+#endif
+      }
+    }
+#endif
     double fx = 0, fy = 0, fz = 0;
     far_row<R, VIRIAL, ENERGY || VIRIAL, MORSE, SG>(A, i, s0, s1, s2, s3, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
+#if AB_FAR_PREF >= 3 && AB_FAR_SWEEP
+    // first partner positions of the warp's next row (its indices were prefetched a row ago)
+    int jp[2] = {-1, -1};
+    {
+      const int inx = i + wpb;
+      if (inx < b1) {
+        const int cn = A.cnt[1][inx];
+        const int* rn = A.nbr[1] + (size_t)inx * A.cap[1];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int q = s0 + 32 * u + lane;
+          const int j = q < A.cap[1] ? rn[q] : -1;
+          jp[u] = q < cn ? j : -1;
+        }
+      }
+    }
+#endif
     fx = warp_sum<SG>(fx);
     fy = warp_sum<SG>(fy);
     fz = warp_sum<SG>(fz);
     if (lane == 0) atomic_add3<SG>(F, i, fx, fy, fz);
     if (lane == 0) ne += (unsigned long long)(s3 - s0);
+#if AB_FAR_PREF >= 3 && AB_FAR_SWEEP
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (jp[u] >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.pos + jp[u]));
+#endif
   }
   }
   red_add_d(rs, ACC_ELJ, 0.5 * en);
