@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 // Branch-free bodies (out-of-range lanes weighted by 0), 4 independent gathers in flight per lane;
 // the taper (half-cosine polynomial) only runs when some lane of the warp is in the taper band.
 #ifndef AB_FAR_UNROLL
-#define AB_FAR_UNROLL 4
+#define AB_FAR_UNROLL 2  // with the row prefetch and 256-bit gathers (cfg4): 4 chunks x 4 blocks/SM 2.326 ms, 2 x 6 2.153, 1 x 8 2.145, 2 x 7 2.155, 2 x 8 2.184, 3 x 5 2.351
 #endif
 #ifndef AB_FAR_PIPE
 #define AB_FAR_PIPE 0
@@ -791,7 +791,7 @@ __device__ __forceinline__ void far_segments(const LJArgs& A, int i, double4 pi,
 
 template <typename R, bool VIRIAL, bool MORSE, bool SG = false, bool RANGED = false, bool ENERGY = true>
 #ifndef AB_FAR_MINBLOCKS
-#define AB_FAR_MINBLOCKS 4
+#define AB_FAR_MINBLOCKS 6
 #endif
 __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, const int* gid, const char4* shift, double* F, double* acc,
                                                unsigned long long* ct, StageBuf stage, RedRows RR) {

@@ -20,6 +20,6 @@ def one(spec):
     return name, r.returncode, r.stderr[-2000:]
 
 
-with ThreadPoolExecutor(max_workers=4) as ex:
+with ThreadPoolExecutor(max_workers=7) as ex:
     for name, rc, err in ex.map(one, sys.argv[1:]):
         print(name, "ok" if rc == 0 else "FAILED\n" + err)
