@@ -196,6 +196,7 @@ struct ab_engine {
   DBuf<signed char> typ;
   DBuf<int> ljc[3], ljn[3], in_cnt, in_nbr;  // LJ near / far / (unused) lists, intermediate list
   DBuf<unsigned short> ljboff;               // far-row bin ends (k_lists.cuh FB_*)
+  DBuf<int> smq;                             // k_lj_far per-SM queue counters (AB_FAR_SMQ)
   int capL[3] = {0, 0, 0};
   // j-cluster LJ path (k_cluster.cuh, k_ljc.cuh), AB_LJ_CLUSTER=1; default: per-atom near / far lists
   bool cl_path = false;
@@ -1199,6 +1200,7 @@ LJArgs lj_args(ab_engine* e) {
   }
   A.binned = binned ? 1 : 0;
   A.maxreach = reinterpret_cast<unsigned long long*>(e->scratch.p + SCRATCH_MAXREACH);
+  A.smq = nullptr, A.nq = 0, A.qper = 0;
   return A;
 }
 
@@ -1211,7 +1213,15 @@ Grids grids_of(const ab_engine* e) {
 #ifndef AB_FAR_GRID
 #define AB_FAR_GRID 32  // blocks per SM of the far-LJ grid (contiguous ranges of ~N / (32 nsm) atoms)
 #endif
+#if AB_FAR_SMQ
+#ifndef AB_FAR_SMQ_BLOCKS
+#define AB_FAR_SMQ_BLOCKS AB_FAR_MINBLOCKS
+#endif
+  // per-SM queues: one resident wave (slab mode keeps the static ranges and their finer grid)
+  G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * (slabbed(e) ? AB_FAR_GRID : AB_FAR_SMQ_BLOCKS));
+#else
   G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * AB_FAR_GRID);
+#endif
   G.g_bstar = e->nsm * 4, G.g_lite = e->nsm * AB_LITE_GRID, G.g_slow = e->nsm * 2;
   G.base = G.g_short + 2 * G.g_rebo + 2 * G.g_slow + G.g_near + G.g_far + G.g_lite + G.g_bstar + 2 * G.g_slow;
   return G;
@@ -1380,6 +1390,13 @@ ab_status enqueue_forces(ab_engine* e) {
     auto far = [&](auto kern) {
       if (!(e->skip & 2)) kern<<<g_far, 128, 0, s_far>>>(A, e->gid.p, e->shift.p, Fk, e->acc.p, e->ct.p, sb1, R6);
     };
+#if AB_FAR_SMQ
+    if (!far_split && !slabbed(e) && !(e->skip & 2)) {
+      CK(e->smq.ensure((size_t)e->nsm));
+      CK(cudaMemsetAsync(e->smq.p, 0, sizeof(int) * e->nsm, s_far));
+      A.smq = e->smq.p, A.nq = e->nsm, A.qper = (N + e->nsm - 1) / e->nsm;
+    }
+#endif
     if (far_split) {
       if (e->want_virial) morse ? far(k_lj_far<R, true, true, SG, true>) : far(k_lj_far<R, true, false, SG, true>);
       else if (e->want_energy) morse ? far(k_lj_far<R, false, true, SG, true>) : far(k_lj_far<R, false, false, SG, true>);
@@ -1928,6 +1945,7 @@ void free_engine(ab_engine* e) {
   for (auto* b : bu) b->release();
   e->Ff.release();
   e->ljboff.release();
+  e->smq.release();
   e->shift.release();
   e->rshift.release();
   e->typ.release();

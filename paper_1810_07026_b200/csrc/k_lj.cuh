@@ -140,6 +140,8 @@ struct LJArgs {
   double skin, i2, i8;                 // skin, 4 / skin, 8 / skin
   int binned;                          // 0: every far entry through the fully tested body
   unsigned long long* maxreach;        // k_lj_near: persistent max reach-set size (nullptr: off)
+  int* smq;                            // k_lj_far: per-SM queue counters [nq], zero at launch (nullptr: static ranges)
+  int nq, qper;                        // queues, atoms per queue
 };
 
 __device__ __forceinline__ void stage_lj_row(StageBuf stage, int gi, int gj, char4 sh, double C, double bs) {
@@ -208,6 +210,22 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
   const int i = blockIdx.x * NEAR_ATOMS + grp;
   const bool active = i < A.N;
   const int cntN = active ? A.cnt[0][i] : 0;
+#if AB_NEAR_PREF
+  // the atom's window row (step 2) requested now, so it arrives while the reach set is built
+  if (active) {
+    const int* prow = A.nbr[0] + (size_t)i * A.cap[0];
+    for (int q = gl * 32; q < cntN; q += NEAR_GROUP * 32) {
+#if AB_NEAR_PREF == 2
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(prow + q));
+#else
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(prow + q));
+#endif
+    }
+#if AB_NEAR_PREF == 3
+    for (int q = gl; q < cntN; q += NEAR_GROUP) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.pos + prow[q]));
+#endif
+  }
+#endif
 
   // 1. reach set of i: lane per neighbour k of i enumerates k, l in N(k), m in N(l)
   for (int q = gl; q < SL / 4; q += NEAR_GROUP)
@@ -513,13 +531,16 @@ __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_
 #define AB_FAR_TAIL 0
 #endif
 #ifndef AB_FAR_PREF
-#define AB_FAR_PREF 1  // 1: next row of the warp prefetched into L2 (measured cfg4: far 2.557 -> 2.402 ms), 2: into L1 (same), 3: + its first positions
+#define AB_FAR_PREF 1  // 1: next row of the warp prefetched into L2 (measured cfg4: far 2.557 -> 2.402 ms), 2: into L1 (same), (its first positions too: slower)
 #endif
 #ifndef AB_FAR_IDX
 #define AB_FAR_IDX 2  // (measured cfg4: 2.341 -> 2.332 ms) 1: far-row indices loaded with the streaming policy (ld.global.cs), 2: L1::no_allocate
 #endif
 #ifndef AB_FAR_POS256
 #define AB_FAR_POS256 1  // partner positions gathered with one 256-bit load (ld_pos; measured cfg4: far 2.41 -> 2.34 ms)
+#endif
+#ifndef AB_FAR_SMQ
+#define AB_FAR_SMQ 0
 #endif
 #ifndef AB_FAR_PJ
 #define AB_FAR_PJ 0
@@ -798,36 +819,24 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
   __shared__ RedSmem rs;
   red_init(rs);
   const int lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
   double en = 0;
   double W[6] = {0, 0, 0, 0, 0, 0};
   unsigned nlj = 0, ntp = 0;
   unsigned long long ne = 0;
   const double D = A.dbound ? sqrt(__longlong_as_double((long long)*A.dbound)) : 0.5 * A.skin;
-  // grid-stride over atoms: a resident grid, one warp per atom at a time
-  // RANGED (slab interior / boundary split): the two atom ranges one after the other; otherwise
-  // every atom (a separate instantiation: the range bookkeeping cost 6 % of the kernel on cfg4)
-  for (int range = 0; range < (RANGED ? 2 : 1); ++range) {
-  const int rb = RANGED ? (range ? A.r1b : A.r0b) : 0, re = RANGED ? (range ? A.r1e : A.r0e) : A.N;
-#if AB_FAR_SWEEP
-  // each block sweeps a contiguous (cell-ordered, hence compact) range of atoms with its warps
-  // interleaved, so the neighbourhoods of successive atoms meet in the SM's L1
-  const int per = (re - rb + gridDim.x - 1) / gridDim.x, wpb = blockDim.x >> 5;
-  const int b0 = rb + blockIdx.x * per, b1 = min(re, b0 + per);
-  for (int i = b0 + (threadIdx.x >> 5); i < b1; i += wpb) {
-#else
-  for (int i = rb + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < re; i += nwarps) {
-#endif
+  // one atom's far row by this warp; inx = the atom this warp takes next (-1: none): its row is
+  // requested now (a fresh DRAM stream whose first indices nothing else would have asked for
+  // before the row starts), one 128-byte line per lane, as far as this row reaches
+  auto atom = [&](int i, int inx) {
     const double4 pi = A.pos[i];
     const int ti = type_of(pi);
     const long long ki = key_of(pi);
     int s0, s1, s2, s3;
     far_segments(A, i, pi, D, s0, s1, s2, s3);
-#if AB_FAR_PREF && AB_FAR_SWEEP
-    {  // the warp's next row (a fresh DRAM stream whose first indices nothing else would have
-       // requested before the row starts): one 128-byte line per lane, as far as this row reaches
-      const int inx = i + wpb, off = lane * 32;
-      if (inx < b1 && off < s3 + 32 && off < A.cap[1]) {
+#if AB_FAR_PREF
+    {
+      const int off = lane * 32;
+      if (inx >= 0 && off < s3 + 32 && off < A.cap[1]) {
         const int* q = A.nbr[1] + (size_t)inx * A.cap[1] + off;
 #if AB_FAR_PREF == 2
         asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
@@ -839,34 +848,74 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
 #endif
     double fx = 0, fy = 0, fz = 0;
     far_row<R, VIRIAL, ENERGY || VIRIAL, MORSE, SG>(A, i, s0, s1, s2, s3, pi, ti, ki, gid, shift, stage, fx, fy, fz, en, W, nlj, ntp);
-#if AB_FAR_PREF >= 3 && AB_FAR_SWEEP
-    // first partner positions of the warp's next row (its indices were prefetched a row ago)
-    int jp[2] = {-1, -1};
-    {
-      const int inx = i + wpb;
-      if (inx < b1) {
-        const int cn = A.cnt[1][inx];
-        const int* rn = A.nbr[1] + (size_t)inx * A.cap[1];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int q = s0 + 32 * u + lane;
-          const int j = q < A.cap[1] ? rn[q] : -1;
-          jp[u] = q < cn ? j : -1;
-        }
-      }
-    }
-#endif
     fx = warp_sum<SG>(fx);
     fy = warp_sum<SG>(fy);
     fz = warp_sum<SG>(fz);
     if (lane == 0) atomic_add3<SG>(F, i, fx, fy, fz);
     if (lane == 0) ne += (unsigned long long)(s3 - s0);
-#if AB_FAR_PREF >= 3 && AB_FAR_SWEEP
-#pragma unroll
-    for (int u = 0; u < 2; ++u)
-      if (jp[u] >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.pos + jp[u]));
+  };
+#if AB_FAR_SMQ
+  // Per-SM queues: the cell-ordered atoms are cut into A.nq contiguous ranges of A.qper atoms;
+  // every warp draws single atoms from the range of the SM it runs on (%smid), so all the warps
+  // of an SM work through neighbouring atoms at the same time and their partner gathers meet in
+  // that SM's L1.  A warp whose range is used up moves on to the next range that still has atoms
+  // (ranges of SMs that received fewer blocks, e.g. beside a concurrent kernel, are finished by
+  // the others).  Tickets are drawn two atoms ahead: the atomic's latency and the next row's
+  // prefetch both hide behind the current row.
+  if (!RANGED && A.smq) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    const int nq = A.nq, per = A.qper;
+    int q = (int)(smid % (unsigned)nq);
+    auto draw = [&]() {  // lane 0 holds the ticket
+      int t = 0;
+      if (lane == 0) t = atomicAdd(A.smq + q, 1);
+      return t;
+    };
+    auto resolve = [&](int t) {  // ticket -> atom (-1: range used up)
+      t = __shfl_sync(0xffffffffu, t, 0);
+      const int i = q * per + t;
+      return (t < per && i < A.N) ? i : -1;
+    };
+    int cur = resolve(draw());
+    int nraw = draw();
+    for (;;) {
+      if (cur < 0) {  // this range is used up: the next range with atoms left (32 ranges per look)
+        int found = -1;
+        for (int o = 1; o < nq && found < 0; o += 32) {
+          const int c = o + lane;
+          const int qq = (q + c) % nq;
+          const bool has = c < nq && *(volatile int*)(A.smq + qq) < min(per, A.N - qq * per);
+          const unsigned m = __ballot_sync(0xffffffffu, has);
+          if (m) found = (q + o + __ffs(m) - 1) % nq;
+        }
+        if (found < 0) break;
+        q = found;
+        cur = resolve(draw());
+        nraw = draw();
+        continue;
+      }
+      const int nxt = resolve(nraw);
+      nraw = draw();
+      atom(cur, nxt);
+      cur = nxt;
+    }
+  } else
 #endif
-  }
+  // RANGED (slab interior / boundary split): the two atom ranges one after the other; otherwise
+  // every atom (a separate instantiation: the range bookkeeping cost 6 % of the kernel on cfg4)
+  for (int range = 0; range < (RANGED ? 2 : 1); ++range) {
+    const int rb = RANGED ? (range ? A.r1b : A.r0b) : 0, re = RANGED ? (range ? A.r1e : A.r0e) : A.N;
+#if AB_FAR_SWEEP
+    // each block sweeps a contiguous (cell-ordered, hence compact) range of atoms with its warps
+    // interleaved, so the neighbourhoods of successive atoms meet in the SM's L1
+    const int per = (re - rb + gridDim.x - 1) / gridDim.x, wpb = blockDim.x >> 5;
+    const int b0 = rb + blockIdx.x * per, b1 = min(re, b0 + per);
+    for (int i = b0 + (threadIdx.x >> 5); i < b1; i += wpb) atom(i, i + wpb < b1 ? i + wpb : -1);
+#else
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int i = rb + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < re; i += nwarps) atom(i, i + nwarps < re ? i + nwarps : -1);
+#endif
   }
   red_add_d(rs, ACC_ELJ, 0.5 * en);
   if (VIRIAL)
