@@ -179,7 +179,7 @@ __device__ __forceinline__ double reach_lookup_fast(const ReachSmem<SL>& s, int 
 
 template <typename R, bool VIRIAL, bool MORSE, bool SG = false, int SL = NEAR_SLOTS>
 #ifndef AB_NEAR_MINBLOCKS
-#define AB_NEAR_MINBLOCKS 6  // measured (cfg4, 4-lane groups): 6 blocks beat 7
+#define AB_NEAR_MINBLOCKS 7  // measured (cfg4, 4-lane groups, with the window-row prefetch): 5 / 6 / 7 blocks 1.239 / 1.073 / 1.017 ms (7 = the shared-memory limit with 64-slot tables)
 #endif
 __global__ void __launch_bounds__(NEAR_GROUP * NEAR_ATOMS, AB_NEAR_MINBLOCKS) k_lj_near(LJArgs A, ShortList<R> S, const int* owner,
                                                                     const int* gid, const char4* shift, double* F,
