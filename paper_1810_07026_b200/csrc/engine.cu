@@ -1218,7 +1218,7 @@ Grids grids_of(const ab_engine* e) {
 #define AB_FAR_SMQ_BLOCKS AB_FAR_MINBLOCKS
 #endif
   // per-SM queues: one resident wave (slab mode keeps the static ranges and their finer grid)
-  G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * (slabbed(e) ? AB_FAR_GRID : AB_FAR_SMQ_BLOCKS));
+  G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * ((slabbed(e) || AB_FAR_SMQ == 2) ? AB_FAR_GRID : AB_FAR_SMQ_BLOCKS));
 #else
   G.g_far = clp ? 0 : std::min(nblk((long long)N * 32, 128), e->nsm * AB_FAR_GRID);
 #endif

@@ -98,6 +98,9 @@ __global__ void k_cell_keys(int NT, const double4* pos, Grid g, int* key, int* v
 #ifndef AB_SHORT_POS256
 #define AB_SHORT_POS256 1  // measured cfg4: k_short 0.2455 -> 0.2439 ms
 #endif
+#ifndef AB_BUILD_SEL
+#define AB_BUILD_SEL 0
+#endif
 #ifndef AB_BUILD_POS256
 #define AB_BUILD_POS256 1  // measured cfg4: rebuild 0.6764 -> 0.6731 ms per step
 #endif
@@ -245,6 +248,10 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
   int* hist = s_hist[w];
   if (lane <= FB_N) hist[lane] = 0;
   const int total = stencil_columns(g, p, nr, Lg.reach_t[ta], cell_start, cb, pre);
+#if AB_BUILD_SEL
+  const double rcs_a = c_geo.rc_s2[ta], rcs_b = c_geo.rc_s2[ta + 1], bq_a = Lg.bq2[ta], bq_b = Lg.bq2[ta + 1];
+  const double flo_a = Lg.flo2[ta], flo_b = Lg.flo2[ta + 1];
+#endif
   int k = 0;  // column of the chunk's first candidate (warp-uniform)
   // software pipeline: the next chunk's index and position loads are in flight while this
   // chunk is classified and appended
@@ -264,9 +271,18 @@ __global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, con
       r2 = r2_exact(__dsub_rn(pb.x, p.x), __dsub_rn(pb.y, p.y), __dsub_rn(pb.z, p.z));
       pr = ta + type_of(pb);
     }
+#if AB_BUILD_SEL
+    // the atom's species is warp-uniform, so the pair's is one of two: selects from registers
+    // instead of constant-bank loads indexed per lane (replayed per distinct address)
+    const bool hb = pr != ta;
+    const bool in = ok && r2 <= (hb ? rcs_b : rcs_a);
+    const bool nearp = in && r2 <= (hb ? bq_b : bq_a);
+    const bool farp = in && r2 >= (hb ? flo_b : flo_a);
+#else
     const bool in = ok && r2 <= c_geo.rc_s2[pr];
     const bool nearp = in && r2 <= Lg.bq2[pr];
     const bool farp = in && r2 >= Lg.flo2[pr];
+#endif
     warp_append(nearp, row0, Lg.cap[0], n0, b);
     {  // stage far entries with their bin (candidate order) and count them per bin
       const unsigned m = __ballot_sync(0xffffffffu, farp);

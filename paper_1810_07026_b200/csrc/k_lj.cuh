@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     if (lane == 0) atomic_add3<SG>(F, i, fx, fy, fz);
     if (lane == 0) ne += (unsigned long long)(s3 - s0);
   };
-#if AB_FAR_SMQ
+#if AB_FAR_SMQ == 1
   // Per-SM queues: the cell-ordered atoms are cut into A.nq contiguous ranges of A.qper atoms;
   // every warp draws single atoms from the range of the SM it runs on (%smid), so all the warps
   // of an SM work through neighbouring atoms at the same time and their partner gathers meet in
@@ -910,7 +910,35 @@ __global__ void __launch_bounds__(128, AB_FAR_MINBLOCKS) k_lj_far(LJArgs A, cons
     // each block sweeps a contiguous (cell-ordered, hence compact) range of atoms with its warps
     // interleaved, so the neighbourhoods of successive atoms meet in the SM's L1
     const int per = (re - rb + gridDim.x - 1) / gridDim.x, wpb = blockDim.x >> 5;
-    const int b0 = rb + blockIdx.x * per, b1 = min(re, b0 + per);
+    int bid = blockIdx.x;
+#if AB_FAR_SMQ == 2
+    // Block ranges drawn per SM: the gridDim.x block ranges are dealt to A.nq queues of
+    // consecutive ranges, and a block takes the next range of the queue of the SM it runs on
+    // (%smid), so the blocks resident on one SM sweep adjacent ranges and their partner gathers
+    // meet in that SM's L1.  A block whose queue is used up takes a range of the next queue that
+    // has one left; there are exactly as many ranges as blocks and every block takes exactly one.
+    if (!RANGED && A.smq) {
+      __shared__ int s_bid;
+      if (threadIdx.x == 0) {
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        const int nq = A.nq, tpq = (gridDim.x + nq - 1) / nq;
+        int q = (int)(smid % (unsigned)nq), got = -1;
+        while (got < 0) {
+          const int cntq = min(tpq, (int)gridDim.x - q * tpq);  // ranges of queue q (<= 0: none)
+          if (cntq > 0 && *(volatile int*)(A.smq + q) < cntq) {
+            const int t = atomicAdd(A.smq + q, 1);
+            if (t < cntq) got = q * tpq + t;
+          }
+          q = q + 1 == nq ? 0 : q + 1;
+        }
+        s_bid = got;
+      }
+      __syncthreads();
+      bid = s_bid;
+    }
+#endif
+    const int b0 = rb + bid * per, b1 = min(re, b0 + per);
     for (int i = b0 + (threadIdx.x >> 5); i < b1; i += wpb) atom(i, i + wpb < b1 ? i + wpb : -1);
 #else
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
