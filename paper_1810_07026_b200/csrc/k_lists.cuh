@@ -225,7 +225,10 @@ __global__ void k_sorted_pos(int NT, const int* cell_atoms, const double4* pos, 
   if (q < NT) spos[q] = pos[cell_atoms[q]];
 }
 
-__global__ void __launch_bounds__(128) k_build_lj(int N, const double4* pos, const double4* spos, Grid g,
+#ifndef AB_BUILD_MINBLOCKS
+#define AB_BUILD_MINBLOCKS 1
+#endif
+__global__ void __launch_bounds__(128, AB_BUILD_MINBLOCKS) k_build_lj(int N, const double4* pos, const double4* spos, Grid g,
                                                   const int* cell_start, const int* cell_atoms, int nr, LJLists Lg,
                                                   int* maxcnt) {
   __shared__ int s_cb[4][STENCIL_MAXCOL], s_pre[4][STENCIL_MAXCOL + 1];
