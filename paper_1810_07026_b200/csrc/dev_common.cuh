@@ -228,6 +228,9 @@ __device__ __forceinline__ void halfcos_poly(float t, float& S, float& dSdt) {
 }
 
 // ------------------------------------------------------------------ splines
+#ifndef AB_GSPLINE_COUNT
+#define AB_GSPLINE_COUNT 0
+#endif
 // g_i(c): cubic Hermite on the species' non-uniform knots; clamped (zero slope) outside
 template <typename R>
 __device__ __forceinline__ R gspline(int sp, R c, R& dg) {
@@ -245,8 +248,17 @@ __device__ __forceinline__ R gspline(int sp, R c, R& dg) {
     return __ldg(gy + n - 1);
   }
   int i = 0;
+#if AB_GSPLINE_COUNT
+  // interval index = number of interior knots <= c (ascending knots): independent loads and
+  // compares instead of a dependent load-compare-branch chain per knot (same index)
+#pragma unroll
+  for (int k = 1; k <= 7; ++k) i += (k <= n - 2 && __ldg(gx + k) <= c) ? 1 : 0;
+  if (n > 9)
+    for (int k = 8; k <= n - 2; ++k) i += __ldg(gx + k) <= c ? 1 : 0;
+#else
 #pragma unroll 1
   while (i < n - 2 && __ldg(gx + i + 1) <= c) ++i;
+#endif
   R h = __ldg(gx + i + 1) - __ldg(gx + i);
   R t = (c - __ldg(gx + i)) / h;
   R t2 = t * t, t3 = t2 * t;
